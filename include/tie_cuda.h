@@ -1,0 +1,140 @@
+/* include/tie_cuda.h -- the drop-in C-ABI of the B200 TIE score / rank / fit path.
+ *
+ * The reference (TIE, arXiv 2604.00499; /root/reference/proj) has no FFI or plugin
+ * registry: its boundary is the C++ header API in namespace tie (proj/include/tiesched/
+ * *.hpp) plus the pybind11 module `_core` (proj/bindings/module.cpp).  Every entry point
+ * below is the batched, device-resident replacement for one reference interface, cited
+ * inline.  Plain pointers and sizes only -- no torch or C++ types cross this line.
+ *
+ * Pointers:   tie_* device entry points take DEVICE pointers and a cudaStream_t passed as
+ *             void* (NULL = legacy default stream); they enqueue work and return.  The
+ *             *_host variants take HOST pointers (pinned for full PCIe speed), copy in,
+ *             compute, copy out and synchronise.
+ * Errors:     return 0 on success, else
+ *               TIE_EDOMAIN   (1)  the reference throws std::domain_error
+ *               TIE_EINVALID  (2)  the reference throws std::invalid_argument
+ *               TIE_ECUDA     (3)  CUDA / NCCL / allocation failure
+ *             with a thread-local message in tie_last_error().  Per-request validation
+ *             runs on the device: the kernels record the FIRST failing request index in
+ *             the context; tie_sync() (and every *_host call) reports it with the
+ *             reference's exception type and message.
+ * Threading:  one tie_ctx per device; calls on one context are serialised per stream.
+ */
+#ifndef TIE_CUDA_H
+#define TIE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TIE_OK 0
+#define TIE_EDOMAIN 1
+#define TIE_EINVALID 2
+#define TIE_ECUDA 3
+
+/* score flags */
+#define TIE_SCORE_MOMENT 0u /* default: sigma-grid moment tables */
+#define TIE_SCORE_EXACT 1u  /* one exp per sample-term, ascending sequential sum     */
+#define TIE_SCORE_RAW 2u    /* per-item semantics: E and censored_cvar as returned by
+                               dist.cpp:179-189 (no max(C,E), no compute_score checks) */
+
+typedef struct tie_ctx tie_ctx;
+
+const char* tie_last_error(void);
+const char* tie_version(void);
+
+/* ---- context: the device-resident McContext ------------------------------------------
+ * Replaces McContext (proj/include/tiesched/dist.hpp:33-45, proj/src/dist.cpp:122-129):
+ * uploads the caller's sorted standard-t sample set once and builds the per-context
+ * tables (y-bucket index, sigma-grid moment prefix tables).  sigma_table_max <= 0 selects
+ * the default (4.0); requests with sigma beyond it take the exact per-term path. */
+int tie_ctx_create(int device, const double* samples, int n_samples, double nu,
+                   double sigma_table_max, tie_ctx** out);
+/* McContext(nu, n_samples, seed) generated on the host bit-identically to the reference
+ * (rng.hpp:21-83 student_t draws, then ascending sort), then uploaded. */
+int tie_ctx_create_mc(int device, double nu, int n_samples, uint64_t seed, tie_ctx** out);
+void tie_ctx_destroy(tie_ctx* ctx);
+int tie_ctx_samples(const tie_ctx* ctx, double* host_out, int n); /* copy of the set */
+int tie_ctx_info(const tie_ctx* ctx, double* nu, int* n_samples, int* device);
+
+/* Wait for `stream` and report the first device-side validation failure since the last
+ * check (reference exception type + message), then clear it. */
+int tie_sync(tie_ctx* ctx, void* stream);
+
+/* ---- scalar helpers (host) -------------------------------------------------------------
+ * compute_beta (proj/src/sched.cpp:9-17); beta is a per-batch scalar computed from the
+ * GLOBAL waiting-queue length. */
+int tie_compute_beta(int adaptive, double beta_fixed, double beta_max, double q_sat,
+                     uint64_t queue_len, double* beta_out);
+/* t_quantile / t_cdf (proj/src/dist.cpp:73-106), host, bit-identical to the reference. */
+double tie_t_quantile(double p, double nu);
+double tie_t_cdf(double y, double nu);
+
+/* ---- K1 score -------------------------------------------------------------------------
+ * Batched replacement for, per request i,
+ *   CensoredLogT cl(LogTParams(mu[i], sigma[i], nu), x_max[i]);      dist.cpp:108-120
+ *   E = censored_expectation(cl, mc);                                dist.cpp:179-181
+ *   C = max(censored_cvar(cl, mc, alpha), E);                        dist.cpp:183-189, sim.cpp:94
+ *   S = compute_score(E, C, beta);                                   sched.cpp:19-26
+ * (the run_sim precompute loop, proj/src/sim.cpp:77-96).  E, cvar, score may be NULL. */
+int tie_score(tie_ctx* ctx, const double* mu, const double* sigma, const double* x_max,
+              uint64_t n, double alpha, double beta, double* E, double* cvar, double* score,
+              unsigned flags, void* stream);
+/* Same, with the reference's Request::max_tokens (u32, workload.hpp:11-19) as x_max. */
+int tie_score_u32(tie_ctx* ctx, const double* mu, const double* sigma,
+                  const uint32_t* max_tokens, uint64_t n, double alpha, double beta, double* E,
+                  double* cvar, double* score, unsigned flags, void* stream);
+
+/* ---- K2 rank --------------------------------------------------------------------------
+ * Dispatch order of a static waiting queue: replaces WaitingQueue::push x n followed by
+ * pop_min until empty (proj/src/sched.cpp:28-94), i.e. order by (key asc, id asc).
+ * ids == NULL means id = index.  Non-finite key -> TIE_EDOMAIN, duplicate id ->
+ * TIE_EINVALID (sched.cpp:59-63), reported at tie_sync. */
+int tie_rank(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n,
+             uint64_t* order, void* stream);
+
+/* ---- K1+K2 fused: score the queue and emit its dispatch order (ids = index) ---------- */
+int tie_score_rank(tie_ctx* ctx, const double* mu, const double* sigma,
+                   const uint32_t* max_tokens, uint64_t n, double alpha, double beta,
+                   double* E, double* cvar, double* score, uint64_t* order, unsigned flags,
+                   void* stream);
+
+/* ---- K3 fit ---------------------------------------------------------------------------
+ * Batched fit_logt_fixed_nu (proj/src/fit.cpp:73-178) over P prompts x K samples (x is
+ * row-major P*K).  Outputs mirror FitResult (fit.hpp:15-25); any output except mu/sigma
+ * may be NULL.  K < 3 -> TIE_EINVALID; nu invalid -> TIE_EDOMAIN (immediate); a sample
+ * <= 0 or non-finite -> TIE_EDOMAIN at tie_sync (check_samples, fit.cpp:18-25). */
+int tie_fit(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu, double* mu,
+            double* sigma, double* log_likelihood, int32_t* iterations, uint8_t* converged,
+            uint8_t* degenerate, void* stream);
+/* logt_loglik / logt_loglik_grad (fit.cpp:44-71) for P parameter points over one sample
+ * vector x[K]; grad may be NULL (else 2*P: d/dmu, d/dsigma interleaved). */
+int tie_logt_loglik(tie_ctx* ctx, const double* x, uint64_t K, const double* mu,
+                    const double* sigma, uint64_t P, double nu, double* ll, double* grad,
+                    void* stream);
+
+/* ---- host-buffer (end-to-end) variants ------------------------------------------------ */
+int tie_score_host(tie_ctx* ctx, const double* mu, const double* sigma, const double* x_max,
+                   uint64_t n, double alpha, double beta, double* E, double* cvar,
+                   double* score, unsigned flags);
+int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
+                        const uint32_t* max_tokens, uint64_t n, double alpha, double beta,
+                        double* score, uint64_t* order, unsigned flags);
+int tie_rank_host(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n,
+                  uint64_t* order);
+int tie_fit_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
+                 double* mu, double* sigma, double* log_likelihood, int32_t* iterations,
+                 uint8_t* converged, uint8_t* degenerate);
+
+/* ---- diagnostics ------------------------------------------------------------------------
+ * Number of this library's kernels launched by the calling thread since the last reset
+ * (bench.py's gpu_launches claim). */
+uint64_t tie_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TIE_CUDA_H */

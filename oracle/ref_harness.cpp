@@ -1,0 +1,288 @@
+// oracle/ref_harness.cpp -- TEST INFRASTRUCTURE ONLY (never the product path).
+//
+// A C-ABI shim over the UNTOUCHED reference library (/root/reference/proj/src/*.cpp,
+// compiled where it lies by oracle/Makefile into oracle/_ref/libtie_ref.so).  It lets
+// the tests, the golden-fixture generator and bench.py's cpu_baseline / --impl reference
+// legs drive the reference's own functions in bulk:
+//
+//   score  : censored_expectation + censored_cvar + max + compute_score, exactly as the
+//            reference's run_sim precompute loop does it (proj/src/sim.cpp:77-96,
+//            proj/src/sched.cpp:19-26), fanned out over host threads (pure functions,
+//            shared const McContext -- SPEC.md:139).
+//   rank   : WaitingQueue push x n then pop_min until empty (proj/src/sched.cpp:28-94).
+//   fit    : fit_logt_fixed_nu per prompt (proj/src/fit.cpp:73-178), threaded.
+//   inputs : gen_logt_workload (proj/src/workload.cpp:50-78), McContext
+//            (proj/src/dist.cpp:122-129), sample_logt (proj/src/dist.cpp:142-147).
+//
+// Nothing here re-implements reference arithmetic; every number comes out of the
+// reference's own functions.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "tiesched/dist.hpp"
+#include "tiesched/fit.hpp"
+#include "tiesched/rng.hpp"
+#include "tiesched/sched.hpp"
+#include "tiesched/sim.hpp"
+#include "tiesched/workload.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception& e, int code) {
+  g_err = e.what();
+  return code;
+}
+
+template <class F>
+void parallel_for(size_t n, int threads, F&& body) {
+  if (threads <= 1 || n < 2) {
+    for (size_t i = 0; i < n; ++i) body(i);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  const size_t chunk = 256;
+  std::vector<std::thread> pool;
+  std::vector<std::exception_ptr> errs((size_t)threads);
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        for (;;) {
+          size_t b = next.fetch_add(chunk);
+          if (b >= n) break;
+          size_t e = std::min(n, b + chunk);
+          for (size_t i = b; i < e; ++i) body(i);
+        }
+      } catch (...) {
+        errs[(size_t)t] = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_hw_threads() { return (int)std::max(1u, std::thread::hardware_concurrency()); }
+
+// McContext(nu, n, seed).samples -> out[n]
+int ref_mc_samples(double nu, int n, uint64_t seed, double* out) {
+  try {
+    tie::McContext mc(nu, n, seed);
+    std::memcpy(out, mc.samples.data(), sizeof(double) * mc.samples.size());
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
+  } catch (const std::exception& e) {
+    return fail(e, 2);
+  }
+}
+
+double ref_t_cdf(double y, double nu) { return tie::t_cdf(y, nu); }
+double ref_t_quantile(double p, double nu) { return tie::t_quantile(p, nu); }
+double ref_t_pdf(double y, double nu) { return tie::t_pdf(y, nu); }
+uint64_t ref_mix64(uint64_t a, uint64_t b) { return tie::mix64(a, b); }
+
+// gen_logt_workload(spec, seed) -> SoA arrays (ids are 0..n-1 by construction)
+int ref_gen_workload(uint64_t n, uint64_t seed, double mu_lo, double mu_hi, double sg_lo,
+                     double sg_hi, double nu, uint32_t max_tokens, double rps, double* mu,
+                     double* sigma, uint32_t* max_tok, double* arrival, uint32_t* prompt_tokens,
+                     uint32_t* true_len) {
+  try {
+    tie::WorkloadSpec ws;
+    ws.n_requests = (size_t)n;
+    ws.mu_range = {mu_lo, mu_hi};
+    ws.sigma_range = {sg_lo, sg_hi};
+    ws.nu = nu;
+    ws.max_tokens = max_tokens;
+    ws.rps = rps;
+    auto reqs = tie::gen_logt_workload(ws, seed);
+    for (size_t i = 0; i < reqs.size(); ++i) {
+      mu[i] = *reqs[i].true_mu;
+      sigma[i] = *reqs[i].true_sigma;
+      max_tok[i] = reqs[i].max_tokens;
+      if (arrival) arrival[i] = reqs[i].arrival_s;
+      if (prompt_tokens) prompt_tokens[i] = reqs[i].prompt_tokens;
+      if (true_len) true_len[i] = reqs[i].true_output_tokens;
+    }
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
+  } catch (const std::exception& e) {
+    return fail(e, 2);
+  }
+}
+
+// Per request, the reference scoring chain of run_sim (sim.cpp:85-95) followed by
+// compute_score (sched.cpp:19-26).  Any of E/C/S may be null.
+int ref_score(const double* mu, const double* sigma, const double* x_max, uint64_t n, double nu,
+              int mc_n, uint64_t mc_seed, double alpha, double beta, double* E, double* C,
+              double* S, int threads) {
+  try {
+    tie::McContext mc(nu, mc_n, mc_seed);
+    parallel_for((size_t)n, threads, [&](size_t i) {
+      tie::CensoredLogT cl(tie::LogTParams(mu[i], sigma[i], nu), x_max[i]);
+      double e = tie::censored_expectation(cl, mc);
+      double c = tie::censored_cvar(cl, mc, alpha);
+      c = std::max(c, e);
+      if (E) E[i] = e;
+      if (C) C[i] = c;
+      if (S) S[i] = tie::compute_score(e, c, beta);
+    });
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 2);
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
+}
+
+double ref_compute_beta(int adaptive, double beta_fixed, double beta_max, double q_sat,
+                        uint64_t queue_len) {
+  tie::ScoreConfig cfg;
+  cfg.beta_mode = adaptive ? tie::BetaMode::AdaptiveLinear : tie::BetaMode::Fixed;
+  cfg.beta_fixed = beta_fixed;
+  cfg.beta_max = beta_max;
+  cfg.q_sat = q_sat;
+  return tie::compute_beta(cfg, (size_t)queue_len);
+}
+
+// Dispatch order of a static queue: WaitingQueue push x n, pop_min until empty.
+// ids may be null (then id = index).
+int ref_rank(const double* key, const uint64_t* ids, uint64_t n, uint64_t* order) {
+  try {
+    tie::WaitingQueue q;
+    for (uint64_t i = 0; i < n; ++i) {
+      tie::QueueEntry e;
+      e.req_id = ids ? ids[i] : i;
+      e.key = key[i];
+      q.push(e);
+    }
+    uint64_t k = 0;
+    while (auto e = q.pop_min()) order[k++] = e->req_id;
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
+  } catch (const std::exception& e) {
+    return fail(e, 2);
+  }
+}
+
+// fit_logt_fixed_nu over P prompts of K samples each (row-major x[P*K]).
+int ref_fit(const double* x, uint64_t P, uint64_t K, double nu, double* mu, double* sigma,
+            double* ll, int32_t* iters, uint8_t* converged, uint8_t* degenerate, int threads) {
+  try {
+    parallel_for((size_t)P, threads, [&](size_t p) {
+      std::vector<double> v(x + p * K, x + (p + 1) * K);
+      tie::FitResult r = tie::fit_logt_fixed_nu(v, nu);
+      mu[p] = r.mu;
+      sigma[p] = r.sigma;
+      if (ll) ll[p] = r.log_likelihood;
+      if (iters) iters[p] = r.iterations;
+      if (converged) converged[p] = r.converged;
+      if (degenerate) degenerate[p] = r.degenerate;
+    });
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 2);
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
+}
+
+double ref_logt_loglik(const double* x, uint64_t K, double mu, double sigma, double nu) {
+  return tie::logt_loglik(std::vector<double>(x, x + K), mu, sigma, nu);
+}
+
+// Config-3 prompt generator (following main.cpp:841-845): truths drawn
+// sequentially from Rng(seed); samples sample_logt(LogTParams(mu,sigma,nu), K,
+// mix64(seed, p)); integerised max(1, llround(x)) with a u32 ceiling (the reference's
+// fit CSV carries integer lengths >= 1, main.cpp:458-465).
+int ref_gen_fit_data(uint64_t P, uint64_t K, uint64_t seed, double mu_lo, double mu_hi,
+                     double sg_lo, double sg_hi, double nu, int integerise, double* x,
+                     double* true_mu, double* true_sigma) {
+  try {
+    tie::Rng rng(seed);
+    std::vector<double> m(P), s(P);
+    for (uint64_t p = 0; p < P; ++p) {
+      m[p] = rng.uniform(mu_lo, mu_hi);
+      s[p] = rng.uniform(sg_lo, sg_hi);
+    }
+    for (uint64_t p = 0; p < P; ++p) {
+      auto v = tie::sample_logt(tie::LogTParams(m[p], s[p], nu), (size_t)K, tie::mix64(seed, p));
+      for (uint64_t k = 0; k < K; ++k) {
+        double val = v[k];
+        if (integerise) {
+          val = val >= 4294967295.0 ? 4294967295.0 : (double)std::max(1LL, std::llround(val));
+        }
+        x[p * K + k] = val;
+      }
+      if (true_mu) true_mu[p] = m[p];
+      if (true_sigma) true_sigma[p] = s[p];
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, 1);
+  }
+}
+
+// Scheduler-level mirror used by the schedule-step tests: apply a scripted sequence of
+// (op, id, E, CVaR) events to a reference tie::Scheduler and record pops.
+// op: 0 = on_arrival(id, arrival=E, max_tokens=(uint32)CVaR), 1 = on_prediction(id, E, CVaR),
+//     2 = next_request (writes popped id or UINT64_MAX into out[k++]).
+int ref_scheduler_script(int policy, int adaptive, double beta_fixed, double beta_max,
+                         double q_sat, double rebuild_threshold, uint64_t n_ops,
+                         const int32_t* op, const uint64_t* id, const double* a,
+                         const double* b, uint64_t* out, uint64_t* n_out) {
+  try {
+    tie::ScoreConfig cfg;
+    cfg.beta_mode = adaptive ? tie::BetaMode::AdaptiveLinear : tie::BetaMode::Fixed;
+    cfg.beta_fixed = beta_fixed;
+    cfg.beta_max = beta_max;
+    cfg.q_sat = q_sat;
+    cfg.rebuild_threshold = rebuild_threshold;
+    tie::Scheduler s((tie::Policy)policy, cfg);
+    uint64_t k = 0;
+    for (uint64_t i = 0; i < n_ops; ++i) {
+      if (op[i] == 0) {
+        tie::Request r{};
+        r.id = id[i];
+        r.arrival_s = a[i];
+        r.max_tokens = (uint32_t)b[i];
+        s.on_arrival(r);
+      } else if (op[i] == 1) {
+        s.on_prediction(id[i], a[i], b[i]);
+      } else {
+        auto got = s.next_request();
+        out[k++] = got ? *got : UINT64_MAX;
+      }
+    }
+    *n_out = k;
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 2);
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
+}
+
+}  // extern "C"

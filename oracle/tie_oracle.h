@@ -1,0 +1,75 @@
+/* oracle/tie_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain-C restatement of the reference's score / rank / fit path (TIE, arXiv
+ * 2604.00499, /root/reference/proj).  It is the CHECKER the parity tests, smoke() and
+ * bench.py's cpu_baseline leg compare the CUDA path against; nothing in the product
+ * (paper_2604_00499_b200/) may link, load or call it.
+ *
+ * Parity pinning: tests/test_oracle.py checks every function here against the compiled
+ * reference (oracle/_ref/libtie_ref.so, built from the untouched sources by
+ * `make -C oracle ref`) bit-for-bit, and against the committed golden fixtures in
+ * tests/golden/ (generated from that same reference by tests/golden/make_golden.py).
+ *
+ * Return codes mirror the reference's exception types:
+ *   0 ok, 1 std::domain_error, 2 std::invalid_argument; message in tor_last_error().
+ */
+#ifndef TIE_ORACLE_H
+#define TIE_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char* tor_last_error(void);
+
+/* rng.hpp:10-16 */
+uint64_t tor_mix64(uint64_t a, uint64_t b);
+
+/* McContext::McContext, dist.cpp:122-129 (student_t draws, then ascending sort) */
+int tor_mc_samples(double nu, int n, uint64_t seed, double* out);
+
+/* dist.cpp:52-106 */
+double tor_regularized_incomplete_beta(double a, double b, double x);
+double tor_t_pdf(double y, double nu);
+double tor_t_cdf(double y, double nu);
+double tor_t_quantile(double p, double nu);
+
+/* dist.cpp:142-147 */
+int tor_sample_logt(double mu, double sigma, double nu, uint64_t n, uint64_t seed, double* out);
+
+/* Score a batch: censored_expectation, censored_cvar, max (sim.cpp:85-94) and
+ * compute_score (sched.cpp:19-26).  samples = sorted McContext set of size N.
+ * E/C/S may be NULL.  *bad_index receives the first failing request (or UINT64_MAX). */
+int tor_score(const double* samples, int N, double nu, const double* mu, const double* sigma,
+              const double* x_max, uint64_t n, double alpha, double beta, double* E, double* C,
+              double* S, uint64_t* bad_index, int threads);
+
+/* sched.cpp:9-17 */
+int tor_compute_beta(int adaptive, double beta_fixed, double beta_max, double q_sat,
+                     uint64_t queue_len, double* beta);
+
+/* WaitingQueue pop order of a static queue == lexicographic (key, id) (sched.cpp:28-31).
+ * ids may be NULL (id = index). */
+int tor_rank(const double* key, const uint64_t* ids, uint64_t n, uint64_t* order);
+
+/* fit_logt_fixed_nu, fit.cpp:73-178, over P prompts x K samples (row-major). */
+int tor_fit(const double* x, uint64_t P, uint64_t K, double nu, double* mu, double* sigma,
+            double* ll, int32_t* iters, uint8_t* converged, uint8_t* degenerate, int threads);
+double tor_logt_loglik(const double* x, uint64_t K, double mu, double sigma, double nu);
+
+/* gen_logt_workload, workload.cpp:50-78 (SoA view; ids are 0..n-1) */
+int tor_gen_workload(uint64_t n, uint64_t seed, double mu_lo, double mu_hi, double sg_lo,
+                     double sg_hi, double nu, uint32_t max_tokens, double rps, double* mu,
+                     double* sigma, uint32_t* max_tok, double* arrival, uint32_t* prompt_tokens,
+                     uint32_t* true_len);
+
+/* Config-3 prompt generator (main.cpp:841-845 pattern). */
+int tor_gen_fit_data(uint64_t P, uint64_t K, uint64_t seed, double mu_lo, double mu_hi,
+                     double sg_lo, double sg_hi, double nu, int integerise, double* x,
+                     double* true_mu, double* true_sigma, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,517 @@
+// C-ABI (include/tie_cuda.h): context lifetime, error model, device and host-buffer entry
+// points.  No torch or C++ types cross the boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/tie_cuda.h"
+#include "tie_internal.cuh"
+
+namespace tie {
+namespace capi {
+
+namespace {
+thread_local std::string g_msg;
+thread_local uint64_t g_launches = 0;
+}  // namespace
+
+int set_error(int code, const std::string& msg) {
+  g_msg = msg;
+  return code;
+}
+
+int cuda_error(cudaError_t e, const char* where) {
+  return set_error(TIE_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+void count_launch(uint64_t k) { g_launches += k; }
+
+void* scratch(tie_ctx* ctx, size_t bytes, cudaStream_t s) {
+  if (bytes <= ctx->scratch_bytes) return ctx->scratch;
+  // growth happens outside steady state (first call at a new size): drain users first
+  cudaStreamSynchronize(s);
+  cudaDeviceSynchronize();
+  if (ctx->scratch) cudaFree(ctx->scratch);
+  ctx->scratch = nullptr;
+  ctx->scratch_bytes = 0;
+  const size_t want = bytes + bytes / 8 + (1 << 20);
+  if (cudaMalloc(&ctx->scratch, want) != cudaSuccess) return nullptr;
+  ctx->scratch_bytes = want;
+  return ctx->scratch;
+}
+
+}  // namespace capi
+}  // namespace tie
+
+using tie::capi::cuda_error;
+using tie::capi::set_error;
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+#define TIE_CUDA_TRY(expr, where)                      \
+  do {                                                 \
+    cudaError_t _e = (expr);                           \
+    if (_e != cudaSuccess) return cuda_error(_e, where); \
+  } while (0)
+
+int check_ctx(const tie_ctx* ctx) {
+  if (!ctx) return set_error(TIE_EINVALID, "tie: null context");
+  return TIE_OK;
+}
+
+// decode the device error word into the reference's exception type + message
+int decode_error(uint64_t word, const char* op) {
+  using namespace tie::dev;
+  const uint64_t idx = word >> 8;
+  const uint32_t why = (uint32_t)(word & 0xff);
+  const std::string at = std::string(op) + ": item " + std::to_string(idx) + ": ";
+  switch (why) {
+    case kMuNotFinite: return set_error(TIE_EDOMAIN, at + "LogTParams: mu must be finite");
+    case kSigmaBad:
+      return set_error(TIE_EDOMAIN, at + "LogTParams: sigma must be finite and > 0");
+    case kXmaxBad:
+      return set_error(TIE_EDOMAIN, at + "CensoredLogT: x_max must be finite and > 0");
+    case kScoreNotFinite:
+      return set_error(TIE_EDOMAIN, at + "compute_score: arguments must be finite");
+    case kExpectationNonPos:
+      return set_error(TIE_EDOMAIN, at + "compute_score: expectation must be > 0");
+    case kCvarBelowE:
+      return set_error(TIE_EINVALID,
+                       at + "compute_score: cvar below expectation violates the invariant");
+    case kKeyNotFinite:
+      return set_error(TIE_EDOMAIN, at + "WaitingQueue::push: key must be finite");
+    case kDuplicateId: return set_error(TIE_EINVALID, at + "WaitingQueue::push: id already queued");
+    case kSampleBad:
+      return set_error(TIE_EDOMAIN, at + "fit_logt_fixed_nu: samples must be finite and > 0");
+    default: return set_error(TIE_ECUDA, at + "unknown device error");
+  }
+}
+
+int validate_alpha(double alpha) {
+  if (!(alpha >= 0.0 && alpha < 1.0))
+    return set_error(TIE_EDOMAIN, "censored_cvar: alpha must lie in [0, 1)");
+  return TIE_OK;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+// ====================================================================== context
+extern "C" {
+
+const char* tie_last_error(void) { return tie::capi::g_msg.c_str(); }
+const char* tie_version(void) { return "tie-b200 0.1.0 (sm_100a)"; }
+
+uint64_t tie_launch_count(int reset) {
+  const uint64_t v = tie::capi::g_launches;
+  if (reset) tie::capi::g_launches = 0;
+  return v;
+}
+
+int tie_ctx_create(int device, const double* samples, int n_samples, double nu,
+                   double sigma_table_max, tie_ctx** out) {
+  if (!out) return set_error(TIE_EINVALID, "tie_ctx_create: null output handle");
+  *out = nullptr;
+  if (!(nu > 0.0) || !std::isfinite(nu))
+    return set_error(TIE_EDOMAIN, "McContext: nu must be finite and > 0");
+  if (n_samples <= 0 || !samples)
+    return set_error(TIE_EDOMAIN, "McContext: n_samples must be > 0");
+  for (int i = 0; i < n_samples; ++i) {
+    if (!std::isfinite(samples[i]))
+      return set_error(TIE_EINVALID, "tie_ctx_create: samples must be finite");
+    if (i && samples[i] < samples[i - 1])
+      return set_error(TIE_EINVALID, "tie_ctx_create: samples must be sorted ascending");
+  }
+  if (!(sigma_table_max > 0.0)) sigma_table_max = 4.0;
+  sigma_table_max = std::min(sigma_table_max, 32.0);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_error(TIE_ECUDA, "tie_ctx_create: no CUDA device available");
+  if (device < 0 || device >= ndev) return set_error(TIE_EINVALID, "tie_ctx_create: bad device");
+  DeviceGuard g(device);
+
+  tie_ctx* ctx = new tie_ctx();
+  ctx->device = device;
+  ctx->nu = nu;
+  ctx->N = n_samples;
+  ctx->sigma_table_max = sigma_table_max;
+  ctx->host_samples.assign(samples, samples + n_samples);
+  // request-invariant Student-t constants, computed with the host libm like the reference
+  auto& td = ctx->td;
+  td.nu = nu;
+  td.a = 0.5 * nu;
+  td.b = 0.5;
+  td.logbeta = std::lgamma(td.a) + std::lgamma(td.b) - std::lgamma(td.a + td.b);
+  td.thresh = (td.a + 1.0) / (td.a + td.b + 2.0);
+  tie::host::make_cf_table(td.a, td.b, &td.ab);
+  tie::host::make_cf_table(td.b, td.a, &td.ba);
+
+  auto fail = [&](cudaError_t e, const char* where) {
+    tie_ctx_destroy(ctx);
+    return cuda_error(e, where);
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&ctx->d_err, sizeof(unsigned long long))) != cudaSuccess)
+    return fail(e, "tie_ctx_create(err)");
+  if ((e = cudaMemset(ctx->d_err, 0xff, sizeof(unsigned long long))) != cudaSuccess)
+    return fail(e, "tie_ctx_create(err)");
+  if ((e = cudaMallocHost(&ctx->h_err, sizeof(unsigned long long))) != cudaSuccess)
+    return fail(e, "tie_ctx_create(pinned)");
+  if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(e, "tie_ctx_create(stream)");
+  if ((e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(e, "tie_ctx_create(stream)");
+  for (auto& ev : ctx->ev)
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+      return fail(e, "tie_ctx_create(event)");
+  if ((e = tie::dev::build_context_tables(ctx)) != cudaSuccess)
+    return fail(e, "tie_ctx_create(tables)");
+  *out = ctx;
+  return TIE_OK;
+}
+
+int tie_ctx_create_mc(int device, double nu, int n_samples, uint64_t seed, tie_ctx** out) {
+  std::vector<double> y;
+  try {
+    y = tie::host::mc_samples(nu, n_samples, seed);
+  } catch (const std::domain_error& ex) {
+    return set_error(TIE_EDOMAIN, ex.what());
+  }
+  return tie_ctx_create(device, y.data(), n_samples, nu, 0.0, out);
+}
+
+void tie_ctx_destroy(tie_ctx* ctx) {
+  if (!ctx) return;
+  DeviceGuard g(ctx->device);
+  cudaDeviceSynchronize();
+  cudaFree(ctx->d_Y);
+  cudaFree(ctx->d_ybucket);
+  cudaFree(ctx->d_table);
+  cudaFree(ctx->d_err);
+  cudaFree(ctx->scratch);
+  cudaFree(ctx->io);
+  if (ctx->h_err) cudaFreeHost(ctx->h_err);
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  delete ctx;
+}
+
+int tie_ctx_samples(const tie_ctx* ctx, double* host_out, int n) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (n != ctx->N) return set_error(TIE_EINVALID, "tie_ctx_samples: size mismatch");
+  std::memcpy(host_out, ctx->host_samples.data(), sizeof(double) * n);
+  return TIE_OK;
+}
+
+int tie_ctx_info(const tie_ctx* ctx, double* nu, int* n_samples, int* device) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (nu) *nu = ctx->nu;
+  if (n_samples) *n_samples = ctx->N;
+  if (device) *device = ctx->device;
+  return TIE_OK;
+}
+
+int tie_sync(tie_ctx* ctx, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = as_stream(stream);
+  TIE_CUDA_TRY(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s),
+               "tie_sync");
+  TIE_CUDA_TRY(cudaStreamSynchronize(s), "tie_sync");
+  const unsigned long long w = *ctx->h_err;
+  if (w == ~0ull) return TIE_OK;
+  TIE_CUDA_TRY(cudaMemsetAsync(ctx->d_err, 0xff, sizeof(unsigned long long), s), "tie_sync");
+  TIE_CUDA_TRY(cudaStreamSynchronize(s), "tie_sync");
+  return decode_error(w, ctx->err_op);
+}
+
+// ====================================================================== scalar helpers
+int tie_compute_beta(int adaptive, double beta_fixed, double beta_max, double q_sat,
+                     uint64_t queue_len, double* beta_out) {
+  if (!beta_out) return set_error(TIE_EINVALID, "tie_compute_beta: null output");
+  if (!adaptive) {
+    if (beta_fixed < 0.0) return set_error(TIE_EDOMAIN, "compute_beta: beta_fixed must be >= 0");
+    *beta_out = beta_fixed;
+    return TIE_OK;
+  }
+  if (!(beta_max >= 0.0) || !(q_sat > 0.0))
+    return set_error(TIE_EDOMAIN, "compute_beta: beta_max must be >= 0 and q_sat > 0");
+  *beta_out = beta_max * std::min(1.0, (double)queue_len / q_sat);
+  return TIE_OK;
+}
+
+double tie_t_quantile(double p, double nu) {
+  try {
+    return tie::host::t_quantile(p, nu);
+  } catch (const std::exception& e) {
+    set_error(TIE_EDOMAIN, e.what());
+    return std::nan("");
+  }
+}
+
+double tie_t_cdf(double y, double nu) {
+  try {
+    return tie::host::t_cdf(y, nu);
+  } catch (const std::exception& e) {
+    set_error(TIE_EDOMAIN, e.what());
+    return std::nan("");
+  }
+}
+
+// ====================================================================== device entry points
+static int score_impl(tie_ctx* ctx, const double* mu, const double* sigma, const void* x_max,
+                      bool u32, uint64_t n, double alpha, double beta, double* E, double* C,
+                      double* S, uint64_t* keys, unsigned flags, cudaStream_t s,
+                      const char* op) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = validate_alpha(alpha)) return rc;
+  if (n && (!mu || !sigma || !x_max)) return set_error(TIE_EINVALID, std::string(op) + ": null input");
+  DeviceGuard g(ctx->device);
+  ctx->err_op = op;
+  const cudaError_t e =
+      tie::dev::launch_score(ctx, mu, sigma, x_max, u32, n, alpha, beta, E, C, S, keys, flags, s);
+  if (e != cudaSuccess) return cuda_error(e, op);
+  return TIE_OK;
+}
+
+int tie_score(tie_ctx* ctx, const double* mu, const double* sigma, const double* x_max,
+              uint64_t n, double alpha, double beta, double* E, double* cvar, double* score,
+              unsigned flags, void* stream) {
+  return score_impl(ctx, mu, sigma, x_max, false, n, alpha, beta, E, cvar, score, nullptr,
+                    flags, as_stream(stream), "tie_score");
+}
+
+int tie_score_u32(tie_ctx* ctx, const double* mu, const double* sigma,
+                  const uint32_t* max_tokens, uint64_t n, double alpha, double beta, double* E,
+                  double* cvar, double* score, unsigned flags, void* stream) {
+  return score_impl(ctx, mu, sigma, max_tokens, true, n, alpha, beta, E, cvar, score, nullptr,
+                    flags, as_stream(stream), "tie_score");
+}
+
+int tie_rank(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n, uint64_t* order,
+             void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (n && (!key || !order)) return set_error(TIE_EINVALID, "tie_rank: null pointer");
+  DeviceGuard g(ctx->device);
+  ctx->err_op = "tie_rank";
+  const cudaError_t e = tie::dev::launch_rank(ctx, key, nullptr, ids, n, order, as_stream(stream));
+  if (e != cudaSuccess) return cuda_error(e, "tie_rank");
+  return TIE_OK;
+}
+
+int tie_score_rank(tie_ctx* ctx, const double* mu, const double* sigma,
+                   const uint32_t* max_tokens, uint64_t n, double alpha, double beta, double* E,
+                   double* cvar, double* score, uint64_t* order, unsigned flags, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (n && !order) return set_error(TIE_EINVALID, "tie_score_rank: null order");
+  if (n == 0) return TIE_OK;
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = as_stream(stream);
+  uint64_t* keys = tie::dev::rank_key_buffer(ctx, n, s);
+  if (!keys) return set_error(TIE_ECUDA, "tie_score_rank: scratch allocation failed");
+  if (int rc = score_impl(ctx, mu, sigma, max_tokens, true, n, alpha, beta, E, cvar, score, keys,
+                          flags, s, "tie_score_rank"))
+    return rc;
+  const cudaError_t e = tie::dev::launch_rank(ctx, nullptr, keys, nullptr, n, order, s);
+  if (e != cudaSuccess) return cuda_error(e, "tie_score_rank");
+  return TIE_OK;
+}
+
+int tie_fit(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu, double* mu,
+            double* sigma, double* log_likelihood, int32_t* iterations, uint8_t* converged,
+            uint8_t* degenerate, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (K < 3)
+    return set_error(TIE_EINVALID, "fit_logt_fixed_nu: need at least 3 samples, got " +
+                                       std::to_string(K));
+  if (!(nu > 0.0) || !std::isfinite(nu))
+    return set_error(TIE_EDOMAIN, "fit_logt_fixed_nu: nu must be finite and > 0");
+  if (P && (!x || !mu || !sigma)) return set_error(TIE_EINVALID, "tie_fit: null pointer");
+  DeviceGuard g(ctx->device);
+  ctx->err_op = "tie_fit";
+  const cudaError_t e = tie::dev::launch_fit(ctx, x, P, K, nu, mu, sigma, log_likelihood,
+                                             iterations, converged, degenerate, as_stream(stream));
+  if (e != cudaSuccess) return cuda_error(e, "tie_fit");
+  return TIE_OK;
+}
+
+int tie_logt_loglik(tie_ctx* ctx, const double* x, uint64_t K, const double* mu,
+                    const double* sigma, uint64_t P, double nu, double* ll, double* grad,
+                    void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (K < 1) return set_error(TIE_EINVALID, "logt_loglik: need at least 1 samples, got 0");
+  if (!(nu > 0.0)) return set_error(TIE_EDOMAIN, "logt_loglik: sigma and nu must be > 0");
+  DeviceGuard g(ctx->device);
+  ctx->err_op = "tie_logt_loglik";
+  const cudaError_t e =
+      tie::dev::launch_loglik(ctx, x, K, mu, sigma, P, nu, ll, grad, as_stream(stream));
+  if (e != cudaSuccess) return cuda_error(e, "tie_logt_loglik");
+  return TIE_OK;
+}
+
+// ====================================================================== host-buffer variants
+// Each copies inputs H2D on the context's streams, runs the device path, copies results
+// back and synchronises; the device error word is checked before returning.
+
+static char* io_buffer(tie_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->io_bytes) return (char*)ctx->io;
+  cudaDeviceSynchronize();
+  if (ctx->io) cudaFree(ctx->io);
+  ctx->io = nullptr;
+  ctx->io_bytes = 0;
+  const size_t want = bytes + bytes / 8 + (1 << 20);
+  if (cudaMalloc(&ctx->io, want) != cudaSuccess) return nullptr;
+  ctx->io_bytes = want;
+  return (char*)ctx->io;
+}
+
+static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int tie_score_host(tie_ctx* ctx, const double* mu, const double* sigma, const double* x_max,
+                   uint64_t n, double alpha, double beta, double* E, double* cvar, double* score,
+                   unsigned flags) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (n == 0) return TIE_OK;
+  DeviceGuard g(ctx->device);
+  char* b = io_buffer(ctx, 6 * al(8 * n));
+  if (!b) return set_error(TIE_ECUDA, "tie_score_host: device allocation failed");
+  double* d_mu = (double*)b;
+  double* d_sg = (double*)(b + al(8 * n));
+  double* d_xm = (double*)(b + 2 * al(8 * n));
+  double* d_E = E ? (double*)(b + 3 * al(8 * n)) : nullptr;
+  double* d_C = cvar ? (double*)(b + 4 * al(8 * n)) : nullptr;
+  double* d_S = score ? (double*)(b + 5 * al(8 * n)) : nullptr;
+  cudaStream_t s = ctx->stream;
+  TIE_CUDA_TRY(cudaMemcpyAsync(d_mu, mu, 8 * n, cudaMemcpyHostToDevice, s), "tie_score_host");
+  TIE_CUDA_TRY(cudaMemcpyAsync(d_sg, sigma, 8 * n, cudaMemcpyHostToDevice, s), "tie_score_host");
+  TIE_CUDA_TRY(cudaMemcpyAsync(d_xm, x_max, 8 * n, cudaMemcpyHostToDevice, s), "tie_score_host");
+  if (int rc = tie_score(ctx, d_mu, d_sg, d_xm, n, alpha, beta, d_E, d_C, d_S, flags, s)) return rc;
+  if (E) TIE_CUDA_TRY(cudaMemcpyAsync(E, d_E, 8 * n, cudaMemcpyDeviceToHost, s), "tie_score_host");
+  if (cvar)
+    TIE_CUDA_TRY(cudaMemcpyAsync(cvar, d_C, 8 * n, cudaMemcpyDeviceToHost, s), "tie_score_host");
+  if (score)
+    TIE_CUDA_TRY(cudaMemcpyAsync(score, d_S, 8 * n, cudaMemcpyDeviceToHost, s), "tie_score_host");
+  return tie_sync(ctx, s);
+}
+
+int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
+                        const uint32_t* max_tokens, uint64_t n, double alpha, double beta,
+                        double* score, uint64_t* order, unsigned flags) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (int rc = validate_alpha(alpha)) return rc;
+  if (n == 0) return TIE_OK;
+  DeviceGuard g(ctx->device);
+  char* b = io_buffer(ctx, 2 * al(8 * n) + al(4 * n) + al(8 * n) + al(8 * n));
+  if (!b) return set_error(TIE_ECUDA, "tie_score_rank_host: device allocation failed");
+  double* d_mu = (double*)b;
+  double* d_sg = (double*)(b + al(8 * n));
+  uint32_t* d_mt = (uint32_t*)(b + 2 * al(8 * n));
+  double* d_S = score ? (double*)(b + 2 * al(8 * n) + al(4 * n)) : nullptr;
+  uint64_t* d_order = (uint64_t*)(b + 3 * al(8 * n) + al(4 * n));
+  cudaStream_t s = ctx->stream, cs = ctx->copy_stream;
+  uint64_t* keys = tie::dev::rank_key_buffer(ctx, n, s);
+  if (!keys) return set_error(TIE_ECUDA, "tie_score_rank_host: scratch allocation failed");
+  ctx->err_op = "tie_score_rank_host";
+  // pipeline: H2D of chunk c+1 (copy stream) overlaps scoring of chunk c (compute stream)
+  const int chunks = n >= (1u << 20) ? 4 : 1;
+  const uint64_t step = (n + chunks - 1) / chunks;
+  TIE_CUDA_TRY(cudaEventRecord(ctx->ev[0], s), "tie_score_rank_host");
+  TIE_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[0], 0), "tie_score_rank_host");
+  for (int c = 0; c < chunks; ++c) {
+    const uint64_t lo = std::min<uint64_t>(n, c * step), hi = std::min<uint64_t>(n, lo + step);
+    if (lo >= hi) break;
+    const uint64_t m = hi - lo;
+    TIE_CUDA_TRY(cudaMemcpyAsync(d_mu + lo, mu + lo, 8 * m, cudaMemcpyHostToDevice, cs), "h2d");
+    TIE_CUDA_TRY(cudaMemcpyAsync(d_sg + lo, sigma + lo, 8 * m, cudaMemcpyHostToDevice, cs), "h2d");
+    TIE_CUDA_TRY(cudaMemcpyAsync(d_mt + lo, max_tokens + lo, 4 * m, cudaMemcpyHostToDevice, cs),
+                 "h2d");
+    TIE_CUDA_TRY(cudaEventRecord(ctx->ev[1 + (c & 3)], cs), "tie_score_rank_host");
+    TIE_CUDA_TRY(cudaStreamWaitEvent(s, ctx->ev[1 + (c & 3)], 0), "tie_score_rank_host");
+    const cudaError_t e = tie::dev::launch_score(ctx, d_mu + lo, d_sg + lo, d_mt + lo, true, m,
+                                                 alpha, beta, nullptr, nullptr,
+                                                 d_S ? d_S + lo : nullptr, keys + lo,
+                                                 flags & TIE_SCORE_EXACT, s);
+    if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
+  }
+  cudaError_t e = tie::dev::launch_rank(ctx, nullptr, keys, nullptr, n, d_order, s);
+  if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
+  TIE_CUDA_TRY(cudaMemcpyAsync(order, d_order, 8 * n, cudaMemcpyDeviceToHost, s), "d2h");
+  if (score) TIE_CUDA_TRY(cudaMemcpyAsync(score, d_S, 8 * n, cudaMemcpyDeviceToHost, s), "d2h");
+  return tie_sync(ctx, s);
+}
+
+int tie_rank_host(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n,
+                  uint64_t* order) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (n == 0) return TIE_OK;
+  DeviceGuard g(ctx->device);
+  char* b = io_buffer(ctx, 3 * al(8 * n));
+  if (!b) return set_error(TIE_ECUDA, "tie_rank_host: device allocation failed");
+  double* d_key = (double*)b;
+  uint64_t* d_ids = ids ? (uint64_t*)(b + al(8 * n)) : nullptr;
+  uint64_t* d_order = (uint64_t*)(b + 2 * al(8 * n));
+  cudaStream_t s = ctx->stream;
+  TIE_CUDA_TRY(cudaMemcpyAsync(d_key, key, 8 * n, cudaMemcpyHostToDevice, s), "h2d");
+  if (ids) TIE_CUDA_TRY(cudaMemcpyAsync(d_ids, ids, 8 * n, cudaMemcpyHostToDevice, s), "h2d");
+  if (int rc = tie_rank(ctx, d_key, d_ids, n, d_order, s)) return rc;
+  TIE_CUDA_TRY(cudaMemcpyAsync(order, d_order, 8 * n, cudaMemcpyDeviceToHost, s), "d2h");
+  return tie_sync(ctx, s);
+}
+
+int tie_fit_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu, double* mu,
+                 double* sigma, double* log_likelihood, int32_t* iterations, uint8_t* converged,
+                 uint8_t* degenerate) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (K < 3)
+    return set_error(TIE_EINVALID, "fit_logt_fixed_nu: need at least 3 samples, got " +
+                                       std::to_string(K));
+  if (P == 0) return TIE_OK;
+  DeviceGuard g(ctx->device);
+  char* b = io_buffer(ctx, al(8 * P * K) + 3 * al(8 * P) + al(4 * P) + 2 * al(P));
+  if (!b) return set_error(TIE_ECUDA, "tie_fit_host: device allocation failed");
+  size_t off = 0;
+  double* d_x = (double*)(b + off); off += al(8 * P * K);
+  double* d_mu = (double*)(b + off); off += al(8 * P);
+  double* d_sg = (double*)(b + off); off += al(8 * P);
+  double* d_ll = (double*)(b + off); off += al(8 * P);
+  int32_t* d_it = (int32_t*)(b + off); off += al(4 * P);
+  uint8_t* d_cv = (uint8_t*)(b + off); off += al(P);
+  uint8_t* d_dg = (uint8_t*)(b + off);
+  cudaStream_t s = ctx->stream;
+  TIE_CUDA_TRY(cudaMemcpyAsync(d_x, x, 8 * P * K, cudaMemcpyHostToDevice, s), "h2d");
+  if (int rc = tie_fit(ctx, d_x, P, K, nu, d_mu, d_sg, d_ll, d_it, d_cv, d_dg, s)) return rc;
+  TIE_CUDA_TRY(cudaMemcpyAsync(mu, d_mu, 8 * P, cudaMemcpyDeviceToHost, s), "d2h");
+  TIE_CUDA_TRY(cudaMemcpyAsync(sigma, d_sg, 8 * P, cudaMemcpyDeviceToHost, s), "d2h");
+  if (log_likelihood)
+    TIE_CUDA_TRY(cudaMemcpyAsync(log_likelihood, d_ll, 8 * P, cudaMemcpyDeviceToHost, s), "d2h");
+  if (iterations)
+    TIE_CUDA_TRY(cudaMemcpyAsync(iterations, d_it, 4 * P, cudaMemcpyDeviceToHost, s), "d2h");
+  if (converged) TIE_CUDA_TRY(cudaMemcpyAsync(converged, d_cv, P, cudaMemcpyDeviceToHost, s), "d2h");
+  if (degenerate)
+    TIE_CUDA_TRY(cudaMemcpyAsync(degenerate, d_dg, P, cudaMemcpyDeviceToHost, s), "d2h");
+  return tie_sync(ctx, s);
+}
+
+}  // extern "C"

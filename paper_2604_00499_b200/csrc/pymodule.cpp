@@ -1,0 +1,324 @@
+// pybind11 `_core`: the Python surface of the B200 TIE path.  Same names and argument
+// names as the reference module for the score / rank / fit path (proj/bindings/module.cpp:
+// 22-83, 171-172), plus batched NumPy entry points and raw device-pointer entry points
+// (for torch CUDA tensors: pass tensor.data_ptr() and the CUDA stream handle).
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "tie_cuda.h"
+#include "tiesched_b200.hpp"
+
+namespace py = pybind11;
+using namespace tie;
+
+namespace {
+
+template <class T>
+using carray = py::array_t<T, py::array::c_style | py::array::forcecast>;
+
+void throw_code(int rc) {
+  if (rc == TIE_OK) return;
+  const std::string msg = tie_last_error();
+  if (rc == TIE_EDOMAIN) throw std::domain_error(msg);
+  if (rc == TIE_EINVALID) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+template <class T>
+const T* ptr_or_null(const py::object& o) {
+  if (o.is_none()) return nullptr;
+  return o.cast<carray<T>>().data();
+}
+
+void* vp(uintptr_t p) { return reinterpret_cast<void*>(p); }
+
+}  // namespace
+
+PYBIND11_MODULE(_core, m) {
+  m.doc() = "B200 TIE score / rank / fit path (sm_100a kernels behind the tiesched API)";
+  m.attr("__version__") = tie_version();
+
+  // ------------------------------------------------------------- distribution
+  py::class_<LogTParams>(m, "LogTParams")
+      .def(py::init<double, double, double>(), py::arg("mu"), py::arg("sigma"), py::arg("nu"))
+      .def_readonly("mu", &LogTParams::mu)
+      .def_readonly("sigma", &LogTParams::sigma)
+      .def_readonly("nu", &LogTParams::nu)
+      .def_readonly("sigma_clamped", &LogTParams::sigma_clamped)
+      .def("__repr__", [](const LogTParams& p) {
+        return "LogTParams(mu=" + std::to_string(p.mu) + ", sigma=" + std::to_string(p.sigma) +
+               ", nu=" + std::to_string(p.nu) + ")";
+      });
+
+  py::class_<CensoredLogT>(m, "CensoredLogT")
+      .def(py::init<LogTParams, double>(), py::arg("dist"), py::arg("x_max"))
+      .def_readonly("dist", &CensoredLogT::dist)
+      .def_readonly("x_max", &CensoredLogT::x_max);
+
+  py::class_<McContext>(m, "McContext")
+      .def(py::init<double, int, uint64_t, int>(), py::arg("nu"),
+           py::arg("n_samples") = McContext::kDefaultSamples,
+           py::arg("seed") = McContext::kDefaultSeed, py::arg("device") = 0)
+      .def_readonly("nu", &McContext::nu)
+      .def_readonly("seed", &McContext::seed)
+      .def_property_readonly("n_samples", &McContext::n_samples)
+      .def_property_readonly("samples",
+                             [](const McContext& mc) {
+                               return carray<double>((py::ssize_t)mc.n_samples(),
+                                                     mc.samples().data());
+                             })
+      .def_property_readonly("handle",
+                             [](const McContext& mc) { return (uintptr_t)mc.handle(); });
+
+  m.def("t_pdf", &t_pdf, py::arg("y"), py::arg("nu"));
+  m.def("t_cdf", &t_cdf, py::arg("y"), py::arg("nu"));
+  m.def("t_quantile", &t_quantile, py::arg("p"), py::arg("nu"));
+  m.def("sample_logt", &sample_logt, py::arg("params"), py::arg("n"), py::arg("seed"));
+  m.def("censored_expectation", &censored_expectation, py::arg("censored"), py::arg("mc"));
+  m.def("censored_cvar", &censored_cvar, py::arg("censored"), py::arg("mc"), py::arg("alpha"));
+
+  // ------------------------------------------------------------- scoring / policy
+  py::enum_<Policy>(m, "Policy")
+      .value("FCFS", Policy::FCFS)
+      .value("SEPT", Policy::SEPT)
+      .value("TIE", Policy::TIE);
+  py::enum_<BetaMode>(m, "BetaMode")
+      .value("Fixed", BetaMode::Fixed)
+      .value("AdaptiveLinear", BetaMode::AdaptiveLinear);
+  py::class_<ScoreConfig>(m, "ScoreConfig")
+      .def(py::init<>())
+      .def_readwrite("alpha", &ScoreConfig::alpha)
+      .def_readwrite("beta_mode", &ScoreConfig::beta_mode)
+      .def_readwrite("beta_fixed", &ScoreConfig::beta_fixed)
+      .def_readwrite("beta_max", &ScoreConfig::beta_max)
+      .def_readwrite("q_sat", &ScoreConfig::q_sat)
+      .def_readwrite("rebuild_threshold", &ScoreConfig::rebuild_threshold);
+  m.def("compute_beta", &compute_beta, py::arg("config"), py::arg("queue_len"));
+  m.def("compute_score", &compute_score, py::arg("expectation"), py::arg("cvar"),
+        py::arg("beta"));
+
+  // batched, NumPy in / NumPy out (host buffers; H2D/D2H inside)
+  m.def(
+      "score_batch",
+      [](carray<double> mu, carray<double> sigma, carray<double> x_max, const McContext& mc,
+         const ScoreConfig& cfg, py::object queue_len, bool exact) {
+        const size_t n = (size_t)mu.size();
+        if ((size_t)sigma.size() != n || (size_t)x_max.size() != n)
+          throw std::invalid_argument("score_batch: mu, sigma, x_max must have equal length");
+        const size_t q = queue_len.is_none() ? n : queue_len.cast<size_t>();
+        carray<double> E(n), C(n), S(n);
+        {
+          py::gil_scoped_release nogil;
+          score_batch(mu.data(), sigma.data(), x_max.data(), n, mc, cfg, q, E.mutable_data(),
+                      C.mutable_data(), S.mutable_data(), exact);
+        }
+        return py::make_tuple(E, C, S);
+      },
+      py::arg("mu"), py::arg("sigma"), py::arg("x_max"), py::arg("mc"), py::arg("config"),
+      py::arg("queue_len") = py::none(), py::arg("exact") = false,
+      "E, CVaR (max'ed with E) and score for every request; beta from compute_beta(config, "
+      "queue_len) with queue_len defaulting to the batch size");
+  m.def(
+      "rank",
+      [](carray<double> key, py::object ids, py::object mc) {
+        const size_t n = (size_t)key.size();
+        const uint64_t* id = ptr_or_null<uint64_t>(ids);
+        carray<uint64_t> idarr;
+        if (id) {
+          idarr = ids.cast<carray<uint64_t>>();
+          if ((size_t)idarr.size() != n) throw std::invalid_argument("rank: ids length mismatch");
+          id = idarr.data();
+        }
+        const McContext* ctx = mc.is_none() ? nullptr : mc.cast<const McContext*>();
+        carray<uint64_t> order(n);
+        {
+          py::gil_scoped_release nogil;
+          rank(key.data(), n, order.mutable_data(), id, ctx);
+        }
+        return order;
+      },
+      py::arg("key"), py::arg("ids") = py::none(), py::arg("mc") = py::none(),
+      "dispatch order by (key asc, id asc): the WaitingQueue pop order of a static queue");
+  m.def(
+      "score_rank",
+      [](carray<double> mu, carray<double> sigma, carray<uint32_t> max_tokens,
+         const McContext& mc, const ScoreConfig& cfg, py::object queue_len, bool exact) {
+        const size_t n = (size_t)mu.size();
+        if ((size_t)sigma.size() != n || (size_t)max_tokens.size() != n)
+          throw std::invalid_argument("score_rank: input lengths differ");
+        const size_t q = queue_len.is_none() ? n : queue_len.cast<size_t>();
+        carray<double> S(n);
+        carray<uint64_t> order(n);
+        {
+          py::gil_scoped_release nogil;
+          score_rank(mu.data(), sigma.data(), max_tokens.data(), n, mc, cfg, q,
+                     S.mutable_data(), order.mutable_data(), exact);
+        }
+        return py::make_tuple(S, order);
+      },
+      py::arg("mu"), py::arg("sigma"), py::arg("max_tokens"), py::arg("mc"), py::arg("config"),
+      py::arg("queue_len") = py::none(), py::arg("exact") = false);
+
+  // ------------------------------------------------------------- fitting
+  py::enum_<FitFamily>(m, "FitFamily")
+      .value("LogTFixedNu", FitFamily::LogTFixedNu)
+      .value("LogTFreeNu", FitFamily::LogTFreeNu)
+      .value("LogNormal", FitFamily::LogNormal)
+      .value("Exponential", FitFamily::Exponential);
+  py::class_<FitResult>(m, "FitResult")
+      .def_readonly("family", &FitResult::family)
+      .def_readonly("mu", &FitResult::mu)
+      .def_readonly("sigma", &FitResult::sigma)
+      .def_readonly("nu", &FitResult::nu)
+      .def_readonly("rate", &FitResult::rate)
+      .def_readonly("log_likelihood", &FitResult::log_likelihood)
+      .def_readonly("converged", &FitResult::converged)
+      .def_readonly("iterations", &FitResult::iterations)
+      .def_readonly("degenerate", &FitResult::degenerate);
+  m.def("logt_loglik", &logt_loglik, py::arg("x"), py::arg("mu"), py::arg("sigma"),
+        py::arg("nu"));
+  m.def("logt_loglik_grad", &logt_loglik_grad, py::arg("x"), py::arg("mu"), py::arg("sigma"),
+        py::arg("nu"));
+  m.def("fit_logt_fixed_nu", &fit_logt_fixed_nu, py::arg("x"), py::arg("nu") = 3.5);
+  m.def(
+      "fit_logt_fixed_nu_batch",
+      [](carray<double> x, double nu) {
+        if (x.ndim() != 2) throw std::invalid_argument("fit_logt_fixed_nu_batch: x must be P x K");
+        const size_t P = (size_t)x.shape(0), K = (size_t)x.shape(1);
+        carray<double> mu(P), sg(P), ll(P);
+        carray<int32_t> it(P);
+        carray<uint8_t> cv(P), dg(P);
+        int rc;
+        {
+          py::gil_scoped_release nogil;
+          rc = tie_fit_host(default_context(), x.data(), P, K, nu, mu.mutable_data(),
+                            sg.mutable_data(), ll.mutable_data(), it.mutable_data(),
+                            cv.mutable_data(), dg.mutable_data());
+        }
+        throw_code(rc);
+        py::dict out;
+        out["mu"] = mu;
+        out["sigma"] = sg;
+        out["log_likelihood"] = ll;
+        out["iterations"] = it;
+        out["converged"] = cv.attr("astype")("bool");
+        out["degenerate"] = dg.attr("astype")("bool");
+        return out;
+      },
+      py::arg("x"), py::arg("nu") = 3.5,
+      "fit_logt_fixed_nu over every row of a P x K array; returns a dict of arrays");
+
+  // ------------------------------------------------------------- device-pointer entry points
+  // (torch CUDA tensors: tensor.data_ptr(), torch.cuda.current_stream().cuda_stream)
+  m.def(
+      "score_device",
+      [](uintptr_t ctx, uintptr_t mu, uintptr_t sigma, uintptr_t x_max, bool x_is_u32,
+         uint64_t n, double alpha, double beta, uintptr_t E, uintptr_t C, uintptr_t S,
+         unsigned flags, uintptr_t stream) {
+        auto* c = reinterpret_cast<tie_ctx*>(ctx);
+        const int rc =
+            x_is_u32 ? tie_score_u32(c, (const double*)mu, (const double*)sigma,
+                                     (const uint32_t*)x_max, n, alpha, beta, (double*)E,
+                                     (double*)C, (double*)S, flags, vp(stream))
+                     : tie_score(c, (const double*)mu, (const double*)sigma,
+                                 (const double*)x_max, n, alpha, beta, (double*)E, (double*)C,
+                                 (double*)S, flags, vp(stream));
+        throw_code(rc);
+      },
+      py::arg("ctx"), py::arg("mu"), py::arg("sigma"), py::arg("x_max"), py::arg("x_is_u32"),
+      py::arg("n"), py::arg("alpha"), py::arg("beta"), py::arg("E"), py::arg("cvar"),
+      py::arg("score"), py::arg("flags") = 0u, py::arg("stream") = 0);
+  m.def(
+      "rank_device",
+      [](uintptr_t ctx, uintptr_t key, uintptr_t ids, uint64_t n, uintptr_t order,
+         uintptr_t stream) {
+        throw_code(tie_rank(reinterpret_cast<tie_ctx*>(ctx), (const double*)key,
+                            (const uint64_t*)ids, n, (uint64_t*)order, vp(stream)));
+      },
+      py::arg("ctx"), py::arg("key"), py::arg("ids"), py::arg("n"), py::arg("order"),
+      py::arg("stream") = 0);
+  m.def(
+      "score_rank_device",
+      [](uintptr_t ctx, uintptr_t mu, uintptr_t sigma, uintptr_t max_tokens, uint64_t n,
+         double alpha, double beta, uintptr_t E, uintptr_t C, uintptr_t S, uintptr_t order,
+         unsigned flags, uintptr_t stream) {
+        throw_code(tie_score_rank(reinterpret_cast<tie_ctx*>(ctx), (const double*)mu,
+                                  (const double*)sigma, (const uint32_t*)max_tokens, n, alpha,
+                                  beta, (double*)E, (double*)C, (double*)S, (uint64_t*)order,
+                                  flags, vp(stream)));
+      },
+      py::arg("ctx"), py::arg("mu"), py::arg("sigma"), py::arg("max_tokens"), py::arg("n"),
+      py::arg("alpha"), py::arg("beta"), py::arg("E"), py::arg("cvar"), py::arg("score"),
+      py::arg("order"), py::arg("flags") = 0u, py::arg("stream") = 0);
+  m.def(
+      "fit_device",
+      [](uintptr_t ctx, uintptr_t x, uint64_t P, uint64_t K, double nu, uintptr_t mu,
+         uintptr_t sigma, uintptr_t ll, uintptr_t iters, uintptr_t conv, uintptr_t degen,
+         uintptr_t stream) {
+        throw_code(tie_fit(reinterpret_cast<tie_ctx*>(ctx), (const double*)x, P, K, nu,
+                           (double*)mu, (double*)sigma, (double*)ll, (int32_t*)iters,
+                           (uint8_t*)conv, (uint8_t*)degen, vp(stream)));
+      },
+      py::arg("ctx"), py::arg("x"), py::arg("P"), py::arg("K"), py::arg("nu"), py::arg("mu"),
+      py::arg("sigma"), py::arg("ll"), py::arg("iters"), py::arg("conv"), py::arg("degen"),
+      py::arg("stream") = 0);
+  m.def(
+      "sync",
+      [](uintptr_t ctx, uintptr_t stream) {
+        throw_code(tie_sync(reinterpret_cast<tie_ctx*>(ctx), vp(stream)));
+      },
+      py::arg("ctx"), py::arg("stream") = 0);
+  m.def("default_context", []() { return (uintptr_t)default_context(); });
+  m.def("launch_count", [](bool reset) { return tie_launch_count(reset ? 1 : 0); },
+        py::arg("reset") = false);
+  m.def(
+      "gen_logt_workload_soa",
+      [](size_t n, uint64_t seed, std::pair<double, double> mu_range,
+         std::pair<double, double> sigma_range, double nu, std::pair<uint32_t, uint32_t> prompt,
+         uint32_t max_tokens, double rps) {
+        carray<double> mu(n), sg(n), arr(n);
+        carray<uint32_t> mt(n), pt(n), tl(n);
+        {
+          py::gil_scoped_release nogil;
+          gen_logt_workload_soa(n, seed, mu_range.first, mu_range.second, sigma_range.first,
+                               sigma_range.second, nu, prompt.first, prompt.second, max_tokens,
+                               rps, mu.mutable_data(), sg.mutable_data(), mt.mutable_data(),
+                               arr.mutable_data(), pt.mutable_data(), tl.mutable_data());
+        }
+        py::dict d;
+        d["mu"] = mu;
+        d["sigma"] = sg;
+        d["max_tokens"] = mt;
+        d["arrival_s"] = arr;
+        d["prompt_tokens"] = pt;
+        d["true_output_tokens"] = tl;
+        return d;
+      },
+      py::arg("n"), py::arg("seed"), py::arg("mu_range") = std::make_pair(3.0, 5.0),
+      py::arg("sigma_range") = std::make_pair(0.5, 1.2), py::arg("nu") = 3.5,
+      py::arg("prompt_range") = std::make_pair(64u, 512u), py::arg("max_tokens") = 2048u,
+      py::arg("rps") = 100.0);
+  m.def(
+      "gen_fit_data",
+      [](size_t P, size_t K, uint64_t seed, std::pair<double, double> mu_range,
+         std::pair<double, double> sigma_range, double nu, bool integerise, int threads) {
+        carray<double> x({(py::ssize_t)P, (py::ssize_t)K});
+        carray<double> tm(P), ts(P);
+        {
+          py::gil_scoped_release nogil;
+          gen_fit_data(P, K, seed, mu_range.first, mu_range.second, sigma_range.first,
+                       sigma_range.second, nu, integerise, x.mutable_data(), tm.mutable_data(),
+                       ts.mutable_data(), threads);
+        }
+        return py::make_tuple(x, tm, ts);
+      },
+      py::arg("P"), py::arg("K") = 16, py::arg("seed") = 1,
+      py::arg("mu_range") = std::make_pair(3.0, 5.0),
+      py::arg("sigma_range") = std::make_pair(0.5, 1.2), py::arg("nu") = 3.5,
+      py::arg("integerise") = true, py::arg("threads") = 0);
+}

@@ -1,0 +1,139 @@
+// Internal declarations shared by the .cu translation units of libtie_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "host_numerics.hpp"
+
+namespace tie {
+namespace dev {
+
+// ---------------------------------------------------------------- error reporting
+// First failing request of a batch: kernels atomicMin((index << 8) | reason) into the
+// context's device error word; tie_sync() decodes it into the reference's exception.
+enum Reason : uint32_t {
+  kOk = 0,
+  kMuNotFinite = 1,      // LogTParams: mu must be finite                 (dist.cpp:109)
+  kSigmaBad = 2,         // LogTParams: sigma must be finite and > 0      (dist.cpp:110)
+  kXmaxBad = 3,          // CensoredLogT: x_max must be finite and > 0    (dist.cpp:119)
+  kScoreNotFinite = 4,   // compute_score: arguments must be finite       (sched.cpp:20-21)
+  kExpectationNonPos = 5,// compute_score: expectation must be > 0        (sched.cpp:22)
+  kCvarBelowE = 6,       // compute_score: cvar below expectation         (sched.cpp:23-24)
+  kKeyNotFinite = 7,     // WaitingQueue::push: key must be finite        (sched.cpp:60)
+  kDuplicateId = 8,      // WaitingQueue::push: id already queued         (sched.cpp:61-63)
+  kSampleBad = 9,        // fit_logt_fixed_nu: samples must be finite and > 0 (fit.cpp:22-24)
+};
+
+__device__ __forceinline__ void report(unsigned long long* err, uint64_t index, uint32_t why) {
+  atomicMin(err, (unsigned long long)((index << 8) | why));
+}
+
+// ---------------------------------------------------------------- Student-t constants
+// Everything t_cdf needs that does not depend on the request (computed on the host with
+// glibc, so bit-identical to the reference's own constants).
+struct TdistConst {
+  double nu, a, b;  // a = nu/2, b = 1/2
+  double logbeta;   // lgamma(a) + lgamma(b) - lgamma(a+b)
+  double thresh;    // (a+1)/(a+b+2): CF(a,b,x) below, 1 - CF(b,a,1-x) above
+  host::CfTable ab, ba;
+};
+
+// ---------------------------------------------------------------- score parameters
+// Sigma-grid moment tables:
+//   P[g][k][m] = sum_{i<k} Y_i^m / m! * exp(sigma_g * Y_i),   sigma_g = g * kGridH
+// so that for |delta| = |sigma - sigma_g| <= kGridH/2
+//   sum_{i<k} exp(sigma * Y_i) = sum_m delta^m P[g][k][m]   (truncation < 1e-24 rel.)
+constexpr int kMoments = 16;            // one 128-byte row per (g, k)
+constexpr double kGridH = 1.0 / 32.0;   // power of two: g*h and sigma - g*h are exact
+constexpr double kGridInvH = 32.0;
+constexpr int kYBuckets = 8192;         // uniform-y bucket index over the sample range
+
+struct ScoreParams {
+  TdistConst td;
+  const double* Y;          // sorted samples [N]
+  const uint32_t* ybucket;  // [kYBuckets + 1] upper_bound(Y, edge_b)
+  const double* table;      // [G][N+1][kMoments]
+  double y0, y_scale;       // bucket b = floor((y - y0) * y_scale)
+  double yN;                // Y[N-1]
+  int N;
+  int G;                    // grid points in the table (0 => no table)
+  uint32_t k_alpha;         // upper_bound(Y, t_quantile(alpha, nu)); 0 when alpha == 0
+  double alpha, beta;
+  int raw;                  // TIE_SCORE_RAW: skip max(C,E) and compute_score
+  unsigned long long* err;
+};
+
+}  // namespace dev
+}  // namespace tie
+
+// The opaque C handle (include/tie_cuda.h).
+struct tie_ctx {
+  int device = 0;
+  double nu = 0.0;
+  int N = 0;
+  double sigma_table_max = 0.0;
+  std::vector<double> host_samples;
+  tie::dev::TdistConst td{};
+  // device state
+  double* d_Y = nullptr;
+  uint32_t* d_ybucket = nullptr;
+  double* d_table = nullptr;
+  int G = 0;
+  double y0 = 0, y_scale = 0, yN = 0;
+  unsigned long long* d_err = nullptr;   // first failure (index << 8 | reason)
+  unsigned long long* h_err = nullptr;   // pinned mirror
+  const char* err_op = "";               // API call the pending error belongs to
+  // scratch arena (grown on demand, reused; never freed inside a call)
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  // device I/O arena of the *_host entry points
+  void* io = nullptr;
+  size_t io_bytes = 0;
+  // cached k_alpha = upper_bound(Y, t_quantile(alpha, nu)) of the last alpha seen
+  double ka_alpha = -1.0;
+  uint32_t ka_k = 0;
+  // pinned host staging for the *_host entry points
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  cudaStream_t stream = nullptr;         // internal stream for *_host calls
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev[8] = {};
+};
+
+namespace tie {
+namespace capi {
+// thread-local error message plumbing (capi.cu)
+int set_error(int code, const std::string& msg);
+int cuda_error(cudaError_t e, const char* where);
+void count_launch(uint64_t k = 1);
+void* scratch(tie_ctx* ctx, size_t bytes, cudaStream_t s);
+}  // namespace capi
+
+// kernels' host-side launchers (score.cu, rank.cu, fit.cu)
+namespace dev {
+cudaError_t build_context_tables(tie_ctx* ctx);
+cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma,
+                         const void* x_max, bool x_is_u32, uint64_t n, double alpha,
+                         double beta, double* E, double* C, double* S, uint64_t* keys_out,
+                         unsigned flags, cudaStream_t s);
+// Radix sort by (key, id); keys are IEEE doubles (scores or raw keys) viewed as u64 after
+// an order-preserving transform.  keys_are_positive_bits: keys already u64 bit patterns of
+// positive finite doubles (the fused score path writes these).
+cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* key_bits,
+                        const uint64_t* ids, uint64_t n, uint64_t* order, cudaStream_t s);
+size_t rank_scratch_bytes(uint64_t n, bool with_ids);
+// where a producer (the fused score kernel) should write transformed u64 keys so that
+// launch_rank(key_bits = this pointer) sorts them in place without a copy
+uint64_t* rank_key_buffer(tie_ctx* ctx, uint64_t n, cudaStream_t s);
+cudaError_t launch_fit(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
+                       double* mu, double* sigma, double* ll, int32_t* iters, uint8_t* conv,
+                       uint8_t* degen, cudaStream_t s);
+cudaError_t launch_loglik(tie_ctx* ctx, const double* x, uint64_t K, const double* mu,
+                          const double* sigma, uint64_t P, double nu, double* ll, double* grad,
+                          cudaStream_t s);
+}  // namespace dev
+}  // namespace tie

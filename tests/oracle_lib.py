@@ -1,0 +1,262 @@
+"""ctypes wrappers over the CHECKERS (test infrastructure only).
+
+* ``Oracle``  -- oracle/_build/libtie_oracle.so, the plain-C restatement (oracle/tie_oracle.c).
+* ``RefLib``  -- oracle/_ref/libtie_ref.so, the untouched reference sources compiled by
+  ``make -C oracle ref`` (only present where /root/reference was available at build time).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may use this module.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_DIR = os.path.join(ROOT, "oracle")
+ORACLE_SO = os.path.join(ORACLE_DIR, "_build", "libtie_oracle.so")
+REF_SO = os.path.join(ORACLE_DIR, "_ref", "libtie_ref.so")
+
+_d = ctypes.c_double
+_u64 = ctypes.c_uint64
+_i32 = ctypes.c_int
+_p = ctypes.c_void_p
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _threads(threads):
+    return int(threads) if threads else (os.cpu_count() or 1)
+
+
+class _Base:
+    prefix = ""
+
+    def _fn(self, name, argtypes, restype=ctypes.c_int):
+        f = getattr(self.lib, self.prefix + name)
+        f.argtypes = argtypes
+        f.restype = restype
+        return f
+
+    def _check(self, rc, what):
+        if rc:
+            msg = self._err().decode()
+            if rc == 1:
+                raise ValueError(f"{what}: domain_error: {msg}")
+            if rc == 2:
+                raise ValueError(f"{what}: invalid_argument: {msg}")
+            raise RuntimeError(f"{what}: rc={rc}: {msg}")
+
+    # -- common API ------------------------------------------------------------------
+    def mc_samples(self, nu=3.5, n=10000, seed=12):
+        out = np.empty(n, np.float64)
+        self._check(self._mc(nu, n, seed, _ptr(out)), "mc_samples")
+        return out
+
+    def gen_workload(self, n, seed=1, mu_range=(3.0, 5.0), sigma_range=(0.5, 1.2), nu=3.5,
+                     max_tokens=2048, rps=100.0, extras=False):
+        mu = np.empty(n, np.float64)
+        sg = np.empty(n, np.float64)
+        mt = np.empty(n, np.uint32)
+        arr = np.empty(n, np.float64) if extras else None
+        pt = np.empty(n, np.uint32) if extras else None
+        tl = np.empty(n, np.uint32) if extras else None
+        rc = self._gw(n, seed, mu_range[0], mu_range[1], sigma_range[0], sigma_range[1], nu,
+                      max_tokens, rps, _ptr(mu), _ptr(sg), _ptr(mt), _ptr(arr), _ptr(pt),
+                      _ptr(tl))
+        self._check(rc, "gen_workload")
+        if extras:
+            return mu, sg, mt, arr, pt, tl
+        return mu, sg, mt
+
+    def rank(self, key, ids=None):
+        key = np.ascontiguousarray(key, np.float64)
+        ids = None if ids is None else np.ascontiguousarray(ids, np.uint64)
+        out = np.empty(len(key), np.uint64)
+        self._check(self._rank(_ptr(key), _ptr(ids), len(key), _ptr(out)), "rank")
+        return out
+
+    def fit(self, x, nu=3.5, threads=None):
+        x = np.ascontiguousarray(x, np.float64)
+        P, K = x.shape
+        mu = np.empty(P)
+        sg = np.empty(P)
+        ll = np.empty(P)
+        it = np.empty(P, np.int32)
+        cv = np.empty(P, np.uint8)
+        dg = np.empty(P, np.uint8)
+        rc = self._fit(_ptr(x), P, K, nu, _ptr(mu), _ptr(sg), _ptr(ll), _ptr(it), _ptr(cv),
+                       _ptr(dg), _threads(threads))
+        self._check(rc, "fit")
+        return dict(mu=mu, sigma=sg, log_likelihood=ll, iterations=it,
+                    converged=cv.astype(bool), degenerate=dg.astype(bool))
+
+
+class Oracle(_Base):
+    """The C restatement (the parity checker)."""
+
+    prefix = "tor_"
+
+    def __init__(self, path=ORACLE_SO):
+        if not os.path.exists(path):
+            subprocess.run(["make", "-s", "-C", ORACLE_DIR], check=True)
+        self.lib = ctypes.CDLL(path)
+        self._err = self._fn("last_error", [], ctypes.c_char_p)
+        self._mc = self._fn("mc_samples", [_d, _i32, _u64, _p])
+        self.t_cdf = self._fn("t_cdf", [_d, _d], _d)
+        self.t_pdf = self._fn("t_pdf", [_d, _d], _d)
+        self.t_quantile = self._fn("t_quantile", [_d, _d], _d)
+        self.mix64 = self._fn("mix64", [_u64, _u64], _u64)
+        self.regularized_incomplete_beta = self._fn("regularized_incomplete_beta",
+                                                    [_d, _d, _d], _d)
+        self._score = self._fn("score", [_p, _i32, _d, _p, _p, _p, _u64, _d, _d, _p, _p, _p,
+                                         ctypes.POINTER(_u64), _i32])
+        self._beta = self._fn("compute_beta", [_i32, _d, _d, _d, _u64, ctypes.POINTER(_d)])
+        self._rank = self._fn("rank", [_p, _p, _u64, _p])
+        self._fit = self._fn("fit", [_p, _u64, _u64, _d, _p, _p, _p, _p, _p, _p, _i32])
+        self.logt_loglik_raw = self._fn("logt_loglik", [_p, _u64, _d, _d, _d], _d)
+        self._gw = self._fn("gen_workload", [_u64, _u64, _d, _d, _d, _d, _d, ctypes.c_uint32,
+                                             _d, _p, _p, _p, _p, _p, _p])
+        self._gf = self._fn("gen_fit_data", [_u64, _u64, _u64, _d, _d, _d, _d, _d, _i32, _p,
+                                             _p, _p, _i32])
+        self._sl = self._fn("sample_logt", [_d, _d, _d, _u64, _u64, _p])
+
+    def score(self, samples, mu, sigma, x_max, alpha=0.9, beta=0.5, nu=3.5, threads=None):
+        samples = np.ascontiguousarray(samples, np.float64)
+        mu = np.ascontiguousarray(mu, np.float64)
+        sigma = np.ascontiguousarray(sigma, np.float64)
+        x_max = np.ascontiguousarray(x_max, np.float64)
+        n = len(mu)
+        E = np.empty(n)
+        C = np.empty(n)
+        S = np.empty(n)
+        bad = _u64(0)
+        rc = self._score(_ptr(samples), len(samples), nu, _ptr(mu), _ptr(sigma), _ptr(x_max),
+                         n, alpha, beta, _ptr(E), _ptr(C), _ptr(S), ctypes.byref(bad),
+                         _threads(threads))
+        self._check(rc, f"score (request {bad.value})")
+        return E, C, S
+
+    def compute_beta(self, adaptive, beta_fixed, beta_max, q_sat, queue_len):
+        out = _d(0)
+        self._check(self._beta(int(adaptive), beta_fixed, beta_max, q_sat, queue_len,
+                               ctypes.byref(out)), "compute_beta")
+        return out.value
+
+    def gen_fit_data(self, P, K=16, seed=1, mu_range=(3.0, 5.0), sigma_range=(0.5, 1.2),
+                     nu=3.5, integerise=True, threads=None):
+        x = np.empty((P, K), np.float64)
+        tm = np.empty(P)
+        ts = np.empty(P)
+        rc = self._gf(P, K, seed, mu_range[0], mu_range[1], sigma_range[0], sigma_range[1], nu,
+                      int(integerise), _ptr(x), _ptr(tm), _ptr(ts), _threads(threads))
+        self._check(rc, "gen_fit_data")
+        return x, tm, ts
+
+    def sample_logt(self, mu, sigma, nu, n, seed):
+        out = np.empty(n)
+        self._sl(mu, sigma, nu, n, seed, _ptr(out))
+        return out
+
+    def logt_loglik(self, x, mu, sigma, nu):
+        x = np.ascontiguousarray(x, np.float64)
+        return self.logt_loglik_raw(_ptr(x), len(x), mu, sigma, nu)
+
+
+def ref_available():
+    return os.path.exists(REF_SO)
+
+
+class RefLib(_Base):
+    """The untouched reference library behind oracle/ref_harness.cpp."""
+
+    prefix = "ref_"
+
+    def __init__(self, path=REF_SO):
+        self.lib = ctypes.CDLL(path)
+        self._err = self._fn("last_error", [], ctypes.c_char_p)
+        self._mc = self._fn("mc_samples", [_d, _i32, _u64, _p])
+        self.t_cdf = self._fn("t_cdf", [_d, _d], _d)
+        self.t_pdf = self._fn("t_pdf", [_d, _d], _d)
+        self.t_quantile = self._fn("t_quantile", [_d, _d], _d)
+        self.mix64 = self._fn("mix64", [_u64, _u64], _u64)
+        self.hw_threads = self._fn("hw_threads", [], _i32)
+        self._score = self._fn("score", [_p, _p, _p, _u64, _d, _i32, _u64, _d, _d, _p, _p, _p,
+                                         _i32])
+        self.compute_beta_raw = self._fn("compute_beta", [_i32, _d, _d, _d, _u64], _d)
+        self._rank = self._fn("rank", [_p, _p, _u64, _p])
+        self._fit = self._fn("fit", [_p, _u64, _u64, _d, _p, _p, _p, _p, _p, _p, _i32])
+        self.logt_loglik_raw = self._fn("logt_loglik", [_p, _u64, _d, _d, _d], _d)
+        self._gw = self._fn("gen_workload", [_u64, _u64, _d, _d, _d, _d, _d, ctypes.c_uint32,
+                                             _d, _p, _p, _p, _p, _p, _p])
+        self._gf = self._fn("gen_fit_data", [_u64, _u64, _u64, _d, _d, _d, _d, _d, _i32, _p,
+                                             _p, _p])
+        self._sched = self._fn("scheduler_script", [_i32, _i32, _d, _d, _d, _d, _u64, _p, _p,
+                                                    _p, _p, _p, ctypes.POINTER(_u64)])
+
+    def score(self, mu, sigma, x_max, alpha=0.9, beta=0.5, nu=3.5, mc_n=10000, mc_seed=12,
+              threads=None):
+        mu = np.ascontiguousarray(mu, np.float64)
+        sigma = np.ascontiguousarray(sigma, np.float64)
+        x_max = np.ascontiguousarray(x_max, np.float64)
+        n = len(mu)
+        E = np.empty(n)
+        C = np.empty(n)
+        S = np.empty(n)
+        rc = self._score(_ptr(mu), _ptr(sigma), _ptr(x_max), n, nu, mc_n, mc_seed, alpha, beta,
+                         _ptr(E), _ptr(C), _ptr(S), _threads(threads))
+        self._check(rc, "score")
+        return E, C, S
+
+    def gen_fit_data(self, P, K=16, seed=1, mu_range=(3.0, 5.0), sigma_range=(0.5, 1.2),
+                     nu=3.5, integerise=True):
+        x = np.empty((P, K), np.float64)
+        tm = np.empty(P)
+        ts = np.empty(P)
+        rc = self._gf(P, K, seed, mu_range[0], mu_range[1], sigma_range[0], sigma_range[1], nu,
+                      int(integerise), _ptr(x), _ptr(tm), _ptr(ts))
+        self._check(rc, "gen_fit_data")
+        return x, tm, ts
+
+    def logt_loglik(self, x, mu, sigma, nu):
+        x = np.ascontiguousarray(x, np.float64)
+        return self.logt_loglik_raw(_ptr(x), len(x), mu, sigma, nu)
+
+    def scheduler_script(self, policy, ops, ids, a, b, adaptive=True, beta_fixed=0.1,
+                         beta_max=0.5, q_sat=128.0, rebuild_threshold=0.1):
+        ops = np.ascontiguousarray(ops, np.int32)
+        ids = np.ascontiguousarray(ids, np.uint64)
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        out = np.empty(len(ops), np.uint64)
+        n_out = _u64(0)
+        rc = self._sched(policy, int(adaptive), beta_fixed, beta_max, q_sat, rebuild_threshold,
+                         len(ops), _ptr(ops), _ptr(ids), _ptr(a), _ptr(b), _ptr(out),
+                         ctypes.byref(n_out))
+        self._check(rc, "scheduler_script")
+        return out[: n_out.value]
+
+
+def fnv1a64(buf: bytes) -> str:
+    h = 0xCBF29CE484222325
+    for byte in buf:
+        h ^= byte
+        h = (h * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return f"{h:016x}"
+
+
+def fnv1a64_np(arr) -> str:
+    """FNV-1a-64 over the raw little-endian bytes of an array (vectorised over 8-byte words
+    would change the definition, so this hashes bytes; fine for <= a few MB)."""
+    a = np.ascontiguousarray(arr)
+    b = a.view(np.uint8)
+    h = np.uint64(0xCBF29CE484222325)
+    prime = np.uint64(0x100000001B3)
+    with np.errstate(over="ignore"):
+        for byte in b:
+            h = (h ^ np.uint64(byte)) * prime
+    return f"{int(h):016x}"
