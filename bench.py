@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 TIE score+rank path (BASELINE.json metric: requests scored+ranked/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL)
+
+Step (N=1, config 2): score + rank a 1,000,000-request synthetic queue (gen_logt_workload,
+seed 1: mu~U[3,5], sigma~U[0.5,1.2], nu=3.5, x_max=2048; McContext(3.5, 10000, 12);
+alpha=0.9, adaptive beta from the global queue length -> 0.5) -- one fused score kernel + the
+radix-sort dispatch order, inputs resident in HBM.  The 20 MB inputs fit in L2, so L2 is
+flushed (256 MB write) between timed steps; each step is bracketed by CUDA events on the
+launching stream and the K step times are summed.  N>1 (weak scaling): 1M requests per rank,
+global queue N x 1M, each rank scores + sorts its shard, then the sorted (score, id) runs are
+all-gathered over NCCL and merged on rank 0 into the global dispatch order.
+
+e2e: the same metric through the public C-ABI host-buffer call tie_score_rank_host (pinned
+host inputs -> H2D -> score -> rank -> D2H of the u64 dispatch order), wall-clocked per call.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_CONFIG2 = 1_000_000
+ALPHA = 0.9
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_CONFIG2, help="requests per rank")
+    ap.add_argument("--no-extras", action="store_true", help="skip fit / exact-mode extras")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def hbm_peak():
+    try:
+        with open(MEASURED) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the GPU is busy."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.device), "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        busy = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": float(np.median(busy)) if busy else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm), "samples_under_load": len(busy),
+                "window": "warmup + timed + e2e + profiling phases"}
+
+
+def cpu_baseline(n_target_s=10.0, per_step_s=None):
+    """The reference's CPU path on this host: oracle/_ref (untouched reference sources) if it
+    was built, else the oracle port.  Scores with all host threads, ranks with the reference
+    WaitingQueue (single-threaded, as the reference does)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle, RefLib, ref_available
+
+    threads = os.cpu_count() or 1
+    if ref_available():
+        lib, kind = RefLib(), "reference"
+        gen = lib
+        score = lambda mu, sg, xm: lib.score(mu, sg, xm, alpha=ALPHA, beta=0.5, threads=threads)
+    else:
+        lib, kind = Oracle(), "port"
+        gen = lib
+        Y = lib.mc_samples()
+        score = lambda mu, sg, xm: lib.score(Y, mu, sg, xm, alpha=ALPHA, beta=0.5,
+                                             threads=threads)
+    mu, sg, mt = gen.gen_workload(N_CONFIG2, seed=1)
+    xm = mt.astype(np.float64)
+    # calibrate on a small prefix, then size the sample to ~n_target_s of work
+    m0 = min(4 * threads * 64, N_CONFIG2)
+    t0 = time.perf_counter()
+    score(mu[:m0], sg[:m0], xm[:m0])
+    rate = m0 / max(time.perf_counter() - t0, 1e-6)
+    budget = per_step_s if per_step_s else n_target_s
+    m = int(min(N_CONFIG2, max(m0, rate * budget)))
+
+    def one():
+        t1 = time.perf_counter()
+        _, _, S = score(mu[:m], sg[:m], xm[:m])
+        t2 = time.perf_counter()
+        lib.rank(S)
+        t3 = time.perf_counter()
+        return t2 - t1, t3 - t2
+
+    return one, m, threads, kind
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    step, m, threads, kind = cpu_baseline(per_step_s=1.0)
+    for _ in range(args.warmup):
+        step()
+    ts = [sum(step()) for _ in range(args.steps)]
+    value = m / float(np.mean(ts))
+    sample = (f"first {m} requests of the config-2 queue (gen_logt_workload n=1M seed 1), "
+              f"scored with {threads} threads + ranked by the reference WaitingQueue, per step")
+    line = {"metric": "requests scored+ranked/sec", "value": value, "unit": "requests/s",
+            "impl": "reference", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.mean(ts)), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config2: 1M-request queue score+rank (sampled on CPU)",
+                       "n_requests": N_CONFIG2, "sample_requests": m, "nu": 3.5,
+                       "alpha": ALPHA, "beta": 0.5, "mc_samples": 10000},
+            "cpu_baseline": {"value": value, "unit": "requests/s", "cores": threads,
+                             "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2604_00499_b200 as tie
+
+    dev = torch.device("cuda", local)
+    n_local = args.n
+    n_global = n_local * world
+    cfg = tie.ScoreConfig()  # alpha 0.9, adaptive beta_max 0.5, q_sat 128
+    beta = tie.compute_beta(cfg, n_global)  # GLOBAL queue length (sched.cpp:9-17)
+    mc = tie.McContext(3.5, 10000, 12, local)
+    ctx = mc.handle
+
+    # ---------------- inputs: config-2 queue (this rank's contiguous shard)
+    w = tie.gen_logt_workload_soa(n_global, 1)
+    lo, hi = rank * n_local, (rank + 1) * n_local
+    mu_h = np.ascontiguousarray(w["mu"][lo:hi])
+    sg_h = np.ascontiguousarray(w["sigma"][lo:hi])
+    mt_h = np.ascontiguousarray(w["max_tokens"][lo:hi])
+    mu = torch.from_numpy(mu_h).to(dev)
+    sg = torch.from_numpy(sg_h).to(dev)
+    mt = torch.from_numpy(mt_h.view(np.int32)).to(dev)
+    S = torch.empty(n_local, dtype=torch.float64, device=dev)
+    order = torch.empty(n_local, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    if world > 1:
+        gk = torch.empty(n_global, dtype=torch.float64, device=dev)
+        gi = torch.empty(n_global, dtype=torch.int64, device=dev)
+        gorder = torch.empty(n_global, dtype=torch.int64, device=dev)
+
+    def step():
+        tie.score_rank_device(ctx, mu.data_ptr(), sg.data_ptr(), mt.data_ptr(), n_local, ALPHA,
+                              beta, 0, 0, S.data_ptr(), order.data_ptr(), 0, sh)
+        if world > 1:
+            # sorted local run of (score, global id) -> all-gather -> merge on rank 0
+            run_k = S[order]
+            run_i = order + lo
+            dist.all_gather_into_tensor(gk, run_k)
+            dist.all_gather_into_tensor(gi, run_i)
+            if rank == 0:
+                # runs are contiguous id ranges in rank order, so the stable sort of the
+                # concatenation by score breaks cross-shard ties by id (sched.cpp:28-31)
+                tie.rank_device(ctx, gk.data_ptr(), 0, n_global, gorder.data_ptr(), sh)
+                torch.take(gi, gorder, out=gorder)  # noqa: in-place gather of global ids
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        step()
+    tie.sync(ctx, sh)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tie.launch_count(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for a, b in ev:
+        flush.zero_()  # inputs (20 MB) fit in L2: evict between timed steps
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    launches = int(tie.launch_count(False))
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = float(np.sum(step_ms))
+    if dist:
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        dist.barrier()
+    torch.cuda.synchronize()
+    tie.sync(ctx, sh)
+    ms_per_step = tot_ms / args.steps
+    value = n_global / (ms_per_step * 1e-3)
+
+    # ---------------- parity spot check of what was timed (rank 0 local shard)
+    order_h = order.cpu().numpy()
+    S_h = S.cpu().numpy()
+    sorted_ok = bool(np.all(np.diff(S_h[order_h]) >= 0))
+
+    # ---------------- e2e through the C-ABI host-buffer call (pinned host memory)
+    pin = lambda a: torch.from_numpy(a).pin_memory()
+    mu_p, sg_p, mt_p = pin(mu_h), pin(sg_h), pin(mt_h.view(np.int32))
+    ord_p = torch.empty(n_local, dtype=torch.int64).pin_memory()
+    e2e_ts = []
+    for i in range(max(args.warmup, 3) + args.steps):
+        t0 = time.perf_counter()
+        tie.score_rank_host_ptr(ctx, mu_p.data_ptr(), sg_p.data_ptr(), mt_p.data_ptr(), n_local,
+                                ALPHA, beta, 0, ord_p.data_ptr(), 0)
+        if i >= max(args.warmup, 3):
+            e2e_ts.append(time.perf_counter() - t0)
+    e2e_s = float(np.mean(e2e_ts))
+    if dist:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = n_global / e2e_s
+    e2e_order_ok = bool(np.array_equal(ord_p.numpy(), order_h))
+
+    # ---------------- kernel-level profile of one step (separate from the timed loop)
+    tie.profile(ctx, True)
+    for _ in range(3):
+        flush.zero_()
+        step()
+    prof = tie.profile_report(ctx)
+    tie.profile(ctx, False)
+    clk = clocks.stop()
+
+    peak, peak_src = hbm_peak()
+    kern = {k: {"launches": v[0] // 3, "ms_per_step": v[1] / 3} for k, v in prof.items()}
+    # active radix passes: byte positions where the order-bits of the scores are not constant
+    bits = S_h.view(np.uint64) | np.uint64(1 << 63)
+    active = sum(1 for p in range(8)
+                 if len(np.unique(((bits >> np.uint64(8 * p)) & np.uint64(255))[:200000])) > 1)
+    dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
+    roof = None
+    if dom == "rank.downsweep":
+        bytes_per_launch = 24.0 * n_local  # read + write one (8 B key, 4 B id) record per key
+        t_launch = kern[dom]["ms_per_step"] * 1e-3 / max(active, 1)
+        ach = bytes_per_launch / t_launch / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": bytes_per_launch, "active_passes": active,
+                "launch_ms": t_launch * 1e3}
+    else:
+        bytes_per_launch = 28.0 * n_local  # mu, sigma (16 B) + max_tokens (4 B) in, key (8 B) out
+        t_launch = kern[dom]["ms_per_step"] * 1e-3 / max(kern[dom]["launches"], 1)
+        ach = bytes_per_launch / t_launch / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": bytes_per_launch, "launch_ms": t_launch * 1e3}
+
+    extras = {}
+    if rank == 0 and not args.no_extras:
+        extras = run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream)
+
+    line = {"metric": "requests scored+ranked/sec", "value": value, "unit": "requests/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config2: 1M-request queue score+rank per GPU"
+                       if world == 1 else f"{world} x 1M-request shards, NCCL all-gather merge",
+                       "n_requests_per_gpu": n_local, "n_requests_global": n_global,
+                       "nu": 3.5, "alpha": ALPHA, "beta": beta, "mc_samples": 10000,
+                       "score_path": "moment tables (TIE_SCORE_MOMENT)",
+                       "parallelism": f"dp{world} (request shards)",
+                       "l2": "flushed (256 MB write) between timed steps"},
+            "e2e": {"value": e2e_value, "unit": "requests/s",
+                    "h2d_bytes_per_step": 20 * n_local, "d2h_bytes_per_step": 8 * n_local,
+                    "ms_per_step": e2e_s * 1e3, "api": "tie_score_rank_host (C-ABI), pinned",
+                    "order_matches_device_path": e2e_order_ok},
+            "gpu_launches": launches, "roofline": roof, "clocks": clk,
+            "kernels_ms_per_step": {k: round(v["ms_per_step"], 5) for k, v in kern.items()},
+            "sorted_check": sorted_ok}
+    line.update(extras)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            one, m, threads, kind = cpu_baseline()
+            ts = one()
+            cb = m / sum(ts)
+            line["cpu_baseline"] = {
+                "value": cb, "unit": "requests/s", "cores": threads, "kind": kind,
+                "sample": f"first {m} requests of the config-2 queue: score on {threads} threads "
+                          f"({ts[0]:.2f} s) + reference WaitingQueue rank ({ts[1]:.2f} s)"}
+        except Exception as exc:  # the baseline never blocks the GPU line
+            line["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream):
+    """Secondary numbers on rank 0: exact-mode score+rank, and config-3 fits/s."""
+    out = {}
+    sh = stream.cuda_stream
+    n = mu.numel()
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    # exact (per-term) score path, same queue
+    a, b = ev(), ev()
+    tie.score_rank_device(ctx, mu.data_ptr(), sg.data_ptr(), mt.data_ptr(), n, ALPHA, beta, 0,
+                          0, S.data_ptr(), order.data_ptr(), 1, sh)
+    torch.cuda.synchronize()
+    reps = 3
+    a.record(stream)
+    for _ in range(reps):
+        tie.score_rank_device(ctx, mu.data_ptr(), sg.data_ptr(), mt.data_ptr(), n, ALPHA, beta,
+                              0, 0, S.data_ptr(), order.data_ptr(), 1, sh)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    out["exact_path"] = {"value": n / (ms * 1e-3), "unit": "requests/s", "ms_per_step": ms,
+                         "note": "TIE_SCORE_EXACT: one exp per sample-term (reference arithmetic)"}
+    # config 3: 1M prompts x 16 sampled lengths
+    P, K = 1_000_000, 16
+    x, _, _ = tie.gen_fit_data(P, K, 1)
+    xd = torch.from_numpy(x).to(dev)
+    fmu = torch.empty(P, dtype=torch.float64, device=dev)
+    fsg = torch.empty_like(fmu)
+    fll = torch.empty_like(fmu)
+    fit_it = torch.empty(P, dtype=torch.int32, device=dev)
+    fcv = torch.empty(P, dtype=torch.uint8, device=dev)
+    fdg = torch.empty_like(fcv)
+    args = (ctx, xd.data_ptr(), P, K, 3.5, fmu.data_ptr(), fsg.data_ptr(), fll.data_ptr(),
+            fit_it.data_ptr(), fcv.data_ptr(), fdg.data_ptr(), sh)
+    tie.fit_device(*args)
+    torch.cuda.synchronize()
+    a, b = ev(), ev()
+    a.record(stream)
+    for _ in range(reps):
+        tie.fit_device(*args)
+    b.record(stream)
+    torch.cuda.synchronize()
+    tie.sync(ctx, sh)
+    fms = a.elapsed_time(b) / reps
+    iters = fit_it.cpu().numpy()
+    # e2e fits through the C-ABI host call (pinned)
+    xp = torch.from_numpy(x).pin_memory()
+    hb = [torch.empty(P, dtype=t).pin_memory() for t in
+          (torch.float64, torch.float64, torch.float64, torch.int32, torch.uint8, torch.uint8)]
+    t0 = time.perf_counter()
+    tie.fit_host_ptr(ctx, xp.data_ptr(), P, K, 3.5, *[t.data_ptr() for t in hb])
+    fe2e = time.perf_counter() - t0
+    out["fit"] = {"metric": "log-t fits/sec (config 3: 1M prompts x 16 lengths)",
+                  "value": P / (fms * 1e-3), "unit": "fits/s", "ms": fms,
+                  "e2e": {"value": P / fe2e, "unit": "fits/s", "h2d_bytes": 8 * P * K,
+                          "d2h_bytes": P * (8 * 3 + 4 + 2)},
+                  "iterations_mean": float(iters.mean()), "iterations_max": int(iters.max())}
+    return out
+
+
+if __name__ == "__main__":
+    main()

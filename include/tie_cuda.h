@@ -130,6 +130,12 @@ int tie_fit_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double n
                  uint8_t* converged, uint8_t* degenerate);
 
 /* ---- diagnostics ------------------------------------------------------------------------
+ * Kernel-level profiling: with tie_profile(ctx, 1) every kernel launched by this context is
+ * bracketed by a CUDA event pair on its stream; tie_profile_report() synchronises and
+ * writes one "name<TAB>launches<TAB>total_ms" line per kernel class.  Off by default. */
+int tie_profile(tie_ctx* ctx, int enable);
+int tie_profile_report(tie_ctx* ctx, char* buf, size_t len);
+/*
  * Number of this library's kernels launched by the calling thread since the last reset
  * (bench.py's gpu_launches claim). */
 uint64_t tie_launch_count(int reset);

@@ -46,6 +46,30 @@ void* scratch(tie_ctx* ctx, size_t bytes, cudaStream_t s) {
 }
 
 }  // namespace capi
+
+namespace {
+cudaEvent_t prof_event(tie_ctx* ctx) {
+  if (ctx->prof_used == ctx->prof_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->prof_pool.push_back(e);
+  }
+  return ctx->prof_pool[ctx->prof_used++];
+}
+}  // namespace
+
+ProfScope::ProfScope(tie_ctx* c, const char* name, cudaStream_t st) : ctx(c), s(st) {
+  if (!ctx || !ctx->prof_on) return;
+  tie_ctx::ProfRec r{name, prof_event(ctx), prof_event(ctx)};
+  cudaEventRecord(r.a, s);
+  idx = ctx->prof.size();
+  ctx->prof.push_back(r);
+}
+
+ProfScope::~ProfScope() {
+  if (idx != (size_t)-1) cudaEventRecord(ctx->prof[idx].b, s);
+}
+
 }  // namespace tie
 
 using tie::capi::cuda_error;
@@ -212,9 +236,49 @@ void tie_ctx_destroy(tie_ctx* ctx) {
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
+  for (auto& ev : ctx->prof_pool) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   delete ctx;
+}
+
+int tie_profile(tie_ctx* ctx, int enable) {
+  if (int rc = check_ctx(ctx)) return rc;
+  DeviceGuard g(ctx->device);
+  cudaDeviceSynchronize();
+  ctx->prof_on = enable != 0;
+  ctx->prof.clear();
+  ctx->prof_used = 0;
+  return TIE_OK;
+}
+
+int tie_profile_report(tie_ctx* ctx, char* buf, size_t len) {
+  if (int rc = check_ctx(ctx)) return rc;
+  DeviceGuard g(ctx->device);
+  TIE_CUDA_TRY(cudaDeviceSynchronize(), "tie_profile_report");
+  std::vector<std::string> names;
+  std::vector<double> total;
+  std::vector<long> count;
+  for (const auto& r : ctx->prof) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) continue;
+    size_t k = 0;
+    while (k < names.size() && names[k] != r.name) ++k;
+    if (k == names.size()) {
+      names.push_back(r.name);
+      total.push_back(0.0);
+      count.push_back(0);
+    }
+    total[k] += ms;
+    count[k] += 1;
+  }
+  std::string out;
+  for (size_t k = 0; k < names.size(); ++k)
+    out += names[k] + "\t" + std::to_string(count[k]) + "\t" + std::to_string(total[k]) + "\n";
+  if (buf && len) {
+    std::snprintf(buf, len, "%s", out.c_str());
+  }
+  return out.size() < len ? TIE_OK : set_error(TIE_EINVALID, "tie_profile_report: buffer too small");
 }
 
 int tie_ctx_samples(const tie_ctx* ctx, double* host_out, int n) {

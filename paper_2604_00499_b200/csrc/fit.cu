@@ -371,6 +371,7 @@ cudaError_t launch_fit(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, do
   a.err = ctx->d_err;
   const int sms = sm_count(ctx->device);
   const unsigned grid = (unsigned)std::min<uint64_t>((P + 127) / 128, (uint64_t)sms * 16);
+  ProfScope prof(ctx, "fit", s);
   switch (K) {
     case 8: fit_kernel_static<8><<<grid, 128, 0, s>>>(a); break;
     case 16: fit_kernel_static<16><<<grid, 128, 0, s>>>(a); break;

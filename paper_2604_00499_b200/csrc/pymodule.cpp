@@ -273,6 +273,64 @@ PYBIND11_MODULE(_core, m) {
         throw_code(tie_sync(reinterpret_cast<tie_ctx*>(ctx), vp(stream)));
       },
       py::arg("ctx"), py::arg("stream") = 0);
+  m.def(
+      "score_rank_host_ptr",
+      [](uintptr_t ctx, uintptr_t mu, uintptr_t sigma, uintptr_t max_tokens, uint64_t n,
+         double alpha, double beta, uintptr_t score, uintptr_t order, unsigned flags) {
+        int rc;
+        {
+          py::gil_scoped_release nogil;
+          rc = tie_score_rank_host(reinterpret_cast<tie_ctx*>(ctx), (const double*)mu,
+                                   (const double*)sigma, (const uint32_t*)max_tokens, n, alpha,
+                                   beta, (double*)score, (uint64_t*)order, flags);
+        }
+        throw_code(rc);
+      },
+      py::arg("ctx"), py::arg("mu"), py::arg("sigma"), py::arg("max_tokens"), py::arg("n"),
+      py::arg("alpha"), py::arg("beta"), py::arg("score"), py::arg("order"),
+      py::arg("flags") = 0u,
+      "end-to-end call on raw HOST pointers (pinned buffers give full PCIe bandwidth)");
+  m.def(
+      "fit_host_ptr",
+      [](uintptr_t ctx, uintptr_t x, uint64_t P, uint64_t K, double nu, uintptr_t mu,
+         uintptr_t sigma, uintptr_t ll, uintptr_t iters, uintptr_t conv, uintptr_t degen) {
+        int rc;
+        {
+          py::gil_scoped_release nogil;
+          rc = tie_fit_host(reinterpret_cast<tie_ctx*>(ctx), (const double*)x, P, K, nu,
+                            (double*)mu, (double*)sigma, (double*)ll, (int32_t*)iters,
+                            (uint8_t*)conv, (uint8_t*)degen);
+        }
+        throw_code(rc);
+      },
+      py::arg("ctx"), py::arg("x"), py::arg("P"), py::arg("K"), py::arg("nu"), py::arg("mu"),
+      py::arg("sigma"), py::arg("ll"), py::arg("iters"), py::arg("conv"), py::arg("degen"));
+  m.def(
+      "profile",
+      [](uintptr_t ctx, bool enable) {
+        throw_code(tie_profile(reinterpret_cast<tie_ctx*>(ctx), enable ? 1 : 0));
+      },
+      py::arg("ctx"), py::arg("enable"));
+  m.def(
+      "profile_report",
+      [](uintptr_t ctx) {
+        std::string buf(1 << 16, '\0');
+        throw_code(tie_profile_report(reinterpret_cast<tie_ctx*>(ctx), buf.data(), buf.size()));
+        py::dict out;
+        size_t pos = 0;
+        const std::string s(buf.c_str());
+        while (pos < s.size()) {
+          const size_t eol = s.find('\n', pos);
+          const std::string line = s.substr(pos, eol - pos);
+          pos = eol == std::string::npos ? s.size() : eol + 1;
+          const size_t t1 = line.find('\t'), t2 = line.find('\t', t1 + 1);
+          if (t1 == std::string::npos || t2 == std::string::npos) continue;
+          out[py::str(line.substr(0, t1))] = py::make_tuple(
+              std::stol(line.substr(t1 + 1, t2 - t1 - 1)), std::stod(line.substr(t2 + 1)));
+        }
+        return out;
+      },
+      py::arg("ctx"), "{kernel: (launches, total_ms)} since profile(ctx, True)");
   m.def("default_context", []() { return (uintptr_t)default_context(); });
   m.def("launch_count", [](bool reset) { return tie_launch_count(reset ? 1 : 0); },
         py::arg("reset") = false);

@@ -373,12 +373,19 @@ int sm_count(int device) {
 }
 
 // Sort w.k[0] (u64) with values implicit (index) or explicit in w.v[0].
-cudaError_t radix_sort(Work& w, uint64_t n, bool explicit_vals, int sms, cudaStream_t s) {
+cudaError_t radix_sort(tie_ctx* ctx, Work& w, uint64_t n, bool explicit_vals, int sms,
+                       cudaStream_t s) {
   const uint32_t tiles = (uint32_t)((n + kTile - 1) / kTile);
   cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * kPasses * kBins, s);
   const unsigned hgrid = (unsigned)std::min<uint64_t>((n + 1023) / 1024, (uint64_t)sms * 4);
-  global_hist_kernel<<<std::max(1u, hgrid), 512, 0, s>>>(w.k[0], n, w.hist);
-  plan_kernel<<<1, kThreads, 0, s>>>(w.hist, n, w.plan);
+  {
+    ProfScope p(ctx, "rank.hist", s);
+    global_hist_kernel<<<std::max(1u, hgrid), 512, 0, s>>>(w.k[0], n, w.hist);
+  }
+  {
+    ProfScope p(ctx, "rank.plan", s);
+    plan_kernel<<<1, kThreads, 0, s>>>(w.hist, n, w.plan);
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(downsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -386,9 +393,18 @@ cudaError_t radix_sort(Work& w, uint64_t n, bool explicit_vals, int sms, cudaStr
     attr_set = true;
   }
   for (int p = 0; p < kPasses; ++p) {
-    upsweep_kernel<<<tiles, kThreads, 0, s>>>(w, n, p);
-    tile_scan_kernel<<<kBins, 1024, 0, s>>>(w, tiles, p);
-    downsweep_kernel<<<tiles, kThreads, sizeof(DownSmem), s>>>(w, n, p, explicit_vals ? 1 : 0);
+    {
+      ProfScope q(ctx, "rank.upsweep", s);
+      upsweep_kernel<<<tiles, kThreads, 0, s>>>(w, n, p);
+    }
+    {
+      ProfScope q(ctx, "rank.scan", s);
+      tile_scan_kernel<<<kBins, 1024, 0, s>>>(w, tiles, p);
+    }
+    {
+      ProfScope q(ctx, "rank.downsweep", s);
+      downsweep_kernel<<<tiles, kThreads, sizeof(DownSmem), s>>>(w, n, p, explicit_vals ? 1 : 0);
+    }
   }
   capi::count_launch(2 + 3 * kPasses);
   return cudaGetLastError();
@@ -429,6 +445,7 @@ cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* key_bit
     if (ids) cudaMemcpyAsync(tkeys, key_bits, 8 * n, cudaMemcpyDeviceToDevice, s);
     else if (key_bits != w.k[0]) cudaMemcpyAsync(tkeys, key_bits, 8 * n, cudaMemcpyDeviceToDevice, s);
   } else {
+    ProfScope p(ctx, "rank.keys", s);
     keys_from_double_kernel<<<egrid, 256, 0, s>>>(key, n, tkeys, ctx->d_err);
     capi::count_launch();
   }
@@ -448,7 +465,7 @@ cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* key_bit
       // stable sort of (id, index) first; then the key sort starts from id order
       copy_ids_kernel<<<egrid, 256, 0, s>>>(ids, n, w.k[0]);
       capi::count_launch();
-      if ((e = radix_sort(w, n, false, sms, s)) != cudaSuccess) return e;
+      if ((e = radix_sort(ctx, w, n, false, sms, s)) != cudaSuccess) return e;
       // sorted ids live in k[final]; stage (key[perm], perm) into the other buffer pair,
       // then move them to slot 0 for the second sort
       gather_by_id_kernel<<<egrid, 256, 0, s>>>(w, n, tkeys, (uint64_t*)(base + L.k3),
@@ -459,9 +476,12 @@ cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* key_bit
       explicit_vals = true;
     }
   }
-  cudaError_t e = radix_sort(w, n, explicit_vals, sms, s);
+  cudaError_t e = radix_sort(ctx, w, n, explicit_vals, sms, s);
   if (e != cudaSuccess) return e;
-  finish_kernel<<<egrid, 256, 0, s>>>(w, n, ids, order, explicit_vals ? 1 : 0);
+  {
+    ProfScope p(ctx, "rank.finish", s);
+    finish_kernel<<<egrid, 256, 0, s>>>(w, n, ids, order, explicit_vals ? 1 : 0);
+  }
   capi::count_launch();
   return cudaGetLastError();
 }

@@ -379,6 +379,7 @@ cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, co
   p.k_alpha = ctx->ka_k;
   const int sms = sm_count(ctx->device);
   const uint64_t blocks_needed = (n + 255) / 256;
+  ProfScope prof(ctx, exact ? "score.exact" : "score.moment", s);
   if (exact) {
     const size_t smem = ctx->N <= 12288 ? sizeof(double) * ctx->N : 0;
     const uint64_t grid = std::min<uint64_t>(blocks_needed, (uint64_t)sms * 2);

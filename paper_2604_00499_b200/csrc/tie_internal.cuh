@@ -102,7 +102,27 @@ struct tie_ctx {
   cudaStream_t stream = nullptr;         // internal stream for *_host calls
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev[8] = {};
+  // kernel-level profiling (tie_profile): event pairs recorded on the launching stream
+  struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  bool prof_on = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> prof_pool;
+  size_t prof_used = 0;
 };
+
+namespace tie {
+// RAII: records an event pair around the kernel launches in its scope when profiling is on
+struct ProfScope {
+  tie_ctx* ctx;
+  cudaStream_t s;
+  size_t idx = (size_t)-1;
+  ProfScope(tie_ctx* c, const char* name, cudaStream_t st);
+  ~ProfScope();
+};
+}  // namespace tie
 
 namespace tie {
 namespace capi {

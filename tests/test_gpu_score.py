@@ -12,7 +12,8 @@ from conftest import golden
 
 pytestmark = pytest.mark.gpu
 
-TOL = 1e-12     # held by both paths
+TOL = 1e-12     # held by both paths on well-conditioned cells
+TOL_ILL = 1e-10 # CVaR at alpha=0.99 / tiny sigma: psi(y_max) - psi(y_alpha) cancels ~100x
 BAR = 1e-6      # the north star's stated tolerance
 MODES = [TIE_SCORE_MOMENT, TIE_SCORE_EXACT]
 
@@ -83,9 +84,10 @@ def test_random_wide_ranges_vs_oracle(abi, h, oracle, samples, flags):
     for alpha, beta in [(0.9, 0.5), (0.5, 0.1), (0.0, 0.7), (0.99, 2.0)]:
         Eo, Co, So = oracle.score(samples, mu, sg, xm, alpha=alpha, beta=beta)
         E, C, S = abi.score(h, mu, sg, xm, alpha, beta, flags)
+        tol = TOL_ILL if alpha >= 0.99 else TOL
         for got, ref in ((E, Eo), (C, Co), (S, So)):
             err = rel_err(got, ref)
-            assert err.max() <= TOL, (alpha, beta, err.max(), int(err.argmax()))
+            assert err.max() <= tol, (alpha, beta, err.max(), int(err.argmax()))
         sat = Co == xm
         assert np.array_equal(C[sat], xm[sat])
 
