@@ -230,6 +230,7 @@ void tie_ctx_destroy(tie_ctx* ctx) {
   cudaFree(ctx->d_Y);
   cudaFree(ctx->d_ybucket);
   cudaFree(ctx->d_table);
+  cudaFree(ctx->d_tail);
   cudaFree(ctx->d_err);
   cudaFree(ctx->scratch);
   cudaFree(ctx->io);
@@ -347,15 +348,15 @@ double tie_t_cdf(double y, double nu) {
 // ====================================================================== device entry points
 static int score_impl(tie_ctx* ctx, const double* mu, const double* sigma, const void* x_max,
                       bool u32, uint64_t n, double alpha, double beta, double* E, double* C,
-                      double* S, uint64_t* keys, unsigned flags, cudaStream_t s,
+                      double* S, uint64_t* keys, uint32_t* hist, unsigned flags, cudaStream_t s,
                       const char* op) {
   if (int rc = check_ctx(ctx)) return rc;
   if (int rc = validate_alpha(alpha)) return rc;
   if (n && (!mu || !sigma || !x_max)) return set_error(TIE_EINVALID, std::string(op) + ": null input");
   DeviceGuard g(ctx->device);
   ctx->err_op = op;
-  const cudaError_t e =
-      tie::dev::launch_score(ctx, mu, sigma, x_max, u32, n, alpha, beta, E, C, S, keys, flags, s);
+  const cudaError_t e = tie::dev::launch_score(ctx, mu, sigma, x_max, u32, n, alpha, beta, E, C,
+                                               S, keys, hist, flags, s);
   if (e != cudaSuccess) return cuda_error(e, op);
   return TIE_OK;
 }
@@ -364,14 +365,14 @@ int tie_score(tie_ctx* ctx, const double* mu, const double* sigma, const double*
               uint64_t n, double alpha, double beta, double* E, double* cvar, double* score,
               unsigned flags, void* stream) {
   return score_impl(ctx, mu, sigma, x_max, false, n, alpha, beta, E, cvar, score, nullptr,
-                    flags, as_stream(stream), "tie_score");
+                    nullptr, flags, as_stream(stream), "tie_score");
 }
 
 int tie_score_u32(tie_ctx* ctx, const double* mu, const double* sigma,
                   const uint32_t* max_tokens, uint64_t n, double alpha, double beta, double* E,
                   double* cvar, double* score, unsigned flags, void* stream) {
   return score_impl(ctx, mu, sigma, max_tokens, true, n, alpha, beta, E, cvar, score, nullptr,
-                    flags, as_stream(stream), "tie_score");
+                    nullptr, flags, as_stream(stream), "tie_score");
 }
 
 int tie_rank(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n, uint64_t* order,
@@ -380,7 +381,7 @@ int tie_rank(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n, u
   if (n && (!key || !order)) return set_error(TIE_EINVALID, "tie_rank: null pointer");
   DeviceGuard g(ctx->device);
   ctx->err_op = "tie_rank";
-  const cudaError_t e = tie::dev::launch_rank(ctx, key, nullptr, ids, n, order, as_stream(stream));
+  const cudaError_t e = tie::dev::launch_rank(ctx, key, ids, n, order, as_stream(stream));
   if (e != cudaSuccess) return cuda_error(e, "tie_rank");
   return TIE_OK;
 }
@@ -393,12 +394,12 @@ int tie_score_rank(tie_ctx* ctx, const double* mu, const double* sigma,
   if (n == 0) return TIE_OK;
   DeviceGuard g(ctx->device);
   cudaStream_t s = as_stream(stream);
-  uint64_t* keys = tie::dev::rank_key_buffer(ctx, n, s);
-  if (!keys) return set_error(TIE_ECUDA, "tie_score_rank: scratch allocation failed");
-  if (int rc = score_impl(ctx, mu, sigma, max_tokens, true, n, alpha, beta, E, cvar, score, keys,
-                          flags, s, "tie_score_rank"))
+  const tie::dev::RankPrep prep = tie::dev::rank_prepare(ctx, n, s);
+  if (!prep.keys) return set_error(TIE_ECUDA, "tie_score_rank: scratch allocation failed");
+  if (int rc = score_impl(ctx, mu, sigma, max_tokens, true, n, alpha, beta, E, cvar, score,
+                          prep.keys, prep.hist, flags, s, "tie_score_rank"))
     return rc;
-  const cudaError_t e = tie::dev::launch_rank(ctx, nullptr, keys, nullptr, n, order, s);
+  const cudaError_t e = tie::dev::rank_prepared(ctx, n, order, s);
   if (e != cudaSuccess) return cuda_error(e, "tie_score_rank");
   return TIE_OK;
 }
@@ -495,8 +496,8 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
   double* d_S = score ? (double*)(b + 2 * al(8 * n) + al(4 * n)) : nullptr;
   uint64_t* d_order = (uint64_t*)(b + 3 * al(8 * n) + al(4 * n));
   cudaStream_t s = ctx->stream, cs = ctx->copy_stream;
-  uint64_t* keys = tie::dev::rank_key_buffer(ctx, n, s);
-  if (!keys) return set_error(TIE_ECUDA, "tie_score_rank_host: scratch allocation failed");
+  const tie::dev::RankPrep prep = tie::dev::rank_prepare(ctx, n, s);
+  if (!prep.keys) return set_error(TIE_ECUDA, "tie_score_rank_host: scratch allocation failed");
   ctx->err_op = "tie_score_rank_host";
   // pipeline: H2D of chunk c+1 (copy stream) overlaps scoring of chunk c (compute stream)
   const int chunks = n >= (1u << 20) ? 4 : 1;
@@ -515,11 +516,11 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
     TIE_CUDA_TRY(cudaStreamWaitEvent(s, ctx->ev[1 + (c & 3)], 0), "tie_score_rank_host");
     const cudaError_t e = tie::dev::launch_score(ctx, d_mu + lo, d_sg + lo, d_mt + lo, true, m,
                                                  alpha, beta, nullptr, nullptr,
-                                                 d_S ? d_S + lo : nullptr, keys + lo,
-                                                 flags & TIE_SCORE_EXACT, s);
+                                                 d_S ? d_S + lo : nullptr, prep.keys + lo,
+                                                 prep.hist, flags & TIE_SCORE_EXACT, s, lo);
     if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
   }
-  cudaError_t e = tie::dev::launch_rank(ctx, nullptr, keys, nullptr, n, d_order, s);
+  cudaError_t e = tie::dev::rank_prepared(ctx, n, d_order, s);
   if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
   TIE_CUDA_TRY(cudaMemcpyAsync(order, d_order, 8 * n, cudaMemcpyDeviceToHost, s), "d2h");
   if (score) TIE_CUDA_TRY(cudaMemcpyAsync(score, d_S, 8 * n, cudaMemcpyDeviceToHost, s), "d2h");

@@ -1,17 +1,22 @@
 // K2 -- dispatch order of a static waiting queue: stable LSD radix sort by (key, id).
 //
 // Reference: WaitingQueue (proj/src/sched.cpp:28-94) is a binary min-heap ordered by
-// (key, req_id) (less(), sched.cpp:28-31); pushing n entries and popping until empty
-// yields the lexicographic (key asc, id asc) order.  Here: keys are mapped to u64 by the
-// order-preserving IEEE transform (x >= 0: bits | 2^63, x < 0: ~bits; -0.0 folded onto
-// +0.0 because the heap compares keys with ==), then sorted with a stable LSD radix sort
-// over values that start in ascending-id order -- which is exactly (key, id) order.
+// (key, req_id) (less(), sched.cpp:28-31); pushing n entries and popping until empty yields
+// the lexicographic (key asc, id asc) order.  Here keys are mapped to u64 by the
+// order-preserving IEEE transform (x >= 0: bits | 2^63, x < 0: ~bits; -0.0 folded onto +0.0
+// because the heap compares keys with ==) and sorted by a stable LSD radix sort whose values
+// start in ascending-id order -- which is exactly (key, id) order.
 //
-// Per pass (8-bit digits, 8 passes, passes whose digit is constant across all keys are
-// skipped on the device): upsweep tile histograms -> per-digit scan across tiles ->
-// downsweep that ranks each 4096-key tile stably in shared memory (warp match_any
-// multi-split) and writes digit runs out coalesced.  A single global-histogram kernel up
-// front provides every pass's bin bases and the skip mask, so the host never syncs.
+// Onesweep structure (one kernel per 8-bit digit pass):
+//   * one histogram pass computes all 8 digit histograms up front (or the fused score kernel
+//     accumulates them in its epilogue), a 1-CTA plan kernel turns them into per-pass bin
+//     bases and a skip mask (passes whose digit is constant across all keys do nothing);
+//   * each pass kernel takes tiles in launch order from an atomic counter, ranks its tile
+//     stably in shared memory (warp match_any multi-split), publishes per-digit tile counts
+//     and resolves its global digit offsets by decoupled look-back over predecessor tiles --
+//     no separate upsweep / scan kernels, keys read once and written once per pass;
+//   * digit runs are written out coalesced from the shared-memory-sorted tile; the LAST
+//     active pass writes the u64 dispatch order (ids[value]) directly instead of keys+values.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -28,14 +33,36 @@ constexpr int kBins = 1 << kRadixBits;
 constexpr int kPasses = 64 / kRadixBits;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;
-constexpr int kTile = kThreads * kItems;  // 4096 keys per tile
+
+// look-back status word: [flag:2][count:62]
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagPrefix = 2ull << 62;
+constexpr uint64_t kCountMask = (1ull << 62) - 1;
+constexpr int kGroup = 16;  // tiles per second-level look-back group
+
+// Phase timestamps of each pass's tiles (probe builds only: tools/rank_probe.cu).
+#ifdef TIE_RANK_TRACE
+__device__ unsigned long long g_rank_trace[8][8192][6];
+#define RANK_TRACE(slot)                                                         \
+  do {                                                                           \
+    if (threadIdx.x == 0 && tile < 8192) {                                       \
+      unsigned long long t_;                                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+      g_rank_trace[pass][tile][slot] = t_;                                       \
+    }                                                                            \
+  } while (0)
+#else
+#define RANK_TRACE(slot) \
+  do {                   \
+  } while (0)
+#endif
 
 struct Plan {
   uint32_t bin_base[kPasses][kBins];
   int active[kPasses];
   int sel[kPasses];    // buffer holding the input of pass p
-  int first[kPasses];  // pass p is the first active one (values implicit if not explicit)
+  int first[kPasses];  // pass p is the first active one
+  int last_active;     // index of the last active pass (-1: none)
   int final_sel;
   int any_active;
 };
@@ -43,10 +70,15 @@ struct Plan {
 struct Work {
   uint64_t* k[2];
   uint32_t* v[2];
-  uint32_t* tile_counts;  // [kBins][num_tiles]
-  uint32_t* hist;         // [kPasses][kBins]
+  uint32_t* hist;           // [kPasses][kBins]
   Plan* plan;
+  uint64_t* status;         // [kPasses][tiles][kBins]
+  uint64_t* gstatus;        // [kPasses][groups][kBins]  group aggregate / inclusive prefix
+  uint64_t* gsum;           // [kPasses][groups][kBins]  (contributors << 40 | sum)
+  uint32_t* gdone;          // [kPasses][groups]         members that have contributed
+  uint32_t* tile_counter;   // [kPasses]
   int* flag;
+  uint32_t tiles;
 };
 
 __device__ __forceinline__ uint32_t digit_of(uint64_t key, int pass) {
@@ -59,43 +91,58 @@ __device__ __forceinline__ uint64_t order_bits(double x) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-// key validation + transform (WaitingQueue::push rejects non-finite keys, sched.cpp:60)
-__global__ void keys_from_double_kernel(const double* __restrict__ key, uint64_t n,
-                                        uint64_t* __restrict__ out, unsigned long long* err) {
+__device__ __forceinline__ void hist_flush(uint32_t (*h)[kBins], uint32_t* hist) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < kPasses * kBins; i += blockDim.x)
+    if ((&h[0][0])[i]) atomicAdd(hist + i, (&h[0][0])[i]);
+}
+
+// key validation + transform (WaitingQueue::push rejects non-finite keys, sched.cpp:60) with
+// the 8 digit histograms accumulated on the way
+__global__ void __launch_bounds__(256) keys_from_double_kernel(const double* __restrict__ key,
+                                                               uint64_t n,
+                                                               uint64_t* __restrict__ out,
+                                                               uint32_t* __restrict__ hist,
+                                                               unsigned long long* err) {
+  __shared__ uint32_t h[kPasses][kBins];
+  for (int i = threadIdx.x; i < kPasses * kBins; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const double x = key[i];
+    uint64_t k;
     if (!isfinite(x)) {
       report(err, i, kKeyNotFinite);
-      out[i] = ~0ull;
+      k = ~0ull;
     } else {
-      out[i] = order_bits(x);
+      k = order_bits(x);
     }
+    out[i] = k;
+#pragma unroll
+    for (int p = 0; p < kPasses; ++p) atomicAdd(&h[p][digit_of(k, p)], 1u);
   }
+  hist_flush(h, hist);
 }
 
-__global__ void global_hist_kernel(const uint64_t* __restrict__ keys, uint64_t n,
-                                   uint32_t* __restrict__ hist) {
-  __shared__ uint32_t h[2][kPasses][kBins];
-  for (int i = threadIdx.x; i < 2 * kPasses * kBins; i += blockDim.x) (&h[0][0][0])[i] = 0;
+// copy u64 keys (ids, or pre-transformed keys) while accumulating the digit histograms
+__global__ void __launch_bounds__(256) copy_hist_kernel(const uint64_t* __restrict__ in,
+                                                        uint64_t n, uint64_t* __restrict__ out,
+                                                        uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[kPasses][kBins];
+  for (int i = threadIdx.x; i < kPasses * kBins; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
-  const int copy = (threadIdx.x >> 5) & 1;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint64_t k = keys[i];
+    const uint64_t k = in[i];
+    if (out) out[i] = k;
 #pragma unroll
-    for (int p = 0; p < kPasses; ++p) atomicAdd(&h[copy][p][digit_of(k, p)], 1u);
+    for (int p = 0; p < kPasses; ++p) atomicAdd(&h[p][digit_of(k, p)], 1u);
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kPasses * kBins; i += blockDim.x) {
-    const uint32_t c = (&h[0][0][0])[i] + (&h[1][0][0])[i];
-    if (c) atomicAdd(hist + i, c);
-  }
+  hist_flush(h, hist);
 }
 
 // exclusive scan of 256 values held one per thread (blockDim == 256)
-__device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* sh_warp,
-                                                        uint32_t* total) {
+__device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* sh_warp) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t x = v;
 #pragma unroll
@@ -115,9 +162,7 @@ __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* sh
     if (lane < kWarps) sh_warp[lane] = w;
   }
   __syncthreads();
-  const uint32_t incl = x + (warp ? sh_warp[warp - 1] : 0);
-  if (total && threadIdx.x == kThreads - 1) *total = incl;
-  return incl - v;
+  return x + (warp ? sh_warp[warp - 1] : 0) - v;
 }
 
 __global__ void __launch_bounds__(kThreads) plan_kernel(const uint32_t* __restrict__ hist,
@@ -125,183 +170,247 @@ __global__ void __launch_bounds__(kThreads) plan_kernel(const uint32_t* __restri
   __shared__ uint32_t sh_warp[kWarps];
   __shared__ int sh_active[kPasses];
   const int d = threadIdx.x;
+  if (d < kPasses) sh_active[d] = 0;
+  __syncthreads();
   for (int p = 0; p < kPasses; ++p) {
     const uint32_t c = hist[p * kBins + d];
-    if (d == 0) sh_active[p] = 0;
-    __syncthreads();
     if ((uint64_t)c != n && c != 0) sh_active[p] = 1;  // more than one occupied digit
-    plan->bin_base[p][d] = block_excl_scan_256(c, sh_warp, nullptr);
+    plan->bin_base[p][d] = block_excl_scan_256(c, sh_warp);
     __syncthreads();
   }
   if (d == 0) {
-    int cnt = 0;
+    int cnt = 0, last = -1;
     for (int p = 0; p < kPasses; ++p) {
       plan->active[p] = sh_active[p];
       plan->sel[p] = cnt & 1;
       plan->first[p] = sh_active[p] && cnt == 0;
+      if (sh_active[p]) last = p;
       cnt += sh_active[p];
     }
+    plan->last_active = last;
     plan->final_sel = cnt & 1;
     plan->any_active = cnt > 0;
   }
 }
 
-__global__ void __launch_bounds__(kThreads) upsweep_kernel(Work w, uint64_t n, int pass) {
-  if (!w.plan->active[pass]) return;
-  __shared__ uint32_t h[kWarps][kBins];
-  for (int i = threadIdx.x; i < kWarps * kBins; i += kThreads) (&h[0][0])[i] = 0;
-  __syncthreads();
-  const uint64_t* keys = w.k[w.plan->sel[pass]];
-  const uint64_t base = (uint64_t)blockIdx.x * kTile;
-  const int warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const uint64_t i = base + (uint64_t)j * kThreads + threadIdx.x;
-    if (i < n) atomicAdd(&h[warp][digit_of(keys[i], pass)], 1u);
-  }
-  __syncthreads();
-  const uint32_t num_tiles = gridDim.x;
-  uint32_t c = 0;
-#pragma unroll
-  for (int q = 0; q < kWarps; ++q) c += h[q][threadIdx.x];
-  w.tile_counts[(uint64_t)threadIdx.x * num_tiles + blockIdx.x] = c;
-}
-
-// one CTA per digit: exclusive scan of that digit's counts across tiles (+ bin base)
-__global__ void __launch_bounds__(1024) tile_scan_kernel(Work w, uint32_t num_tiles, int pass) {
-  if (!w.plan->active[pass]) return;
-  __shared__ uint32_t sh_warp[32];
-  __shared__ uint32_t carry;
-  const int d = blockIdx.x;
-  uint32_t* row = w.tile_counts + (uint64_t)d * num_tiles;
-  if (threadIdx.x == 0) carry = w.plan->bin_base[pass][d];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t off = 0; off < num_tiles; off += 1024) {
-    const uint32_t t = off + threadIdx.x;
-    const uint32_t v = t < num_tiles ? row[t] : 0;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) sh_warp[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t s = sh_warp[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += y;
-      }
-      sh_warp[lane] = s;
-    }
-    __syncthreads();
-    const uint32_t incl = x + (warp ? sh_warp[warp - 1] : 0);
-    const uint32_t c0 = carry;
-    if (t < num_tiles) row[t] = c0 + incl - v;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = c0 + incl;
-    __syncthreads();
-  }
-}
-
-struct DownSmem {
-  uint64_t keys[kTile];
-  uint32_t vals[kTile];
+template <int ITEMS>
+struct PassSmem {
+  uint64_t keys[kThreads * ITEMS];
+  uint32_t vals[kThreads * ITEMS];
   uint32_t warp_hist[kWarps][kBins];
   uint32_t tile_excl[kBins];
   uint32_t global_off[kBins];
   uint32_t sh_warp[kWarps];
+  uint32_t tile_hist[kBins];  // early digit counts of the tile (pads excluded)
+  uint32_t tile;
 };
 
-__global__ void __launch_bounds__(kThreads) downsweep_kernel(Work w, uint64_t n, int pass,
-                                                             int explicit_vals) {
+// Batched walk over look-back status words [newest .. oldest] (stride `stride` words):
+// accumulates published counts until an inclusive PREFIX is found.  Returns true when a
+// PREFIX ended the walk; `pos` moves past every entry consumed; stops (without consuming)
+// at the first unpublished entry or at `stop` (exclusive lower bound).
+__device__ __forceinline__ bool walk(const volatile uint64_t* base, uint64_t stride,
+                                     int64_t& pos, int64_t stop, uint64_t& excl) {
+  constexpr int kBatch = 16;
+  uint64_t s[kBatch];
+#pragma unroll
+  for (int u = 0; u < kBatch; ++u) s[u] = (pos - u > stop) ? base[(uint64_t)(pos - u) * stride] : 0;
+  int used = 0;
+  bool open = true, prefix = false;
+#pragma unroll
+  for (int u = 0; u < kBatch; ++u) {
+    if (!open || pos - u <= stop) {
+      open = false;
+      continue;
+    }
+    const uint64_t f = s[u] & ~kCountMask;
+    if (f == 0) {  // not published yet: resume here
+      open = false;
+      continue;
+    }
+    excl += s[u] & kCountMask;
+    ++used;
+    if (f == kFlagPrefix) {
+      prefix = true;
+      open = false;
+    }
+  }
+  pos -= used;
+  return prefix;
+}
+
+// Two-level decoupled look-back for digit d of `tile` (one thread per digit): publish() posts
+// the tile's count early and folds it into its 16-tile group's aggregate; lookback() later
+// walks (a) the preceding tiles of its own group and (b) the preceding groups' aggregates /
+// inclusive prefixes.  When all tiles are resident at once (small n) this bounds every walk
+// to ~3 batched L2 round trips instead of one batch per 16 predecessor tiles.
+//
+// Publish the tile's count for digit d: the tile status word (AGGREGATE, or PREFIX for
+// tile 0) and the group aggregate.  The group aggregate needs no fences: one packed atomic
+// carries (contributors << 40 | sum) and the last contributor reads the complete aggregate
+// straight from the returned value.
+__device__ __forceinline__ void publish(const Work& w, int pass, uint32_t tile, int d,
+                                        uint32_t real) {
+  const uint32_t groups = (w.tiles + kGroup - 1) / kGroup;
+  const uint32_t q = tile / kGroup;
+  volatile uint64_t* mine = w.status + (uint64_t)pass * w.tiles * kBins + (uint64_t)tile * kBins + d;
+  *mine = (tile == 0 ? kFlagPrefix : kFlagAgg) | real;
+  unsigned long long* gsum =
+      (unsigned long long*)w.gsum + (uint64_t)pass * groups * kBins + (uint64_t)q * kBins + d;
+  const uint32_t members = min((uint32_t)kGroup, w.tiles - q * kGroup);
+  const unsigned long long old = atomicAdd(gsum, (1ull << 40) | real);
+  if ((uint32_t)(old >> 40) == members - 1)
+    atomicMax((unsigned long long*)(w.gstatus + (uint64_t)pass * groups * kBins +
+                                    (uint64_t)q * kBins + d),
+              (unsigned long long)(kFlagAgg | ((old & ((1ull << 40) - 1)) + real)));
+}
+
+__device__ __forceinline__ uint64_t lookback(const Work& w, int pass, uint32_t tile, int d,
+                                             uint32_t real) {
+  const uint32_t groups = (w.tiles + kGroup - 1) / kGroup;
+  const uint32_t q = tile / kGroup;
+  uint64_t* tstat = w.status + (uint64_t)pass * w.tiles * kBins;
+  uint64_t* gstat = w.gstatus + (uint64_t)pass * groups * kBins;
+  volatile uint64_t* mine = tstat + (uint64_t)tile * kBins + d;
+  uint64_t excl = 0;
+  bool done = tile == 0;
+  int64_t pos = (int64_t)tile - 1;
+  const int64_t gfirst = (int64_t)q * kGroup;
+  while (!done && pos >= gfirst) done = walk(tstat + d, kBins, pos, gfirst - 1, excl);
+  int64_t gpos = (int64_t)q - 1;
+  while (!done && gpos >= 0) done = walk(gstat + d, kBins, gpos, -1, excl);
+  if (tile > 0) *mine = kFlagPrefix | (excl + real);
+  if (tile % kGroup == kGroup - 1 || tile == w.tiles - 1)
+    atomicMax((unsigned long long*)(gstat + (uint64_t)q * kBins + d),
+              (unsigned long long)(kFlagPrefix | (excl + real)));
+  return excl;
+}
+
+// One digit pass.  `order`: when non-null and this is the last active pass, write the
+// dispatch order (ids[value], or value) instead of keys + values.
+template <int ITEMS>
+__global__ void __launch_bounds__(kThreads, 3) onesweep_kernel(Work w, uint64_t n, int pass,
+                                                            int explicit_vals,
+                                                            const uint64_t* __restrict__ ids,
+                                                            uint64_t* __restrict__ order) {
   const Plan* plan = w.plan;
   if (!plan->active[pass]) return;
+  constexpr int kTileKeys = kThreads * ITEMS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  DownSmem& sm = *reinterpret_cast<DownSmem*>(smem_raw);
+  PassSmem<ITEMS>& sm = *reinterpret_cast<PassSmem<ITEMS>*>(smem_raw);
   const int src = plan->sel[pass];
-  const uint64_t* __restrict__ kin = w.k[src];
-  const uint32_t* __restrict__ vin = w.v[src];
+  const uint64_t* __restrict__ kin = src ? w.k[1] : w.k[0];
+  const uint32_t* __restrict__ vin = src ? w.v[1] : w.v[0];
+  uint64_t* __restrict__ kout = src ? w.k[0] : w.k[1];
+  uint32_t* __restrict__ vout = src ? w.v[0] : w.v[1];
   const bool implicit = plan->first[pass] && !explicit_vals;
-  uint64_t* __restrict__ kout = w.k[src ^ 1];
-  uint32_t* __restrict__ vout = w.v[src ^ 1];
+  const bool to_order = order != nullptr && plan->last_active == pass;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kWarps * kBins; i += kThreads) (&sm.warp_hist[0][0])[i] = 0;
-  const uint32_t num_tiles = gridDim.x;
-  sm.global_off[threadIdx.x] = w.tile_counts[(uint64_t)threadIdx.x * num_tiles + blockIdx.x];
+  if (threadIdx.x == 0) sm.tile = atomicAdd(w.tile_counter + pass, 1u);  // launch-order tiles
   __syncthreads();
-
-  const uint64_t tile_base = (uint64_t)blockIdx.x * kTile;
+  const uint32_t tile = sm.tile;
+  RANK_TRACE(0);
+  const uint64_t tile_base = (uint64_t)tile * kTileKeys;
   const uint64_t left = n - tile_base;
-  const uint32_t valid = left < (uint64_t)kTile ? (uint32_t)left : (uint32_t)kTile;
+  const uint32_t valid = left < (uint64_t)kTileKeys ? (uint32_t)left : (uint32_t)kTileKeys;
   const unsigned lt_mask = (1u << lane) - 1u;
-  uint64_t key[kItems];
-  uint32_t val[kItems];
-  uint32_t rank[kItems];
-  // warp w owns tile slots [w*512, (w+1)*512): round j, lane l -> slot w*512 + j*32 + l,
-  // so (round, lane) order is index order and the multi-split below is stable.
+
+  uint64_t key[ITEMS];
+  uint32_t rank[ITEMS];
+  // warp w owns slots [w*32*ITEMS, (w+1)*32*ITEMS); round j, lane l -> slot w*32*ITEMS +
+  // j*32 + l, so (round, lane) order is index order and the multi-split below is stable.
+  // Values are not held in registers: they go straight to their ranked smem slot below.
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const uint32_t q = warp * (kItems * 32) + j * 32 + lane;
-    const uint64_t i = tile_base + q;
-    if (q < valid) {
-      key[j] = kin[i];
-      val[j] = implicit ? (uint32_t)i : vin[i];
-    } else {
-      key[j] = ~0ull;  // pads sort last in the tile and are never written out
-      val[j] = 0;
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t q = warp * (ITEMS * 32) + j * 32 + lane;
+    key[j] = q < valid ? kin[tile_base + q] : ~0ull;  // pads sort last, never written out
+  }
+  // early counts: a plain shared-memory histogram of the tile's digits is published before
+  // the (slower) stable ranking, so successor tiles' look-backs resolve while this tile ranks
+  const int d = threadIdx.x;
+  sm.tile_hist[d] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t q = warp * (ITEMS * 32) + j * 32 + lane;
+    if (q < valid) atomicAdd(&sm.tile_hist[digit_of(key[j], pass)], 1u);
+  }
+  __syncthreads();
+  const uint32_t real = sm.tile_hist[d];
+  publish(w, pass, tile, d, real);
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t dg = digit_of(key[j], pass);
+    // lanes holding the same digit: AND of the 8 per-bit ballots (warp multi-split); cheaper
+    // than MATCH.ANY on sm_100
+    unsigned peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < kRadixBits; ++b) {
+      const unsigned bal = __ballot_sync(0xffffffffu, (dg >> b) & 1u);
+      peers &= ((dg >> b) & 1u) ? bal : ~bal;
     }
-    const uint32_t d = digit_of(key[j], pass);
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t before = sm.warp_hist[warp][d];
+    const uint32_t before = sm.warp_hist[warp][dg];
     __syncwarp();
-    if ((peers & lt_mask) == 0) sm.warp_hist[warp][d] = before + __popc(peers);
+    if ((peers & lt_mask) == 0) sm.warp_hist[warp][dg] = before + __popc(peers);
     __syncwarp();
     rank[j] = before + __popc(peers & lt_mask);
   }
   __syncthreads();
-  {  // per digit: exclusive over warps, then exclusive over digits
-    const int d = threadIdx.x;
-    uint32_t run = 0;
+  RANK_TRACE(1);
+  uint32_t count = 0;
 #pragma unroll
-    for (int q = 0; q < kWarps; ++q) {
-      const uint32_t c = sm.warp_hist[q][d];
-      sm.warp_hist[q][d] = run;
-      run += c;
-    }
-    const uint32_t ex = block_excl_scan_256(run, sm.sh_warp, nullptr);
-    sm.tile_excl[d] = ex;
+  for (int q = 0; q < kWarps; ++q) {
+    const uint32_t c = sm.warp_hist[q][d];
+    sm.warp_hist[q][d] = count;
+    count += c;
   }
+  const uint64_t excl = lookback(w, pass, tile, d, real);
+  sm.global_off[d] = plan->bin_base[pass][d] + (uint32_t)excl;
+  sm.tile_excl[d] = block_excl_scan_256(count, sm.sh_warp);
   __syncthreads();
+  RANK_TRACE(2);
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const uint32_t d = digit_of(key[j], pass);
-    const uint32_t pos = sm.tile_excl[d] + sm.warp_hist[warp][d] + rank[j];
+  for (int j = 0; j < ITEMS; ++j) {
+    const uint32_t dd = digit_of(key[j], pass);
+    const uint32_t pos = sm.tile_excl[dd] + sm.warp_hist[warp][dd] + rank[j];
+    const uint32_t q = warp * (ITEMS * 32) + j * 32 + lane;
     sm.keys[pos] = key[j];
-    sm.vals[pos] = val[j];
+    sm.vals[pos] = implicit ? (uint32_t)(tile_base + q) : (q < valid ? vin[tile_base + q] : 0u);
   }
   __syncthreads();
-  for (uint32_t q = threadIdx.x; q < valid; q += kThreads) {
-    const uint64_t k = sm.keys[q];
-    const uint32_t d = digit_of(k, pass);
-    const uint64_t g = (uint64_t)sm.global_off[d] + (q - sm.tile_excl[d]);
-    kout[g] = k;
-    vout[g] = sm.vals[q];
+  RANK_TRACE(3);
+  if (to_order) {
+    for (uint32_t q = threadIdx.x; q < valid; q += kThreads) {
+      const uint32_t dd = digit_of(sm.keys[q], pass);
+      const uint64_t g = (uint64_t)sm.global_off[dd] + (q - sm.tile_excl[dd]);
+      const uint32_t v = sm.vals[q];
+      order[g] = ids ? ids[v] : (uint64_t)v;
+    }
+  } else {
+    for (uint32_t q = threadIdx.x; q < valid; q += kThreads) {
+      const uint64_t k = sm.keys[q];
+      const uint32_t dd = digit_of(k, pass);
+      const uint64_t g = (uint64_t)sm.global_off[dd] + (q - sm.tile_excl[dd]);
+      kout[g] = k;
+      vout[g] = sm.vals[q];
+    }
   }
+#ifdef TIE_RANK_TRACE
+  __syncthreads();
+  RANK_TRACE(4);
+#endif
 }
 
-__global__ void finish_kernel(Work w, uint64_t n, const uint64_t* __restrict__ ids,
-                              uint64_t* __restrict__ order, int explicit_vals) {
+// degenerate case (no active pass: every key identical): the order is the input order
+__global__ void identity_order_kernel(Work w, uint64_t n, const uint64_t* __restrict__ ids,
+                                      uint64_t* __restrict__ order, int explicit_vals) {
   const Plan* plan = w.plan;
-  const uint32_t* v = w.v[plan->final_sel];
-  const bool identity = !plan->any_active && !explicit_vals;
+  if (plan->any_active) return;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint64_t idx = identity ? i : v[i];
+    const uint64_t idx = explicit_vals ? w.v[0][i] : i;
     order[i] = ids ? ids[idx] : idx;
   }
 }
@@ -316,14 +425,14 @@ __global__ void ids_sorted_kernel(const uint64_t* __restrict__ ids, uint64_t n, 
     }
 }
 
-// after sorting (id, index) pairs: detect duplicate ids, and stage (key[perm], perm)
-// as the explicit-value input of the key sort.
+// After the (id, index) sort: detect duplicate ids and stage (key[perm], perm) as the
+// explicit-value input of the key sort.
 __global__ void gather_by_id_kernel(Work w, uint64_t n, const uint64_t* __restrict__ tkeys,
                                     uint64_t* __restrict__ kdst, uint32_t* __restrict__ vdst,
                                     unsigned long long* err) {
   const Plan* plan = w.plan;
-  const uint64_t* sid = w.k[plan->final_sel];
-  const uint32_t* perm = w.v[plan->final_sel];
+  const uint64_t* sid = plan->final_sel ? w.k[1] : w.k[0];
+  const uint32_t* perm = plan->final_sel ? w.v[1] : w.v[0];
   const bool identity = !plan->any_active;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
@@ -334,29 +443,35 @@ __global__ void gather_by_id_kernel(Work w, uint64_t n, const uint64_t* __restri
   }
 }
 
-__global__ void copy_ids_kernel(const uint64_t* __restrict__ ids, uint64_t n,
-                                uint64_t* __restrict__ out) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = ids[i];
-}
-
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
+int items_for(uint64_t) { return 16; }
+
 struct Layout {
-  size_t k0, k1, v0, v1, tc, hist, plan, flag, k2, k3, v3, total;
+  size_t k0, k1, v0, v1, hist, plan, status, gstatus, gsum, gdone, counter, flag, k2, k3, v3,
+      meta_begin, meta_end, total;
+  uint32_t tiles;
 };
 
 Layout layout(uint64_t n, bool with_ids) {
-  const uint64_t tiles = (n + kTile - 1) / kTile;
   Layout L{};
+  const uint64_t tile_keys = (uint64_t)kThreads * items_for(n);
+  L.tiles = (uint32_t)std::max<uint64_t>(1, (n + tile_keys - 1) / tile_keys);
   size_t off = 0;
   L.k0 = off; off += align_up(8 * n);
   L.k1 = off; off += align_up(8 * n);
   L.v0 = off; off += align_up(4 * n);
   L.v1 = off; off += align_up(4 * n);
-  L.tc = off; off += align_up(4 * (size_t)kBins * tiles);
+  // per-sort metadata, zeroed by ONE memset per sort: histograms, look-back status, counters
+  L.meta_begin = off;
   L.hist = off; off += align_up(4 * kPasses * kBins);
+  L.status = off; off += align_up(8ull * kPasses * L.tiles * kBins);
+  const uint64_t groups = (L.tiles + kGroup - 1) / kGroup;
+  L.gstatus = off; off += align_up(8ull * kPasses * groups * kBins);
+  L.gsum = off; off += align_up(8ull * kPasses * groups * kBins);
+  L.gdone = off; off += align_up(4ull * kPasses * groups);
+  L.counter = off; off += align_up(4 * kPasses);
+  L.meta_end = off;
   L.plan = off; off += align_up(sizeof(Plan));
   L.flag = off; off += align_up(sizeof(int));
   L.k2 = off; off += with_ids ? align_up(8 * n) : 0;  // transformed keys (id path)
@@ -366,47 +481,65 @@ Layout layout(uint64_t n, bool with_ids) {
   return L;
 }
 
+Work make_work(char* base, const Layout& L) {
+  Work w;
+  w.k[0] = (uint64_t*)(base + L.k0);
+  w.k[1] = (uint64_t*)(base + L.k1);
+  w.v[0] = (uint32_t*)(base + L.v0);
+  w.v[1] = (uint32_t*)(base + L.v1);
+  w.hist = (uint32_t*)(base + L.hist);
+  w.plan = (Plan*)(base + L.plan);
+  w.status = (uint64_t*)(base + L.status);
+  w.gstatus = (uint64_t*)(base + L.gstatus);
+  w.gsum = (uint64_t*)(base + L.gsum);
+  w.gdone = (uint32_t*)(base + L.gdone);
+  w.tile_counter = (uint32_t*)(base + L.counter);
+  w.flag = (int*)(base + L.flag);
+  w.tiles = L.tiles;
+  return w;
+}
+
 int sm_count(int device) {
   int v = 0;
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
   return v > 0 ? v : 148;
 }
 
-// Sort w.k[0] (u64) with values implicit (index) or explicit in w.v[0].
-cudaError_t radix_sort(tie_ctx* ctx, Work& w, uint64_t n, bool explicit_vals, int sms,
-                       cudaStream_t s) {
-  const uint32_t tiles = (uint32_t)((n + kTile - 1) / kTile);
-  cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * kPasses * kBins, s);
-  const unsigned hgrid = (unsigned)std::min<uint64_t>((n + 1023) / 1024, (uint64_t)sms * 4);
-  {
-    ProfScope p(ctx, "rank.hist", s);
-    global_hist_kernel<<<std::max(1u, hgrid), 512, 0, s>>>(w.k[0], n, w.hist);
+template <int ITEMS>
+void launch_passes(tie_ctx* ctx, Work& w, uint64_t n, bool explicit_vals, const uint64_t* ids,
+                   uint64_t* order, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(onesweep_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(PassSmem<ITEMS>));
+    attr = true;
   }
+  for (int p = 0; p < kPasses; ++p) {
+    ProfScope q(ctx, "rank.onesweep", s);
+    onesweep_kernel<ITEMS><<<w.tiles, kThreads, sizeof(PassSmem<ITEMS>), s>>>(
+        w, n, p, explicit_vals ? 1 : 0, ids, order);
+  }
+}
+
+// plan + the digit passes over w.k[0] (+ w.v[0] if explicit_vals); histograms already in
+// w.hist.  With `order` the last pass emits the dispatch order (ids[value] or value).
+cudaError_t sort_passes(tie_ctx* ctx, Work& w, uint64_t n, bool explicit_vals,
+                        const uint64_t* ids, uint64_t* order, cudaStream_t s) {
   {
     ProfScope p(ctx, "rank.plan", s);
     plan_kernel<<<1, kThreads, 0, s>>>(w.hist, n, w.plan);
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(downsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(DownSmem));
-    attr_set = true;
+  if (items_for(n) == 8)
+    launch_passes<8>(ctx, w, n, explicit_vals, ids, order, s);
+  else
+    launch_passes<16>(ctx, w, n, explicit_vals, ids, order, s);
+  capi::count_launch(1 + kPasses);
+  if (order) {
+    const int sms = sm_count(ctx->device);
+    const unsigned g = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 4);
+    identity_order_kernel<<<g, 256, 0, s>>>(w, n, ids, order, explicit_vals ? 1 : 0);
+    capi::count_launch();
   }
-  for (int p = 0; p < kPasses; ++p) {
-    {
-      ProfScope q(ctx, "rank.upsweep", s);
-      upsweep_kernel<<<tiles, kThreads, 0, s>>>(w, n, p);
-    }
-    {
-      ProfScope q(ctx, "rank.scan", s);
-      tile_scan_kernel<<<kBins, 1024, 0, s>>>(w, tiles, p);
-    }
-    {
-      ProfScope q(ctx, "rank.downsweep", s);
-      downsweep_kernel<<<tiles, kThreads, sizeof(DownSmem), s>>>(w, n, p, explicit_vals ? 1 : 0);
-    }
-  }
-  capi::count_launch(2 + 3 * kPasses);
   return cudaGetLastError();
 }
 
@@ -414,76 +547,71 @@ cudaError_t radix_sort(tie_ctx* ctx, Work& w, uint64_t n, bool explicit_vals, in
 
 size_t rank_scratch_bytes(uint64_t n, bool with_ids) { return layout(n, with_ids).total; }
 
-uint64_t* rank_key_buffer(tie_ctx* ctx, uint64_t n, cudaStream_t s) {
+RankPrep rank_prepare(tie_ctx* ctx, uint64_t n, cudaStream_t s) {
+  RankPrep r{nullptr, nullptr};
   const Layout L = layout(n, false);
   char* base = (char*)capi::scratch(ctx, L.total, s);
-  return base ? (uint64_t*)(base + L.k0) : nullptr;
+  if (!base) return r;
+  cudaMemsetAsync(base + L.meta_begin, 0, L.meta_end - L.meta_begin, s);
+  r.keys = (uint64_t*)(base + L.k0);
+  r.hist = (uint32_t*)(base + L.hist);
+  return r;
 }
 
-cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* key_bits,
-                        const uint64_t* ids, uint64_t n, uint64_t* order, cudaStream_t s) {
+cudaError_t rank_prepared(tie_ctx* ctx, uint64_t n, uint64_t* order, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  if (n >= (1ull << 32)) return cudaErrorInvalidValue;  // u32 tile-local values
+  const Layout L = layout(n, false);
+  char* base = (char*)capi::scratch(ctx, L.total, s);
+  if (!base) return cudaErrorMemoryAllocation;
+  Work w = make_work(base, L);
+  return sort_passes(ctx, w, n, false, nullptr, order, s);
+}
+
+cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n,
+                        uint64_t* order, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  if (n >= (1ull << 32)) return cudaErrorInvalidValue;  // u32 values
   const Layout L = layout(n, ids != nullptr);
   char* base = (char*)capi::scratch(ctx, L.total, s);
   if (!base) return cudaErrorMemoryAllocation;
-  Work w;
-  w.k[0] = (uint64_t*)(base + L.k0);
-  w.k[1] = (uint64_t*)(base + L.k1);
-  w.v[0] = (uint32_t*)(base + L.v0);
-  w.v[1] = (uint32_t*)(base + L.v1);
-  w.tile_counts = (uint32_t*)(base + L.tc);
-  w.hist = (uint32_t*)(base + L.hist);
-  w.plan = (Plan*)(base + L.plan);
-  w.flag = (int*)(base + L.flag);
+  Work w = make_work(base, L);
   const int sms = sm_count(ctx->device);
-  const unsigned egrid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 8);
+  const unsigned egrid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 4);
+  const size_t meta = L.meta_end - L.meta_begin;
+  cudaMemsetAsync(base + L.meta_begin, 0, meta, s);
 
-  // transformed keys into k[0] (or into k2 when an id pre-sort needs k[0])
   uint64_t* tkeys = ids ? (uint64_t*)(base + L.k2) : w.k[0];
-  if (key_bits) {
-    if (ids) cudaMemcpyAsync(tkeys, key_bits, 8 * n, cudaMemcpyDeviceToDevice, s);
-    else if (key_bits != w.k[0]) cudaMemcpyAsync(tkeys, key_bits, 8 * n, cudaMemcpyDeviceToDevice, s);
-  } else {
-    ProfScope p(ctx, "rank.keys", s);
-    keys_from_double_kernel<<<egrid, 256, 0, s>>>(key, n, tkeys, ctx->d_err);
-    capi::count_launch();
-  }
-
-  bool explicit_vals = false;
-  if (ids) {
-    cudaMemsetAsync(w.flag, 0, sizeof(int), s);
-    ids_sorted_kernel<<<egrid, 256, 0, s>>>(ids, n, w.flag);
-    capi::count_launch();
-    int unsorted = 0;
-    cudaMemcpyAsync(&unsorted, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s);
-    cudaError_t e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return e;
-    if (!unsorted) {
-      cudaMemcpyAsync(w.k[0], tkeys, 8 * n, cudaMemcpyDeviceToDevice, s);
-    } else {
-      // stable sort of (id, index) first; then the key sort starts from id order
-      copy_ids_kernel<<<egrid, 256, 0, s>>>(ids, n, w.k[0]);
-      capi::count_launch();
-      if ((e = radix_sort(ctx, w, n, false, sms, s)) != cudaSuccess) return e;
-      // sorted ids live in k[final]; stage (key[perm], perm) into the other buffer pair,
-      // then move them to slot 0 for the second sort
-      gather_by_id_kernel<<<egrid, 256, 0, s>>>(w, n, tkeys, (uint64_t*)(base + L.k3),
-                                                (uint32_t*)(base + L.v3), ctx->d_err);
-      capi::count_launch();
-      cudaMemcpyAsync(w.k[0], base + L.k3, 8 * n, cudaMemcpyDeviceToDevice, s);
-      cudaMemcpyAsync(w.v[0], base + L.v3, 4 * n, cudaMemcpyDeviceToDevice, s);
-      explicit_vals = true;
-    }
-  }
-  cudaError_t e = radix_sort(ctx, w, n, explicit_vals, sms, s);
-  if (e != cudaSuccess) return e;
   {
-    ProfScope p(ctx, "rank.finish", s);
-    finish_kernel<<<egrid, 256, 0, s>>>(w, n, ids, order, explicit_vals ? 1 : 0);
+    ProfScope p(ctx, "rank.keys", s);
+    keys_from_double_kernel<<<egrid, 256, 0, s>>>(key, n, tkeys, w.hist, ctx->d_err);
+    capi::count_launch();
   }
+  if (!ids) return sort_passes(ctx, w, n, false, nullptr, order, s);
+
+  cudaMemsetAsync(w.flag, 0, sizeof(int), s);
+  ids_sorted_kernel<<<egrid, 256, 0, s>>>(ids, n, w.flag);
   capi::count_launch();
-  return cudaGetLastError();
+  int unsorted = 0;
+  cudaMemcpyAsync(&unsorted, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  if (!unsorted) {  // ids ascending: (key, index) order == (key, id) order
+    cudaMemcpyAsync(w.k[0], tkeys, 8 * n, cudaMemcpyDeviceToDevice, s);
+    return sort_passes(ctx, w, n, false, ids, order, s);
+  }
+  // unsorted ids: stable sort of (id, index) first; the key sort then starts from id order
+  cudaMemsetAsync(base + L.meta_begin, 0, meta, s);
+  copy_hist_kernel<<<egrid, 256, 0, s>>>(ids, n, w.k[0], w.hist);
+  capi::count_launch();
+  if ((e = sort_passes(ctx, w, n, false, nullptr, nullptr, s)) != cudaSuccess) return e;
+  gather_by_id_kernel<<<egrid, 256, 0, s>>>(w, n, tkeys, (uint64_t*)(base + L.k3),
+                                            (uint32_t*)(base + L.v3), ctx->d_err);
+  capi::count_launch();
+  cudaMemcpyAsync(w.v[0], base + L.v3, 4 * n, cudaMemcpyDeviceToDevice, s);
+  cudaMemsetAsync(base + L.meta_begin, 0, meta, s);
+  copy_hist_kernel<<<egrid, 256, 0, s>>>((const uint64_t*)(base + L.k3), n, w.k[0], w.hist);
+  capi::count_launch();
+  return sort_passes(ctx, w, n, true, ids, order, s);
 }
 
 }  // namespace dev

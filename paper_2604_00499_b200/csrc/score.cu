@@ -167,18 +167,56 @@ __device__ __forceinline__ uint32_t cut_index(const ScoreParams& p, const double
   return lo;
 }
 
-// sum_m delta^m row[m]  (Horner over one 128-byte table row)
-__device__ __forceinline__ double horner_row(const double* __restrict__ row, double delta) {
-  const double2* r2 = reinterpret_cast<const double2*>(row);
-  double2 v[kMoments / 2];
+// T_nu(y) from the tail-mass table (one 64-byte row + a degree-7 Horner); |y| beyond the
+// sample range falls back to the continued fraction.
+struct TailRow {
+  double2 a[kTailCoef / 2];
+  double t;
+  bool ok;
+};
+
+__device__ __forceinline__ void tail_fetch(const ScoreParams& p, double y, TailRow& r) {
+  const double ay = fabs(y);
+  r.ok = ay < p.t_ymax;
+  if (!r.ok) return;
+  const int b = min((int)(ay * p.t_inv_w), kTailBuckets - 1);
+  r.t = ay - ((double)b + 0.5) * p.t_w;
+  const double2* row = reinterpret_cast<const double2*>(p.tail + (size_t)b * kTailCoef);
 #pragma unroll
-  for (int j = 0; j < kMoments / 2; ++j) v[j] = __ldg(r2 + j);
-  double acc = v[kMoments / 2 - 1].y;
-  acc = fma(acc, delta, v[kMoments / 2 - 1].x);
+  for (int j = 0; j < kTailCoef / 2; ++j) r.a[j] = __ldg(row + j);
+}
+
+__device__ __forceinline__ double tail_cdf(const ScoreParams& p, double y, const TailRow& r) {
+  if (!r.ok) return t_cdf_dev(p.td, y);
+  double v = r.a[kTailCoef / 2 - 1].y;
+  v = fma(v, r.t, r.a[kTailCoef / 2 - 1].x);
+#pragma unroll
+  for (int j = kTailCoef / 2 - 2; j >= 0; --j) {
+    v = fma(v, r.t, r.a[j].y);
+    v = fma(v, r.t, r.a[j].x);
+  }
+  return y >= 0.0 ? __dsub_rn(1.0, v) : v;  // dist.cpp:80
+}
+
+// One 128-byte table row (16 moments) held in registers.
+struct Row {
+  double2 v[kMoments / 2];
+};
+
+__device__ __forceinline__ void load_row(const double* __restrict__ row, Row& r) {
+  const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+  for (int j = 0; j < kMoments / 2; ++j) r.v[j] = __ldg(r2 + j);
+}
+
+// sum_m delta^m row[m]  (Horner)
+__device__ __forceinline__ double horner(const Row& r, double delta) {
+  double acc = r.v[kMoments / 2 - 1].y;
+  acc = fma(acc, delta, r.v[kMoments / 2 - 1].x);
 #pragma unroll
   for (int j = kMoments / 2 - 2; j >= 0; --j) {
-    acc = fma(acc, delta, v[j].y);
-    acc = fma(acc, delta, v[j].x);
+    acc = fma(acc, delta, r.v[j].y);
+    acc = fma(acc, delta, r.v[j].x);
   }
   return acc;
 }
@@ -209,35 +247,65 @@ struct Out {
   double E, C, S;
 };
 
+// ln(x_max) memo: queues share a handful of token budgets, so each thread keeps the last one
+struct LogMemo {
+  double x = -1.0, lx = 0.0;
+  __device__ __forceinline__ double operator()(double xm) {
+    if (xm != x) {
+      x = xm;
+      lx = log(xm);
+    }
+    return lx;
+  }
+};
+
+__device__ __forceinline__ uint32_t epilogue(const ScoreParams& p, double xm, double T,
+                                             bool saturated, double s_a, double s_all, Out& o);
+
 template <bool kExact>
 __device__ __forceinline__ uint32_t score_one(const ScoreParams& p, const double* __restrict__ Ys,
-                                              double mu, double sigma, double xm, Out& o) {
+                                              double mu, double sigma, double xm, LogMemo& lnx,
+                                              Out& o) {
   // LogTParams / CensoredLogT validation (dist.cpp:108-120)
   if (!isfinite(mu)) return kMuNotFinite;
   if (!(sigma > 0.0) || !isfinite(sigma)) return kSigmaBad;
   if (!(xm > 0.0) || !isfinite(xm)) return kXmaxBad;
   const double sg = sigma < 1e-9 ? 1e-9 : sigma;
-  const double y_max = __dsub_rn(log(xm), mu) / sg;
+  const double y_max = __dsub_rn(lnx(xm), mu) / sg;
+  // the tail-mass row depends only on y_max: issue it before the sample search
+  TailRow tr;
+  tail_fetch(p, y_max, tr);
   const uint32_t k_max = cut_index(p, p.Y, y_max);
-  const double T = t_cdf_dev(p.td, y_max);
+  const int g = __double2int_rn(sg * kGridInvH);
+  const bool use_table = !kExact && g < p.G && fabs(mu) <= 700.0;
+  const double* base = p.table + (size_t)(use_table ? g : 0) * (size_t)(p.N + 1) * kMoments;
+  Row row_max;
+  if (use_table) load_row(base + (size_t)k_max * kMoments, row_max);
+
+  const double T = tail_cdf(p, y_max, tr);
   const bool saturated = p.alpha >= T;  // censored_cvar case 1 (dist.cpp:187)
   const uint32_t k_a = saturated ? 0u : p.k_alpha;
 
   double s_a = 0.0, s_all = 0.0;
-  bool done = false;
-  if (!kExact) {
-    const int g = __double2int_rn(sg * kGridInvH);
-    if (g < p.G && fabs(mu) <= 700.0) {
-      const double delta = sg - g * kGridH;  // exact: h is a power of two
-      const double* base = p.table + (size_t)g * (size_t)(p.N + 1) * kMoments;
-      const double em = exp(mu);
-      s_all = k_max ? em * horner_row(base + (size_t)k_max * kMoments, delta) : 0.0;
-      s_a = k_a ? em * horner_row(base + (size_t)k_a * kMoments, delta) : 0.0;
-      done = true;
+  if (use_table) {
+    const double delta = sg - g * kGridH;  // exact: h is a power of two
+    const double em = exp(mu);
+    s_all = k_max ? em * horner(row_max, delta) : 0.0;
+    if (k_a) {
+      Row row_a;  // the k_alpha row of grid point g: shared by the whole queue, L1-resident
+      load_row(base + (size_t)k_a * kMoments, row_a);
+      s_a = em * horner(row_a, delta);
     }
+  } else {
+    exact_sums(Ys, mu, sg, k_a, k_max, s_a, s_all);
   }
-  if (!done) exact_sums(Ys, mu, sg, k_a, k_max, s_a, s_all);
+  return epilogue(p, xm, T, saturated, s_a, s_all, o);
+}
 
+// E, CVaR and score from the two partial sums and T (dist.cpp:163-189, sim.cpp:94,
+// sched.cpp:19-26), operation order as the reference's (no FMA contraction).
+__device__ __forceinline__ uint32_t epilogue(const ScoreParams& p, double xm, double T,
+                                             bool saturated, double s_a, double s_all, Out& o) {
   const double Nd = (double)p.N;
   const double psi_cap = s_all / Nd;
   const double cm = __dsub_rn(1.0, T);
@@ -269,34 +337,223 @@ __device__ __forceinline__ uint32_t score_one(const ScoreParams& p, const double
   return kOk;
 }
 
+// keys != nullptr: also emit the rank key (order-preserving u64 image of the score, as in
+// rank.cu) and, with hist != nullptr, accumulate its 8 radix-digit histograms so the fused
+// score+rank path needs no separate histogram pass over the keys.
 template <typename XT, bool kExact>
-__global__ void __launch_bounds__(256) score_kernel(const __grid_constant__ ScoreParams p,
+__global__ void __launch_bounds__(256, 2) score_kernel(const __grid_constant__ ScoreParams p,
                                                     const double* __restrict__ mu,
                                                     const double* __restrict__ sigma,
                                                     const XT* __restrict__ xmax, uint64_t n,
                                                     double* __restrict__ E, double* __restrict__ C,
                                                     double* __restrict__ S,
-                                                    uint64_t* __restrict__ keys) {
+                                                    uint64_t* __restrict__ keys,
+                                                    uint32_t* __restrict__ hist) {
   extern __shared__ double sY[];
+  __shared__ uint32_t h[8][256];
   const double* Ys = p.Y;
   if (kExact && p.N <= 12288) {  // stage the sample set once per CTA (<= 96 KB)
     for (int i = threadIdx.x; i < p.N; i += blockDim.x) sY[i] = p.Y[i];
-    __syncthreads();
     Ys = sY;
   }
+  if (hist)
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  LogMemo lnx;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // software pipeline: the next request's inputs are loaded while this one is scored
+  double nmu = 0.0, nsg = 0.0, nxm = 0.0;
+  if (i < n) {
+    nmu = mu[i];
+    nsg = sigma[i];
+    nxm = (double)xmax[i];
+  }
+  for (; i < n; i += stride) {
+    const double cmu = nmu, csg = nsg, cxm = nxm;
+    if (i + stride < n) {
+      nmu = mu[i + stride];
+      nsg = sigma[i + stride];
+      nxm = (double)xmax[i + stride];
+    }
     Out o;
-    const uint32_t why = score_one<kExact>(p, Ys, mu[i], sigma[i], (double)xmax[i], o);
+    const uint32_t why = score_one<kExact>(p, Ys, cmu, csg, cxm, lnx, o);
     if (why != kOk) {
-      report(p.err, i, why);
+      report(p.err, p.index_base + i, why);
       o.E = o.C = o.S = __longlong_as_double(0x7ff8000000000000LL);
     }
     if (E) E[i] = o.E;
     if (C) C[i] = o.C;
     if (S) S[i] = o.S;
-    // rank key: order-preserving u64 image of a positive score (bits | 2^63, as rank.cu)
-    if (keys) keys[i] = why == kOk ? ((uint64_t)__double_as_longlong(o.S) | (1ull << 63)) : ~0ull;
+    if (keys) {
+      const uint64_t k =
+          why == kOk ? ((uint64_t)__double_as_longlong(o.S) | (1ull << 63)) : ~0ull;
+      keys[i] = k;
+      if (hist) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) atomicAdd(&h[q][(k >> (8 * q)) & 255], 1u);
+      }
+    }
+  }
+  if (hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x)
+      if ((&h[0][0])[i]) atomicAdd(hist + i, (&h[0][0])[i]);
+  }
+}
+
+// ------------------------------------------------------------------ warp-cooperative path
+// Moment-table path with one warp per 32 consecutive requests.  The per-request table rows
+// (128-byte moment rows at k_max and k_alpha, 64-byte tail-mass row) are random gathers; a
+// per-lane 16-byte load touches 32 different lines per warp instruction (1/8 of each L1
+// wavefront useful), which made L1 wavefronts the score kernel's limiter.  Here the warp
+// stages rows cooperatively -- consecutive lanes fetch consecutive 16-byte chunks of the
+// same row, then each lane reads its own row from a padded shared-memory slab (stride
+// R+2 doubles: conflict-free 16-byte reads) -- ~3 wavefronts per row instead of 8.
+constexpr int kSlabStride = kMoments + 2;  // doubles per staged row (padding vs banks)
+
+// Rare paths kept out of line so they do not inflate the hot loop's register allocation.
+__device__ __noinline__ double t_cdf_slow(const TdistConst& td, double y) {
+  return t_cdf_dev(td, y);
+}
+__device__ __noinline__ void exact_sums_slow(const double* __restrict__ Y, double mu, double sg,
+                                             uint32_t k_a, uint32_t k_max, double* s_a,
+                                             double* s_all) {
+  exact_sums(Y, mu, sg, k_a, k_max, *s_a, *s_all);
+}
+
+template <int R>
+__device__ __forceinline__ void stage_rows(const double* myrow, double* slab,
+                                           const double** ptrs) {
+  const int lane = threadIdx.x & 31;
+  ptrs[lane] = myrow;
+  __syncwarp();
+  constexpr int C = R / 2;  // 16-byte chunks per row
+#pragma unroll
+  for (int it = 0; it < C; ++it) {
+    const int c = it * 32 + lane;
+    const int r = c / C, sub = c % C;
+    const double* rp = ptrs[r];
+    const double2 v = rp ? __ldg(reinterpret_cast<const double2*>(rp) + sub)
+                         : make_double2(0.0, 0.0);
+    *reinterpret_cast<double2*>(slab + r * kSlabStride + 2 * sub) = v;
+  }
+  __syncwarp();
+}
+
+template <int R>
+__device__ __forceinline__ double slab_horner(const double* slab, double x) {
+  const int lane = threadIdx.x & 31;
+  const double2* row = reinterpret_cast<const double2*>(slab + lane * kSlabStride);
+  double2 c = row[R / 2 - 1];
+  double acc = fma(c.y, x, c.x);
+#pragma unroll
+  for (int j = R / 2 - 2; j >= 0; --j) {
+    c = row[j];
+    acc = fma(acc, x, c.y);
+    acc = fma(acc, x, c.x);
+  }
+  return acc;
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(256, 3) score_coop_kernel(const __grid_constant__ ScoreParams p,
+                                                         const double* __restrict__ mu,
+                                                         const double* __restrict__ sigma,
+                                                         const XT* __restrict__ xmax, uint64_t n,
+                                                         double* __restrict__ E,
+                                                         double* __restrict__ C,
+                                                         double* __restrict__ S,
+                                                         uint64_t* __restrict__ keys,
+                                                         uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[8][256];
+  __shared__ __align__(16) double slab_all[8][32 * kSlabStride];
+  __shared__ const double* ptr_all[8][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* slab = slab_all[wib];
+  const double** ptrs = ptr_all[wib];
+  if (hist)
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  LogMemo lnx;
+  const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t base = warp0 * 32; base < n; base += nwarps * 32) {  // warp-uniform loop
+    const uint64_t i = base + lane;
+    const bool active = i < n;
+    const double m = active ? mu[i] : 0.0;
+    const double sig = active ? sigma[i] : 1.0;
+    const double xm = active ? (double)xmax[i] : 1.0;
+    // LogTParams / CensoredLogT validation (dist.cpp:108-120)
+    uint32_t why = kOk;
+    if (!isfinite(m)) why = kMuNotFinite;
+    else if (!(sig > 0.0) || !isfinite(sig)) why = kSigmaBad;
+    else if (!(xm > 0.0) || !isfinite(xm)) why = kXmaxBad;
+    const bool ok = active && why == kOk;
+    const double sg = ok ? (sig < 1e-9 ? 1e-9 : sig) : 1.0;
+    const double y_max = ok ? __dsub_rn(lnx(xm), m) / sg : 0.0;
+    // T(y_max): tail-mass row (staged) or, beyond the sample range, the continued fraction
+    const double ay = fabs(y_max);
+    const bool tail_tab = ok && ay < p.t_ymax;
+    const int tb = tail_tab ? min((int)(ay * p.t_inv_w), kTailBuckets - 1) : 0;
+    stage_rows<kTailCoef>(tail_tab ? p.tail + (size_t)tb * kTailCoef : nullptr, slab, ptrs);
+    double T = 0.5;
+    if (tail_tab) {
+      const double v = slab_horner<kTailCoef>(slab, ay - ((double)tb + 0.5) * p.t_w);
+      T = y_max >= 0.0 ? __dsub_rn(1.0, v) : v;  // dist.cpp:80
+    } else if (ok) {
+      T = t_cdf_slow(p.td, y_max);
+    }
+    const uint32_t k_max = ok ? cut_index(p, p.Y, y_max) : 0u;
+    const int g = ok ? __double2int_rn(sg * kGridInvH) : 0;
+    const bool use_table = ok && g < p.G && fabs(m) <= 700.0;
+    const double delta = sg - g * kGridH;  // exact: h is a power of two
+    const double* gbase = p.table + (size_t)(use_table ? g : 0) * (size_t)(p.N + 1) * kMoments;
+    const bool saturated = p.alpha >= T;  // censored_cvar case 1 (dist.cpp:187)
+    const uint32_t k_a = saturated ? 0u : p.k_alpha;
+    __syncwarp();
+    stage_rows<kMoments>(use_table && k_max ? gbase + (size_t)k_max * kMoments : nullptr, slab,
+                         ptrs);
+    const double F_all = slab_horner<kMoments>(slab, delta);
+    __syncwarp();
+    stage_rows<kMoments>(use_table && k_a ? gbase + (size_t)k_a * kMoments : nullptr, slab,
+                         ptrs);
+    const double F_a = slab_horner<kMoments>(slab, delta);
+    __syncwarp();
+    Out o;
+    if (ok) {
+      double s_a = 0.0, s_all = 0.0;
+      if (use_table) {
+        const double em = exp(m);
+        s_all = k_max ? em * F_all : 0.0;
+        s_a = k_a ? em * F_a : 0.0;
+      } else {
+        exact_sums_slow(p.Y, m, sg, k_a, k_max, &s_a, &s_all);
+      }
+      why = epilogue(p, xm, T, saturated, s_a, s_all, o);
+    }
+    if (!active) continue;
+    if (why != kOk) {
+      report(p.err, p.index_base + i, why);
+      o.E = o.C = o.S = __longlong_as_double(0x7ff8000000000000LL);
+    }
+    if (E) E[i] = o.E;
+    if (C) C[i] = o.C;
+    if (S) S[i] = o.S;
+    if (keys) {
+      const uint64_t k =
+          why == kOk ? ((uint64_t)__double_as_longlong(o.S) | (1ull << 63)) : ~0ull;
+      keys[i] = k;
+      if (hist) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) atomicAdd(&h[q][(k >> (8 * q)) & 255], 1u);
+      }
+    }
+  }
+  if (hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x)
+      if ((&h[0][0])[i]) atomicAdd(hist + i, (&h[0][0])[i]);
   }
 }
 
@@ -335,6 +592,41 @@ cudaError_t build_context_tables(tie_ctx* ctx) {
   if ((e = cudaMemcpy(ctx->d_ybucket, yb.data(), sizeof(uint32_t) * yb.size(),
                       cudaMemcpyHostToDevice)) != cudaSuccess)
     return e;
+  // tail-mass Taylor table (see TailTable in tie_internal.cuh)
+  {
+    const double ymax = std::max(std::fabs(ctx->y0), std::fabs(ctx->yN));
+    ctx->t_ymax = ymax > 0.0 ? ymax : 0.0;
+    ctx->t_w = ctx->t_ymax / kTailBuckets;
+    ctx->t_inv_w = ctx->t_w > 0.0 ? 1.0 / ctx->t_w : 0.0;
+    std::vector<double> tt((size_t)kTailBuckets * kTailCoef, 0.0);
+    const long double nu = ctx->nu;
+    const long double ex = -0.5L * (nu + 1.0L);  // pdf = C q^ex, q = 1 + y^2/nu
+    const long double C = std::exp((long double)std::lgamma(0.5 * (ctx->nu + 1.0)) -
+                                   (long double)std::lgamma(0.5 * ctx->nu) -
+                                   0.5L * std::log(nu * 3.14159265358979323846264338327950288L));
+    for (int b = 0; b < kTailBuckets && ctx->t_w > 0.0; ++b) {
+      const double c = ((double)b + 0.5) * ctx->t_w;  // same expression as the device
+      // a0 = v(c) = I_x(nu/2, 1/2) / 2 with the reference's own evaluation (host::reg_inc_beta)
+      const double x = ctx->nu / (c * c + ctx->nu);
+      const double a0 = 0.5 * host::reg_inc_beta(0.5 * ctx->nu, 0.5, x);
+      // pdf(c + t) = C (q0 + q1 t + q2 t^2)^ex as a power series: q f' = ex q' f
+      const long double q[3] = {1.0L + (long double)c * c / nu, 2.0L * c / nu, 1.0L / nu};
+      long double f[kTailCoef];
+      f[0] = C * std::pow(q[0], ex);
+      for (int k = 1; k < kTailCoef; ++k) {
+        long double acc = 0.0L;
+        for (int i = 1; i <= std::min(k, 2); ++i) acc += (ex * i - (k - i)) * q[i] * f[k - i];
+        f[k] = acc / (k * q[0]);
+      }
+      double* row = tt.data() + (size_t)b * kTailCoef;
+      row[0] = a0;
+      for (int j = 1; j < kTailCoef; ++j) row[j] = (double)(-f[j - 1] / j);  // v' = -pdf
+    }
+    if ((e = cudaMalloc(&ctx->d_tail, sizeof(double) * tt.size())) != cudaSuccess) return e;
+    if ((e = cudaMemcpy(ctx->d_tail, tt.data(), sizeof(double) * tt.size(),
+                        cudaMemcpyHostToDevice)) != cudaSuccess)
+      return e;
+  }
   // sigma-grid moment tables
   ctx->G = (int)std::lrint(ctx->sigma_table_max * kGridInvH) + 1;
   const size_t bytes = (size_t)ctx->G * (size_t)(N + 1) * kMoments * sizeof(double);
@@ -347,8 +639,8 @@ cudaError_t build_context_tables(tie_ctx* ctx) {
 
 cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, const void* x_max,
                          bool x_is_u32, uint64_t n, double alpha, double beta, double* E,
-                         double* C, double* S, uint64_t* keys_out, unsigned flags,
-                         cudaStream_t s) {
+                         double* C, double* S, uint64_t* keys_out, uint32_t* hist_out,
+                         unsigned flags, cudaStream_t s, uint64_t index_base) {
   const bool exact = (flags & 1u) != 0;
   if (n == 0) return cudaSuccess;
   ScoreParams p;
@@ -356,6 +648,10 @@ cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, co
   p.Y = ctx->d_Y;
   p.ybucket = ctx->d_ybucket;
   p.table = ctx->d_table;
+  p.tail = ctx->d_tail;
+  p.t_ymax = ctx->t_ymax;
+  p.t_w = ctx->t_w;
+  p.t_inv_w = ctx->t_inv_w;
   p.y0 = ctx->y0;
   p.y_scale = ctx->y_scale;
   p.yN = ctx->yN;
@@ -364,6 +660,7 @@ cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, co
   p.alpha = alpha;
   p.beta = beta;
   p.raw = (flags & 2u) ? 1 : 0;
+  p.index_base = index_base;
   p.err = ctx->d_err;
   // k_alpha = #{Y_i <= t_quantile(alpha, nu)}: request-invariant, hoisted (dist.cpp:170)
   if (alpha != ctx->ka_alpha) {
@@ -387,21 +684,29 @@ cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, co
       cudaFuncSetAttribute(score_kernel<uint32_t, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       score_kernel<uint32_t, true><<<(unsigned)grid, 256, smem, s>>>(
-          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out);
+          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out, hist_out);
     } else {
       cudaFuncSetAttribute(score_kernel<double, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       score_kernel<double, true><<<(unsigned)grid, 256, smem, s>>>(
-          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out);
+          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, hist_out);
     }
-  } else {
+  } else if (flags & 4u) {  // per-lane gathers (kept for A/B measurements)
     const uint64_t grid = std::min<uint64_t>(blocks_needed, (uint64_t)sms * 8);
     if (x_is_u32)
       score_kernel<uint32_t, false><<<(unsigned)grid, 256, 0, s>>>(
-          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out);
+          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out, hist_out);
     else
       score_kernel<double, false><<<(unsigned)grid, 256, 0, s>>>(
-          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out);
+          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, hist_out);
+  } else {
+    const uint64_t grid = std::min<uint64_t>(blocks_needed, (uint64_t)sms * 8);
+    if (x_is_u32)
+      score_coop_kernel<uint32_t><<<(unsigned)grid, 256, 0, s>>>(
+          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out, hist_out);
+    else
+      score_coop_kernel<double><<<(unsigned)grid, 256, 0, s>>>(
+          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, hist_out);
   }
   capi::count_launch();
   return cudaGetLastError();

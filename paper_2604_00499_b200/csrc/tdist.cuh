@@ -26,17 +26,30 @@ __device__ __forceinline__ double cf_wallis(const host::CfTable& t, double p, do
   double d = t.d1 * x;
   double A_prev = 1.0, B_prev = 1.0;            // n = 0
   double A = 1.0 + d, B = 1.0;                  // n = 1
-  double det = d;                               // |A_1 B_0 - A_0 B_1| = |d1|
-  for (int m = 1; m <= 100000; ++m) {
-    double ce, co;
-    if (m <= host::CfTable::kTerms) {
-      ce = t.even[m - 1];
-      co = t.odd[m - 1];
-    } else {  // long tails (extreme nu): same coefficients, computed on the fly
-      const double m2 = 2.0 * m;
-      ce = m * (q - m) / ((p - 1.0 + m2) * (p + m2));
-      co = -(p + m) * (p + q + m) / ((p + m2) * (p + 1.0 + m2));
+  // Fast path: tabulated coefficients, two iterations (four partial numerators) per
+  // convergence test.  The test is the reference's |h_n / h_{n-1} - 1| < 1e-15 with
+  // h = B/A, evaluated as |A_{n-1} B_n - A_n B_{n-1}| < 1e-15 |A_n B_{n-1}| (one FMA).
+  // Iterating past the reference's stopping point only adds terms below 1e-15 relative.
+  for (int m = 1; m + 1 <= host::CfTable::kTerms; m += 2) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      d = t.even[m - 1 + u] * x;
+      double An = fma(d, A_prev, A), Bn = fma(d, B_prev, B);
+      A_prev = A; B_prev = B; A = An; B = Bn;
+      d = t.odd[m - 1 + u] * x;
+      An = fma(d, A_prev, A); Bn = fma(d, B_prev, B);
+      A_prev = A; B_prev = B; A = An; B = Bn;
     }
+    const double c1 = A * B_prev;
+    if (fabs(fma(A_prev, B, -c1)) < 1e-15 * fabs(c1)) return B / A;
+  }
+  // Slow path (extreme nu, x near the switch point): per-iteration test with the
+  // determinant identity A_n B_{n-1} - A_{n-1} B_n = (-1)^n prod d_k, rescaling A, B.
+  double det = fabs(fma(A, B_prev, -A_prev * B));
+  for (int m = host::CfTable::kTerms + 1; m <= 100000; ++m) {
+    const double m2 = 2.0 * m;
+    const double ce = m * (q - m) / ((p - 1.0 + m2) * (p + m2));
+    const double co = -(p + m) * (p + q + m) / ((p + m2) * (p + 1.0 + m2));
     // n = 2m (even numerator)
     d = ce * x;
     double An = fma(d, A_prev, A), Bn = fma(d, B_prev, B);

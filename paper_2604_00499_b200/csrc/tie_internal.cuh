@@ -51,12 +51,22 @@ constexpr int kMoments = 16;            // one 128-byte row per (g, k)
 constexpr double kGridH = 1.0 / 32.0;   // power of two: g*h and sigma - g*h are exact
 constexpr double kGridInvH = 32.0;
 constexpr int kYBuckets = 8192;         // uniform-y bucket index over the sample range
+// Tail-mass table: v(y) = 1 - T_nu(y) = I_x(nu/2, 1/2)/2 for y >= 0 as a degree-7 Taylor
+// expansion about each of kTailBuckets bucket centres c_b over [0, max|Y|]:
+//   a_0 = v(c_b) (the reference's own continued-fraction value), a_j = -pdf^(j-1)(c_b)/j!,
+// the t-density's derivatives from the exact power series of C (1 + (c+t)^2/nu)^-(nu+1)/2.
+// The series converges within sqrt(c^2+nu) >= 1.87 of c_b; at half-width 2.2e-3 the
+// truncation is < 1e-23 relative.  T(y) = y >= 0 ? 1 - v(|y|) : v(|y|)  (dist.cpp:80).
+constexpr int kTailBuckets = 4096;
+constexpr int kTailCoef = 8;
 
 struct ScoreParams {
   TdistConst td;
   const double* Y;          // sorted samples [N]
   const uint32_t* ybucket;  // [kYBuckets + 1] upper_bound(Y, edge_b)
   const double* table;      // [G][N+1][kMoments]
+  const double* tail;       // [kTailBuckets][kTailCoef]
+  double t_ymax, t_w, t_inv_w;
   double y0, y_scale;       // bucket b = floor((y - y0) * y_scale)
   double yN;                // Y[N-1]
   int N;
@@ -64,6 +74,7 @@ struct ScoreParams {
   uint32_t k_alpha;         // upper_bound(Y, t_quantile(alpha, nu)); 0 when alpha == 0
   double alpha, beta;
   int raw;                  // TIE_SCORE_RAW: skip max(C,E) and compute_score
+  uint64_t index_base;      // added to reported request indices (chunked callers)
   unsigned long long* err;
 };
 
@@ -82,6 +93,8 @@ struct tie_ctx {
   double* d_Y = nullptr;
   uint32_t* d_ybucket = nullptr;
   double* d_table = nullptr;
+  double* d_tail = nullptr;
+  double t_ymax = 0, t_w = 0, t_inv_w = 0;
   int G = 0;
   double y0 = 0, y_scale = 0, yN = 0;
   unsigned long long* d_err = nullptr;   // first failure (index << 8 | reason)
@@ -139,16 +152,21 @@ cudaError_t build_context_tables(tie_ctx* ctx);
 cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma,
                          const void* x_max, bool x_is_u32, uint64_t n, double alpha,
                          double beta, double* E, double* C, double* S, uint64_t* keys_out,
-                         unsigned flags, cudaStream_t s);
-// Radix sort by (key, id); keys are IEEE doubles (scores or raw keys) viewed as u64 after
-// an order-preserving transform.  keys_are_positive_bits: keys already u64 bit patterns of
-// positive finite doubles (the fused score path writes these).
-cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* key_bits,
-                        const uint64_t* ids, uint64_t n, uint64_t* order, cudaStream_t s);
+                         uint32_t* hist_out, unsigned flags, cudaStream_t s,
+                         uint64_t index_base = 0);
+// Dispatch order by (key asc, id asc) of double keys (ids == nullptr: id = index).
+cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n,
+                        uint64_t* order, cudaStream_t s);
 size_t rank_scratch_bytes(uint64_t n, bool with_ids);
-// where a producer (the fused score kernel) should write transformed u64 keys so that
-// launch_rank(key_bits = this pointer) sorts them in place without a copy
-uint64_t* rank_key_buffer(tie_ctx* ctx, uint64_t n, cudaStream_t s);
+// Fused producer path: rank_prepare() zeroes the sort metadata and returns where the
+// producer (the score kernel) writes order-preserving u64 keys and accumulates the 8 digit
+// histograms; rank_prepared() then runs plan + digit passes and emits the order.
+struct RankPrep {
+  uint64_t* keys;
+  uint32_t* hist;
+};
+RankPrep rank_prepare(tie_ctx* ctx, uint64_t n, cudaStream_t s);
+cudaError_t rank_prepared(tie_ctx* ctx, uint64_t n, uint64_t* order, cudaStream_t s);
 cudaError_t launch_fit(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
                        double* mu, double* sigma, double* ll, int32_t* iters, uint8_t* conv,
                        uint8_t* degen, cudaStream_t s);
