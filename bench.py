@@ -222,30 +222,32 @@ def main():
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
     if world > 1:
-        gk = torch.empty(n_global, dtype=torch.float64, device=dev)
-        gi = torch.empty(n_global, dtype=torch.int64, device=dev)
-        gorder = torch.empty(n_global, dtype=torch.int64, device=dev)
+        from paper_2604_00499_b200.dist import DeviceOps, ShardedScoreRank
+
+        sharded = ShardedScoreRank(DeviceOps(mc, ALPHA), beta)
 
     def step():
-        tie.score_rank_device(ctx, mu.data_ptr(), sg.data_ptr(), mt.data_ptr(), n_local, ALPHA,
-                              beta, 0, 0, S.data_ptr(), order.data_ptr(), 0, sh)
-        if world > 1:
-            # sorted local run of (score, global id) -> all-gather -> merge on rank 0
-            run_k = S[order]
-            run_i = order + lo
-            dist.all_gather_into_tensor(gk, run_k)
-            dist.all_gather_into_tensor(gi, run_i)
-            if rank == 0:
-                # runs are contiguous id ranges in rank order, so the stable sort of the
-                # concatenation by score breaks cross-shard ties by id (sched.cpp:28-31)
-                tie.rank_device(ctx, gk.data_ptr(), 0, n_global, gorder.data_ptr(), sh)
-                torch.take(gi, gorder, out=gorder)  # noqa: in-place gather of global ids
+        if world == 1:
+            tie.score_rank_device(ctx, mu.data_ptr(), sg.data_ptr(), mt.data_ptr(), n_local,
+                                  ALPHA, beta, 0, 0, S.data_ptr(), order.data_ptr(), 0, sh)
+        else:
+            # local K1+K2 -> NCCL all-gather of sorted (score, id) runs -> merge on rank 0
+            res = sharded(mu, sg, mt, n_global)
+            S.copy_(res.scores)
+            order.copy_(res.local_order)
 
     clocks = ClockSampler(local)
     clocks.start()
     for _ in range(max(args.warmup, 3)):
         flush.zero_()
         step()
+    # untimed soak (~1.5 s of back-to-back steps) so the clock sampler sees the GPU under this
+    # load: the timed region itself lasts only milliseconds at config 2
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < 1.5:
+        for _ in range(20):
+            step()
+        torch.cuda.synchronize()
     tie.sync(ctx, sh)
     torch.cuda.synchronize()
     if dist:
@@ -314,7 +316,7 @@ def main():
                  if len(np.unique(((bits >> np.uint64(8 * p)) & np.uint64(255))[:200000])) > 1)
     dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
     roof = None
-    if dom == "rank.downsweep":
+    if dom in ("rank.downsweep", "rank.onesweep"):
         bytes_per_launch = 24.0 * n_local  # read + write one (8 B key, 4 B id) record per key
         t_launch = kern[dom]["ms_per_step"] * 1e-3 / max(active, 1)
         ach = bytes_per_launch / t_launch / 1e9
@@ -329,6 +331,18 @@ def main():
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak, "traffic": None, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_per_launch, "launch_ms": t_launch * 1e3}
+
+    # DRAM traffic per launch of the dominant kernel from the committed ncu --set full capture
+    # of this same configuration (profiles/ncu_traffic_r01.json), scaled to this n
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")) as f:
+            tr = json.load(f)
+        if dom in tr:
+            roof["traffic"] = (tr[dom]["dram_read_bytes"] + tr[dom]["dram_write_bytes"]) * (
+                n_local / tr["n"])
+            roof["traffic_source"] = "profiles/ncu_traffic_r01.json: " + tr[dom]["capture"]
+    except (OSError, KeyError, ValueError):
+        pass
 
     extras = {}
     if rank == 0 and not args.no_extras:

@@ -1,0 +1,136 @@
+"""Request-sharded score + rank over G GPUs: one process per GPU, NCCL.
+
+The reference is single-process (a binary heap in one thread, proj/src/sched.cpp:28-94); the
+order it defines -- (score asc, request id asc) over the whole queue -- is reproduced here
+exactly across shards:
+
+1. shard the queue into contiguous id ranges [lo_g, hi_g)  (``shard_bounds``);
+2. beta = compute_beta(cfg, GLOBAL queue length)  (sched.cpp:9-17 -- NOT the shard length);
+3. each rank scores its shard and sorts it locally (fused K1+K2 on its GPU);
+4. the sorted (score, id) runs are all-gathered over NCCL (NVLink / NVSwitch), padded to
+   the longest shard with DBL_MAX sentinels (scores are finite, so sentinels sort last);
+5. rank 0 merges the G runs with a stable device sort of the concatenation by score.  The
+   runs are concatenated in rank order and shards are contiguous ascending id ranges, so
+   among equal scores the concatenation order IS ascending id order, and the stable sort
+   breaks ties by id exactly as the reference heap does (sched.cpp:28-31).
+
+Device work is behind ``DeviceOps`` (the C-ABI through ``_core``); tests substitute
+reference-semantics NumPy ops to exercise the sharding / padding / gather / merge logic on
+CPU with the gloo backend.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+SENTINEL = np.finfo(np.float64).max
+
+
+def shard_bounds(n_global: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous id range of ``rank``; sizes differ by at most one (the first n % world
+    ranks take one extra request)."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError("shard_bounds: bad world/rank")
+    base, extra = divmod(int(n_global), world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def global_beta(cfg, n_global: int) -> float:
+    """beta from the GLOBAL queue length (sched.cpp:9-17)."""
+    from . import _core
+
+    return _core.compute_beta(cfg, int(n_global))
+
+
+class DeviceOps:
+    """K1+K2 on this rank's GPU through the C-ABI (torch CUDA tensors in and out)."""
+
+    def __init__(self, mc, alpha: float, exact: bool = False):
+        import torch
+
+        from . import _core
+
+        self.torch = torch
+        self.core = _core
+        self.ctx = mc.handle
+        self.alpha = alpha
+        self.flags = 1 if exact else 0
+
+    def score_sort(self, mu, sigma, max_tokens, beta):
+        """-> (scores in queue order, local order (int64 indices sorted by (score, index)))."""
+        torch = self.torch
+        n = mu.numel()
+        S = torch.empty(n, dtype=torch.float64, device=mu.device)
+        order = torch.empty(n, dtype=torch.int64, device=mu.device)
+        stream = torch.cuda.current_stream(mu.device).cuda_stream
+        self.core.score_rank_device(self.ctx, mu.data_ptr(), sigma.data_ptr(),
+                                    max_tokens.data_ptr(), n, self.alpha, beta, 0, 0,
+                                    S.data_ptr(), order.data_ptr(), self.flags, stream)
+        return S, order
+
+    def stable_sort(self, keys):
+        """-> int64 permutation sorting ``keys`` by (key, position)."""
+        torch = self.torch
+        n = keys.numel()
+        order = torch.empty(n, dtype=torch.int64, device=keys.device)
+        stream = torch.cuda.current_stream(keys.device).cuda_stream
+        self.core.rank_device(self.ctx, keys.data_ptr(), 0, n, order.data_ptr(), stream)
+        return order
+
+    def sync(self):
+        stream = self.torch.cuda.current_stream().cuda_stream
+        self.core.sync(self.ctx, stream)
+
+
+@dataclass
+class ShardResult:
+    scores: object            # this rank's scores, queue order (device tensor)
+    local_order: object       # this rank's sorted local indices
+    global_order: object      # rank 0 (or every rank with merge_on="all"): global ids; else None
+
+
+class ShardedScoreRank:
+    """score + rank a globally-indexed queue sharded over the ranks of ``group``."""
+
+    def __init__(self, ops, cfg_beta: float, group=None, merge_on: str = "root"):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.ops = ops
+        self.beta = cfg_beta
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if merge_on not in ("root", "all"):
+            raise ValueError("merge_on must be 'root' or 'all'")
+        self.merge_on = merge_on
+
+    def __call__(self, mu, sigma, max_tokens, n_global: int) -> ShardResult:
+        import torch
+
+        lo, hi = shard_bounds(n_global, self.world, self.rank)
+        if mu.numel() != hi - lo:
+            raise ValueError(f"rank {self.rank}: shard holds {mu.numel()} requests, expected "
+                             f"{hi - lo} (ids [{lo}, {hi}))")
+        S, order = self.ops.score_sort(mu, sigma, max_tokens, self.beta)
+        if self.world == 1:
+            return ShardResult(S, order, order)
+        width = shard_bounds(n_global, self.world, 0)[1]  # the longest shard
+        run_k = torch.full((width,), SENTINEL, dtype=torch.float64, device=S.device)
+        run_i = torch.full((width,), -1, dtype=torch.int64, device=S.device)
+        m = hi - lo
+        run_k[:m] = S[order]
+        run_i[:m] = order + lo
+        gk = [torch.empty_like(run_k) for _ in range(self.world)]
+        gi = [torch.empty_like(run_i) for _ in range(self.world)]
+        self.dist.all_gather(gk, run_k, group=self.group)
+        self.dist.all_gather(gi, run_i, group=self.group)
+        merged = None
+        if self.merge_on == "all" or self.rank == 0:
+            keys = torch.cat(gk)
+            ids = torch.cat(gi)
+            perm = self.ops.stable_sort(keys)
+            merged = ids[perm][:n_global]  # sentinels (DBL_MAX) sort after every real score
+        return ShardResult(S, order, merged)

@@ -1,0 +1,114 @@
+"""CPU, world_size 2 (gloo): the sharded score+rank host logic of paper_2604_00499_b200.dist --
+shard bounds, global-queue beta, run padding, all-gather and the stable merge -- must yield
+exactly the reference's single-queue dispatch order.  Device kernels are replaced by
+reference-semantics NumPy ops (the oracle) so the collective plumbing is what is tested."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2604_00499_b200.dist import SENTINEL, ShardedScoreRank, shard_bounds
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class OracleOps:
+    """score_sort / stable_sort with the reference's semantics, on CPU tensors."""
+
+    def __init__(self, alpha=0.9):
+        from oracle_lib import Oracle
+
+        self.o = Oracle()
+        self.Y = self.o.mc_samples()
+        self.alpha = alpha
+
+    def score_sort(self, mu, sigma, mt, beta):
+        _, _, S = self.o.score(self.Y, mu.numpy(), sigma.numpy(), mt.numpy().astype(float),
+                               alpha=self.alpha, beta=beta, threads=2)
+        order = self.o.rank(S).astype(np.int64)
+        return torch.from_numpy(S), torch.from_numpy(order)
+
+    def stable_sort(self, keys):
+        return torch.from_numpy(np.argsort(keys.numpy(), kind="stable").astype(np.int64))
+
+
+def _worker(rank, world, port, n_global, case, out_q):
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.dirname(here))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle_lib import Oracle
+
+        o = Oracle()
+        if case == "workload":
+            mu, sg, mt = o.gen_workload(n_global, seed=1)
+        else:  # every request identical: all cross-shard ties must break by id
+            mu = np.full(n_global, 4.0)
+            sg = np.full(n_global, 0.8)
+            mt = np.full(n_global, 2048, np.uint32)
+        lo, hi = shard_bounds(n_global, world, rank)
+        beta = o.compute_beta(True, 0.1, 0.5, 128.0, n_global)  # GLOBAL queue length
+        ops = OracleOps()
+        for merge_on in ("root", "all"):
+            res = ShardedScoreRank(ops, beta, merge_on=merge_on)(
+                torch.from_numpy(mu[lo:hi].copy()), torch.from_numpy(sg[lo:hi].copy()),
+                torch.from_numpy(mt[lo:hi].copy()), n_global)
+            if res.global_order is not None:
+                out_q.put((rank, merge_on, res.global_order.numpy().tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_global,case", [(2001, "workload"), (64, "ties"), (3, "workload")])
+def test_two_rank_order_matches_single_queue(n_global, case, oracle):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_global, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    got = [q.get(timeout=5) for _ in range(3)]  # root-merge on rank 0, all-merge on both
+    # the reference: one queue, one heap
+    if case == "workload":
+        mu, sg, mt = oracle.gen_workload(n_global, seed=1)
+    else:
+        mu, sg, mt = np.full(n_global, 4.0), np.full(n_global, 0.8), np.full(n_global, 2048)
+    beta = oracle.compute_beta(True, 0.1, 0.5, 128.0, n_global)
+    _, _, S = oracle.score(oracle.mc_samples(), mu, sg, np.asarray(mt, float), alpha=0.9,
+                           beta=beta)
+    ref = oracle.rank(S).tolist()
+    for rank, merge_on, order in got:
+        assert order == ref, (rank, merge_on)
+    if case == "ties":
+        assert ref == list(range(n_global))
+
+
+def test_shard_bounds_cover_queue():
+    for n in (0, 1, 7, 1000, 1001):
+        for w in (1, 2, 3, 8):
+            spans = [shard_bounds(n, w, r) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1 and sizes == sorted(sizes, reverse=True)
+    with pytest.raises(ValueError):
+        shard_bounds(10, 2, 2)
+    assert SENTINEL > 1e300
