@@ -9,6 +9,7 @@ raw little-endian bytes.
 """
 from __future__ import annotations
 
+import hashlib
 import json
 import math
 import os
@@ -117,6 +118,8 @@ def main():
     np.savez(os.path.join(HERE, "config2_sample.npz"), idx=idx, E=E[idx], C=C[idx], S=S[idx],
              order_head=order[:4096], order_tail=order[-4096:])
     out["config2"] = {"n": n2, "fnv_order": fnv_fast(order), "fnv_S": fnv_fast(S),
+                      "sha256_order": hashlib.sha256(order.tobytes()).hexdigest(),
+                      "sha256_E": hashlib.sha256(E.tobytes()).hexdigest(),
                       "fnv_mu": fnv_fast(mu), "fnv_sigma": fnv_fast(sg),
                       "sum_S": float(S.sum()), "pairs_rel_gap_lt_1e-12": int((rel_gap < 1e-12).sum()),
                       "pairs_rel_gap_lt_1e-9": int((rel_gap < 1e-9).sum()),

@@ -62,6 +62,21 @@ def test_config1_scores_and_order(abi, h, flags):
     assert order[:8].tolist() == [25, 142, 172, 568, 266, 840, 699, 270]
 
 
+@pytest.mark.parametrize("flags", MODES)
+def test_config2_full_order_bit_exact(abi, h, oracle, flags):
+    """Config 2: the 1M-request queue's complete dispatch order equals the reference's
+    (WaitingQueue pop order, sha256 of the u64 id sequence in tests/golden/golden.json)."""
+    import hashlib
+
+    g = golden("golden.json")["config2"]
+    mu, sg, mt = oracle.gen_workload(1_000_000, seed=1)
+    S, order = abi.score_rank(h, mu, sg, mt, 0.9, 0.5, flags)
+    assert hashlib.sha256(order.tobytes()).hexdigest() == g["sha256_order"]
+    smp = golden("config2_sample.npz")
+    assert rel_err(S[smp["idx"]], smp["S"]).max() <= TOL
+    assert np.array_equal(order[:4096], smp["order_head"])
+
+
 def test_canonical_config_queue(abi, h):
     g = golden("canonical20k.npz")
     from oracle_lib import Oracle
