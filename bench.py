@@ -347,6 +347,19 @@ def main():
     extras = {}
     if rank == 0 and not args.no_extras:
         extras = run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream)
+        # second half of the metric: p50 schedule-step latency vs queue size (bench_sched.py)
+        try:
+            import bench_sched
+
+            extras["schedule_step"] = {
+                "metric": "p50 schedule-step latency vs resident queue size (32 arrivals + "
+                          "32 scored predictions + 8 pops per step)",
+                "unit": "us", "higher_is_better": False,
+                "cpu": "reference Scheduler (oracle/_ref), 1 thread; GPU: tie_queue, "
+                       "wall-clocked incl. H2D/D2H",
+                "results": bench_sched.run(tie, mc, cpu=not args.no_cpu)}
+        except Exception as exc:  # never blocks the headline line
+            extras["schedule_step"] = {"error": repr(exc)}
 
     line = {"metric": "requests scored+ranked/sec", "value": value, "unit": "requests/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

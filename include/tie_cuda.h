@@ -129,6 +129,33 @@ int tie_fit_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double n
                  double* mu, double* sigma, double* log_likelihood, int32_t* iterations,
                  uint8_t* converged, uint8_t* degenerate);
 
+/* ---- GPU-resident waiting queue (the scheduler step) ------------------------------------
+ * Replaces Scheduler + WaitingQueue (proj/include/tiesched/sched.hpp:43-90,
+ * proj/src/sched.cpp:28-175): keys live on the device with a block-min index; the pop
+ * sequence -- including drift rebuilds before pops -- is the reference's.  policy: 0 FCFS,
+ * 1 SEPT, 2 TIE (sched.hpp:11).  Host buffers; each call completes before returning.  A
+ * batch is validated before any of it is applied (the reference applies items one by one). */
+typedef struct tie_queue tie_queue;
+int tie_queue_create(tie_ctx* ctx, int policy, int adaptive, double beta_fixed,
+                     double beta_max, double q_sat, double rebuild_threshold, double alpha,
+                     uint64_t capacity, tie_queue** out);
+void tie_queue_destroy(tie_queue* q);
+uint64_t tie_queue_size(const tie_queue* q);       /* Scheduler::waiting()      */
+double tie_queue_current_beta(const tie_queue* q); /* Scheduler::current_beta() */
+/* Scheduler::on_arrival x m (sched.cpp:125-132) */
+int tie_queue_arrive(tie_queue* q, const uint64_t* ids, const double* arrival_s,
+                     const uint32_t* max_tokens, uint64_t m);
+/* Scheduler::on_prediction x m with (E, CVaR) (sched.cpp:134-150) */
+int tie_queue_predict(tie_queue* q, const uint64_t* ids, const double* expectation,
+                      const double* cvar, uint64_t m);
+/* run_sim's scoring chain (sim.cpp:85-95) on the GPU for (mu, sigma), then on_prediction */
+int tie_queue_predict_logt(tie_queue* q, const uint64_t* ids, const double* mu,
+                           const double* sigma, const uint32_t* max_tokens, uint64_t m);
+/* Scheduler::next_request() up to max_pops times (sched.cpp:169-175); out_ids[max_pops] */
+int tie_queue_next(tie_queue* q, uint64_t max_pops, uint64_t* out_ids, uint64_t* n_out);
+/* Scheduler::rebuild_if_drifted() (sched.cpp:152-167) */
+int tie_queue_rebuild_if_drifted(tie_queue* q, int* rebuilt);
+
 /* ---- diagnostics ------------------------------------------------------------------------
  * Kernel-level profiling: with tie_profile(ctx, 1) every kernel launched by this context is
  * bracketed by a CUDA event pair on its stream; tie_profile_report() synchronises and

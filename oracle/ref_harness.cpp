@@ -17,6 +17,7 @@
 // Nothing here re-implements reference arithmetic; every number comes out of the
 // reference's own functions.
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -275,6 +276,67 @@ int ref_scheduler_script(int policy, int adaptive, double beta_fixed, double bet
       }
     }
     *n_out = k;
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 2);
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
+}
+
+// Schedule-step benchmark on the reference Scheduler (sched.cpp:125-175): preload n_pre
+// requests (on_arrival + on_prediction with the given E/CVaR, untimed), then `steps` timed
+// steps of: on_arrival x per_step, score those requests with the reference functions
+// (censored_expectation / censored_cvar / max, sim.cpp:85-94) + on_prediction, then
+// next_request() x pops.  Per-step seconds and the popped ids are returned.
+int ref_sched_bench(int policy, int adaptive, double beta_max, double q_sat, double threshold,
+                    double alpha, uint64_t n_pre, const uint64_t* pre_ids,
+                    const uint32_t* pre_mt, const double* pre_E, const double* pre_C,
+                    uint64_t steps, uint64_t per_step, const uint64_t* new_ids,
+                    const double* new_mu, const double* new_sigma, const uint32_t* new_mt,
+                    uint32_t pops, double* step_seconds, uint64_t* popped, uint64_t* n_popped) {
+  try {
+    tie::ScoreConfig cfg;
+    cfg.beta_mode = adaptive ? tie::BetaMode::AdaptiveLinear : tie::BetaMode::Fixed;
+    cfg.beta_max = beta_max;
+    cfg.q_sat = q_sat;
+    cfg.rebuild_threshold = threshold;
+    cfg.alpha = alpha;
+    tie::Scheduler s((tie::Policy)policy, cfg);
+    tie::McContext mc(3.5);
+    for (uint64_t i = 0; i < n_pre; ++i) {
+      tie::Request r{};
+      r.id = pre_ids[i];
+      r.max_tokens = pre_mt[i];
+      s.on_arrival(r);
+    }
+    for (uint64_t i = 0; i < n_pre; ++i) s.on_prediction(pre_ids[i], pre_E[i], pre_C[i]);
+    uint64_t k = 0;
+    for (uint64_t st = 0; st < steps; ++st) {
+      const auto t0 = std::chrono::steady_clock::now();
+      for (uint64_t j = 0; j < per_step; ++j) {
+        tie::Request r{};
+        r.id = new_ids[st * per_step + j];
+        r.max_tokens = new_mt[st * per_step + j];
+        s.on_arrival(r);
+      }
+      for (uint64_t j = 0; j < per_step; ++j) {
+        const uint64_t i = st * per_step + j;
+        tie::CensoredLogT cl(tie::LogTParams(new_mu[i], new_sigma[i], 3.5), (double)new_mt[i]);
+        const double e = tie::censored_expectation(cl, mc);
+        const double c = std::max(tie::censored_cvar(cl, mc, alpha), e);
+        s.on_prediction(new_ids[i], e, c);
+      }
+      for (uint32_t j = 0; j < pops; ++j) {
+        auto got = s.next_request();
+        popped[k++] = got ? *got : UINT64_MAX;
+      }
+      step_seconds[st] =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    *n_popped = k;
     return 0;
   } catch (const std::domain_error& e) {
     return fail(e, 1);

@@ -704,3 +704,82 @@ int tor_gen_fit_data(uint64_t P, uint64_t K, uint64_t seed, double mu_lo, double
   if (!true_sigma) free(s);
   return 0;
 }
+
+/* ---------------------------------------------------------------- scheduler */
+typedef struct {
+  uint64_t id;
+  double key, E, C, beta;
+  int predicted, alive;
+} qent_t;
+
+/* sched.cpp:9-26 with the reference's validation */
+static int sched_beta(int adaptive, double bf, double bm, double qs, uint64_t q, double* out) {
+  return tor_compute_beta(adaptive, bf, bm, qs, q, out);
+}
+
+int tor_scheduler_script(int policy, int adaptive, double beta_fixed, double beta_max,
+                         double q_sat, double rebuild_threshold, uint64_t n_ops,
+                         const int32_t* op, const uint64_t* id, const double* a,
+                         const double* b, uint64_t* out, uint64_t* n_out) {
+  qent_t* e = (qent_t*)calloc(n_ops ? n_ops : 1, sizeof(qent_t));
+  double* betas = (double*)malloc(sizeof(double) * (n_ops ? n_ops : 1)); /* multiset */
+  uint64_t n = 0, nb = 0, size = 0, k = 0;
+  int rc = 0;
+#define FIND(x) ({ uint64_t f_ = UINT64_MAX; for (uint64_t j_ = 0; j_ < n; ++j_) \
+                   if (e[j_].alive && e[j_].id == (x)) { f_ = j_; break; } f_; })
+  for (uint64_t i = 0; i < n_ops && !rc; ++i) {
+    if (op[i] == 0) { /* on_arrival (sched.cpp:125-132) + push (59-67) */
+      double key = policy == 0 ? a[i] : (double)(uint32_t)b[i];
+      if (!isfinite(key)) { rc = fail(1, "WaitingQueue::push: key must be finite"); break; }
+      if (FIND(id[i]) != UINT64_MAX) { rc = fail(2, "WaitingQueue::push: id already queued"); break; }
+      e[n].id = id[i]; e[n].key = key; e[n].alive = 1; e[n].predicted = 0;
+      ++n; ++size;
+    } else if (op[i] == 1) { /* on_prediction (sched.cpp:134-150) */
+      uint64_t j = FIND(id[i]);
+      if (j == UINT64_MAX) { rc = fail(2, "Scheduler::on_prediction: id not waiting"); break; }
+      if (policy == 0) continue;
+      double beta = 0.0;
+      if (policy == 2 && (rc = sched_beta(adaptive, beta_fixed, beta_max, q_sat, size, &beta))) break;
+      if (e[j].predicted) { rc = fail(2, "Scheduler::on_prediction: id already predicted"); break; }
+      double E = a[i], C = b[i];
+      if (!isfinite(E) || !isfinite(C) || !isfinite(beta)) { rc = fail(1, "compute_score: arguments must be finite"); break; }
+      if (!(E > 0.0)) { rc = fail(1, "compute_score: expectation must be > 0"); break; }
+      if (C < E) { rc = fail(2, "compute_score: cvar below expectation violates the invariant"); break; }
+      e[j].predicted = 1; e[j].E = E; e[j].C = C; e[j].beta = beta;
+      betas[nb++] = beta;
+      e[j].key = E + beta * C;
+    } else { /* next_request (sched.cpp:169-175) with rebuild_if_drifted (152-167) */
+      if (policy == 2 && nb > 0) {
+        double now, lo = betas[0], hi = betas[0];
+        if ((rc = sched_beta(adaptive, beta_fixed, beta_max, q_sat, size, &now))) break;
+        for (uint64_t t = 1; t < nb; ++t) { if (betas[t] < lo) lo = betas[t]; if (betas[t] > hi) hi = betas[t]; }
+        double worst = std_max(fabs(now - lo), fabs(now - hi));
+        if (worst > rebuild_threshold) {
+          nb = 0;
+          for (uint64_t j = 0; j < n; ++j)
+            if (e[j].alive && e[j].predicted) {
+              e[j].beta = now; e[j].key = e[j].E + now * e[j].C; betas[nb++] = now;
+            }
+        }
+      }
+      uint64_t best = UINT64_MAX;
+      for (uint64_t j = 0; j < n; ++j) {
+        if (!e[j].alive) continue;
+        if (best == UINT64_MAX || e[j].key < e[best].key ||
+            (e[j].key == e[best].key && e[j].id < e[best].id)) best = j;
+      }
+      if (best == UINT64_MAX) { out[k++] = UINT64_MAX; continue; }
+      e[best].alive = 0; --size;
+      if (e[best].predicted) { /* betas_in_use_.erase(find(beta_at_update)) */
+        for (uint64_t t = 0; t < nb; ++t)
+          if (betas[t] == e[best].beta) { betas[t] = betas[--nb]; break; }
+      }
+      out[k++] = e[best].id;
+    }
+  }
+#undef FIND
+  *n_out = k;
+  free(e);
+  free(betas);
+  return rc;
+}

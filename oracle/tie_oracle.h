@@ -69,6 +69,17 @@ int tor_gen_fit_data(uint64_t P, uint64_t K, uint64_t seed, double mu_lo, double
                      double sg_lo, double sg_hi, double nu, int integerise, double* x,
                      double* true_mu, double* true_sigma, int threads);
 
+/* Scheduler over a WaitingQueue (sched.cpp:28-175), driven by a script of events:
+ * op 0 = on_arrival(id, arrival_s = a, max_tokens = (uint32)b),
+ * op 1 = on_prediction(id, E = a, CVaR = b),
+ * op 2 = next_request() -> writes the popped id (or UINT64_MAX) to out[(*n_out)++].
+ * policy 0 FCFS, 1 SEPT, 2 TIE.  Linear-scan pop_min: (key, id) order is what the heap
+ * produces (sched.cpp:28-31). */
+int tor_scheduler_script(int policy, int adaptive, double beta_fixed, double beta_max,
+                         double q_sat, double rebuild_threshold, uint64_t n_ops,
+                         const int32_t* op, const uint64_t* id, const double* a,
+                         const double* b, uint64_t* out, uint64_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

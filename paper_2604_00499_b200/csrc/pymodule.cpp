@@ -331,6 +331,72 @@ PYBIND11_MODULE(_core, m) {
         return out;
       },
       py::arg("ctx"), "{kernel: (launches, total_ms)} since profile(ctx, True)");
+  // GPU-resident Scheduler (sched.hpp:74-90) with batched event entry points
+  struct GpuQueue {
+    tie_queue* q = nullptr;
+    ~GpuQueue() { tie_queue_destroy(q); }
+  };
+  py::class_<GpuQueue>(m, "GpuScheduler")
+      .def(py::init([](const McContext& mc, Policy policy, const ScoreConfig& cfg,
+                       uint64_t capacity) {
+             auto* g = new GpuQueue();
+             const int rc = tie_queue_create(
+                 mc.handle(), (int)policy, cfg.beta_mode == BetaMode::AdaptiveLinear,
+                 cfg.beta_fixed, cfg.beta_max, cfg.q_sat, cfg.rebuild_threshold, cfg.alpha,
+                 capacity, &g->q);
+             if (rc) {
+               delete g;
+               throw_code(rc);
+             }
+             return g;
+           }),
+           py::arg("mc"), py::arg("policy"), py::arg("config"), py::arg("capacity"),
+           py::keep_alive<1, 2>())
+      .def("on_arrival_batch",
+           [](GpuQueue& g, carray<uint64_t> ids, carray<double> arrival_s,
+              carray<uint32_t> max_tokens) {
+             throw_code(tie_queue_arrive(g.q, ids.data(), arrival_s.data(), max_tokens.data(),
+                                         (uint64_t)ids.size()));
+           },
+           py::arg("ids"), py::arg("arrival_s"), py::arg("max_tokens"))
+      .def("on_prediction_batch",
+           [](GpuQueue& g, carray<uint64_t> ids, carray<double> E, carray<double> C) {
+             throw_code(tie_queue_predict(g.q, ids.data(), E.data(), C.data(),
+                                          (uint64_t)ids.size()));
+           },
+           py::arg("ids"), py::arg("expectation"), py::arg("cvar"))
+      .def("on_prediction_logt",
+           [](GpuQueue& g, carray<uint64_t> ids, carray<double> mu, carray<double> sigma,
+              carray<uint32_t> max_tokens) {
+             throw_code(tie_queue_predict_logt(g.q, ids.data(), mu.data(), sigma.data(),
+                                               max_tokens.data(), (uint64_t)ids.size()));
+           },
+           py::arg("ids"), py::arg("mu"), py::arg("sigma"), py::arg("max_tokens"))
+      .def("next_requests",
+           [](GpuQueue& g, uint64_t k) {
+             std::vector<uint64_t> out(k);
+             uint64_t n = 0;
+             throw_code(tie_queue_next(g.q, k, out.data(), &n));
+             out.resize(n);
+             return carray<uint64_t>((py::ssize_t)n, out.data());
+           },
+           py::arg("k"))
+      .def("next_request",
+           [](GpuQueue& g) -> py::object {
+             uint64_t id = 0, n = 0;
+             throw_code(tie_queue_next(g.q, 1, &id, &n));
+             if (!n) return py::none();
+             return py::int_(id);
+           })
+      .def("rebuild_if_drifted",
+           [](GpuQueue& g) {
+             int r = 0;
+             throw_code(tie_queue_rebuild_if_drifted(g.q, &r));
+             return r != 0;
+           })
+      .def("waiting", [](const GpuQueue& g) { return tie_queue_size(g.q); })
+      .def("current_beta", [](const GpuQueue& g) { return tie_queue_current_beta(g.q); });
+
   m.def("default_context", []() { return (uintptr_t)default_context(); });
   m.def("launch_count", [](bool reset) { return tie_launch_count(reset ? 1 : 0); },
         py::arg("reset") = false);

@@ -124,6 +124,22 @@ class Oracle(_Base):
         self._gf = self._fn("gen_fit_data", [_u64, _u64, _u64, _d, _d, _d, _d, _d, _i32, _p,
                                              _p, _p, _i32])
         self._sl = self._fn("sample_logt", [_d, _d, _d, _u64, _u64, _p])
+        self._sched = self._fn("scheduler_script", [_i32, _i32, _d, _d, _d, _d, _u64, _p, _p,
+                                                    _p, _p, _p, ctypes.POINTER(_u64)])
+
+    def scheduler_script(self, policy, ops, ids, a, b, adaptive=True, beta_fixed=0.1,
+                         beta_max=0.5, q_sat=128.0, rebuild_threshold=0.1):
+        ops = np.ascontiguousarray(ops, np.int32)
+        ids = np.ascontiguousarray(ids, np.uint64)
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        out = np.empty(max(len(ops), 1), np.uint64)
+        n_out = _u64(0)
+        rc = self._sched(policy, int(adaptive), beta_fixed, beta_max, q_sat, rebuild_threshold,
+                         len(ops), _ptr(ops), _ptr(ids), _ptr(a), _ptr(b), _ptr(out),
+                         ctypes.byref(n_out))
+        self._check(rc, "scheduler_script")
+        return out[: n_out.value]
 
     def score(self, samples, mu, sigma, x_max, alpha=0.9, beta=0.5, nu=3.5, threads=None):
         samples = np.ascontiguousarray(samples, np.float64)

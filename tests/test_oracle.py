@@ -110,3 +110,45 @@ def test_oracle_vs_reference_library(oracle):
     r1, r2 = oracle.fit(x), R.fit(x)
     for k in r1:
         assert np.array_equal(r1[k], r2[k]), k
+
+
+# ---------------------------------------------------------------- scheduler (sched.cpp)
+def _drift_script(threshold):
+    """test_sched.cpp:245-292: q_sat=4, predictions at q=4 (beta .5), the pop drops beta to
+    .375 -> drift .125: with threshold .1 the rebuild surfaces X (id 1), with .2 Y (id 2)."""
+    ops = [0, 0, 0, 0, 1, 1, 1, 2, 2, 2, 2]
+    ids = [0, 1, 2, 3, 0, 1, 2, 0, 0, 0, 0]
+    a = [0.0, 0.1, 0.2, 0.30000000000000004, 5.0, 100.0, 671.0, 0, 0, 0, 0]
+    b = [2048, 2048, 2048, 2048, 10.0, 2000.0, 671.0, 0, 0, 0, 0]
+    return ops, ids, a, b, dict(adaptive=True, beta_max=0.5, q_sat=4.0,
+                                rebuild_threshold=threshold)
+
+
+def test_scheduler_reference_scenarios(oracle):
+    ops, ids, a, b, cfg = _drift_script(0.1)
+    assert oracle.scheduler_script(2, ops, ids, a, b, **cfg).tolist()[:2] == [0, 1]
+    ops, ids, a, b, cfg = _drift_script(0.2)
+    assert oracle.scheduler_script(2, ops, ids, a, b, **cfg).tolist()[:2] == [0, 2]
+    # FCFS ignores predictions; equal max_tokens pop by id (test_sched.cpp:199-243)
+    out = oracle.scheduler_script(0, [0, 0, 1, 2, 2, 2], [5, 3, 5, 0, 0, 0],
+                                  [1.0, 2.0, 5000.0, 0, 0, 0], [2048, 2048, 6000.0, 0, 0, 0],
+                                  adaptive=False, beta_fixed=0.3)
+    assert out.tolist() == [5, 3, np.iinfo(np.uint64).max]
+    out = oracle.scheduler_script(2, [0, 0, 2], [9, 4, 0], [0.0, 0.1, 0], [1024, 1024, 0],
+                                  adaptive=False, beta_fixed=0.3)
+    assert out.tolist() == [4]
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built (no /root/reference)")
+@pytest.mark.parametrize("policy,thr", [(2, 0.1), (2, 0.0), (2, 0.2), (1, 0.1), (0, 0.1)])
+def test_scheduler_oracle_vs_reference(oracle, policy, thr):
+    from sched_scripts import make_script
+
+    R = RefLib()
+    cfg = dict(adaptive=True, beta_max=0.5, q_sat=64.0, rebuild_threshold=thr)
+    for seed in range(4):
+        ops, ids, a, b = make_script(seed, oracle, policy=policy, **cfg)
+        got = oracle.scheduler_script(policy, ops, ids, a, b, **cfg)
+        ref = R.scheduler_script(policy, ops, ids, a, b, **cfg)
+        assert np.array_equal(got, ref), (policy, thr, seed)
+        assert len(got) > 50
