@@ -129,6 +129,20 @@ int tie_fit_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double n
                  double* mu, double* sigma, double* log_likelihood, int32_t* iterations,
                  uint8_t* converged, uint8_t* degenerate);
 
+/* ---- run_sim's scoring precompute -------------------------------------------------------
+ * Replaces the loop of proj/src/sim.cpp:77-96: predictor 0 = oracle_predict, 1 =
+ * noisy_predict(noise, seed) with the per-request Rng(mix64(seed, id)) (predictor.cpp:15-31);
+ * family 0 = log-t (K1), 1 = log-normal closed forms (dist.cpp:227-249); CVaR = max(CVaR, E).
+ * mu/sigma are the requests' TRUE parameters (Request::true_mu / true_sigma). */
+int tie_sim_scores(tie_ctx* ctx, const double* mu, const double* sigma, const uint64_t* ids,
+                   const uint32_t* max_tokens, uint64_t n, int predictor, double mu_sd,
+                   double log_sigma_sd, uint64_t seed, int family, double alpha, double* E,
+                   double* cvar, void* stream);
+int tie_sim_scores_host(tie_ctx* ctx, const double* mu, const double* sigma,
+                        const uint64_t* ids, const uint32_t* max_tokens, uint64_t n,
+                        int predictor, double mu_sd, double log_sigma_sd, uint64_t seed,
+                        int family, double alpha, double* E, double* cvar);
+
 /* ---- GPU-resident waiting queue (the scheduler step) ------------------------------------
  * Replaces Scheduler + WaitingQueue (proj/include/tiesched/sched.hpp:43-90,
  * proj/src/sched.cpp:28-175): keys live on the device with a block-min index; the pop

@@ -286,6 +286,46 @@ int ref_scheduler_script(int policy, int adaptive, double beta_fixed, double bet
   }
 }
 
+// run_sim's precompute loop (sim.cpp:77-96) through the reference's own predictor and
+// scoring functions: predictor 0 oracle_predict / 1 noisy_predict(seed), family 0 log-t /
+// 1 log-normal, CVaR = max(CVaR, E).  Requests carry true (mu, sigma) and their ids.
+int ref_sim_scores(const double* mu, const double* sigma, const uint64_t* ids,
+                   const uint32_t* max_tokens, uint64_t n, int predictor, double mu_sd,
+                   double ls_sd, uint64_t seed, int family, double alpha, double* E, double* C,
+                   int threads) {
+  try {
+    tie::McContext mc(3.5);
+    tie::NoiseSpec noise;
+    noise.mu_sd = mu_sd;
+    noise.log_sigma_sd = ls_sd;
+    parallel_for((size_t)n, threads, [&](size_t i) {
+      tie::Request r{};
+      r.id = ids[i];
+      r.max_tokens = max_tokens[i];
+      r.true_mu = mu[i];
+      r.true_sigma = sigma[i];
+      const tie::PredictedDist p =
+          predictor == 1 ? tie::noisy_predict(r, noise, seed) : tie::oracle_predict(r);
+      double e, c;
+      if (family == 0) {
+        tie::CensoredLogT cl(tie::LogTParams(p.mu_hat, p.sigma_hat, 3.5), (double)r.max_tokens);
+        e = tie::censored_expectation(cl, mc);
+        c = tie::censored_cvar(cl, mc, alpha);
+      } else {
+        e = tie::lognormal_censored_expectation(p.mu_hat, p.sigma_hat, (double)r.max_tokens);
+        c = tie::lognormal_censored_cvar(p.mu_hat, p.sigma_hat, (double)r.max_tokens, alpha);
+      }
+      E[i] = e;
+      C[i] = std::max(c, e);
+    });
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
+  } catch (const std::exception& e) {
+    return fail(e, 2);
+  }
+}
+
 // Schedule-step benchmark on the reference Scheduler (sched.cpp:125-175): preload n_pre
 // requests (on_arrival + on_prediction with the given E/CVaR, untimed), then `steps` timed
 // steps of: on_arrival x per_step, score those requests with the reference functions

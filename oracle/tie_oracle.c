@@ -783,3 +783,95 @@ int tor_scheduler_script(int policy, int adaptive, double beta_fixed, double bet
   free(betas);
   return rc;
 }
+
+/* ---------------------------------------------------------------- run_sim scoring chain */
+/* dist.cpp:191-249: standard normal CDF / quantile, log-normal censored moments */
+static double normal_cdf(double z) { return 0.5 * erfc(-z * 0.7071067811865475244); }
+
+static double normal_quantile(double p) {
+  static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                             1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                             6.680131188771972e+01, -1.328068155288572e+01};
+  static const double c[] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                             -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00};
+  static const double d[] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+                             3.754408661907416e+00};
+  const double plow = 0.02425, phigh = 1.0 - plow;
+  double q, r, z;
+  if (p < plow) {
+    q = sqrt(-2.0 * log(p));
+    z = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  } else if (p <= phigh) {
+    q = p - 0.5;
+    r = q * q;
+    z = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1.0);
+  } else {
+    q = sqrt(-2.0 * log1p(-p));
+    z = -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  }
+  double e = normal_cdf(z) - p;
+  double u = e * sqrt(2.0 * 3.14159265358979323846) * exp(0.5 * z * z);
+  return z - u / (1.0 + 0.5 * z * u);
+}
+
+double tor_normal_quantile(double p) { return normal_quantile(p); }
+
+static double ln_censored_expectation(double mu, double sigma, double x_max) {
+  double y_max = (log(x_max) - mu) / sigma;
+  double body = exp(mu + 0.5 * sigma * sigma) * normal_cdf(y_max - sigma);
+  double v = body + x_max * (1.0 - normal_cdf(y_max));
+  return (x_max < v) ? x_max : v;
+}
+
+static double ln_censored_cvar(double mu, double sigma, double x_max, double alpha) {
+  double y_max = (log(x_max) - mu) / sigma;
+  if (alpha >= normal_cdf(y_max)) return x_max;
+  double lo = alpha > 0.0 ? normal_cdf(normal_quantile(alpha) - sigma) : 0.0;
+  double body = exp(mu + 0.5 * sigma * sigma) * (normal_cdf(y_max - sigma) - lo);
+  double v = (body + x_max * (1.0 - normal_cdf(y_max))) / (1.0 - alpha);
+  return (x_max < v) ? x_max : v;
+}
+
+/* predictor.cpp:22-31: noisy_predict with Rng(mix64(seed, id)) */
+static void noisy(double mu, double sigma, uint64_t id, double mu_sd, double ls_sd,
+                  uint64_t seed, double* mu_hat, double* sigma_hat) {
+  rng_t r;
+  rng_seed(&r, tor_mix64(seed, id));
+  double m = mu + mu_sd * rng_normal(&r);
+  double st = log1p(sigma) + ls_sd * rng_normal(&r);
+  double s = expm1(st);
+  *mu_hat = m;
+  *sigma_hat = (s < 1e-6) ? 1e-6 : s; /* std::max(expm1(st), 1e-6) */
+}
+
+/* The run_sim precompute loop (sim.cpp:77-96): predictor (0 oracle, 1 noisy), family (0 logt,
+ * 1 lognormal), CVaR = max(CVaR, E).  samples = the McContext set (logt family). */
+int tor_sim_scores(const double* samples, int N, double nu, const double* mu,
+                   const double* sigma, const uint64_t* ids, const double* x_max, uint64_t n,
+                   int predictor, double mu_sd, double ls_sd, uint64_t seed, int family,
+                   double alpha, double* E, double* C) {
+  double* m = (double*)malloc(sizeof(double) * (n ? n : 1));
+  double* s = (double*)malloc(sizeof(double) * (n ? n : 1));
+  for (uint64_t i = 0; i < n; ++i) {
+    if (predictor == 1) noisy(mu[i], sigma[i], ids[i], mu_sd, ls_sd, seed, &m[i], &s[i]);
+    else { m[i] = mu[i]; s[i] = sigma[i]; }
+  }
+  int rc = 0;
+  if (family == 0) {
+    rc = tor_score(samples, N, nu, m, s, x_max, n, alpha, 0.0, E, C, NULL, NULL, 1);
+  } else {
+    for (uint64_t i = 0; i < n; ++i) {
+      double e = ln_censored_expectation(m[i], s[i], x_max[i]);
+      double c = ln_censored_cvar(m[i], s[i], x_max[i], alpha);
+      E[i] = e;
+      C[i] = (c < e) ? e : c;
+    }
+  }
+  free(m);
+  free(s);
+  return rc;
+}

@@ -80,6 +80,14 @@ int tor_scheduler_script(int policy, int adaptive, double beta_fixed, double bet
                          const int32_t* op, const uint64_t* id, const double* a,
                          const double* b, uint64_t* out, uint64_t* n_out);
 
+/* run_sim's precompute loop (sim.cpp:77-96): predictor 0 oracle / 1 noisy (predictor.cpp:
+ * 15-31), family 0 log-t / 1 log-normal (dist.cpp:191-249), CVaR = max(CVaR, E). */
+int tor_sim_scores(const double* samples, int N, double nu, const double* mu,
+                   const double* sigma, const uint64_t* ids, const double* x_max, uint64_t n,
+                   int predictor, double mu_sd, double ls_sd, uint64_t seed, int family,
+                   double alpha, double* E, double* C);
+double tor_normal_quantile(double p);
+
 #ifdef __cplusplus
 }
 #endif

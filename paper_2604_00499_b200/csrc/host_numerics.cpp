@@ -166,6 +166,41 @@ double t_quantile(double p, double nu) {
   return y;
 }
 
+double normal_quantile(double p) {
+  if (!(p > 0.0 && p < 1.0)) throw std::domain_error("normal_quantile: p must lie in (0, 1)");
+  // Acklam's coefficients (central region a/b, tails c/d)
+  static const double a[6] = {-3.969683028665376e+01, 2.209460984245205e+02,
+                              -2.759285104469687e+02, 1.383577518672690e+02,
+                              -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[5] = {-5.447609879822406e+01, 1.615858368580409e+02,
+                              -1.556989798598866e+02, 6.680131188771972e+01,
+                              -1.328068155288572e+01};
+  static const double c[6] = {-7.784894002430293e-03, -3.223964580411365e-01,
+                              -2.400758277161838e+00, -2.549732539343734e+00,
+                              4.374664141464968e+00, 2.938163982698783e+00};
+  static const double d[4] = {7.784695709041462e-03, 3.224671290700398e-01,
+                              2.445134137142996e+00, 3.754408661907416e+00};
+  auto tail = [&](double q) {
+    return (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+           ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  };
+  constexpr double kLow = 0.02425;
+  double z;
+  if (p < kLow) {
+    z = tail(std::sqrt(-2.0 * std::log(p)));
+  } else if (p <= 1.0 - kLow) {
+    const double q = p - 0.5, r = q * q;
+    z = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1.0);
+  } else {
+    z = -tail(std::sqrt(-2.0 * std::log1p(-p)));
+  }
+  // one Newton-type (Halley) polish against the exact CDF
+  const double e = 0.5 * std::erfc(-z * 0.7071067811865475244) - p;
+  const double u = e * std::sqrt(2.0 * 3.14159265358979323846) * std::exp(0.5 * z * z);
+  return z - u / (1.0 + 0.5 * z * u);
+}
+
 std::vector<double> sample_logt(double mu, double sigma, double nu, size_t n, uint64_t seed) {
   if (sigma < 1e-9) sigma = 1e-9;
   Sampler s(seed);

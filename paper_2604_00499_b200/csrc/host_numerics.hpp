@@ -44,6 +44,10 @@ double t_pdf(double y, double nu);
 double t_cdf(double y, double nu);
 double t_quantile(double p, double nu);
 
+// standard normal quantile: Acklam's rational approximation + one Newton polish
+// (dist.cpp:193-225); host-hoisted for the log-normal family's request-invariant z_alpha
+double normal_quantile(double p);
+
 // sample_logt (dist.cpp:142-147)
 std::vector<double> sample_logt(double mu, double sigma, double nu, size_t n, uint64_t seed);
 

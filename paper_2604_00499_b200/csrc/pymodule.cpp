@@ -37,6 +37,10 @@ const T* ptr_or_null(const py::object& o) {
 
 void* vp(uintptr_t p) { return reinterpret_cast<void*>(p); }
 
+// sim.hpp:24-28 (the simulator's own enums; only the scoring-relevant values)
+enum class PredictorKindPy { Oracle = 0, Noisy = 1 };
+enum class ScoreFamilyPy { LogT = 0, LogNormal = 1 };
+
 }  // namespace
 
 PYBIND11_MODULE(_core, m) {
@@ -396,6 +400,35 @@ PYBIND11_MODULE(_core, m) {
            })
       .def("waiting", [](const GpuQueue& g) { return tie_queue_size(g.q); })
       .def("current_beta", [](const GpuQueue& g) { return tie_queue_current_beta(g.q); });
+
+  py::enum_<PredictorKindPy>(m, "PredictorKind")
+      .value("Oracle", PredictorKindPy::Oracle)
+      .value("Noisy", PredictorKindPy::Noisy);
+  py::enum_<ScoreFamilyPy>(m, "ScoreFamily")
+      .value("LogT", ScoreFamilyPy::LogT)
+      .value("LogNormal", ScoreFamilyPy::LogNormal);
+  m.def(
+      "sim_scores",
+      [](carray<double> mu, carray<double> sigma, carray<uint64_t> ids,
+         carray<uint32_t> max_tokens, const McContext& mc, PredictorKindPy predictor,
+         double mu_sd, double log_sigma_sd, uint64_t seed, ScoreFamilyPy family, double alpha) {
+        const size_t n = (size_t)mu.size();
+        carray<double> E(n), C(n);
+        int rc;
+        {
+          py::gil_scoped_release nogil;
+          rc = tie_sim_scores_host(mc.handle(), mu.data(), sigma.data(), ids.data(),
+                                   max_tokens.data(), n, (int)predictor, mu_sd, log_sigma_sd,
+                                   seed, (int)family, alpha, E.mutable_data(), C.mutable_data());
+        }
+        throw_code(rc);
+        return py::make_tuple(E, C);
+      },
+      py::arg("mu"), py::arg("sigma"), py::arg("ids"), py::arg("max_tokens"), py::arg("mc"),
+      py::arg("predictor") = PredictorKindPy::Oracle, py::arg("mu_sd") = 0.0,
+      py::arg("log_sigma_sd") = 0.0, py::arg("seed") = 0,
+      py::arg("family") = ScoreFamilyPy::LogT, py::arg("alpha") = 0.9,
+      "run_sim's scoring precompute (sim.cpp:77-96) on the GPU: (E, max(CVaR, E)) per request");
 
   m.def("default_context", []() { return (uintptr_t)default_context(); });
   m.def("launch_count", [](bool reset) { return tie_launch_count(reset ? 1 : 0); },

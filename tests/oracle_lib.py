@@ -127,6 +127,21 @@ class Oracle(_Base):
         self._sched = self._fn("scheduler_script", [_i32, _i32, _d, _d, _d, _d, _u64, _p, _p,
                                                     _p, _p, _p, ctypes.POINTER(_u64)])
 
+    def sim_scores(self, mu, sigma, ids, max_tokens, predictor=0, mu_sd=0.0, ls_sd=0.0,
+                   seed=0, family=0, alpha=0.9, samples=None):
+        f = self._fn("sim_scores", [_p, _i32, _d, _p, _p, _p, _p, _u64, _i32, _d, _d, _u64,
+                                    _i32, _d, _p, _p])
+        Y = self.mc_samples() if samples is None else np.ascontiguousarray(samples, np.float64)
+        mu = np.ascontiguousarray(mu, np.float64)
+        sigma = np.ascontiguousarray(sigma, np.float64)
+        ids = np.ascontiguousarray(ids, np.uint64)
+        xm = np.ascontiguousarray(max_tokens, np.float64)
+        E, C = np.empty(len(mu)), np.empty(len(mu))
+        self._check(f(_ptr(Y), len(Y), 3.5, _ptr(mu), _ptr(sigma), _ptr(ids), _ptr(xm),
+                      len(mu), predictor, mu_sd, ls_sd, seed, family, alpha, _ptr(E),
+                      _ptr(C)), "sim_scores")
+        return E, C
+
     def scheduler_script(self, policy, ops, ids, a, b, adaptive=True, beta_fixed=0.1,
                          beta_max=0.5, q_sat=128.0, rebuild_threshold=0.1):
         ops = np.ascontiguousarray(ops, np.int32)
@@ -241,6 +256,20 @@ class RefLib(_Base):
     def logt_loglik(self, x, mu, sigma, nu):
         x = np.ascontiguousarray(x, np.float64)
         return self.logt_loglik_raw(_ptr(x), len(x), mu, sigma, nu)
+
+    def sim_scores(self, mu, sigma, ids, max_tokens, predictor=0, mu_sd=0.0, ls_sd=0.0,
+                   seed=0, family=0, alpha=0.9, threads=None):
+        f = self._fn("sim_scores", [_p, _p, _p, _p, _u64, _i32, _d, _d, _u64, _i32, _d, _p, _p,
+                                    _i32])
+        mu = np.ascontiguousarray(mu, np.float64)
+        sigma = np.ascontiguousarray(sigma, np.float64)
+        ids = np.ascontiguousarray(ids, np.uint64)
+        mt = np.ascontiguousarray(max_tokens, np.uint32)
+        E, C = np.empty(len(mu)), np.empty(len(mu))
+        self._check(f(_ptr(mu), _ptr(sigma), _ptr(ids), _ptr(mt), len(mu), predictor, mu_sd,
+                      ls_sd, seed, family, alpha, _ptr(E), _ptr(C), _threads(threads)),
+                    "sim_scores")
+        return E, C
 
     def scheduler_script(self, policy, ops, ids, a, b, adaptive=True, beta_fixed=0.1,
                          beta_max=0.5, q_sat=128.0, rebuild_threshold=0.1):

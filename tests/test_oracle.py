@@ -152,3 +152,17 @@ def test_scheduler_oracle_vs_reference(oracle, policy, thr):
         ref = R.scheduler_script(policy, ops, ids, a, b, **cfg)
         assert np.array_equal(got, ref), (policy, thr, seed)
         assert len(got) > 50
+
+
+# ---------------------------------------------------------------- run_sim scoring chain
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built (no /root/reference)")
+@pytest.mark.parametrize("predictor,family", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_sim_scores_oracle_vs_reference(oracle, predictor, family):
+    R = RefLib()
+    mu, sg, mt = oracle.gen_workload(3000, seed=5, mu_range=(0.1, 2.7), sigma_range=(0.4, 1.2),
+                                     max_tokens=512)
+    ids = np.arange(3000, dtype=np.uint64) * 3 + 1
+    kw = dict(predictor=predictor, mu_sd=0.4, ls_sd=0.3, seed=11, family=family, alpha=0.9)
+    E1, C1 = oracle.sim_scores(mu, sg, ids, mt, **kw)
+    E2, C2 = R.sim_scores(mu, sg, ids, mt, **kw)
+    assert np.array_equal(E1, E2) and np.array_equal(C1, C2)
