@@ -231,6 +231,7 @@ void tie_ctx_destroy(tie_ctx* ctx) {
   cudaFree(ctx->d_ybucket);
   cudaFree(ctx->d_table);
   cudaFree(ctx->d_tail);
+  cudaFree(ctx->d_bins);
   cudaFree(ctx->d_err);
   cudaFree(ctx->scratch);
   cudaFree(ctx->io);
@@ -348,7 +349,7 @@ double tie_t_cdf(double y, double nu) {
 // ====================================================================== device entry points
 static int score_impl(tie_ctx* ctx, const double* mu, const double* sigma, const void* x_max,
                       bool u32, uint64_t n, double alpha, double beta, double* E, double* C,
-                      double* S, uint64_t* keys, uint32_t* hist, unsigned flags, cudaStream_t s,
+                      double* S, uint64_t* keys, unsigned long long* minmax, unsigned flags, cudaStream_t s,
                       const char* op) {
   if (int rc = check_ctx(ctx)) return rc;
   if (int rc = validate_alpha(alpha)) return rc;
@@ -356,7 +357,7 @@ static int score_impl(tie_ctx* ctx, const double* mu, const double* sigma, const
   DeviceGuard g(ctx->device);
   ctx->err_op = op;
   const cudaError_t e = tie::dev::launch_score(ctx, mu, sigma, x_max, u32, n, alpha, beta, E, C,
-                                               S, keys, hist, flags, s);
+                                               S, keys, minmax, flags, s);
   if (e != cudaSuccess) return cuda_error(e, op);
   return TIE_OK;
 }
@@ -397,7 +398,7 @@ int tie_score_rank(tie_ctx* ctx, const double* mu, const double* sigma,
   const tie::dev::RankPrep prep = tie::dev::rank_prepare(ctx, n, s);
   if (!prep.keys) return set_error(TIE_ECUDA, "tie_score_rank: scratch allocation failed");
   if (int rc = score_impl(ctx, mu, sigma, max_tokens, true, n, alpha, beta, E, cvar, score,
-                          prep.keys, prep.hist, flags, s, "tie_score_rank"))
+                          prep.keys, prep.minmax, flags, s, "tie_score_rank"))
     return rc;
   const cudaError_t e = tie::dev::rank_prepared(ctx, n, order, s);
   if (e != cudaSuccess) return cuda_error(e, "tie_score_rank");
@@ -517,7 +518,7 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
     const cudaError_t e = tie::dev::launch_score(ctx, d_mu + lo, d_sg + lo, d_mt + lo, true, m,
                                                  alpha, beta, nullptr, nullptr,
                                                  d_S ? d_S + lo : nullptr, prep.keys + lo,
-                                                 prep.hist, flags & TIE_SCORE_EXACT, s, lo);
+                                                 prep.minmax, flags & TIE_SCORE_EXACT, s, lo);
     if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
   }
   cudaError_t e = tie::dev::rank_prepared(ctx, n, d_order, s);

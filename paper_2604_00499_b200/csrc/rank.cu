@@ -98,15 +98,13 @@ __device__ __forceinline__ void hist_flush(uint32_t (*h)[kBins], uint32_t* hist)
 }
 
 // key validation + transform (WaitingQueue::push rejects non-finite keys, sched.cpp:60) with
-// the 8 digit histograms accumulated on the way
+// the key range folded into mm (the bucket path's range)
 __global__ void __launch_bounds__(256) keys_from_double_kernel(const double* __restrict__ key,
                                                                uint64_t n,
                                                                uint64_t* __restrict__ out,
-                                                               uint32_t* __restrict__ hist,
+                                                               unsigned long long* mm,
                                                                unsigned long long* err) {
-  __shared__ uint32_t h[kPasses][kBins];
-  for (int i = threadIdx.x; i < kPasses * kBins; i += blockDim.x) (&h[0][0])[i] = 0;
-  __syncthreads();
+  uint64_t lo = ~0ull, hi = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const double x = key[i];
@@ -118,10 +116,10 @@ __global__ void __launch_bounds__(256) keys_from_double_kernel(const double* __r
       k = order_bits(x);
     }
     out[i] = k;
-#pragma unroll
-    for (int p = 0; p < kPasses; ++p) atomicAdd(&h[p][digit_of(k, p)], 1u);
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
   }
-  hist_flush(h, hist);
+  key_range_flush(mm, lo, hi);
 }
 
 // copy u64 keys (ids, or pre-transformed keys) while accumulating the digit histograms
@@ -443,6 +441,271 @@ __global__ void gather_by_id_kernel(Work w, uint64_t n, const uint64_t* __restri
   }
 }
 
+// ====================================================================== bucket path
+// Default dispatch-order sort (K2).  The producer folds the key range
+// [kmin, kmax] (key_range_flush); keys are then bucketed by their top bits above kmin --
+// nb = 2^nb_log2 ~ n/8 buckets, contiguous in the output -- and each bucket is ordered in
+// shared memory:
+//   count   : per-bucket counts (global atomics, one per key)
+//   scan_a/b: exclusive prefix of the counts (bucket bases) + segment starts: segment i
+//             begins at the first bucket boundary >= i*kSegStep, so a segment holds
+//             < kSegStep + (largest bucket) <= kSegCap keys
+//   scatter : (key, index) into its bucket's slot range (order within a bucket arbitrary)
+//   local   : one CTA per segment stages it in shared memory; each key's final position is
+//             its bucket base + #{(key', index') < (key, index) in the bucket}, i.e. the
+//             (key, id) heap order with ties broken by index (== id order).
+// 4 passes over the keys instead of 7-8 radix passes.  A bucket larger than kMaxBucket
+// (massive score ties) makes the local kernel tail-launch the stable LSD path above from the
+// device instead (CUDA dynamic parallelism), so the order stays exact for any input.
+constexpr uint32_t kSegCap = 4096;
+constexpr uint32_t kSegStep = kSegCap / 2;
+constexpr uint32_t kMaxBucket = kSegCap - kSegStep;
+constexpr int kScanThreads = 1024;
+constexpr int kScanPer = 4;
+constexpr uint32_t kScanChunk = kScanThreads * kScanPer;
+constexpr uint32_t kMinBucketsLog2 = 12;  // nb >= kScanChunk
+constexpr uint32_t kMaxBucketsLog2 = 24;
+constexpr int kLocalThreads = 256;
+
+struct Bucket {
+  const uint64_t* keys;    // [n] order-preserving keys
+  uint64_t* tk;            // [n] keys grouped by bucket (aliases the LSD ping-pong buffer)
+  uint32_t* tv;            // [n] their indices
+  uint32_t* count;         // [nb]
+  uint32_t* base;          // [nb + 1] exclusive prefix of count
+  uint32_t* cursor;        // [nb]
+  uint32_t* partial;       // [chunks]
+  uint32_t* seg;           // [nseg + 1]
+  unsigned long long* mm;  // [2]: max(~key), max(key)
+  int* overflow;
+  uint32_t nb_log2, nb, chunks, nseg;
+};
+
+struct KeyRange {
+  uint64_t kmin;
+  uint32_t shift;
+};
+
+__device__ __forceinline__ KeyRange key_range(const Bucket& b) {
+  const uint64_t kmin = ~(uint64_t)b.mm[0];
+  const uint64_t span = (uint64_t)b.mm[1] - kmin;
+  const uint32_t bits = span ? 64u - (uint32_t)__clzll((long long)span) : 0u;
+  return {kmin, bits > b.nb_log2 ? bits - b.nb_log2 : 0u};
+}
+
+__device__ __forceinline__ uint32_t bucket_of(const KeyRange& r, uint64_t k) {
+  return (uint32_t)((k - r.kmin) >> r.shift);  // span >> shift < nb
+}
+
+// count / scatter: each thread takes kStreamItems keys of a 256*kStreamItems tile (coalesced,
+// all loads issued before the first atomic, so one L2 round trip is paid per batch)
+constexpr int kStreamItems = 4;
+constexpr uint64_t kStreamTile = 256 * kStreamItems;
+
+__global__ void __launch_bounds__(256) bucket_count_kernel(Bucket b, uint64_t n) {
+  const KeyRange r = key_range(b);
+  const uint64_t t0 = (uint64_t)blockIdx.x * kStreamTile + threadIdx.x;
+  uint64_t k[kStreamItems];
+#pragma unroll
+  for (int j = 0; j < kStreamItems; ++j) {
+    const uint64_t i = t0 + (uint64_t)j * 256;
+    k[j] = i < n ? b.keys[i] : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < kStreamItems; ++j)
+    if (t0 + (uint64_t)j * 256 < n) atomicAdd(b.count + bucket_of(r, k[j]), 1u);
+}
+
+// block-wide reduction / exclusive scan over kScanThreads threads
+__device__ __forceinline__ uint32_t scan_block_sum(uint32_t v, uint32_t* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  uint32_t t = lane < (kScanThreads / 32) ? sh[lane] : 0u;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  __syncthreads();
+  return t;
+}
+
+__device__ __forceinline__ uint32_t scan_block_excl(uint32_t v, uint32_t* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = sh[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    sh[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t r = x - v + (warp ? sh[warp - 1] : 0u);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kScanThreads) bucket_scan_a_kernel(Bucket b) {
+  __shared__ uint32_t sh[32];
+  const uint32_t i0 = blockIdx.x * kScanChunk + threadIdx.x * kScanPer;
+  const uint4 q = *reinterpret_cast<const uint4*>(b.count + i0);
+  const uint32_t t = scan_block_sum(q.x + q.y + q.z + q.w, sh);
+  if (threadIdx.x == 0) b.partial[blockIdx.x] = t;
+}
+
+// bucket boundary `v` (= base of some bucket) preceded by boundary `vprev`: it starts every
+// segment i with vprev < i*kSegStep <= v.  first: the boundary of bucket 0 (vprev = -1).
+__device__ __forceinline__ void claim_segments(const Bucket& b, uint32_t vprev, uint32_t v,
+                                               bool first) {
+  const uint32_t lo = first ? 0u : vprev / kSegStep + 1u;
+  const uint32_t hi = min(v / kSegStep, b.nseg - 1u);
+  if (hi > lo + 1u) {  // a bucket spanning > kSegStep keys: the local sort cannot hold it
+    *b.overflow = 1;
+    return;
+  }
+  for (uint32_t i = lo; i <= hi; ++i) b.seg[i] = v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) bucket_scan_b_kernel(Bucket b, uint64_t n) {
+  __shared__ uint32_t sh[32];
+  const uint32_t c = blockIdx.x;
+  uint32_t acc = 0;
+  for (uint32_t j = threadIdx.x; j < c; j += kScanThreads) acc += b.partial[j];
+  const uint32_t prefix = scan_block_sum(acc, sh);
+  const uint32_t i0 = c * kScanChunk + threadIdx.x * kScanPer;
+  const uint4 q = *reinterpret_cast<const uint4*>(b.count + i0);
+  const uint32_t cnt[4] = {q.x, q.y, q.z, q.w};
+  uint32_t v = prefix + scan_block_excl(q.x + q.y + q.z + q.w, sh);
+  uint32_t vprev = i0 ? v - b.count[i0 - 1] : 0u;
+#pragma unroll
+  for (int j = 0; j < kScanPer; ++j) {
+    const uint32_t bi = i0 + j;
+    b.base[bi] = v;
+    b.cursor[bi] = v;
+    if (cnt[j] > kMaxBucket) *b.overflow = 1;
+    if (bi == 0 || v != vprev) claim_segments(b, vprev, v, bi == 0);
+    vprev = v;
+    v += cnt[j];
+  }
+  if (i0 + kScanPer == b.nb) {  // the sentinel boundary (v == n)
+    b.base[b.nb] = v;
+    if (v != vprev) claim_segments(b, vprev, v, false);
+    b.seg[b.nseg] = (uint32_t)n;
+  }
+}
+
+__global__ void __launch_bounds__(256) bucket_scatter_kernel(Bucket b, uint64_t n) {
+  if (*(volatile int*)b.overflow) return;
+  const KeyRange r = key_range(b);
+  const uint64_t t0 = (uint64_t)blockIdx.x * kStreamTile + threadIdx.x;
+  uint64_t k[kStreamItems];
+  uint32_t p[kStreamItems];
+#pragma unroll
+  for (int j = 0; j < kStreamItems; ++j) {
+    const uint64_t i = t0 + (uint64_t)j * 256;
+    k[j] = i < n ? b.keys[i] : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < kStreamItems; ++j)
+    if (t0 + (uint64_t)j * 256 < n) p[j] = atomicAdd(b.cursor + bucket_of(r, k[j]), 1u);
+#pragma unroll
+  for (int j = 0; j < kStreamItems; ++j) {
+    const uint64_t i = t0 + (uint64_t)j * 256;
+    if (i < n) {
+      b.tk[p[j]] = k[j];
+      b.tv[p[j]] = (uint32_t)i;
+    }
+  }
+}
+
+__global__ void zero_kernel(uint4* p, uint64_t n16) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
+    p[i] = make_uint4(0, 0, 0, 0);
+}
+
+struct Fallback {
+  Work w;           // LSD state (its metadata zeroed here, on the device)
+  uint4* meta;
+  uint64_t meta16;
+  unsigned grid;    // grid of the streaming helper kernels
+};
+
+// The stable LSD path (histograms, plan, digit passes, identity case) as device-side tail
+// launches: they run in order after the launching grid, before anything queued behind it.
+__device__ void lsd_tail_launch(const Fallback& f, const uint64_t* keys, uint64_t n,
+                                const uint64_t* ids, uint64_t* order) {
+  zero_kernel<<<f.grid, 256, 0, cudaStreamTailLaunch>>>(f.meta, f.meta16);
+  copy_hist_kernel<<<f.grid, 256, 0, cudaStreamTailLaunch>>>(
+      keys, n, keys == f.w.k[0] ? nullptr : f.w.k[0], f.w.hist);
+  plan_kernel<<<1, kThreads, 0, cudaStreamTailLaunch>>>(f.w.hist, n, f.w.plan);
+  for (int p = 0; p < kPasses; ++p)
+    onesweep_kernel<16><<<f.w.tiles, kThreads, sizeof(PassSmem<16>), cudaStreamTailLaunch>>>(
+        f.w, n, p, 0, ids, order);
+  identity_order_kernel<<<f.grid, 256, 0, cudaStreamTailLaunch>>>(f.w, n, ids, order, 0);
+}
+
+__global__ void __launch_bounds__(kLocalThreads, 4) bucket_local_kernel(Bucket b, uint64_t n,
+                                                                     const uint64_t* __restrict__ ids,
+                                                                     uint64_t* __restrict__ order,
+                                                                     Fallback f) {
+  if (*(volatile int*)b.overflow) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) lsd_tail_launch(f, b.keys, n, ids, order);
+    return;
+  }
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + kSegCap);
+  constexpr int kItems = kSegCap / kLocalThreads;
+  const uint32_t s0 = b.seg[blockIdx.x], s1 = b.seg[blockIdx.x + 1];
+  const uint32_t m = s1 - s0;  // <= kSegCap
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const uint32_t j = threadIdx.x + it * kLocalThreads;
+    if (j < m) {
+      sk[j] = b.tk[s0 + j];
+      sv[j] = b.tv[s0 + j];
+    }
+  }
+  __syncthreads();
+  const KeyRange r = key_range(b);
+  // every item's bucket bounds fetched up front (independent L2 loads, one round trip)
+  uint32_t lo[kItems], hi[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const uint32_t j = threadIdx.x + it * kLocalThreads;
+    if (j < m) {
+      const uint32_t bk = bucket_of(r, sk[j]);
+      lo[it] = b.base[bk];
+      hi[it] = b.base[bk + 1];
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const uint32_t j = threadIdx.x + it * kLocalThreads;
+    if (j < m) {
+      const uint64_t k = sk[j];
+      const uint32_t v = sv[j];
+      uint32_t rank = 0;
+      for (uint32_t q = lo[it] - s0; q < hi[it] - s0; ++q) {
+        const uint64_t kq = sk[q];
+        rank += (kq < k) | ((kq == k) & (sv[q] < v));
+      }
+      order[lo[it] + rank] = ids ? ids[v] : (uint64_t)v;
+    }
+  }
+}
+
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 int items_for(uint64_t) { return 16; }
@@ -450,19 +713,31 @@ int items_for(uint64_t) { return 16; }
 struct Layout {
   size_t k0, k1, v0, v1, hist, plan, status, gstatus, gsum, gdone, counter, flag, k2, k3, v3,
       meta_begin, meta_end, total;
-  uint32_t tiles;
+  // bucket path: [bzero_begin, bzero_end) = count, mm, overflow (zeroed once per sort)
+  size_t count, mm, overflow, base, cursor, partial, seg, bzero_begin, bzero_end;
+  uint32_t tiles, nb_log2, nseg;
 };
+
+uint32_t bucket_log2(uint64_t n) {
+  uint32_t l = 0;
+  while (l < 63 && (1ull << l) < (n + 1) / 2) ++l;  // ~2-4 keys per occupied bucket
+  return std::min(std::max(l, kMinBucketsLog2), kMaxBucketsLog2);
+}
 
 Layout layout(uint64_t n, bool with_ids) {
   Layout L{};
   const uint64_t tile_keys = (uint64_t)kThreads * items_for(n);
   L.tiles = (uint32_t)std::max<uint64_t>(1, (n + tile_keys - 1) / tile_keys);
+  L.nb_log2 = bucket_log2(n);
+  L.nseg = (uint32_t)std::max<uint64_t>(1, (n + kSegStep - 1) / kSegStep);
+  const uint64_t nb = 1ull << L.nb_log2;
   size_t off = 0;
   L.k0 = off; off += align_up(8 * n);
   L.k1 = off; off += align_up(8 * n);
   L.v0 = off; off += align_up(4 * n);
   L.v1 = off; off += align_up(4 * n);
-  // per-sort metadata, zeroed by ONE memset per sort: histograms, look-back status, counters
+  // LSD metadata, zeroed by ONE memset (or, as the bucket path's fallback, on the device):
+  // histograms, look-back status, counters
   L.meta_begin = off;
   L.hist = off; off += align_up(4 * kPasses * kBins);
   L.status = off; off += align_up(8ull * kPasses * L.tiles * kBins);
@@ -474,11 +749,39 @@ Layout layout(uint64_t n, bool with_ids) {
   L.meta_end = off;
   L.plan = off; off += align_up(sizeof(Plan));
   L.flag = off; off += align_up(sizeof(int));
+  L.bzero_begin = off;
+  L.count = off; off += align_up(4 * nb);
+  L.mm = off; off += align_up(16);
+  L.overflow = off; off += align_up(sizeof(int));
+  L.bzero_end = off;
+  L.base = off; off += align_up(4 * (nb + 1));
+  L.cursor = off; off += align_up(4 * nb);
+  L.partial = off; off += align_up(4 * (nb / kScanChunk));
+  L.seg = off; off += align_up(4 * ((uint64_t)L.nseg + 1));
   L.k2 = off; off += with_ids ? align_up(8 * n) : 0;  // transformed keys (id path)
   L.k3 = off; off += with_ids ? align_up(8 * n) : 0;  // keys gathered into id order
   L.v3 = off; off += with_ids ? align_up(4 * n) : 0;  // the id-order permutation
   L.total = off;
   return L;
+}
+
+Bucket make_bucket(char* base, const Layout& L, const uint64_t* keys) {
+  Bucket b;
+  b.keys = keys;
+  b.tk = (uint64_t*)(base + L.k1);  // the LSD fallback runs only when the scatter did not
+  b.tv = (uint32_t*)(base + L.v0);
+  b.count = (uint32_t*)(base + L.count);
+  b.base = (uint32_t*)(base + L.base);
+  b.cursor = (uint32_t*)(base + L.cursor);
+  b.partial = (uint32_t*)(base + L.partial);
+  b.seg = (uint32_t*)(base + L.seg);
+  b.mm = (unsigned long long*)(base + L.mm);
+  b.overflow = (int*)(base + L.overflow);
+  b.nb_log2 = L.nb_log2;
+  b.nb = 1u << L.nb_log2;
+  b.chunks = b.nb / kScanChunk;
+  b.nseg = L.nseg;
+  return b;
 }
 
 Work make_work(char* base, const Layout& L) {
@@ -543,6 +846,48 @@ cudaError_t sort_passes(tie_ctx* ctx, Work& w, uint64_t n, bool explicit_vals,
   return cudaGetLastError();
 }
 
+// count -> scan -> scatter -> local sort over keys whose range is already folded into the
+// bucket state (zeroed count / mm / overflow).  Emits the dispatch order.
+cudaError_t bucket_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_t* keys,
+                        uint64_t n, const uint64_t* ids, uint64_t* order, cudaStream_t s) {
+  static bool attr = false;
+  const size_t local_smem = (size_t)kSegCap * 12;
+  if (!attr) {  // also covers the device-side (fallback) launches
+    cudaFuncSetAttribute(onesweep_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(PassSmem<16>));
+    cudaFuncSetAttribute(bucket_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)local_smem);
+    attr = true;
+  }
+  Bucket b = make_bucket(base, L, keys);
+  const int sms = sm_count(ctx->device);
+  const unsigned g = (unsigned)((n + kStreamTile - 1) / kStreamTile);
+  {
+    ProfScope p(ctx, "rank.count", s);
+    bucket_count_kernel<<<g, 256, 0, s>>>(b, n);
+  }
+  {
+    ProfScope p(ctx, "rank.scan", s);
+    bucket_scan_a_kernel<<<b.chunks, kScanThreads, 0, s>>>(b);
+    bucket_scan_b_kernel<<<b.chunks, kScanThreads, 0, s>>>(b, n);
+  }
+  {
+    ProfScope p(ctx, "rank.scatter", s);
+    bucket_scatter_kernel<<<g, 256, 0, s>>>(b, n);
+  }
+  Fallback f;
+  f.w = make_work(base, L);
+  f.meta = (uint4*)(base + L.meta_begin);
+  f.meta16 = (L.meta_end - L.meta_begin) / 16;
+  f.grid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 4);
+  {
+    ProfScope p(ctx, "rank.local", s);
+    bucket_local_kernel<<<b.nseg, kLocalThreads, local_smem, s>>>(b, n, ids, order, f);
+  }
+  capi::count_launch(5);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 size_t rank_scratch_bytes(uint64_t n, bool with_ids) { return layout(n, with_ids).total; }
@@ -552,19 +897,19 @@ RankPrep rank_prepare(tie_ctx* ctx, uint64_t n, cudaStream_t s) {
   const Layout L = layout(n, false);
   char* base = (char*)capi::scratch(ctx, L.total, s);
   if (!base) return r;
-  cudaMemsetAsync(base + L.meta_begin, 0, L.meta_end - L.meta_begin, s);
+  cudaMemsetAsync(base + L.bzero_begin, 0, L.bzero_end - L.bzero_begin, s);
   r.keys = (uint64_t*)(base + L.k0);
-  r.hist = (uint32_t*)(base + L.hist);
+  r.minmax = (unsigned long long*)(base + L.mm);
   return r;
 }
 
 cudaError_t rank_prepared(tie_ctx* ctx, uint64_t n, uint64_t* order, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
+  if (n >= (1ull << 32)) return cudaErrorInvalidValue;  // u32 values / bucket positions
   const Layout L = layout(n, false);
   char* base = (char*)capi::scratch(ctx, L.total, s);
   if (!base) return cudaErrorMemoryAllocation;
-  Work w = make_work(base, L);
-  return sort_passes(ctx, w, n, false, nullptr, order, s);
+  return bucket_sort(ctx, base, L, (const uint64_t*)(base + L.k0), n, nullptr, order, s);
 }
 
 cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n,
@@ -578,15 +923,16 @@ cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* ids, ui
   const int sms = sm_count(ctx->device);
   const unsigned egrid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 4);
   const size_t meta = L.meta_end - L.meta_begin;
-  cudaMemsetAsync(base + L.meta_begin, 0, meta, s);
+  cudaMemsetAsync(base + L.bzero_begin, 0, L.bzero_end - L.bzero_begin, s);
 
   uint64_t* tkeys = ids ? (uint64_t*)(base + L.k2) : w.k[0];
   {
     ProfScope p(ctx, "rank.keys", s);
-    keys_from_double_kernel<<<egrid, 256, 0, s>>>(key, n, tkeys, w.hist, ctx->d_err);
+    keys_from_double_kernel<<<egrid, 256, 0, s>>>(key, n, tkeys,
+                                                  (unsigned long long*)(base + L.mm), ctx->d_err);
     capi::count_launch();
   }
-  if (!ids) return sort_passes(ctx, w, n, false, nullptr, order, s);
+  if (!ids) return bucket_sort(ctx, base, L, tkeys, n, nullptr, order, s);
 
   cudaMemsetAsync(w.flag, 0, sizeof(int), s);
   ids_sorted_kernel<<<egrid, 256, 0, s>>>(ids, n, w.flag);
@@ -595,11 +941,10 @@ cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* ids, ui
   cudaMemcpyAsync(&unsorted, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return e;
-  if (!unsorted) {  // ids ascending: (key, index) order == (key, id) order
-    cudaMemcpyAsync(w.k[0], tkeys, 8 * n, cudaMemcpyDeviceToDevice, s);
-    return sort_passes(ctx, w, n, false, ids, order, s);
-  }
-  // unsorted ids: stable sort of (id, index) first; the key sort then starts from id order
+  // ids ascending: (key, index) order == (key, id) order
+  if (!unsorted) return bucket_sort(ctx, base, L, tkeys, n, ids, order, s);
+  // unsorted ids: stable LSD sort of (id, index) first; the stable LSD key sort then starts
+  // from id order
   cudaMemsetAsync(base + L.meta_begin, 0, meta, s);
   copy_hist_kernel<<<egrid, 256, 0, s>>>(ids, n, w.k[0], w.hist);
   capi::count_launch();

@@ -23,6 +23,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
+#include <limits>
 #include <vector>
 
 #include "tdist.cuh"
@@ -259,6 +261,7 @@ struct LogMemo {
   }
 };
 
+template <bool kRecip = false>
 __device__ __forceinline__ uint32_t epilogue(const ScoreParams& p, double xm, double T,
                                              bool saturated, double s_a, double s_all, Out& o);
 
@@ -303,11 +306,14 @@ __device__ __forceinline__ uint32_t score_one(const ScoreParams& p, const double
 }
 
 // E, CVaR and score from the two partial sums and T (dist.cpp:163-189, sim.cpp:94,
-// sched.cpp:19-26), operation order as the reference's (no FMA contraction).
+// sched.cpp:19-26), operation order as the reference's (no FMA contraction).  kRecip (the
+// moment-table path, whose sums are not the reference's sequential ones anyway): the two
+// divisions by N and (1 - alpha) become products with host reciprocals (<= 1 ulp).
+template <bool kRecip>
 __device__ __forceinline__ uint32_t epilogue(const ScoreParams& p, double xm, double T,
                                              bool saturated, double s_a, double s_all, Out& o) {
   const double Nd = (double)p.N;
-  const double psi_cap = s_all / Nd;
+  const double psi_cap = kRecip ? __dmul_rn(s_all, p.inv_N) : s_all / Nd;
   const double cm = __dsub_rn(1.0, T);
   double E = __dadd_rn(psi_cap, __dmul_rn(xm, cm));
   E = (xm < E) ? xm : E;  // std::min(v, x_max)
@@ -315,9 +321,9 @@ __device__ __forceinline__ uint32_t epilogue(const ScoreParams& p, double xm, do
   if (saturated) {
     C = xm;
   } else {
-    const double psi_a = p.alpha > 0.0 ? s_a / Nd : 0.0;
-    const double v = __dadd_rn(__dsub_rn(psi_cap, psi_a), __dmul_rn(xm, cm)) /
-                     __dsub_rn(1.0, p.alpha);
+    const double psi_a = p.alpha > 0.0 ? (kRecip ? __dmul_rn(s_a, p.inv_N) : s_a / Nd) : 0.0;
+    const double num = __dadd_rn(__dsub_rn(psi_cap, psi_a), __dmul_rn(xm, cm));
+    const double v = kRecip ? __dmul_rn(num, p.inv_1ma) : num / __dsub_rn(1.0, p.alpha);
     C = (xm < v) ? xm : v;
   }
   if (p.raw) {  // per-item censored_expectation / censored_cvar semantics
@@ -338,8 +344,9 @@ __device__ __forceinline__ uint32_t epilogue(const ScoreParams& p, double xm, do
 }
 
 // keys != nullptr: also emit the rank key (order-preserving u64 image of the score, as in
-// rank.cu) and, with hist != nullptr, accumulate its 8 radix-digit histograms so the fused
-// score+rank path needs no separate histogram pass over the keys.
+// rank.cu) and, with minmax != nullptr, fold the key range into minmax[0] (max of ~key) and
+// minmax[1] (max key) -- the bucket sort's range, so the fused score+rank path needs no
+// separate pass over the keys before bucketing.
 template <typename XT, bool kExact>
 __global__ void __launch_bounds__(256, 2) score_kernel(const __grid_constant__ ScoreParams p,
                                                     const double* __restrict__ mu,
@@ -348,18 +355,16 @@ __global__ void __launch_bounds__(256, 2) score_kernel(const __grid_constant__ S
                                                     double* __restrict__ E, double* __restrict__ C,
                                                     double* __restrict__ S,
                                                     uint64_t* __restrict__ keys,
-                                                    uint32_t* __restrict__ hist) {
+                                                    unsigned long long* __restrict__ minmax) {
   extern __shared__ double sY[];
-  __shared__ uint32_t h[8][256];
   const double* Ys = p.Y;
   if (kExact && p.N <= 12288) {  // stage the sample set once per CTA (<= 96 KB)
     for (int i = threadIdx.x; i < p.N; i += blockDim.x) sY[i] = p.Y[i];
     Ys = sY;
   }
-  if (hist)
-    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
   LogMemo lnx;
+  uint64_t kmin = ~0ull, kmax = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // software pipeline: the next request's inputs are loaded while this one is scored
@@ -389,17 +394,11 @@ __global__ void __launch_bounds__(256, 2) score_kernel(const __grid_constant__ S
       const uint64_t k =
           why == kOk ? ((uint64_t)__double_as_longlong(o.S) | (1ull << 63)) : ~0ull;
       keys[i] = k;
-      if (hist) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) atomicAdd(&h[q][(k >> (8 * q)) & 255], 1u);
-      }
+      kmin = k < kmin ? k : kmin;
+      kmax = k > kmax ? k : kmax;
     }
   }
-  if (hist) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x)
-      if ((&h[0][0])[i]) atomicAdd(hist + i, (&h[0][0])[i]);
-  }
+  if (minmax) key_range_flush(minmax, kmin, kmax);
 }
 
 // ------------------------------------------------------------------ warp-cooperative path
@@ -456,6 +455,78 @@ __device__ __forceinline__ double slab_horner(const double* slab, double x) {
   return acc;
 }
 
+// Stage two 64-byte rows per lane (a: tail-mass row, b: sample-bin entry) in ONE round of
+// loads: 64 rows x 4 16-byte chunks, 8 per lane, consecutive lanes on consecutive chunks.
+// Lane l's rows land at slab[l*kSlabStride + 0..7] (a) and [.. + 8..15] (b).
+__device__ __forceinline__ void stage_pair(const double* a, const double* b, double* slab,
+                                           const double** ptrs) {
+  const int lane = threadIdx.x & 31;
+  ptrs[2 * lane] = a;
+  ptrs[2 * lane + 1] = b;
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double2 v[4];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int c = (h * 4 + it) * 32 + lane;
+      const double* rp = ptrs[c >> 2];
+      v[it] =
+          rp ? __ldg(reinterpret_cast<const double2*>(rp) + (c & 3)) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int c = (h * 4 + it) * 32 + lane, r = c >> 2;
+      *reinterpret_cast<double2*>(slab + (r >> 1) * kSlabStride + (r & 1) * 8 + 2 * (c & 3)) =
+          v[it];
+    }
+  }
+  __syncwarp();
+}
+
+template <int R>
+__device__ __forceinline__ double smem_horner(const double* row, double x) {
+  const double2* r2 = reinterpret_cast<const double2*>(row);
+  double2 c = r2[R / 2 - 1];
+  double acc = fma(c.y, x, c.x);
+#pragma unroll
+  for (int j = R / 2 - 2; j >= 0; --j) {
+    c = r2[j];
+    acc = fma(acc, x, c.y);
+    acc = fma(acc, x, c.x);
+  }
+  return acc;
+}
+
+// k = #{Y_i <= y} for Y[0] <= y < Y[N-1] from a staged sample-bin entry
+__device__ __noinline__ uint32_t bin_search_slow(const double* __restrict__ Y, uint32_t lo,
+                                                 uint32_t hi, double y) {
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (y < Y[mid]) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint32_t bin_cut(const ScoreParams& p, const double* ent, double y) {
+  const uint64_t head = (uint64_t)__double_as_longlong(ent[0]);
+  const uint32_t kstart = (uint32_t)head, cnt = (uint32_t)(head >> 32);
+  uint32_t k = kstart;
+#pragma unroll
+  for (int j = 0; j < kBinInline; ++j) k += ent[1 + j] <= y ? 1u : 0u;  // pads are +inf
+  if (cnt > (uint32_t)kBinInline && k == kstart + kBinInline)
+    k = bin_search_slow(p.Y, kstart + kBinInline, kstart + cnt, y);
+  return k;
+}
+
+// Default score kernel (moment tables).  Persistent CTAs, one warp per 32 consecutive
+// requests; per request the dependent chain is
+//   inputs (prefetched one iteration ahead) -> y_max -> {tail-mass row, sample-bin entry}
+//   (one staged round of gathers) -> moment row at k_max (one staged gather) -> epilogue,
+// with the k_alpha rows of every sigma grid point (request-invariant) resident in shared
+// memory for the whole kernel.
+constexpr int kKaMaxG = 256;  // grid points whose k_alpha rows fit the smem budget
+
 template <typename XT>
 __global__ void __launch_bounds__(256, 3) score_coop_kernel(const __grid_constant__ ScoreParams p,
                                                          const double* __restrict__ mu,
@@ -465,25 +536,47 @@ __global__ void __launch_bounds__(256, 3) score_coop_kernel(const __grid_constan
                                                          double* __restrict__ C,
                                                          double* __restrict__ S,
                                                          uint64_t* __restrict__ keys,
-                                                         uint32_t* __restrict__ hist) {
-  __shared__ uint32_t h[8][256];
+                                                         unsigned long long* __restrict__ minmax) {
   __shared__ __align__(16) double slab_all[8][32 * kSlabStride];
-  __shared__ const double* ptr_all[8][32];
+  __shared__ const double* ptr_all[8][64];
+  extern __shared__ __align__(16) double ka_rows[];  // [G][kSlabStride] when G <= kKaMaxG
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* slab = slab_all[wib];
   const double** ptrs = ptr_all[wib];
-  if (hist)
-    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+  const bool ka_smem = p.G <= kKaMaxG && p.k_alpha > 0;
+  if (ka_smem) {
+    for (int c = threadIdx.x; c < p.G * (kMoments / 2); c += blockDim.x) {
+      const int g = c / (kMoments / 2), sub = c % (kMoments / 2);
+      const double2 v = __ldg(reinterpret_cast<const double2*>(
+                                  p.table + ((size_t)g * (p.N + 1) + p.k_alpha) * kMoments) +
+                              sub);
+      *reinterpret_cast<double2*>(ka_rows + g * kSlabStride + 2 * sub) = v;
+    }
+  }
   __syncthreads();
   LogMemo lnx;
+  uint64_t kmin = ~0ull, kmax = 0;
   const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t base = warp0 * 32; base < n; base += nwarps * 32) {  // warp-uniform loop
+  uint64_t base = warp0 * 32;
+  double nm = 0.0, nsig = 1.0, nxm = 1.0;
+  if (base + lane < n) {
+    nm = mu[base + lane];
+    nsig = sigma[base + lane];
+    nxm = (double)xmax[base + lane];
+  }
+  for (; base < n; base += nwarps * 32) {  // warp-uniform loop
     const uint64_t i = base + lane;
     const bool active = i < n;
-    const double m = active ? mu[i] : 0.0;
-    const double sig = active ? sigma[i] : 1.0;
-    const double xm = active ? (double)xmax[i] : 1.0;
+    const double m = nm, sig = nsig, xm = nxm;
+    {  // prefetch the next iteration's inputs
+      const uint64_t j = i + nwarps * 32;
+      if (j < n) {
+        nm = mu[j];
+        nsig = sigma[j];
+        nxm = (double)xmax[j];
+      }
+    }
     // LogTParams / CensoredLogT validation (dist.cpp:108-120)
     uint32_t why = kOk;
     if (!isfinite(m)) why = kMuNotFinite;
@@ -492,19 +585,26 @@ __global__ void __launch_bounds__(256, 3) score_coop_kernel(const __grid_constan
     const bool ok = active && why == kOk;
     const double sg = ok ? (sig < 1e-9 ? 1e-9 : sig) : 1.0;
     const double y_max = ok ? __dsub_rn(lnx(xm), m) / sg : 0.0;
-    // T(y_max): tail-mass row (staged) or, beyond the sample range, the continued fraction
+    // round 1: tail-mass row (T) and sample-bin entry (k_max), gathered together
     const double ay = fabs(y_max);
     const bool tail_tab = ok && ay < p.t_ymax;
     const int tb = tail_tab ? min((int)(ay * p.t_inv_w), kTailBuckets - 1) : 0;
-    stage_rows<kTailCoef>(tail_tab ? p.tail + (size_t)tb * kTailCoef : nullptr, slab, ptrs);
+    const bool in_range = ok && y_max >= p.y0 && y_max < p.yN;
+    const double* ent =
+        in_range ? p.bins + (size_t)sample_bin((uint64_t)__double_as_longlong(y_max), p.bin_e0,
+                                               p.bin_m, p.bin_mid) * kBinEntry
+                 : nullptr;
+    stage_pair(tail_tab ? p.tail + (size_t)tb * kTailCoef : nullptr, ent, slab, ptrs);
+    const double* my = slab + lane * kSlabStride;
     double T = 0.5;
     if (tail_tab) {
-      const double v = slab_horner<kTailCoef>(slab, ay - ((double)tb + 0.5) * p.t_w);
+      const double v = smem_horner<kTailCoef>(my, ay - ((double)tb + 0.5) * p.t_w);
       T = y_max >= 0.0 ? __dsub_rn(1.0, v) : v;  // dist.cpp:80
     } else if (ok) {
       T = t_cdf_slow(p.td, y_max);
     }
-    const uint32_t k_max = ok ? cut_index(p, p.Y, y_max) : 0u;
+    uint32_t k_max = 0;
+    if (ok) k_max = in_range ? bin_cut(p, my + 8, y_max) : (y_max >= p.yN ? (uint32_t)p.N : 0u);
     const int g = ok ? __double2int_rn(sg * kGridInvH) : 0;
     const bool use_table = ok && g < p.G && fabs(m) <= 700.0;
     const double delta = sg - g * kGridH;  // exact: h is a power of two
@@ -512,14 +612,21 @@ __global__ void __launch_bounds__(256, 3) score_coop_kernel(const __grid_constan
     const bool saturated = p.alpha >= T;  // censored_cvar case 1 (dist.cpp:187)
     const uint32_t k_a = saturated ? 0u : p.k_alpha;
     __syncwarp();
+    // round 2: the moment row at k_max
     stage_rows<kMoments>(use_table && k_max ? gbase + (size_t)k_max * kMoments : nullptr, slab,
                          ptrs);
     const double F_all = slab_horner<kMoments>(slab, delta);
     __syncwarp();
-    stage_rows<kMoments>(use_table && k_a ? gbase + (size_t)k_a * kMoments : nullptr, slab,
-                         ptrs);
-    const double F_a = slab_horner<kMoments>(slab, delta);
-    __syncwarp();
+    double F_a = 0.0;
+    if (use_table && k_a) {
+      if (ka_smem) {
+        F_a = smem_horner<kMoments>(ka_rows + g * kSlabStride, delta);
+      } else {
+        Row row_a;
+        load_row(gbase + (size_t)k_a * kMoments, row_a);
+        F_a = horner(row_a, delta);
+      }
+    }
     Out o;
     if (ok) {
       double s_a = 0.0, s_all = 0.0;
@@ -527,10 +634,11 @@ __global__ void __launch_bounds__(256, 3) score_coop_kernel(const __grid_constan
         const double em = exp(m);
         s_all = k_max ? em * F_all : 0.0;
         s_a = k_a ? em * F_a : 0.0;
+        why = epilogue<true>(p, xm, T, saturated, s_a, s_all, o);
       } else {
         exact_sums_slow(p.Y, m, sg, k_a, k_max, &s_a, &s_all);
+        why = epilogue<false>(p, xm, T, saturated, s_a, s_all, o);
       }
-      why = epilogue(p, xm, T, saturated, s_a, s_all, o);
     }
     if (!active) continue;
     if (why != kOk) {
@@ -544,17 +652,11 @@ __global__ void __launch_bounds__(256, 3) score_coop_kernel(const __grid_constan
       const uint64_t k =
           why == kOk ? ((uint64_t)__double_as_longlong(o.S) | (1ull << 63)) : ~0ull;
       keys[i] = k;
-      if (hist) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) atomicAdd(&h[q][(k >> (8 * q)) & 255], 1u);
-      }
+      kmin = k < kmin ? k : kmin;
+      kmax = k > kmax ? k : kmax;
     }
   }
-  if (hist) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x)
-      if ((&h[0][0])[i]) atomicAdd(hist + i, (&h[0][0])[i]);
-  }
+  if (minmax) key_range_flush(minmax, kmin, kmax);
 }
 
 int sm_count(int device) {
@@ -592,6 +694,43 @@ cudaError_t build_context_tables(tie_ctx* ctx) {
   if ((e = cudaMemcpy(ctx->d_ybucket, yb.data(), sizeof(uint32_t) * yb.size(),
                       cudaMemcpyHostToDevice)) != cudaSuccess)
     return e;
+  // sample-bin index (kBinEntry in tie_internal.cuh)
+  if (N > 0) {
+    auto bits = [](double x) {
+      uint64_t u;
+      std::memcpy(&u, &x, 8);
+      return u;
+    };
+    const double maxabs = std::max(std::fabs(Y.front()), std::fabs(Y.back()));
+    const uint32_t etop = (uint32_t)(bits(maxabs) >> 52) & 0x7ffu;
+    const uint32_t e0 = std::min<uint32_t>(1023u - 12u, etop);
+    uint32_t m = 10;
+    while (m > 0 && ((uint64_t)(etop - e0 + 1) << m) > (1u << 19)) --m;
+    ctx->bin_e0 = e0;
+    ctx->bin_m = m;
+    ctx->bin_mid = (etop - e0 + 1) << m;
+    const size_t nbins = 2 * (size_t)ctx->bin_mid + 1;
+    std::vector<uint32_t> cnt(nbins, 0);
+    std::vector<uint32_t> first(nbins, 0);
+    for (int i = N - 1; i >= 0; --i) {
+      const uint32_t b = sample_bin(bits(Y[i]), e0, m, ctx->bin_mid);
+      ++cnt[b];
+      first[b] = (uint32_t)i;  // ascending Y: the lowest index of the bin
+    }
+    std::vector<double> ent(nbins * kBinEntry, std::numeric_limits<double>::infinity());
+    uint32_t before = 0;
+    for (size_t b = 0; b < nbins; ++b) {
+      const uint64_t head = (uint64_t)before | ((uint64_t)cnt[b] << 32);
+      std::memcpy(&ent[b * kBinEntry], &head, 8);
+      for (uint32_t j = 0; j < std::min<uint32_t>(cnt[b], kBinInline); ++j)
+        ent[b * kBinEntry + 1 + j] = Y[first[b] + j];
+      before += cnt[b];
+    }
+    if ((e = cudaMalloc(&ctx->d_bins, sizeof(double) * ent.size())) != cudaSuccess) return e;
+    if ((e = cudaMemcpy(ctx->d_bins, ent.data(), sizeof(double) * ent.size(),
+                        cudaMemcpyHostToDevice)) != cudaSuccess)
+      return e;
+  }
   // tail-mass Taylor table (see TailTable in tie_internal.cuh)
   {
     const double ymax = std::max(std::fabs(ctx->y0), std::fabs(ctx->yN));
@@ -639,7 +778,7 @@ cudaError_t build_context_tables(tie_ctx* ctx) {
 
 cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, const void* x_max,
                          bool x_is_u32, uint64_t n, double alpha, double beta, double* E,
-                         double* C, double* S, uint64_t* keys_out, uint32_t* hist_out,
+                         double* C, double* S, uint64_t* keys_out, unsigned long long* minmax,
                          unsigned flags, cudaStream_t s, uint64_t index_base) {
   const bool exact = (flags & 1u) != 0;
   if (n == 0) return cudaSuccess;
@@ -649,6 +788,12 @@ cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, co
   p.ybucket = ctx->d_ybucket;
   p.table = ctx->d_table;
   p.tail = ctx->d_tail;
+  p.bins = ctx->d_bins;
+  p.bin_e0 = ctx->bin_e0;
+  p.bin_m = ctx->bin_m;
+  p.bin_mid = ctx->bin_mid;
+  p.inv_N = ctx->N > 0 ? 1.0 / (double)ctx->N : 0.0;
+  p.inv_1ma = 1.0 / (1.0 - alpha);
   p.t_ymax = ctx->t_ymax;
   p.t_w = ctx->t_w;
   p.t_inv_w = ctx->t_inv_w;
@@ -684,29 +829,39 @@ cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, co
       cudaFuncSetAttribute(score_kernel<uint32_t, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       score_kernel<uint32_t, true><<<(unsigned)grid, 256, smem, s>>>(
-          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out, hist_out);
+          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out, minmax);
     } else {
       cudaFuncSetAttribute(score_kernel<double, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       score_kernel<double, true><<<(unsigned)grid, 256, smem, s>>>(
-          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, hist_out);
+          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, minmax);
     }
   } else if (flags & 4u) {  // per-lane gathers (kept for A/B measurements)
     const uint64_t grid = std::min<uint64_t>(blocks_needed, (uint64_t)sms * 8);
     if (x_is_u32)
       score_kernel<uint32_t, false><<<(unsigned)grid, 256, 0, s>>>(
-          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out, hist_out);
+          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out, minmax);
     else
       score_kernel<double, false><<<(unsigned)grid, 256, 0, s>>>(
-          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, hist_out);
+          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, minmax);
   } else {
-    const uint64_t grid = std::min<uint64_t>(blocks_needed, (uint64_t)sms * 8);
+    const uint64_t grid = std::min<uint64_t>(blocks_needed, (uint64_t)sms * 3);
+    const size_t ka_smem = ctx->G <= kKaMaxG ? sizeof(double) * kSlabStride * ctx->G : 0;
+    static bool attr = false;
+    if (!attr) {
+      const int mx = (int)(sizeof(double) * kSlabStride * kKaMaxG);
+      cudaFuncSetAttribute(score_coop_kernel<uint32_t>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(score_coop_kernel<double>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      attr = true;
+    }
     if (x_is_u32)
-      score_coop_kernel<uint32_t><<<(unsigned)grid, 256, 0, s>>>(
-          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out, hist_out);
+      score_coop_kernel<uint32_t><<<(unsigned)grid, 256, ka_smem, s>>>(
+          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out, minmax);
     else
-      score_coop_kernel<double><<<(unsigned)grid, 256, 0, s>>>(
-          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, hist_out);
+      score_coop_kernel<double><<<(unsigned)grid, 256, ka_smem, s>>>(
+          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, minmax);
   }
   capi::count_launch();
   return cudaGetLastError();

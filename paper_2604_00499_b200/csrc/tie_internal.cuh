@@ -32,6 +32,45 @@ __device__ __forceinline__ void report(unsigned long long* err, uint64_t index, 
   atomicMin(err, (unsigned long long)((index << 8) | why));
 }
 
+// Fold a thread's [lo, hi] key range into mm[0] = max(~key) and mm[1] = max(key) with one
+// pair of atomics per CTA (every thread of the CTA must call it; blockDim % 32 == 0).
+__device__ __forceinline__ void key_range_flush(unsigned long long* mm, uint64_t lo,
+                                                uint64_t hi) {
+  __shared__ uint64_t s_lo[32], s_hi[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t a = __shfl_xor_sync(0xffffffffu, lo, o);
+    const uint64_t b = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) {
+    s_lo[warp] = lo;
+    s_hi[warp] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nw; ++w) {
+      lo = s_lo[w] < lo ? s_lo[w] : lo;
+      hi = s_hi[w] > hi ? s_hi[w] : hi;
+    }
+    if (lo <= hi) {  // the CTA saw at least one key
+      atomicMax(mm, (unsigned long long)~lo);
+      atomicMax(mm + 1, (unsigned long long)hi);
+    }
+  }
+}
+
+// sample-bin of y (see kBinEntry); valid for Y[0] <= y <= Y[N-1]
+__host__ __device__ __forceinline__ uint32_t sample_bin(uint64_t bits, uint32_t e0, uint32_t m,
+                                                        uint32_t mid) {
+  const uint32_t e = (uint32_t)(bits >> 52) & 0x7ffu;
+  if (e < e0) return mid;
+  const uint32_t off = ((e - e0) << m) | (uint32_t)((bits >> (52 - m)) & ((1u << m) - 1u));
+  return (bits >> 63) ? mid - 1u - off : mid + 1u + off;
+}
+
 // ---------------------------------------------------------------- Student-t constants
 // Everything t_cdf needs that does not depend on the request (computed on the host with
 // glibc, so bit-identical to the reference's own constants).
@@ -59,6 +98,14 @@ constexpr int kYBuckets = 8192;         // uniform-y bucket index over the sampl
 // truncation is < 1e-23 relative.  T(y) = y >= 0 ? 1 - v(|y|) : v(|y|)  (dist.cpp:80).
 constexpr int kTailBuckets = 4096;
 constexpr int kTailCoef = 8;
+// Sample-bin index (the cut k = upper_bound(Y, y) in ONE 64-byte gather): bins are an exact,
+// monotone integer function of y's IEEE bits -- (exponent, top kBinMant mantissa bits) with
+// |y| < 2^(bin_e0 - 1023) folded into a middle bin -- so every sample in a lower bin is < y
+// and every sample in a higher bin is > y.  Entry: [0] = kstart | count << 32 (samples
+// before the bin | in it), [1..7] = the bin's first samples inline; k = kstart + #{inline
+// <= y}, plus a search of Y for the rare bin holding more than kBinInline samples.
+constexpr int kBinEntry = 8;   // doubles per entry
+constexpr int kBinInline = 7;
 
 struct ScoreParams {
   TdistConst td;
@@ -66,6 +113,10 @@ struct ScoreParams {
   const uint32_t* ybucket;  // [kYBuckets + 1] upper_bound(Y, edge_b)
   const double* table;      // [G][N+1][kMoments]
   const double* tail;       // [kTailBuckets][kTailCoef]
+  const double* bins;       // [2 * bin_mid + 1][kBinEntry]
+  uint32_t bin_e0, bin_m, bin_mid;
+  double inv_N;             // 1 / N  (psi = S / N as S * inv_N)
+  double inv_1ma;           // 1 / (1 - alpha)
   double t_ymax, t_w, t_inv_w;
   double y0, y_scale;       // bucket b = floor((y - y0) * y_scale)
   double yN;                // Y[N-1]
@@ -94,6 +145,8 @@ struct tie_ctx {
   uint32_t* d_ybucket = nullptr;
   double* d_table = nullptr;
   double* d_tail = nullptr;
+  double* d_bins = nullptr;
+  uint32_t bin_e0 = 0, bin_m = 0, bin_mid = 0;
   double t_ymax = 0, t_w = 0, t_inv_w = 0;
   int G = 0;
   double y0 = 0, y_scale = 0, yN = 0;
@@ -152,18 +205,18 @@ cudaError_t build_context_tables(tie_ctx* ctx);
 cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma,
                          const void* x_max, bool x_is_u32, uint64_t n, double alpha,
                          double beta, double* E, double* C, double* S, uint64_t* keys_out,
-                         uint32_t* hist_out, unsigned flags, cudaStream_t s,
+                         unsigned long long* minmax, unsigned flags, cudaStream_t s,
                          uint64_t index_base = 0);
 // Dispatch order by (key asc, id asc) of double keys (ids == nullptr: id = index).
 cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n,
                         uint64_t* order, cudaStream_t s);
 size_t rank_scratch_bytes(uint64_t n, bool with_ids);
 // Fused producer path: rank_prepare() zeroes the sort metadata and returns where the
-// producer (the score kernel) writes order-preserving u64 keys and accumulates the 8 digit
-// histograms; rank_prepared() then runs plan + digit passes and emits the order.
+// producer (the score kernel) writes order-preserving u64 keys and folds their range
+// (key_range_flush); rank_prepared() then bucket-sorts them and emits the order.
 struct RankPrep {
   uint64_t* keys;
-  uint32_t* hist;
+  unsigned long long* minmax;
 };
 RankPrep rank_prepare(tie_ctx* ctx, uint64_t n, cudaStream_t s);
 cudaError_t rank_prepared(tie_ctx* ctx, uint64_t n, uint64_t* order, cudaStream_t s);

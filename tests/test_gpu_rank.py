@@ -74,3 +74,39 @@ def test_order_check_helper_exempts_near_ties():
     key = np.array([1.0, 1.0 + 1e-15, 2.0])
     ok, bad, exempt = order_check(np.array([1, 0, 2]), key, tol=1e-12)
     assert ok and bad == 0 and exempt == 1
+
+
+# ---- bucket path (default): range bucketing + per-bucket shared-memory ranking, with the
+# device-side LSD fallback when one bucket exceeds a local-sort CTA's capacity
+@pytest.mark.parametrize("n", [4096 * 3 + 5, 262_144, 2_000_000])
+def test_bucket_path_continuous_keys(abi, h, oracle, n):
+    rng = np.random.default_rng(n + 11)
+    key = rng.lognormal(5.0, 0.6, n) + 50.0  # score-like: no bucket overflows
+    assert np.array_equal(abi.rank(h, key), oracle.rank(key))
+
+
+def test_bucket_path_moderate_ties_and_signs(abi, h, oracle):
+    rng = np.random.default_rng(3)
+    n = 600_000
+    key = np.round(rng.normal(0.0, 300.0, n), 0)  # ~600 distinct values: ties inside buckets
+    key[::97] = -0.0
+    assert np.array_equal(abi.rank(h, key), oracle.rank(key))
+    ids = np.arange(n, dtype=np.uint64) * 3 + 1  # ascending explicit ids: bucket path too
+    assert np.array_equal(abi.rank(h, key, ids), oracle.rank(key, ids))
+
+
+@pytest.mark.parametrize("distinct", [1, 2, 5])
+def test_bucket_overflow_falls_back_exactly(abi, h, oracle, distinct):
+    rng = np.random.default_rng(distinct)
+    n = 300_000
+    key = rng.integers(0, distinct, n).astype(np.float64) * 17.25 + 100.0
+    assert np.array_equal(abi.rank(h, key), oracle.rank(key))
+    ids = np.arange(n, dtype=np.uint64) + 1000
+    assert np.array_equal(abi.rank(h, key, ids), oracle.rank(key, ids))
+
+
+def test_bucket_extreme_range(abi, h, oracle):
+    rng = np.random.default_rng(5)
+    n = 100_000
+    key = rng.standard_normal(n) * np.exp(rng.uniform(-600, 600, n))  # span of all exponents
+    assert np.array_equal(abi.rank(h, key), oracle.rank(key))
