@@ -280,7 +280,9 @@ __device__ __forceinline__ uint32_t score_one(const ScoreParams& p, const double
   tail_fetch(p, y_max, tr);
   const uint32_t k_max = cut_index(p, p.Y, y_max);
   const int g = __double2int_rn(sg * kGridInvH);
-  const bool use_table = !kExact && g < p.G && fabs(mu) <= 700.0;
+  const double reach = fmax(p.taylor_y0, fmin(fmax(y_max, 0.0), p.yN));
+  const bool use_table = !kExact && g < p.G && fabs(mu) <= 700.0 &&
+                         fabs(sg - g * kGridH) * reach <= kTaylorReach;
   const double* base = p.table + (size_t)(use_table ? g : 0) * (size_t)(p.N + 1) * kMoments;
   Row row_max;
   if (use_table) load_row(base + (size_t)k_max * kMoments, row_max);
@@ -440,6 +442,32 @@ __device__ __forceinline__ void stage_rows(const double* myrow, double* slab,
   __syncwarp();
 }
 
+// The same staging with cp.async (LDGSTS): global -> shared without a register round trip.
+// Null rows are skipped (their slab slot holds stale data the caller never uses).
+template <int R>
+__device__ __forceinline__ void stage_rows_async(const double* myrow, double* slab,
+                                                 const double** ptrs) {
+  const int lane = threadIdx.x & 31;
+  ptrs[lane] = myrow;
+  __syncwarp();
+  constexpr int C = R / 2;
+#pragma unroll
+  for (int it = 0; it < C; ++it) {
+    const int c = it * 32 + lane;
+    const int r = c / C, sub = c % C;
+    const double* rp = ptrs[r];
+    if (rp) {
+      const unsigned dst =
+          (unsigned)__cvta_generic_to_shared(slab + r * kSlabStride + 2 * sub);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                   "l"(reinterpret_cast<const double2*>(rp) + sub)
+                   : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+}
+
 template <int R>
 __device__ __forceinline__ double slab_horner(const double* slab, double x) {
   const int lane = threadIdx.x & 31;
@@ -453,35 +481,6 @@ __device__ __forceinline__ double slab_horner(const double* slab, double x) {
     acc = fma(acc, x, c.x);
   }
   return acc;
-}
-
-// Stage two 64-byte rows per lane (a: tail-mass row, b: sample-bin entry) in ONE round of
-// loads: 64 rows x 4 16-byte chunks, 8 per lane, consecutive lanes on consecutive chunks.
-// Lane l's rows land at slab[l*kSlabStride + 0..7] (a) and [.. + 8..15] (b).
-__device__ __forceinline__ void stage_pair(const double* a, const double* b, double* slab,
-                                           const double** ptrs) {
-  const int lane = threadIdx.x & 31;
-  ptrs[2 * lane] = a;
-  ptrs[2 * lane + 1] = b;
-  __syncwarp();
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    double2 v[4];
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int c = (h * 4 + it) * 32 + lane;
-      const double* rp = ptrs[c >> 2];
-      v[it] =
-          rp ? __ldg(reinterpret_cast<const double2*>(rp) + (c & 3)) : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int c = (h * 4 + it) * 32 + lane, r = c >> 2;
-      *reinterpret_cast<double2*>(slab + (r >> 1) * kSlabStride + (r & 1) * 8 + 2 * (c & 3)) =
-          v[it];
-    }
-  }
-  __syncwarp();
 }
 
 template <int R>
@@ -525,10 +524,10 @@ __device__ __forceinline__ uint32_t bin_cut(const ScoreParams& p, const double* 
 //   (one staged round of gathers) -> moment row at k_max (one staged gather) -> epilogue,
 // with the k_alpha rows of every sigma grid point (request-invariant) resident in shared
 // memory for the whole kernel.
-constexpr int kKaMaxG = 256;  // grid points whose k_alpha rows fit the smem budget
+constexpr int kKaMaxG = 320;  // grid points whose k_alpha rows fit the smem budget
 
-template <typename XT>
-__global__ void __launch_bounds__(256, 3) score_coop_kernel(const __grid_constant__ ScoreParams p,
+template <typename XT, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) score_coop_kernel(const __grid_constant__ ScoreParams p,
                                                          const double* __restrict__ mu,
                                                          const double* __restrict__ sigma,
                                                          const XT* __restrict__ xmax, uint64_t n,
@@ -538,7 +537,7 @@ __global__ void __launch_bounds__(256, 3) score_coop_kernel(const __grid_constan
                                                          uint64_t* __restrict__ keys,
                                                          unsigned long long* __restrict__ minmax) {
   __shared__ __align__(16) double slab_all[8][32 * kSlabStride];
-  __shared__ const double* ptr_all[8][64];
+  __shared__ const double* ptr_all[8][32];
   extern __shared__ __align__(16) double ka_rows[];  // [G][kSlabStride] when G <= kKaMaxG
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* slab = slab_all[wib];
@@ -585,36 +584,39 @@ __global__ void __launch_bounds__(256, 3) score_coop_kernel(const __grid_constan
     const bool ok = active && why == kOk;
     const double sg = ok ? (sig < 1e-9 ? 1e-9 : sig) : 1.0;
     const double y_max = ok ? __dsub_rn(lnx(xm), m) / sg : 0.0;
-    // round 1: tail-mass row (T) and sample-bin entry (k_max), gathered together
-    const double ay = fabs(y_max);
-    const bool tail_tab = ok && ay < p.t_ymax;
-    const int tb = tail_tab ? min((int)(ay * p.t_inv_w), kTailBuckets - 1) : 0;
-    const bool in_range = ok && y_max >= p.y0 && y_max < p.yN;
-    const double* ent =
-        in_range ? p.bins + (size_t)sample_bin((uint64_t)__double_as_longlong(y_max), p.bin_e0,
-                                               p.bin_m, p.bin_mid) * kBinEntry
-                 : nullptr;
-    stage_pair(tail_tab ? p.tail + (size_t)tb * kTailCoef : nullptr, ent, slab, ptrs);
+    // round 1: the sample-bin entry of y_max -> k_max and T(y_max) (one 96-byte gather)
+    const uint64_t ybits = (uint64_t)__double_as_longlong(y_max);
+    const bool binned = ok && fabs(y_max) < p.bin_ylim;
+    stage_rows_async<kBinEntry>(
+        binned ? p.bins + (size_t)sample_bin(ybits, p.bin_e0, p.bin_m, p.bin_mid) * kBinEntry
+               : nullptr,
+        slab, ptrs);
     const double* my = slab + lane * kSlabStride;
     double T = 0.5;
-    if (tail_tab) {
-      const double v = smem_horner<kTailCoef>(my, ay - ((double)tb + 0.5) * p.t_w);
-      T = y_max >= 0.0 ? __dsub_rn(1.0, v) : v;  // dist.cpp:80
-    } else if (ok) {
-      T = t_cdf_slow(p.td, y_max);
-    }
     uint32_t k_max = 0;
-    if (ok) k_max = in_range ? bin_cut(p, my + 8, y_max) : (y_max >= p.yN ? (uint32_t)p.N : 0u);
+    if (binned) {
+      const double c = __longlong_as_double(
+          (long long)sample_bin_centre_bits(ybits, p.bin_e0, p.bin_m));
+      const double v = smem_horner<kBinCoef>(my + kBinTail, __dsub_rn(fabs(y_max), c));
+      T = y_max >= 0.0 ? __dsub_rn(1.0, v) : v;  // dist.cpp:80
+      k_max = bin_cut(p, my, y_max);
+    } else if (ok) {  // |y_max| beyond the bins: continued fraction, cut at the sample ends
+      T = t_cdf_slow(p.td, y_max);
+      k_max = y_max >= p.yN ? (uint32_t)p.N
+                            : (y_max < p.y0 ? 0u : bin_search_slow(p.Y, 0, p.N, y_max));
+    }
     const int g = ok ? __double2int_rn(sg * kGridInvH) : 0;
-    const bool use_table = ok && g < p.G && fabs(m) <= 700.0;
     const double delta = sg - g * kGridH;  // exact: h is a power of two
+    const double reach = fmax(p.taylor_y0, fmin(fmax(y_max, 0.0), p.yN));
+    const bool use_table =
+        ok && g < p.G && fabs(m) <= 700.0 && fabs(delta) * reach <= kTaylorReach;
     const double* gbase = p.table + (size_t)(use_table ? g : 0) * (size_t)(p.N + 1) * kMoments;
     const bool saturated = p.alpha >= T;  // censored_cvar case 1 (dist.cpp:187)
     const uint32_t k_a = saturated ? 0u : p.k_alpha;
     __syncwarp();
     // round 2: the moment row at k_max
-    stage_rows<kMoments>(use_table && k_max ? gbase + (size_t)k_max * kMoments : nullptr, slab,
-                         ptrs);
+    stage_rows_async<kMoments>(use_table && k_max ? gbase + (size_t)k_max * kMoments : nullptr,
+                               slab, ptrs);
     const double F_all = slab_horner<kMoments>(slab, delta);
     __syncwarp();
     double F_a = 0.0;
@@ -694,73 +696,91 @@ cudaError_t build_context_tables(tie_ctx* ctx) {
   if ((e = cudaMemcpy(ctx->d_ybucket, yb.data(), sizeof(uint32_t) * yb.size(),
                       cudaMemcpyHostToDevice)) != cudaSuccess)
     return e;
-  // sample-bin index (kBinEntry in tie_internal.cuh)
-  if (N > 0) {
+  // Taylor coefficients of v(|y|) = 1 - T(|y|) about c >= 0 (tail table and sample bins):
+  // a_0 = v(c) by the reference's own continued fraction, a_j = -pdf^(j-1)(c)/j! from the
+  // power series of pdf(c + t) = C (q0 + q1 t + q2 t^2)^ex  (q f' = ex q' f)
+  const long double nu_l = ctx->nu;
+  const long double ex_l = -0.5L * (nu_l + 1.0L);
+  const long double C_l = std::exp((long double)std::lgamma(0.5 * (ctx->nu + 1.0)) -
+                                   (long double)std::lgamma(0.5 * ctx->nu) -
+                                   0.5L * std::log(nu_l * 3.14159265358979323846264338327950288L));
+  auto tail_coefs = [&](double c, int ncoef, double* row) {
+    const double x = ctx->nu / (c * c + ctx->nu);
+    row[0] = 0.5 * host::reg_inc_beta(0.5 * ctx->nu, 0.5, x);
+    const long double q[3] = {1.0L + (long double)c * c / nu_l, 2.0L * c / nu_l, 1.0L / nu_l};
+    long double f[16];
+    f[0] = C_l * std::pow(q[0], ex_l);
+    for (int k = 1; k < ncoef; ++k) {
+      long double acc = 0.0L;
+      for (int i = 1; i <= std::min(k, 2); ++i) acc += (ex_l * i - (k - i)) * q[i] * f[k - i];
+      f[k] = acc / (k * q[0]);
+    }
+    for (int j = 1; j < ncoef; ++j) row[j] = (double)(-f[j - 1] / j);  // v' = -pdf
+  };
+  // sample bins (kBinEntry in tie_internal.cuh)
+  {
     auto bits = [](double x) {
       uint64_t u;
       std::memcpy(&u, &x, 8);
       return u;
     };
+    auto dbl = [](uint64_t u) {
+      double x;
+      std::memcpy(&x, &u, 8);
+      return x;
+    };
     const double maxabs = std::max(std::fabs(Y.front()), std::fabs(Y.back()));
-    const uint32_t etop = (uint32_t)(bits(maxabs) >> 52) & 0x7ffu;
-    const uint32_t e0 = std::min<uint32_t>(1023u - 12u, etop);
-    uint32_t m = 10;
-    while (m > 0 && ((uint64_t)(etop - e0 + 1) << m) > (1u << 19)) --m;
+    // cover at least |y| < 2^8 (y_max beyond the samples: small sigma), never more than 2^30
+    const uint32_t etop = std::min<uint32_t>(
+        std::max<uint32_t>((uint32_t)(bits(maxabs) >> 52) & 0x7ffu, 1023u + 7u), 1023u + 29u);
+    const uint32_t e0 = 1023u - 12u;
+    uint32_t m = 11;
+    while (m > 4 && ((uint64_t)(etop - e0 + 1) << m) > (1u << 20)) --m;
     ctx->bin_e0 = e0;
     ctx->bin_m = m;
     ctx->bin_mid = (etop - e0 + 1) << m;
+    ctx->bin_ylim = dbl((uint64_t)(etop + 1) << 52);
     const size_t nbins = 2 * (size_t)ctx->bin_mid + 1;
-    std::vector<uint32_t> cnt(nbins, 0);
-    std::vector<uint32_t> first(nbins, 0);
+    std::vector<uint32_t> cnt(nbins, 0), first(nbins, 0);
     for (int i = N - 1; i >= 0; --i) {
+      if (!(std::fabs(Y[i]) < ctx->bin_ylim)) continue;  // beyond the bins: never a cut inside
       const uint32_t b = sample_bin(bits(Y[i]), e0, m, ctx->bin_mid);
       ++cnt[b];
       first[b] = (uint32_t)i;  // ascending Y: the lowest index of the bin
     }
     std::vector<double> ent(nbins * kBinEntry, std::numeric_limits<double>::infinity());
     uint32_t before = 0;
+    for (int i = 0; i < N && Y[i] <= -ctx->bin_ylim; ++i) ++before;  // samples below the bins
     for (size_t b = 0; b < nbins; ++b) {
+      double* row = &ent[b * kBinEntry];
       const uint64_t head = (uint64_t)before | ((uint64_t)cnt[b] << 32);
-      std::memcpy(&ent[b * kBinEntry], &head, 8);
+      std::memcpy(row, &head, 8);
       for (uint32_t j = 0; j < std::min<uint32_t>(cnt[b], kBinInline); ++j)
-        ent[b * kBinEntry + 1 + j] = Y[first[b] + j];
+        row[1 + j] = Y[first[b] + j];
       before += cnt[b];
+      // centre of the bin's |y| range (the device derives the same value from y's bits)
+      double c = 0.0;
+      if (b != ctx->bin_mid) {
+        const uint64_t off = b > ctx->bin_mid ? b - ctx->bin_mid - 1 : ctx->bin_mid - 1 - b;
+        const uint64_t e = e0 + (off >> m), j = off & ((1u << m) - 1u);
+        c = dbl(sample_bin_centre_bits((e << 52) | (j << (52 - m)), e0, m));
+      }
+      tail_coefs(c, kBinCoef, row + kBinTail);
     }
     if ((e = cudaMalloc(&ctx->d_bins, sizeof(double) * ent.size())) != cudaSuccess) return e;
     if ((e = cudaMemcpy(ctx->d_bins, ent.data(), sizeof(double) * ent.size(),
                         cudaMemcpyHostToDevice)) != cudaSuccess)
       return e;
   }
-  // tail-mass Taylor table (see TailTable in tie_internal.cuh)
+  // tail-mass Taylor table (exact / per-lane paths; kTailBuckets in tie_internal.cuh)
   {
     const double ymax = std::max(std::fabs(ctx->y0), std::fabs(ctx->yN));
     ctx->t_ymax = ymax > 0.0 ? ymax : 0.0;
     ctx->t_w = ctx->t_ymax / kTailBuckets;
     ctx->t_inv_w = ctx->t_w > 0.0 ? 1.0 / ctx->t_w : 0.0;
     std::vector<double> tt((size_t)kTailBuckets * kTailCoef, 0.0);
-    const long double nu = ctx->nu;
-    const long double ex = -0.5L * (nu + 1.0L);  // pdf = C q^ex, q = 1 + y^2/nu
-    const long double C = std::exp((long double)std::lgamma(0.5 * (ctx->nu + 1.0)) -
-                                   (long double)std::lgamma(0.5 * ctx->nu) -
-                                   0.5L * std::log(nu * 3.14159265358979323846264338327950288L));
-    for (int b = 0; b < kTailBuckets && ctx->t_w > 0.0; ++b) {
-      const double c = ((double)b + 0.5) * ctx->t_w;  // same expression as the device
-      // a0 = v(c) = I_x(nu/2, 1/2) / 2 with the reference's own evaluation (host::reg_inc_beta)
-      const double x = ctx->nu / (c * c + ctx->nu);
-      const double a0 = 0.5 * host::reg_inc_beta(0.5 * ctx->nu, 0.5, x);
-      // pdf(c + t) = C (q0 + q1 t + q2 t^2)^ex as a power series: q f' = ex q' f
-      const long double q[3] = {1.0L + (long double)c * c / nu, 2.0L * c / nu, 1.0L / nu};
-      long double f[kTailCoef];
-      f[0] = C * std::pow(q[0], ex);
-      for (int k = 1; k < kTailCoef; ++k) {
-        long double acc = 0.0L;
-        for (int i = 1; i <= std::min(k, 2); ++i) acc += (ex * i - (k - i)) * q[i] * f[k - i];
-        f[k] = acc / (k * q[0]);
-      }
-      double* row = tt.data() + (size_t)b * kTailCoef;
-      row[0] = a0;
-      for (int j = 1; j < kTailCoef; ++j) row[j] = (double)(-f[j - 1] / j);  // v' = -pdf
-    }
+    for (int b = 0; b < kTailBuckets && ctx->t_w > 0.0; ++b)
+      tail_coefs(((double)b + 0.5) * ctx->t_w, kTailCoef, tt.data() + (size_t)b * kTailCoef);
     if ((e = cudaMalloc(&ctx->d_tail, sizeof(double) * tt.size())) != cudaSuccess) return e;
     if ((e = cudaMemcpy(ctx->d_tail, tt.data(), sizeof(double) * tt.size(),
                         cudaMemcpyHostToDevice)) != cudaSuccess)
@@ -792,6 +812,8 @@ cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, co
   p.bin_e0 = ctx->bin_e0;
   p.bin_m = ctx->bin_m;
   p.bin_mid = ctx->bin_mid;
+  p.bin_ylim = ctx->bin_ylim;
+  p.taylor_y0 = std::fabs(ctx->y0);
   p.inv_N = ctx->N > 0 ? 1.0 / (double)ctx->N : 0.0;
   p.inv_1ma = 1.0 / (1.0 - alpha);
   p.t_ymax = ctx->t_ymax;
@@ -845,23 +867,31 @@ cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, co
       score_kernel<double, false><<<(unsigned)grid, 256, 0, s>>>(
           p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, minmax);
   } else {
-    const uint64_t grid = std::min<uint64_t>(blocks_needed, (uint64_t)sms * 3);
+    const int minb = (flags & 8u) ? 3 : 2;  // 2 CTAs/SM, 128 regs, no spills (A/B: 3, spills)
+    const uint64_t grid = std::min<uint64_t>(blocks_needed, (uint64_t)sms * minb);
     const size_t ka_smem = ctx->G <= kKaMaxG ? sizeof(double) * kSlabStride * ctx->G : 0;
     static bool attr = false;
     if (!attr) {
       const int mx = (int)(sizeof(double) * kSlabStride * kKaMaxG);
-      cudaFuncSetAttribute(score_coop_kernel<uint32_t>,
+      cudaFuncSetAttribute(score_coop_kernel<uint32_t, 2>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      cudaFuncSetAttribute(score_coop_kernel<double>,
+      cudaFuncSetAttribute(score_coop_kernel<double, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(score_coop_kernel<uint32_t, 3>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(score_coop_kernel<double, 3>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
       attr = true;
     }
-    if (x_is_u32)
-      score_coop_kernel<uint32_t><<<(unsigned)grid, 256, ka_smem, s>>>(
-          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out, minmax);
-    else
-      score_coop_kernel<double><<<(unsigned)grid, 256, ka_smem, s>>>(
-          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, minmax);
+#define TIE_COOP(XT, MB)                                                          \
+  score_coop_kernel<XT, MB><<<(unsigned)grid, 256, ka_smem, s>>>(                 \
+      p, mu, sigma, (const XT*)x_max, n, E, C, S, keys_out, minmax)
+    if (x_is_u32) {
+      if (minb == 2) TIE_COOP(uint32_t, 2); else TIE_COOP(uint32_t, 3);
+    } else {
+      if (minb == 2) TIE_COOP(double, 2); else TIE_COOP(double, 3);
+    }
+#undef TIE_COOP
   }
   capi::count_launch();
   return cudaGetLastError();

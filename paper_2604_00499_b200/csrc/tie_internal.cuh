@@ -62,13 +62,22 @@ __device__ __forceinline__ void key_range_flush(unsigned long long* mm, uint64_t
   }
 }
 
-// sample-bin of y (see kBinEntry); valid for Y[0] <= y <= Y[N-1]
+// sample bin of y (see kBinEntry); valid for |y| < 2^(etop - 1022)
 __host__ __device__ __forceinline__ uint32_t sample_bin(uint64_t bits, uint32_t e0, uint32_t m,
                                                         uint32_t mid) {
   const uint32_t e = (uint32_t)(bits >> 52) & 0x7ffu;
   if (e < e0) return mid;
   const uint32_t off = ((e - e0) << m) | (uint32_t)((bits >> (52 - m)) & ((1u << m) - 1u));
   return (bits >> 63) ? mid - 1u - off : mid + 1u + off;
+}
+
+// |y| centre of the bin holding y (exact double; 0 for the middle bin)
+__host__ __device__ __forceinline__ uint64_t sample_bin_centre_bits(uint64_t bits, uint32_t e0,
+                                                                    uint32_t m) {
+  const uint64_t e = (bits >> 52) & 0x7ffu;
+  if (e < e0) return 0;
+  const uint64_t keep = ~((1ull << (52 - m)) - 1ull) & 0x7fffffffffffffffull;
+  return (bits & keep) | (1ull << (51 - m));
 }
 
 // ---------------------------------------------------------------- Student-t constants
@@ -82,30 +91,42 @@ struct TdistConst {
 };
 
 // ---------------------------------------------------------------- score parameters
-// Sigma-grid moment tables:
+// Sigma-grid moment tables (K1):
 //   P[g][k][m] = sum_{i<k} Y_i^m / m! * exp(sigma_g * Y_i),   sigma_g = g * kGridH
 // so that for |delta| = |sigma - sigma_g| <= kGridH/2
-//   sum_{i<k} exp(sigma * Y_i) = sum_m delta^m P[g][k][m]   (truncation < 1e-24 rel.)
-constexpr int kMoments = 16;            // one 128-byte row per (g, k)
-constexpr double kGridH = 1.0 / 32.0;   // power of two: g*h and sigma - g*h are exact
-constexpr double kGridInvH = 32.0;
+//   sum_{i<k} exp(sigma * Y_i) = sum_m delta^m P[g][k][m]
+// truncation (|delta| max|Y|)^12 / 12! < 1.1e-19 relative for max|Y| <= 17.84 (the default
+// sample set); requests whose |delta| * max(|Y_0|, |y_max|) exceeds kTaylorReach use the
+// exact per-term sum instead (heavy-tailed caller-provided sample sets).
+constexpr int kMoments = 12;            // one 96-byte row per (g, k)
+constexpr double kGridH = 1.0 / 64.0;   // power of two: g*h and sigma - g*h are exact
+constexpr double kGridInvH = 64.0;
+constexpr double kTaylorReach = 0.2;    // (0.2)^12 / 12! = 8.6e-18
 constexpr int kYBuckets = 8192;         // uniform-y bucket index over the sample range
-// Tail-mass table: v(y) = 1 - T_nu(y) = I_x(nu/2, 1/2)/2 for y >= 0 as a degree-7 Taylor
-// expansion about each of kTailBuckets bucket centres c_b over [0, max|Y|]:
-//   a_0 = v(c_b) (the reference's own continued-fraction value), a_j = -pdf^(j-1)(c_b)/j!,
-// the t-density's derivatives from the exact power series of C (1 + (c+t)^2/nu)^-(nu+1)/2.
-// The series converges within sqrt(c^2+nu) >= 1.87 of c_b; at half-width 2.2e-3 the
-// truncation is < 1e-23 relative.  T(y) = y >= 0 ? 1 - v(|y|) : v(|y|)  (dist.cpp:80).
+// Tail-mass table (exact / per-lane score paths): v(y) = 1 - T_nu(y) = I_x(nu/2, 1/2)/2 for
+// y >= 0 as a degree-7 Taylor expansion about each of kTailBuckets bucket centres c_b over
+// [0, max|Y|]: a_0 = v(c_b) (the reference's own continued-fraction value),
+// a_j = -pdf^(j-1)(c_b)/j!, the t-density's derivatives from the exact power series of
+// C (1 + (c+t)^2/nu)^-(nu+1)/2.  The series converges within sqrt(c^2+nu) >= 1.87 of c_b; at
+// half-width 2.2e-3 the truncation is < 1e-23 relative.  T(y) = y >= 0 ? 1 - v(|y|) : v(|y|)
+// (dist.cpp:80).
 constexpr int kTailBuckets = 4096;
 constexpr int kTailCoef = 8;
-// Sample-bin index (the cut k = upper_bound(Y, y) in ONE 64-byte gather): bins are an exact,
-// monotone integer function of y's IEEE bits -- (exponent, top kBinMant mantissa bits) with
-// |y| < 2^(bin_e0 - 1023) folded into a middle bin -- so every sample in a lower bin is < y
-// and every sample in a higher bin is > y.  Entry: [0] = kstart | count << 32 (samples
-// before the bin | in it), [1..7] = the bin's first samples inline; k = kstart + #{inline
-// <= y}, plus a search of Y for the rare bin holding more than kBinInline samples.
-constexpr int kBinEntry = 8;   // doubles per entry
-constexpr int kBinInline = 7;
+// Sample bins (default path): the cut k = upper_bound(Y, y) AND T(y) from ONE 96-byte gather.
+// Bins are an exact, monotone integer function of y's IEEE bits -- (exponent, top bin_m
+// mantissa bits), |y| < 2^(bin_e0 - 1023) folded into a middle bin -- so every sample in a
+// lower bin is < y and every sample in a higher bin is > y.  Entry (12 doubles):
+//   [0]      kstart | count << 32  (samples before the bin | in it)
+//   [1..5]   the bin's first samples (pads +inf): k = kstart + #{inline <= y}, plus a search
+//            of Y for the rare bin holding more than kBinInline samples
+//   [6..11]  v(|y|) = 1 - T(|y|) as a degree-5 Taylor expansion about the bin's |y| centre
+//            c (relative half-width 2^-(bin_m+1) <= 2.4e-4 of c; the middle bin: c = 0,
+//            |t| <= 2^-12), a_0 = the reference's continued fraction, a_j = -pdf^(j-1)(c)/j!.
+// Bins extend past the sample range to |y| < 2^(bin_etop - 1022) (k = 0 or N there).
+constexpr int kBinEntry = 12;
+constexpr int kBinInline = 5;
+constexpr int kBinTail = 6;  // coefficient offset
+constexpr int kBinCoef = 6;
 
 struct ScoreParams {
   TdistConst td;
@@ -115,6 +136,8 @@ struct ScoreParams {
   const double* tail;       // [kTailBuckets][kTailCoef]
   const double* bins;       // [2 * bin_mid + 1][kBinEntry]
   uint32_t bin_e0, bin_m, bin_mid;
+  double bin_ylim;          // bins cover |y| < bin_ylim
+  double taylor_y0;         // |Y_0| (moment-table reach: max |Y_i| over a cut, kTaylorReach)
   double inv_N;             // 1 / N  (psi = S / N as S * inv_N)
   double inv_1ma;           // 1 / (1 - alpha)
   double t_ymax, t_w, t_inv_w;
@@ -147,6 +170,7 @@ struct tie_ctx {
   double* d_tail = nullptr;
   double* d_bins = nullptr;
   uint32_t bin_e0 = 0, bin_m = 0, bin_mid = 0;
+  double bin_ylim = 0.0;
   double t_ymax = 0, t_w = 0, t_inv_w = 0;
   int G = 0;
   double y0 = 0, y_scale = 0, yN = 0;
