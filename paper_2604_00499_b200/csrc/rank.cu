@@ -486,12 +486,15 @@ struct KeyRange {
   uint32_t shift;
 };
 
-__device__ __forceinline__ KeyRange key_range(const Bucket& b) {
-  const uint64_t kmin = ~(uint64_t)b.mm[0];
-  const uint64_t span = (uint64_t)b.mm[1] - kmin;
+// keys in [kmin, kmax] -> B-bit bucket (k - kmin) >> shift
+__device__ __forceinline__ KeyRange key_range(const unsigned long long* mm, uint32_t B) {
+  const uint64_t kmin = ~(uint64_t)mm[0];
+  const uint64_t span = (uint64_t)mm[1] - kmin;
   const uint32_t bits = span ? 64u - (uint32_t)__clzll((long long)span) : 0u;
-  return {kmin, bits > b.nb_log2 ? bits - b.nb_log2 : 0u};
+  return {kmin, bits > B ? bits - B : 0u};
 }
+
+__device__ __forceinline__ KeyRange key_range(const Bucket& b) { return key_range(b.mm, b.nb_log2); }
 
 __device__ __forceinline__ uint32_t bucket_of(const KeyRange& r, uint64_t k) {
   return (uint32_t)((k - r.kmin) >> r.shift);  // span >> shift < nb
@@ -706,6 +709,185 @@ __global__ void __launch_bounds__(kLocalThreads, 4) bucket_local_kernel(Bucket b
   }
 }
 
+// ====================================================================== partition path
+// Default for n <= kPartMaxN (the config-2 queue): the same (key, id) order with no per-key
+// global atomics.  Keys map to a B-bit bucket f = (k - kmin) >> shift, B = p_log2 + fine_log2;
+// the top p_log2 bits pick one of P partitions (~1K keys each), the rest a fine bucket.
+//   count  : persistent CTAs, each a contiguous chunk: shared-memory partition histogram,
+//            then ONE atomicAdd per (CTA, partition) reserving the CTA's slot range
+//   scan   : partition bases (1 CTA); a partition above kPartCap -> device LSD fallback
+//   scatter: the CTA's keys into its reserved ranges (shared-memory cursors)
+//   sort   : one CTA per partition: fine-bucket counting sort in shared memory, then each
+//            key's rank inside its fine bucket (~1-2 keys) by (key, index) -> dispatch order
+constexpr uint32_t kPartCap = 4096;
+constexpr uint64_t kPartMaxN = 1ull << 21;
+constexpr uint32_t kPartMaxP = 2048;
+constexpr uint32_t kPartMaxFineLog2 = 10;
+constexpr int kPartThreads = 256;
+
+struct Part {
+  const uint64_t* keys;
+  uint64_t* tk;  // [n] keys grouped by partition (aliases the LSD ping-pong buffer)
+  uint32_t* tv;
+  uint32_t* pcount;   // [P]   zeroed per sort
+  uint32_t* pbase;    // [P + 1]
+  uint32_t* cta_off;  // [ctas][P]  a CTA's slot offset inside each partition
+  unsigned long long* mm;
+  int* overflow;
+  uint32_t p_log2, P, fine_log2, ctas;
+  uint64_t chunk;
+};
+
+__device__ __forceinline__ uint32_t part_bucket(const Part& q, const KeyRange& r, uint64_t k) {
+  return (uint32_t)((k - r.kmin) >> r.shift);
+}
+
+__global__ void __launch_bounds__(kPartThreads) part_count_kernel(Part q, uint64_t n) {
+  __shared__ uint32_t h[kPartMaxP];
+  for (uint32_t p = threadIdx.x; p < q.P; p += kPartThreads) h[p] = 0;
+  __syncthreads();
+  const KeyRange r = key_range(q.mm, q.p_log2 + q.fine_log2);
+  const uint64_t lo = (uint64_t)blockIdx.x * q.chunk;
+  const uint64_t hi = min(n, lo + q.chunk);
+  uint64_t i = lo + threadIdx.x;
+  for (; i + 3 * kPartThreads < hi; i += 4 * kPartThreads) {
+    uint64_t k[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) k[u] = q.keys[i + u * kPartThreads];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) atomicAdd(&h[part_bucket(q, r, k[u]) >> q.fine_log2], 1u);
+  }
+  for (; i < hi; i += kPartThreads) atomicAdd(&h[part_bucket(q, r, q.keys[i]) >> q.fine_log2], 1u);
+  __syncthreads();
+  for (uint32_t p = threadIdx.x; p < q.P; p += kPartThreads) {
+    const uint32_t c = h[p];
+    q.cta_off[(uint64_t)blockIdx.x * q.P + p] = c ? atomicAdd(q.pcount + p, c) : 0u;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) part_scan_kernel(Part q, uint64_t n) {
+  __shared__ uint32_t sh[32];
+  constexpr int kPer = kPartMaxP / kScanThreads;
+  uint32_t c[kPer], t = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const uint32_t p = threadIdx.x * kPer + j;
+    c[j] = p < q.P ? q.pcount[p] : 0u;
+    t += c[j];
+    if (c[j] > kPartCap) *q.overflow = 1;
+  }
+  uint32_t v = scan_block_excl(t, sh);
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const uint32_t p = threadIdx.x * kPer + j;
+    if (p < q.P) q.pbase[p] = v;
+    v += c[j];
+  }
+  if (threadIdx.x == 0) q.pbase[q.P] = (uint32_t)n;
+}
+
+__global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(Part q, uint64_t n) {
+  if (*(volatile int*)q.overflow) return;
+  __shared__ uint32_t cur[kPartMaxP];
+  for (uint32_t p = threadIdx.x; p < q.P; p += kPartThreads)
+    cur[p] = q.pbase[p] + q.cta_off[(uint64_t)blockIdx.x * q.P + p];
+  __syncthreads();
+  const KeyRange r = key_range(q.mm, q.p_log2 + q.fine_log2);
+  const uint64_t lo = (uint64_t)blockIdx.x * q.chunk;
+  const uint64_t hi = min(n, lo + q.chunk);
+  uint64_t i = lo + threadIdx.x;
+  for (; i + 3 * kPartThreads < hi; i += 4 * kPartThreads) {
+    uint64_t k[4];
+    uint32_t pos[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) k[u] = q.keys[i + u * kPartThreads];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) pos[u] = atomicAdd(&cur[part_bucket(q, r, k[u]) >> q.fine_log2], 1u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      q.tk[pos[u]] = k[u];
+      q.tv[pos[u]] = (uint32_t)(i + u * kPartThreads);
+    }
+  }
+  for (; i < hi; i += kPartThreads) {
+    const uint64_t k = q.keys[i];
+    const uint32_t pos = atomicAdd(&cur[part_bucket(q, r, k) >> q.fine_log2], 1u);
+    q.tk[pos] = k;
+    q.tv[pos] = (uint32_t)i;
+  }
+}
+
+__global__ void __launch_bounds__(kPartThreads, 3) part_sort_kernel(Part q, uint64_t n,
+                                                                   const uint64_t* __restrict__ ids,
+                                                                   uint64_t* __restrict__ order,
+                                                                   Fallback f) {
+  if (*(volatile int*)q.overflow) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) lsd_tail_launch(f, q.keys, n, ids, order);
+    return;
+  }
+  const uint32_t p = blockIdx.x;
+  const uint32_t s0 = q.pbase[p], m = q.pbase[p + 1] - s0;  // m <= kPartCap
+  if (m == 0) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + kPartCap);
+  uint16_t* sf = reinterpret_cast<uint16_t*>(sv + kPartCap);    // fine bucket of key j
+  uint16_t* perm = sf + kPartCap;                                // slot -> key j
+  uint32_t* fb = reinterpret_cast<uint32_t*>(perm + kPartCap);   // [nf + 1] fine bases
+  uint32_t* fc = fb + (1u << kPartMaxFineLog2) + 1;              // [nf] counts / cursors
+  __shared__ uint32_t sh[32];
+  const uint32_t nf = 1u << q.fine_log2, fmask = nf - 1u;
+  for (uint32_t j = threadIdx.x; j < nf; j += kPartThreads) fc[j] = 0;
+  __syncthreads();
+  const KeyRange r = key_range(q.mm, q.p_log2 + q.fine_log2);
+  for (uint32_t j = threadIdx.x; j < m; j += kPartThreads) {
+    const uint64_t k = q.tk[s0 + j];
+    sk[j] = k;
+    sv[j] = q.tv[s0 + j];
+    const uint32_t fine = part_bucket(q, r, k) & fmask;
+    sf[j] = (uint16_t)fine;
+    atomicAdd(&fc[fine], 1u);
+  }
+  __syncthreads();
+  {  // exclusive scan of the nf (<= 1024) fine counts, 4 per thread
+    constexpr int kPer = (1 << kPartMaxFineLog2) / kPartThreads;
+    uint32_t c[kPer], t = 0;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t j = threadIdx.x * kPer + u;
+      c[u] = j < nf ? fc[j] : 0u;
+      t += c[u];
+    }
+    uint32_t v = block_excl_scan_256(t, sh);
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t j = threadIdx.x * kPer + u;
+      if (j < nf) {
+        fb[j] = v;
+        fc[j] = v;
+      }
+      v += c[u];
+    }
+    if (threadIdx.x == 0) fb[nf] = m;
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < m; j += kPartThreads) perm[atomicAdd(&fc[sf[j]], 1u)] = (uint16_t)j;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < m; j += kPartThreads) {
+    const uint64_t k = sk[j];
+    const uint32_t v = sv[j], fine = sf[j];
+    const uint32_t lo = fb[fine], hi = fb[fine + 1];
+    uint32_t below = 0;
+    for (uint32_t s = lo; s < hi; ++s) {
+      const uint32_t o = perm[s];
+      const uint64_t kq = sk[o];
+      below += (kq < k || (kq == k && sv[o] < v)) ? 1u : 0u;
+    }
+    order[s0 + lo + below] = ids ? ids[v] : (uint64_t)v;
+  }
+}
+
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 int items_for(uint64_t) { return 16; }
@@ -713,10 +895,22 @@ int items_for(uint64_t) { return 16; }
 struct Layout {
   size_t k0, k1, v0, v1, hist, plan, status, gstatus, gsum, gdone, counter, flag, k2, k3, v3,
       meta_begin, meta_end, total;
-  // bucket path: [bzero_begin, bzero_end) = count, mm, overflow (zeroed once per sort)
+  // bucket / partition path: [bzero_begin, bzero_end) = count (bucket path) or pcount
+  // (partition path), mm, overflow -- zeroed once per sort
   size_t count, mm, overflow, base, cursor, partial, seg, bzero_begin, bzero_end;
+  size_t pcount, pbase, cta_off;
   uint32_t tiles, nb_log2, nseg;
+  bool part;
+  uint32_t p_log2, fine_log2;
 };
+
+constexpr uint32_t kPartMaxCtas = 512;
+
+uint32_t ceil_log2(uint64_t x) {
+  uint32_t l = 0;
+  while (l < 63 && (1ull << l) < x) ++l;
+  return l;
+}
 
 uint32_t bucket_log2(uint64_t n) {
   uint32_t l = 0;
@@ -749,15 +943,29 @@ Layout layout(uint64_t n, bool with_ids) {
   L.meta_end = off;
   L.plan = off; off += align_up(sizeof(Plan));
   L.flag = off; off += align_up(sizeof(int));
+  L.part = n <= kPartMaxN;
+  L.p_log2 = std::min<uint32_t>(std::max<uint32_t>(ceil_log2((n + 1023) / 1024), 6u), 11u);
+  L.fine_log2 = std::min<uint32_t>(
+      std::max<uint32_t>(ceil_log2((n + (1ull << L.p_log2) - 1) >> L.p_log2), 1u),
+      kPartMaxFineLog2);
   L.bzero_begin = off;
-  L.count = off; off += align_up(4 * nb);
+  if (L.part) {
+    L.pcount = off; off += align_up(4ull << L.p_log2);
+  } else {
+    L.count = off; off += align_up(4 * nb);
+  }
   L.mm = off; off += align_up(16);
   L.overflow = off; off += align_up(sizeof(int));
   L.bzero_end = off;
-  L.base = off; off += align_up(4 * (nb + 1));
-  L.cursor = off; off += align_up(4 * nb);
-  L.partial = off; off += align_up(4 * (nb / kScanChunk));
-  L.seg = off; off += align_up(4 * ((uint64_t)L.nseg + 1));
+  const uint64_t bnb = L.part ? 0 : nb;  // bucket-path arrays (unused on the partition path)
+  L.base = off; off += align_up(4 * (bnb + 1));
+  L.cursor = off; off += align_up(4 * bnb);
+  L.partial = off; off += align_up(4 * (bnb / kScanChunk));
+  L.seg = off; off += align_up(4 * (L.part ? 1 : (uint64_t)L.nseg + 1));
+  if (L.part) {
+    L.pbase = off; off += align_up(4 * ((1ull << L.p_log2) + 1));
+    L.cta_off = off; off += align_up(4ull * kPartMaxCtas << L.p_log2);
+  }
   L.k2 = off; off += with_ids ? align_up(8 * n) : 0;  // transformed keys (id path)
   L.k3 = off; off += with_ids ? align_up(8 * n) : 0;  // keys gathered into id order
   L.v3 = off; off += with_ids ? align_up(4 * n) : 0;  // the id-order permutation
@@ -846,6 +1054,52 @@ cudaError_t sort_passes(tie_ctx* ctx, Work& w, uint64_t n, bool explicit_vals,
   return cudaGetLastError();
 }
 
+cudaError_t part_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_t* keys,
+                      uint64_t n, const uint64_t* ids, uint64_t* order, const Fallback& f,
+                      int sms, cudaStream_t s) {
+  static bool attr = false;
+  const size_t smem = (size_t)kPartCap * (8 + 4 + 2 + 2) +
+                      4 * (2 * (1u << kPartMaxFineLog2) + 1);
+  if (!attr) {
+    cudaFuncSetAttribute(part_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  Part q;
+  q.keys = keys;
+  q.tk = (uint64_t*)(base + L.k1);  // the LSD fallback runs only when the scatter did not
+  q.tv = (uint32_t*)(base + L.v0);
+  q.pcount = (uint32_t*)(base + L.pcount);
+  q.pbase = (uint32_t*)(base + L.pbase);
+  q.cta_off = (uint32_t*)(base + L.cta_off);
+  q.mm = (unsigned long long*)(base + L.mm);
+  q.overflow = (int*)(base + L.overflow);
+  q.p_log2 = L.p_log2;
+  q.P = 1u << L.p_log2;
+  q.fine_log2 = L.fine_log2;
+  q.ctas = (uint32_t)std::min<uint64_t>(
+      std::min<uint64_t>((uint64_t)sms * 2, kPartMaxCtas), (n + 1023) / 1024);
+  q.chunk = (n + q.ctas - 1) / q.ctas;
+  {
+    ProfScope p(ctx, "rank.count", s);
+    part_count_kernel<<<q.ctas, kPartThreads, 0, s>>>(q, n);
+  }
+  {
+    ProfScope p(ctx, "rank.scan", s);
+    part_scan_kernel<<<1, kScanThreads, 0, s>>>(q, n);
+  }
+  {
+    ProfScope p(ctx, "rank.scatter", s);
+    part_scatter_kernel<<<q.ctas, kPartThreads, 0, s>>>(q, n);
+  }
+  {
+    ProfScope p(ctx, "rank.local", s);
+    part_sort_kernel<<<q.P, kPartThreads, smem, s>>>(q, n, ids, order, f);
+  }
+  capi::count_launch(4);
+  return cudaGetLastError();
+}
+
 // count -> scan -> scatter -> local sort over keys whose range is already folded into the
 // bucket state (zeroed count / mm / overflow).  Emits the dispatch order.
 cudaError_t bucket_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_t* keys,
@@ -859,8 +1113,14 @@ cudaError_t bucket_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_
                          (int)local_smem);
     attr = true;
   }
-  Bucket b = make_bucket(base, L, keys);
   const int sms = sm_count(ctx->device);
+  Fallback f;
+  f.w = make_work(base, L);
+  f.meta = (uint4*)(base + L.meta_begin);
+  f.meta16 = (L.meta_end - L.meta_begin) / 16;
+  f.grid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 4);
+  if (L.part) return part_sort(ctx, base, L, keys, n, ids, order, f, sms, s);
+  Bucket b = make_bucket(base, L, keys);
   const unsigned g = (unsigned)((n + kStreamTile - 1) / kStreamTile);
   {
     ProfScope p(ctx, "rank.count", s);
@@ -875,11 +1135,6 @@ cudaError_t bucket_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_
     ProfScope p(ctx, "rank.scatter", s);
     bucket_scatter_kernel<<<g, 256, 0, s>>>(b, n);
   }
-  Fallback f;
-  f.w = make_work(base, L);
-  f.meta = (uint4*)(base + L.meta_begin);
-  f.meta16 = (L.meta_end - L.meta_begin) / 16;
-  f.grid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 4);
   {
     ProfScope p(ctx, "rank.local", s);
     bucket_local_kernel<<<b.nseg, kLocalThreads, local_smem, s>>>(b, n, ids, order, f);

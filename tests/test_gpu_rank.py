@@ -78,7 +78,7 @@ def test_order_check_helper_exempts_near_ties():
 
 # ---- bucket path (default): range bucketing + per-bucket shared-memory ranking, with the
 # device-side LSD fallback when one bucket exceeds a local-sort CTA's capacity
-@pytest.mark.parametrize("n", [4096 * 3 + 5, 262_144, 2_000_000])
+@pytest.mark.parametrize("n", [4096 * 3 + 5, 262_144, 2_000_000, 3_000_000])  # partition | bucket path
 def test_bucket_path_continuous_keys(abi, h, oracle, n):
     rng = np.random.default_rng(n + 11)
     key = rng.lognormal(5.0, 0.6, n) + 50.0  # score-like: no bucket overflows
