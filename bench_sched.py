@@ -10,8 +10,9 @@ next_request() pops (the engine's batch slots, sim.hpp:15-20).  Variants:
   rekey  : q_sat = 1e9, rebuild_threshold = 0: beta moves with every queue-length change, so
            the reference re-keys and re-heapifies the whole queue before EVERY pop.
 
-GPU side: tie_queue (paper_2604_00499_b200.GpuScheduler), wall-clocked per step including
-H2D/D2H.  CPU side: the untouched reference Scheduler (oracle/_ref, one thread -- the
+GPU side: tie_queue (paper_2604_00499_b200.GpuScheduler.step -> tie_queue_step: the whole
+iteration in one packed H2D, the kernels, one packed D2H and one sync), wall-clocked per step
+including H2D/D2H.  CPU side: the untouched reference Scheduler (oracle/_ref, one thread -- the
 reference scheduler is single-threaded) through oracle/ref_harness.cpp:ref_sched_bench,
 timed per step with steady_clock.  Both see identical inputs; the popped id sequences are
 compared (parity).
@@ -65,12 +66,14 @@ def run(tie, mc, sizes=(1000, 10_000, 100_000, 1_000_000), steps=120, per_step=3
             q.on_arrival_batch(ids[:n], np.zeros(n), mt[:n])
             q.on_prediction_batch(ids[:n], E, C)
             lat, popped = [], []
+            zeros = np.zeros(per_step)
             for s in range(steps):
                 lo, hi = n + s * per_step, n + (s + 1) * per_step
                 t0 = time.perf_counter()
-                q.on_arrival_batch(ids[lo:hi], np.zeros(per_step), mt[lo:hi])
-                q.on_prediction_logt(ids[lo:hi], mu[lo:hi], sg[lo:hi], mt[lo:hi])
-                got = q.next_requests(pops)
+                # one fused device round trip (tie_queue_step) == on_arrival_batch +
+                # on_prediction_logt + next_requests (tests/test_gpu_queue.py)
+                got = q.step(ids[lo:hi], zeros, mt[lo:hi], ids[lo:hi], mu[lo:hi], sg[lo:hi],
+                             mt[lo:hi], pops)
                 lat.append(time.perf_counter() - t0)
                 popped.append(got)
             gpu_pop = np.concatenate(popped)

@@ -167,6 +167,13 @@ int tie_queue_predict_logt(tie_queue* q, const uint64_t* ids, const double* mu,
                            const double* sigma, const uint32_t* max_tokens, uint64_t m);
 /* Scheduler::next_request() up to max_pops times (sched.cpp:169-175); out_ids[max_pops] */
 int tie_queue_next(tie_queue* q, uint64_t max_pops, uint64_t* out_ids, uint64_t* n_out);
+/* One scheduler iteration with one device round trip: on_arrival x n_arr, the run_sim scoring
+ * chain + on_prediction x n_pred, next_request() up to max_pops times (sched.cpp:125-175,
+ * sim.cpp:85-95).  Same results / errors as the three calls above in sequence. */
+int tie_queue_step(tie_queue* q, const uint64_t* arr_ids, const double* arr_time,
+                   const uint32_t* arr_max_tokens, uint64_t n_arr, const uint64_t* pred_ids,
+                   const double* mu, const double* sigma, const uint32_t* pred_max_tokens,
+                   uint64_t n_pred, uint64_t max_pops, uint64_t* out_ids, uint64_t* n_out);
 /* Scheduler::rebuild_if_drifted() (sched.cpp:152-167) */
 int tie_queue_rebuild_if_drifted(tie_queue* q, int* rebuilt);
 

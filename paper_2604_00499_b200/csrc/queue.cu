@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <map>
 #include <string>
 #include <unordered_map>
@@ -163,11 +164,91 @@ __global__ void write_predictions_kernel(QDev q, const uint32_t* slots, uint64_t
   q.predicted[s] = 1;
 }
 
+// fused step: run_sim's fixup C = max(C, E) (sim.cpp:94) and the compute_score checks
+// (sched.cpp:19-26) on the device; failures go to the context's error word (first index wins)
+// and make the dependent kernels of the step skip.  key = E + beta C.
+__global__ void predict_keys_kernel(const double* E, double* C, uint64_t m, double beta,
+                                    double* key, unsigned long long* err) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const double e = E[t];
+  double c = C[t];
+  c = c < e ? e : c;
+  C[t] = c;
+  uint32_t why = kOk;
+  if (!isfinite(e) || !isfinite(c) || !isfinite(beta)) why = kScoreNotFinite;
+  else if (!(e > 0.0)) why = kExpectationNonPos;
+  else if (c < e) why = kCvarBelowE;
+  if (why != kOk) report(err, t, why);
+  key[t] = __dadd_rn(e, __dmul_rn(beta, c));
+}
+
+__global__ void write_predictions_checked_kernel(QDev q, const uint32_t* slots, uint64_t m,
+                                                 const double* E, const double* C,
+                                                 const double* key, double beta,
+                                                 const unsigned long long* err) {
+  if (*(const volatile unsigned long long*)err != ~0ull) return;
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const uint32_t s = slots[t];
+  q.key[s] = order_bits(key[t]);
+  q.E[s] = E[t];
+  q.C[s] = C[t];
+  q.beta[s] = beta;
+  q.predicted[s] = 1;
+}
+
+__global__ void __launch_bounds__(256) refresh_blocks_checked_kernel(
+    QDev q, const uint32_t* list, uint32_t nb, uint64_t n_slots, const unsigned long long* err,
+    uint32_t n_unconditional) {
+  __shared__ uint64_t sk[32], si[32];
+  __shared__ uint32_t ss[32];
+  const bool skip = *(const volatile unsigned long long*)err != ~0ull;
+  for (uint32_t j = blockIdx.x; j < nb; j += gridDim.x)
+    if (j < n_unconditional || !skip) refresh_block(q, list[j], n_slots, sk, si, ss);
+}
+
 // key = compute_score(E, C, beta) for the batch (sched.cpp:19-26, arguments pre-validated)
 __global__ void batch_keys_kernel(const double* E, const double* C, uint64_t m, double beta,
                                   double* key) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < m) key[t] = __dadd_rn(E[t], __dmul_rn(beta, C[t]));
+}
+
+// drift rebuild fused with the block-minimum refresh: one CTA per 1024-slot block re-keys its
+// live predicted entries with beta_now (sched.cpp:159-164) and recomputes the block minimum
+__global__ void __launch_bounds__(256) rekey_refresh_kernel(QDev q, uint32_t nb,
+                                                            uint64_t n_slots, double beta_now,
+                                                            const unsigned long long* err) {
+  __shared__ uint64_t sk[32], si[32];
+  __shared__ uint32_t ss[32];
+  if (err && *(const volatile unsigned long long*)err != ~0ull) return;  // failed fused step
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    uint64_t k = kDead, i = kDead;
+    uint32_t s = 0;
+    for (uint32_t t = threadIdx.x; t < kBlockSlots; t += blockDim.x) {
+      const uint64_t slot = (uint64_t)b * kBlockSlots + t;
+      if (slot >= n_slots) break;
+      uint64_t kk = q.key[slot];
+      if (kk != kDead && q.predicted[slot]) {
+        kk = order_bits(__dadd_rn(q.E[slot], __dmul_rn(beta_now, q.C[slot])));
+        q.key[slot] = kk;
+        q.beta[slot] = beta_now;
+      }
+      const uint64_t ii = q.id[slot];
+      if (less_kv(kk, ii, k, i)) {
+        k = kk;
+        i = ii;
+        s = (uint32_t)slot;
+      }
+    }
+    block_argmin(k, i, s, sk, si, ss);
+    if (threadIdx.x == 0) {
+      q.bkey[b] = k;
+      q.bid[b] = i;
+      q.bslot[b] = s;
+    }
+  }
 }
 
 // drift rebuild: re-key every live predicted entry with beta_now (sched.cpp:159-164)
@@ -180,36 +261,255 @@ __global__ void rekey_kernel(QDev q, uint64_t n_slots, double beta_now) {
   }
 }
 
-// up to `pops` pop_min()s with fixed keys (sched.cpp:81-94): argmin over block minima,
-// kill the slot, refresh its block.  Writes popped (id, slot) and the count.
-__global__ void __launch_bounds__(1024) pop_kernel(QDev q, uint32_t nblocks, uint64_t n_slots,
-                                                   uint32_t pops, uint64_t* out_id,
-                                                   uint32_t* out_slot, uint32_t* out_n) {
+// Up to `pops` pop_min()s with fixed keys in ONE pass (no drift rebuild can fire between
+// them): with fixed keys the pop sequence is the `pops` smallest (key, id) entries in order.
+// Let v_1 < ... < v_B be the B smallest block minima; the B smallest entries are all <= v_B
+// and lie in those B blocks, so the candidates are the entries <= v_B of those blocks, ranked
+// by counting.  Then the popped slots die and their blocks' minima are refreshed (one warp
+// per block).  *skip != 0 (an invalid prediction in the same fused step): pop nothing.
+constexpr int kTopB = 32;            // pops per launch
+constexpr int kCandCap = 2048;       // candidates held in shared memory
+__device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64_t n_slots,
+                                         uint32_t pops, uint64_t* out_id, uint32_t* out_slot,
+                                         uint32_t* out_n) {
   __shared__ uint64_t sk[32], si[32];
   __shared__ uint32_t ss[32];
-  uint32_t done = 0;
-  for (; done < pops; ++done) {
-    uint64_t k = kDead, i = kDead;
-    uint32_t s = 0;
-    for (uint32_t b = threadIdx.x; b < nblocks; b += blockDim.x) {
-      const uint64_t kk = q.bkey[b], ii = q.bid[b];
+  __shared__ uint32_t chosen[kTopB];
+  __shared__ uint64_t ck[kCandCap], ci[kCandCap];
+  __shared__ uint32_t cs[kCandCap];
+  __shared__ uint32_t ncand, overflow;
+  if (threadIdx.x == 0) {
+    ncand = 0;
+    overflow = 0;
+  }
+  // 1. the B smallest block minima (B rounds of a CTA argmin; a thread's local best is
+  //    rescanned only when it wins)
+  auto local_best = [&](uint64_t& k, uint64_t& i, uint32_t& b, const uint32_t* excl, int nex) {
+    k = kDead;
+    i = kDead;
+    b = 0xffffffffu;
+    for (uint32_t x = threadIdx.x; x < nblocks; x += blockDim.x) {
+      bool ex = false;
+      for (int e = 0; e < nex; ++e) ex |= excl[e] == x;
+      if (ex) continue;
+      const uint64_t kk = q.bkey[x], ii = q.bid[x];
       if (less_kv(kk, ii, k, i)) {
         k = kk;
         i = ii;
-        s = q.bslot[b];
+        b = x;
       }
     }
-    block_argmin(k, i, s, sk, si, ss);
-    if (k == kDead) break;  // queue empty
-    if (threadIdx.x == 0) {
-      out_id[done] = i;
-      out_slot[done] = s;
-      q.key[s] = kDead;
-    }
+  };
+  uint64_t lk, li;
+  uint32_t lb;
+  local_best(lk, li, lb, chosen, 0);
+  uint32_t nchosen = 0;
+  uint64_t vB_k = kDead, vB_i = kDead;
+  for (uint32_t r = 0; r < pops; ++r) {
+    uint64_t k = lk, i = li;
+    uint32_t b = lb;
+    block_argmin(k, i, b, sk, si, ss);
+    if (k == kDead) break;  // fewer live blocks than pops
+    if (threadIdx.x == 0) chosen[r] = b;
     __syncthreads();
-    refresh_block(q, s / kBlockSlots, n_slots, sk, si, ss);
+    nchosen = r + 1;
+    vB_k = k;
+    vB_i = i;
+    if (lb == b) local_best(lk, li, lb, chosen, (int)nchosen);
   }
-  if (threadIdx.x == 0) *out_n = done;
+  if (nchosen == 0) {
+    if (threadIdx.x == 0) *out_n = 0;
+    return;
+  }
+  if (nchosen < pops) {  // every live block is chosen: all their live entries are candidates
+    vB_k = kDead;
+    vB_i = kDead;
+  }
+  // 2. candidates: entries <= v_B of the chosen blocks
+  for (uint32_t t = threadIdx.x; t < nchosen * kBlockSlots; t += blockDim.x) {
+    const uint64_t slot = (uint64_t)chosen[t / kBlockSlots] * kBlockSlots + t % kBlockSlots;
+    if (slot >= n_slots) continue;
+    const uint64_t kk = q.key[slot];
+    if (kk == kDead) continue;
+    const uint64_t ii = q.id[slot];
+    if (less_kv(vB_k, vB_i, kk, ii)) continue;  // > v_B
+    const uint32_t c = atomicAdd(&ncand, 1u);
+    if (c < kCandCap) {
+      ck[c] = kk;
+      ci[c] = ii;
+      cs[c] = (uint32_t)slot;
+    } else {
+      overflow = 1;
+    }
+  }
+  __syncthreads();
+  const uint32_t nc = min(ncand, (uint32_t)kCandCap);
+  if (overflow) {  // pathological key layout: fall back to one argmin + refresh per pop
+    uint32_t done = 0;
+    for (; done < pops; ++done) {
+      uint64_t k = kDead, i = kDead;
+      uint32_t s = 0;
+      for (uint32_t b = threadIdx.x; b < nblocks; b += blockDim.x) {
+        const uint64_t kk = q.bkey[b], ii = q.bid[b];
+        if (less_kv(kk, ii, k, i)) {
+          k = kk;
+          i = ii;
+          s = q.bslot[b];
+        }
+      }
+      block_argmin(k, i, s, sk, si, ss);
+      if (k == kDead) break;
+      if (threadIdx.x == 0) {
+        out_id[done] = i;
+        out_slot[done] = s;
+        q.key[s] = kDead;
+      }
+      __syncthreads();
+      refresh_block(q, s / kBlockSlots, n_slots, sk, si, ss);
+    }
+    if (threadIdx.x == 0) *out_n = done;
+    return;
+  }
+  // 3. rank the candidates; the first min(pops, nc) in (key, id) order are the pops
+  const uint32_t npop = min(pops, nc);
+  for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
+    uint32_t rank = 0;
+    for (uint32_t d = 0; d < nc; ++d) rank += less_kv(ck[d], ci[d], ck[c], ci[c]) ? 1u : 0u;
+    if (rank < npop) {
+      out_id[rank] = ci[c];
+      out_slot[rank] = cs[c];
+      q.key[cs[c]] = kDead;
+    }
+  }
+  if (threadIdx.x == 0) *out_n = npop;
+  __syncthreads();
+  // 4. refresh every chosen block (popped blocks are among them): one warp per block
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t e = warp; e < nchosen; e += blockDim.x >> 5) {
+    const uint32_t blk = chosen[e];
+    uint64_t k = kDead, i = kDead;
+    uint32_t s = 0;
+    for (uint32_t t = lane; t < kBlockSlots; t += 32) {
+      const uint64_t slot = (uint64_t)blk * kBlockSlots + t;
+      if (slot < n_slots) {
+        const uint64_t kk = q.key[slot], ii = q.id[slot];
+        if (less_kv(kk, ii, k, i)) {
+          k = kk;
+          i = ii;
+          s = (uint32_t)slot;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t k2 = __shfl_down_sync(0xffffffffu, k, o);
+      const uint64_t i2 = __shfl_down_sync(0xffffffffu, i, o);
+      const uint32_t s2 = __shfl_down_sync(0xffffffffu, s, o);
+      if (less_kv(k2, i2, k, i)) {
+        k = k2;
+        i = i2;
+        s = s2;
+      }
+    }
+    if (lane == 0) {
+      q.bkey[blk] = k;
+      q.bid[blk] = i;
+      q.bslot[blk] = s;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) pop_topb_kernel(QDev q, uint32_t nblocks,
+                                                        uint64_t n_slots, uint32_t pops,
+                                                        uint64_t* out_id, uint32_t* out_slot,
+                                                        uint32_t* out_n) {
+  pop_topb(q, nblocks, n_slots, pops, out_id, out_slot, out_n);
+}
+
+// A small scheduler iteration in ONE kernel (one CTA): write the arrivals' slots; check the
+// predictions (run_sim's max(C, E), compute_score, plus the score kernel's own validation
+// in the error word) and -- only if all pass -- key and write them; refresh the touched
+// blocks; then the fixed-key pops.  Any error: no prediction written, nothing popped.
+__global__ void __launch_bounds__(1024) step_apply_kernel(
+    QDev q, uint64_t first, uint64_t n_arr, const uint64_t* arr_ids, const double* arr_keys,
+    const uint32_t* slots, uint64_t np, const double* E, double* C, double beta,
+    const uint32_t* blocks, uint32_t nblk, uint32_t n_uncond, uint32_t nblocks, uint64_t n_slots,
+    uint32_t pops, uint64_t* out_id, uint32_t* out_slot, uint32_t* out_n,
+    unsigned long long* err) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (uint64_t t = threadIdx.x; t < n_arr; t += blockDim.x) {
+    const uint64_t s = first + t;
+    q.key[s] = order_bits(arr_keys[t]);
+    q.id[s] = arr_ids[t];
+    q.predicted[s] = 0;
+  }
+  for (uint64_t t = threadIdx.x; t < np; t += blockDim.x) {
+    const double e = E[t];
+    double c = C[t];
+    c = c < e ? e : c;  // sim.cpp:94
+    C[t] = c;
+    uint32_t why = kOk;
+    if (!isfinite(e) || !isfinite(c) || !isfinite(beta)) why = kScoreNotFinite;
+    else if (!(e > 0.0)) why = kExpectationNonPos;
+    else if (c < e) why = kCvarBelowE;
+    if (why != kOk) {
+      report(err, t, why);
+      bad = 1;
+    }
+  }
+  __syncthreads();
+  const bool skip = bad || *(const volatile unsigned long long*)err != ~0ull;
+  if (!skip)
+    for (uint64_t t = threadIdx.x; t < np; t += blockDim.x) {
+      const uint32_t s = slots[t];
+      q.key[s] = order_bits(__dadd_rn(E[t], __dmul_rn(beta, C[t])));
+      q.E[s] = E[t];
+      q.C[s] = C[t];
+      q.beta[s] = beta;
+      q.predicted[s] = 1;
+    }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t e = warp; e < (skip ? n_uncond : nblk); e += blockDim.x >> 5) {
+    const uint32_t blk = blocks[e];
+    uint64_t k = kDead, i = kDead;
+    uint32_t s = 0;
+    for (uint32_t t = lane; t < kBlockSlots; t += 32) {
+      const uint64_t slot = (uint64_t)blk * kBlockSlots + t;
+      if (slot < n_slots) {
+        const uint64_t kk = q.key[slot], ii = q.id[slot];
+        if (less_kv(kk, ii, k, i)) {
+          k = kk;
+          i = ii;
+          s = (uint32_t)slot;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t k2 = __shfl_down_sync(0xffffffffu, k, o);
+      const uint64_t i2 = __shfl_down_sync(0xffffffffu, i, o);
+      const uint32_t s2 = __shfl_down_sync(0xffffffffu, s, o);
+      if (less_kv(k2, i2, k, i)) {
+        k = k2;
+        i = i2;
+        s = s2;
+      }
+    }
+    if (lane == 0) {
+      q.bkey[blk] = k;
+      q.bid[blk] = i;
+      q.bslot[blk] = s;
+    }
+  }
+  __syncthreads();
+  if (skip || pops == 0) {
+    if (threadIdx.x == 0) *out_n = 0;
+    return;
+  }
+  pop_topb(q, nblocks, n_slots, pops, out_id, out_slot, out_n);
 }
 
 }  // namespace
@@ -249,6 +549,9 @@ struct tie_queue {
   uint32_t* d_out_slot = nullptr;
   uint32_t* d_out_n = nullptr;
   uint64_t stage_cap = 0;
+  char* h_pack = nullptr;         // pinned H2D pack of a fused step
+  char* d_pack = nullptr;
+  uint64_t pack_cap = 0;
   uint64_t* h_out_id = nullptr;   // pinned
   uint32_t* h_out_slot = nullptr;
   uint32_t* h_out_n = nullptr;
@@ -266,15 +569,17 @@ int ensure_stage(tie_queue* Q, uint64_t m) {
   if (m <= Q->stage_cap) return TIE_OK;
   cudaFree(Q->d_ids); cudaFree(Q->d_a); cudaFree(Q->d_b); cudaFree(Q->d_c);
   cudaFree(Q->d_slots); cudaFree(Q->d_blocks); cudaFree(Q->d_out_id); cudaFree(Q->d_out_slot);
-  cudaFreeHost(Q->h_out_id); cudaFreeHost(Q->h_out_slot);
+  cudaFree(Q->d_out_n);
+  cudaFreeHost(Q->h_out_id); cudaFreeHost(Q->h_out_slot); cudaFreeHost(Q->h_out_n);
   const uint64_t cap = std::max<uint64_t>(m, 1024);
   cudaError_t e = cudaSuccess;
   if ((e = cudaMalloc(&Q->d_ids, 8 * cap)) || (e = cudaMalloc(&Q->d_a, 8 * cap)) ||
       (e = cudaMalloc(&Q->d_b, 8 * cap)) || (e = cudaMalloc(&Q->d_c, 8 * cap)) ||
       (e = cudaMalloc(&Q->d_slots, 4 * cap)) || (e = cudaMalloc(&Q->d_blocks, 4 * cap)) ||
       (e = cudaMalloc(&Q->d_out_id, 8 * cap)) || (e = cudaMalloc(&Q->d_out_slot, 4 * cap)) ||
+      (e = cudaMalloc(&Q->d_out_n, 4 * cap)) ||
       (e = cudaMallocHost(&Q->h_out_id, 8 * cap)) ||
-      (e = cudaMallocHost(&Q->h_out_slot, 4 * cap)))
+      (e = cudaMallocHost(&Q->h_out_slot, 4 * cap)) || (e = cudaMallocHost(&Q->h_out_n, 4 * cap)))
     return cuda_error(e, "tie_queue: staging allocation");
   Q->stage_cap = cap;
   return TIE_OK;
@@ -297,18 +602,29 @@ int refresh(tie_queue* Q, const std::vector<uint32_t>& slots, cudaStream_t s) {
   return TIE_OK;
 }
 
+void rebuild_launch(tie_queue* Q, double now, cudaStream_t s,
+                    const unsigned long long* err = nullptr);
+void rebuild_mirror(tie_queue* Q, double now);
+
 int rebuild_all(tie_queue* Q, double now, cudaStream_t s) {  // sched.cpp:156-166
-  const unsigned g = (unsigned)std::min<uint64_t>((Q->n_slots + 255) / 256, 148 * 8);
-  if (g) tie::dev::rekey_kernel<<<g, 256, 0, s>>>(Q->q, Q->n_slots, now);
+  rebuild_launch(Q, now, s);
+  rebuild_mirror(Q, now);
+  return TIE_OK;
+}
+
+void rebuild_launch(tie_queue* Q, double now, cudaStream_t s,
+                    const unsigned long long* err) {
   const uint32_t nb = (uint32_t)((Q->n_slots + tie::dev::kBlockSlots - 1) / tie::dev::kBlockSlots);
-  if (nb) tie::dev::refresh_blocks_kernel<<<std::min<uint32_t>(nb, 148 * 16), 256, 0, s>>>(
-      Q->q, nullptr, nb, Q->n_slots);
-  tie::capi::count_launch(2);
+  if (nb) tie::dev::rekey_refresh_kernel<<<std::min<uint32_t>(nb, 148 * 16), 256, 0, s>>>(
+      Q->q, nb, Q->n_slots, now, err);
+  tie::capi::count_launch(1);
+}
+
+void rebuild_mirror(tie_queue* Q, double now) {
   Q->betas.clear();
   if (Q->n_predicted) Q->betas[now] = Q->n_predicted;
   ++Q->epoch;  // every live predicted slot's beta_at_update is now `now`
   Q->rebuild_beta = now;
-  return TIE_OK;
 }
 
 double drift(const tie_queue* Q, double now) {
@@ -316,19 +632,53 @@ double drift(const tie_queue* Q, double now) {
                   std::fabs(now - Q->betas.rbegin()->first));
 }
 
-// device pops with fixed keys; appends popped ids to `out`, updates the host mirror
-int pop_fixed(tie_queue* Q, uint32_t pops, std::vector<uint64_t>& out, cudaStream_t s) {
-  if (int rc = ensure_stage(Q, pops)) return rc;
-  const uint32_t nb = (uint32_t)((Q->n_slots + tie::dev::kBlockSlots - 1) / tie::dev::kBlockSlots);
-  tie::dev::pop_kernel<<<1, 1024, 0, s>>>(Q->q, nb, Q->n_slots, pops, Q->d_out_id,
-                                          Q->d_out_slot, Q->d_out_n);
-  tie::capi::count_launch();
-  cudaMemcpyAsync(Q->h_out_n, Q->d_out_n, 4, cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(Q->h_out_slot, Q->d_out_slot, 4 * pops, cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(Q->h_out_id, Q->d_out_id, 8 * pops, cudaMemcpyDeviceToHost, s);
-  const cudaError_t e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return cuda_error(e, "tie_queue_next");
-  for (uint32_t j = 0; j < *Q->h_out_n; ++j) {
+// ---- pop planning: Scheduler::next_request() x left (sched.cpp:152-175) as a sequence of
+// segments [drift rebuild?][fixed-key pops], planned on the host as far as the rebuild
+// decisions are certain without seeing which entries the device pops:
+//   * the multiset betas_in_use_ has n_predicted entries and only loses entries to pops, so
+//     its range can only shrink and it is non-empty while n_predicted > pops so far;
+//   * its range is exact at the start, after a rebuild (a single value) and while it holds a
+//     single value; drift <= threshold over the (possibly wider) tracked range means "no
+//     rebuild" for sure;
+//   * a rebuild that would need the exact shrunken range, or the multiset's emptiness, ends
+//     the plan (execute, sync, plan again).
+struct Seg {
+  bool rebuild;
+  double beta;
+  uint32_t pops;
+};
+
+std::vector<Seg> plan_pops(const tie_queue* Q, uint64_t left) {
+  std::vector<Seg> plan;
+  const bool tie_policy = Q->policy == 2;
+  bool empty = Q->betas.empty();
+  double lo = empty ? 0.0 : Q->betas.begin()->first;
+  double hi = empty ? 0.0 : Q->betas.rbegin()->first;
+  bool exact = true;
+  for (uint64_t j = 0; j < left; ++j) {
+    bool rebuild = false;
+    double now = 0.0;
+    if (tie_policy && !empty) {
+      now = beta_at(Q, Q->size - j);
+      const double d = std::max(std::fabs(now - lo), std::fabs(now - hi));
+      if (d > Q->threshold) {
+        if (!(exact && Q->n_predicted > j)) break;  // uncertain: stop here
+        rebuild = true;
+        lo = hi = now;
+        exact = true;
+      }
+    }
+    if (rebuild || plan.empty() || plan.back().pops >= (uint32_t)tie::dev::kTopB)
+      plan.push_back({rebuild, now, 0});
+    ++plan.back().pops;
+    if (lo != hi) exact = false;
+  }
+  return plan;
+}
+
+// host mirror of `cnt` device pops (ids / slots in h_out_*, from offset `off`)
+void apply_pops(tie_queue* Q, uint32_t off, uint32_t cnt, std::vector<uint64_t>& out) {
+  for (uint32_t j = off; j < off + cnt; ++j) {
     const uint32_t sl = Q->h_out_slot[j];
     out.push_back(Q->h_out_id[j]);
     Q->alive[sl] = 0;
@@ -340,6 +690,58 @@ int pop_fixed(tie_queue* Q, uint32_t pops, std::vector<uint64_t>& out, cudaStrea
       --Q->n_predicted;
     }
   }
+}
+
+// launch a plan's kernels: segment g = [rebuild][pops -> d_out_*[off..], d_out_n[g]]; a set
+// error word (a failed fused step) makes every kernel skip
+uint64_t launch_plan(tie_queue* Q, const std::vector<Seg>& plan, size_t first_seg,
+                     uint32_t off, cudaStream_t s, unsigned long long* err) {
+  const uint32_t nb = (uint32_t)((Q->n_slots + tie::dev::kBlockSlots - 1) / tie::dev::kBlockSlots);
+  for (size_t g = first_seg; g < plan.size(); ++g) {
+    if (plan[g].rebuild) rebuild_launch(Q, plan[g].beta, s, err);
+    tie::dev::step_apply_kernel<<<1, 1024, 0, s>>>(
+        Q->q, 0, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0.0, nullptr, 0, 0, nb,
+        Q->n_slots, plan[g].pops, Q->d_out_id + off, Q->d_out_slot + off, Q->d_out_n + g, err);
+    off += plan[g].pops;
+  }
+  tie::capi::count_launch(plan.size() - first_seg);
+  return off;
+}
+
+// D2H of a plan's results (issued after launch_plan)
+void fetch_plan(tie_queue* Q, size_t nseg, uint64_t total, cudaStream_t s) {
+  cudaMemcpyAsync(Q->h_out_n, Q->d_out_n, 4 * std::max<size_t>(nseg, 1), cudaMemcpyDeviceToHost,
+                  s);
+  if (total) {
+    cudaMemcpyAsync(Q->h_out_slot, Q->d_out_slot, 4 * total, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(Q->h_out_id, Q->d_out_id, 8 * total, cudaMemcpyDeviceToHost, s);
+  }
+}
+
+// host mirror of a finished plan, segment by segment (rebuild bookkeeping, then its pops);
+// returns false when the queue ran dry
+bool replay_plan(tie_queue* Q, const std::vector<Seg>& plan, std::vector<uint64_t>& out) {
+  uint32_t off = 0;
+  for (size_t g = 0; g < plan.size(); ++g) {
+    if (plan[g].rebuild) rebuild_mirror(Q, plan[g].beta);
+    apply_pops(Q, off, Q->h_out_n[g], out);
+    if (Q->h_out_n[g] < plan[g].pops) return false;
+    off += plan[g].pops;
+  }
+  return true;
+}
+
+// run a plan: all rebuild + pop kernels back to back, one packed D2H, one sync, replay
+int execute_plan(tie_queue* Q, const std::vector<Seg>& plan, std::vector<uint64_t>& out,
+                 cudaStream_t s) {
+  uint64_t total = 0;
+  for (const Seg& g : plan) total += g.pops;
+  if (int rc = ensure_stage(Q, std::max<uint64_t>(total, plan.size() + 1))) return rc;
+  launch_plan(Q, plan, 0, 0, s, Q->ctx->d_err);
+  fetch_plan(Q, plan.size(), total, s);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_error(e, "tie_queue_next");
+  replay_plan(Q, plan, out);
   return TIE_OK;
 }
 
@@ -379,7 +781,7 @@ int tie_queue_create(tie_ctx* ctx, int policy, int adaptive, double beta_fixed, 
       (e = cudaMalloc(&Q->q.beta, 8 * capacity)) ||
       (e = cudaMalloc(&Q->q.predicted, capacity)) || (e = cudaMalloc(&Q->q.bkey, 8 * nb)) ||
       (e = cudaMalloc(&Q->q.bid, 8 * nb)) || (e = cudaMalloc(&Q->q.bslot, 4 * nb)) ||
-      (e = cudaMalloc(&Q->d_out_n, 4)) || (e = cudaMallocHost(&Q->h_out_n, 4))) {
+      ensure_stage(Q, 1024) != TIE_OK) {
     tie_queue_destroy(Q);
     return cuda_error(e, "tie_queue_create");
   }
@@ -402,6 +804,8 @@ void tie_queue_destroy(tie_queue* Q) {
   cudaFreeHost(Q->h_out_id);
   cudaFreeHost(Q->h_out_slot);
   cudaFreeHost(Q->h_out_n);
+  cudaFreeHost(Q->h_pack);
+  cudaFree(Q->d_pack);
   delete Q;
 }
 
@@ -525,27 +929,224 @@ int tie_queue_next(tie_queue* Q, uint64_t max_pops, uint64_t* out_ids, uint64_t*
   cudaStream_t s = Q->ctx->stream;
   uint64_t left = std::min<uint64_t>(max_pops, Q->size);
   while (left > 0) {
-    const bool tie_policy = Q->policy == 2;
-    // can a rebuild fire during the next `left` pops?  (drift only shrinks as pops erase)
-    uint64_t safe = left;
-    if (tie_policy && !Q->betas.empty()) {
-      safe = 0;
-      while (safe < left && !(drift(Q, beta_at(Q, Q->size - safe)) > Q->threshold)) ++safe;
-    }
-    if (safe == 0) {  // rebuild now (exact check with the current multiset), then one pop
+    std::vector<Seg> plan = plan_pops(Q, left);
+    if (plan.empty()) {  // the very first decision is uncertain only if... never: j = 0 exact
       const double now = beta_at(Q, Q->size);
-      if (drift(Q, now) > Q->threshold)
-        if (int rc = rebuild_all(Q, now, s)) return rc;
-      safe = 1;
+      plan.push_back({true, now, 1});
     }
     const size_t before = got.size();
-    if (int rc = pop_fixed(Q, (uint32_t)safe, got, s)) return rc;
+    if (int rc = execute_plan(Q, plan, got, s)) return rc;
     const uint64_t popped = got.size() - before;
     if (popped == 0) break;
     left -= popped;
   }
   for (size_t j = 0; j < got.size(); ++j) out_ids[j] = got[j];
   *n_out = got.size();
+  return TIE_OK;
+}
+
+// One scheduler iteration in ONE device round trip: Scheduler::on_arrival x n_arr, then
+// run_sim's scoring chain + Scheduler::on_prediction x n_pred (sim.cpp:85-95,
+// sched.cpp:134-150), then Scheduler::next_request() up to max_pops times (sched.cpp:169-175).
+// Same results and errors as tie_queue_arrive + tie_queue_predict_logt + tie_queue_next: all
+// host validation first, then one packed H2D, the kernels (the score / compute_score checks
+// run on the device and make the writes and pops skip), one packed D2H and one sync.  Pops
+// that a drift rebuild could precede continue through tie_queue_next.
+int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time,
+                   const uint32_t* arr_max_tokens, uint64_t n_arr, const uint64_t* pred_ids,
+                   const double* mu, const double* sigma, const uint32_t* pred_max_tokens,
+                   uint64_t n_pred, uint64_t max_pops, uint64_t* out_ids, uint64_t* n_out) {
+  if (!Q || !n_out) return set_error(TIE_EINVALID, "tie_queue: null argument");
+  *n_out = 0;
+  tie_ctx* ctx = Q->ctx;
+  cudaStream_t s = ctx->stream;
+  // ---- arrivals: host validation (tie_queue_arrive)
+  if (Q->n_slots + n_arr > Q->capacity)
+    return set_error(TIE_EINVALID, "tie_queue_arrive: capacity exceeded");
+  std::vector<double> akeys(n_arr);
+  for (uint64_t t = 0; t < n_arr; ++t) {
+    akeys[t] = Q->policy == 0 ? arr_time[t] : (double)arr_max_tokens[t];
+    if (!std::isfinite(akeys[t]))
+      return set_error(TIE_EDOMAIN, "WaitingQueue::push: key must be finite");
+    if (Q->slot_of.count(arr_ids[t]))
+      return set_error(TIE_EINVALID, "WaitingQueue::push: id " + std::to_string(arr_ids[t]) +
+                                         " already queued");
+  }
+  {
+    std::vector<uint64_t> srt(arr_ids, arr_ids + n_arr);
+    std::sort(srt.begin(), srt.end());
+    if (std::adjacent_find(srt.begin(), srt.end()) != srt.end())
+      return set_error(TIE_EINVALID, "WaitingQueue::push: id already queued");
+  }
+  const uint64_t first = Q->n_slots;
+  for (uint64_t t = 0; t < n_arr; ++t) {
+    Q->slot_of.emplace(arr_ids[t], (uint32_t)(first + t));
+    Q->alive[first + t] = 1;
+  }
+  Q->n_slots += n_arr;
+  Q->size += n_arr;
+  std::vector<uint32_t> blocks;  // refreshed unconditionally (arrivals) | if no error (preds)
+  if (n_arr) {
+    for (uint64_t t = 0; t < n_arr; t += tie::dev::kBlockSlots)
+      blocks.push_back((uint32_t)((first + t) / tie::dev::kBlockSlots));
+    blocks.push_back((uint32_t)((first + n_arr - 1) / tie::dev::kBlockSlots));
+    std::sort(blocks.begin(), blocks.end());
+    blocks.erase(std::unique(blocks.begin(), blocks.end()), blocks.end());
+  }
+  const uint32_t n_uncond = (uint32_t)blocks.size();
+  // ---- predictions: host validation (tie_queue_predict); FCFS ignores them
+  const bool use_pred = n_pred > 0 && Q->policy != 0;
+  std::vector<uint32_t> slots(n_pred);
+  for (uint64_t t = 0; t < n_pred; ++t) {
+    auto it = Q->slot_of.find(pred_ids[t]);
+    if (it == Q->slot_of.end())
+      return set_error(TIE_EINVALID, "Scheduler::on_prediction: id " +
+                                         std::to_string(pred_ids[t]) + " not waiting");
+    slots[t] = it->second;
+  }
+  const double beta = Q->policy == 1 ? 0.0 : beta_at(Q, Q->size);
+  if (use_pred) {
+    std::vector<uint32_t> srt(slots);
+    std::sort(srt.begin(), srt.end());
+    for (uint64_t t = 0; t < n_pred; ++t)
+      if (Q->predicted[slots[t]] || (t + 1 < n_pred && srt[t] == srt[t + 1]))
+        return set_error(TIE_EINVALID, "Scheduler::on_prediction: id " +
+                                           std::to_string(pred_ids[t]) + " already predicted");
+    std::vector<uint32_t> pb;
+    for (uint32_t sl : slots) pb.push_back(sl / tie::dev::kBlockSlots);
+    std::sort(pb.begin(), pb.end());
+    pb.erase(std::unique(pb.begin(), pb.end()), pb.end());
+    for (uint32_t b : pb)
+      if (!std::binary_search(blocks.begin(), blocks.begin() + n_uncond, b)) blocks.push_back(b);
+  }
+  // ---- predictions' host mirror, tentatively (rolled back if the device rejects them), so
+  // the pop plan sees betas_in_use_ as the reference's next_request() will
+  auto pred_mirror = [&](bool apply) {
+    for (uint32_t sl : slots) {
+      Q->predicted[sl] = apply ? 1 : 0;
+      Q->pred_beta[sl] = beta;
+      Q->pred_epoch[sl] = Q->epoch;
+    }
+    if (apply) {
+      Q->betas[beta] += n_pred;
+      Q->n_predicted += n_pred;
+    } else {
+      auto it = Q->betas.find(beta);
+      if (it != Q->betas.end() && (it->second -= n_pred) == 0) Q->betas.erase(it);
+      Q->n_predicted -= n_pred;
+    }
+  };
+  if (use_pred) pred_mirror(true);
+  const uint64_t pops = std::min<uint64_t>(max_pops, Q->size);
+  const std::vector<Seg> plan = plan_pops(Q, pops);
+  uint64_t planned = 0;
+  for (const Seg& g : plan) planned += g.pops;
+  // segment 0's pops ride in the apply kernel unless a rebuild must precede them
+  const bool seg0_fused = !plan.empty() && !plan[0].rebuild;
+  const uint32_t fused_pops = seg0_fused ? plan[0].pops : 0;
+  // ---- pack: [arr ids | arr keys | mu | sigma | E | C | key | pred slots | pred max_tokens |
+  //            blocks]  (E, C, key: device-only scratch)
+  auto al = [](uint64_t x) { return (x + 255) & ~(uint64_t)255; };
+  const uint64_t np = use_pred ? n_pred : 0;
+  const uint64_t o_aid = 0, o_akey = o_aid + al(8 * n_arr), o_mu = o_akey + al(8 * n_arr),
+                 o_sg = o_mu + al(8 * np), o_E = o_sg + al(8 * np), o_C = o_E + al(8 * np),
+                 o_key = o_C + al(8 * np), o_slot = o_key + al(8 * np),
+                 o_mt = o_slot + al(4 * np), o_blk = o_mt + al(4 * np),
+                 total = o_blk + al(4 * blocks.size());
+  if (total > Q->pack_cap) {
+    cudaFreeHost(Q->h_pack);
+    cudaFree(Q->d_pack);
+    Q->h_pack = nullptr;
+    Q->d_pack = nullptr;
+    const uint64_t cap = std::max<uint64_t>(total, 1 << 20);
+    cudaError_t e;
+    if ((e = cudaMallocHost(&Q->h_pack, cap)) || (e = cudaMalloc(&Q->d_pack, cap))) {
+      if (use_pred) pred_mirror(false);
+      return cuda_error(e, "tie_queue_step: staging");
+    }
+    Q->pack_cap = cap;
+  }
+  if (int rc = ensure_stage(Q, std::max<uint64_t>(planned, plan.size() + 1))) {
+    if (use_pred) pred_mirror(false);
+    return rc;
+  }
+  char* h = Q->h_pack;
+  std::memcpy(h + o_aid, arr_ids, 8 * n_arr);
+  std::memcpy(h + o_akey, akeys.data(), 8 * n_arr);
+  if (np) {
+    std::memcpy(h + o_mu, mu, 8 * np);
+    std::memcpy(h + o_sg, sigma, 8 * np);
+    std::memcpy(h + o_slot, slots.data(), 4 * np);
+    std::memcpy(h + o_mt, pred_max_tokens, 4 * np);
+  }
+  std::memcpy(h + o_blk, blocks.data(), 4 * blocks.size());
+  char* d = Q->d_pack;
+  // H2D up to E (the arrays behind mu/sigma are device scratch, then slots/mt/blocks)
+  cudaMemcpyAsync(d, h, o_E, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d + o_slot, h + o_slot, total - o_slot, cudaMemcpyHostToDevice, s);
+  ctx->err_op = "tie_queue_step";
+  const uint32_t nb = (uint32_t)((Q->n_slots + tie::dev::kBlockSlots - 1) / tie::dev::kBlockSlots);
+  if (np) {
+    const cudaError_t e = tie::dev::launch_score(
+        ctx, (const double*)(d + o_mu), (const double*)(d + o_sg), d + o_mt, true, np, Q->alpha,
+        0.0, (double*)(d + o_E), (double*)(d + o_C), nullptr, nullptr, nullptr, TIE_SCORE_RAW,
+        s);
+    if (e != cudaSuccess) {
+      pred_mirror(false);
+      return cuda_error(e, "tie_queue_step");
+    }
+  }
+  uint32_t* seg0_n = Q->d_out_n + (seg0_fused ? 0 : plan.size());  // unused slot if not fused
+  const bool small = n_arr <= 16384 && np <= 16384 && blocks.size() <= 4096;
+  if (small) {  // everything after the scoring in one single-CTA kernel
+    tie::dev::step_apply_kernel<<<1, 1024, 0, s>>>(
+        Q->q, first, n_arr, (const uint64_t*)(d + o_aid), (const double*)(d + o_akey),
+        (const uint32_t*)(d + o_slot), np, (const double*)(d + o_E), (double*)(d + o_C), beta,
+        (const uint32_t*)(d + o_blk), (uint32_t)blocks.size(), n_uncond, nb, Q->n_slots,
+        fused_pops, Q->d_out_id, Q->d_out_slot, seg0_n, ctx->d_err);
+    tie::capi::count_launch(1);
+  } else {
+    if (n_arr)
+      tie::dev::write_slots_kernel<<<(unsigned)((n_arr + 255) / 256), 256, 0, s>>>(
+          Q->q, first, n_arr, (const uint64_t*)(d + o_aid), (const double*)(d + o_akey));
+    if (np) {
+      const unsigned g = (unsigned)((np + 255) / 256);
+      tie::dev::predict_keys_kernel<<<g, 256, 0, s>>>((const double*)(d + o_E),
+                                                      (double*)(d + o_C), np, beta,
+                                                      (double*)(d + o_key), ctx->d_err);
+      tie::dev::write_predictions_checked_kernel<<<g, 256, 0, s>>>(
+          Q->q, (const uint32_t*)(d + o_slot), np, (const double*)(d + o_E),
+          (const double*)(d + o_C), (const double*)(d + o_key), beta, ctx->d_err);
+    }
+    if (!blocks.empty())
+      tie::dev::refresh_blocks_checked_kernel<<<
+          (unsigned)std::min<size_t>(blocks.size(), 4096), 256, 0, s>>>(
+          Q->q, (const uint32_t*)(d + o_blk), (uint32_t)blocks.size(), Q->n_slots, ctx->d_err,
+          n_uncond);
+    if (fused_pops)
+      tie::dev::step_apply_kernel<<<1, 1024, 0, s>>>(  // the pops alone (nothing to apply)
+          Q->q, 0, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, beta, nullptr, 0, 0, nb,
+          Q->n_slots, fused_pops, Q->d_out_id, Q->d_out_slot, seg0_n, ctx->d_err);
+    tie::capi::count_launch((n_arr ? 1 : 0) + (np ? 2 : 0) + (blocks.empty() ? 0 : 1) +
+                            (fused_pops ? 1 : 0));
+  }
+  launch_plan(Q, plan, seg0_fused ? 1 : 0, fused_pops, s, ctx->d_err);
+  fetch_plan(Q, plan.size(), planned, s);
+  // the error word (tie_sync decodes + resets it); arrivals stay applied like the reference's
+  if (int rc = tie_sync(ctx, s)) {
+    if (use_pred) pred_mirror(false);
+    return rc;
+  }
+  std::vector<uint64_t> got;
+  const bool dry = !replay_plan(Q, plan, got);
+  uint64_t k = got.size();
+  for (uint64_t j = 0; j < k; ++j) out_ids[j] = got[j];
+  if (!dry && k < pops) {  // the plan stopped at an uncertain rebuild decision
+    uint64_t more = 0;
+    if (int rc = tie_queue_next(Q, pops - k, out_ids + k, &more)) return rc;
+    k += more;
+  }
+  *n_out = k;
   return TIE_OK;
 }
 

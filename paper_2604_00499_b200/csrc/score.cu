@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) score_coop_kernel(const __gri
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* slab = slab_all[wib];
   const double** ptrs = ptr_all[wib];
-  const bool ka_smem = p.G <= kKaMaxG && p.k_alpha > 0;
+  const bool ka_smem = p.ka_smem && p.G <= kKaMaxG && p.k_alpha > 0;
   if (ka_smem) {
     for (int c = threadIdx.x; c < p.G * (kMoments / 2); c += blockDim.x) {
       const int g = c / (kMoments / 2), sub = c % (kMoments / 2);
@@ -869,7 +869,9 @@ cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, co
   } else {
     const int minb = (flags & 8u) ? 3 : 2;  // 2 CTAs/SM, 128 regs, no spills (A/B: 3, spills)
     const uint64_t grid = std::min<uint64_t>(blocks_needed, (uint64_t)sms * minb);
-    const size_t ka_smem = ctx->G <= kKaMaxG ? sizeof(double) * kSlabStride * ctx->G : 0;
+    // the k_alpha rows are staged per CTA: worth it only for batches that keep the CTAs busy
+    p.ka_smem = ctx->G <= kKaMaxG && n >= 8192 ? 1 : 0;
+    const size_t ka_smem = p.ka_smem ? sizeof(double) * kSlabStride * ctx->G : 0;
     static bool attr = false;
     if (!attr) {
       const int mx = (int)(sizeof(double) * kSlabStride * kKaMaxG);

@@ -148,6 +148,7 @@ struct ScoreParams {
   uint32_t k_alpha;         // upper_bound(Y, t_quantile(alpha, nu)); 0 when alpha == 0
   double alpha, beta;
   int raw;                  // TIE_SCORE_RAW: skip max(C,E) and compute_score
+  int ka_smem;              // stage the k_alpha rows of every grid point in shared memory
   uint64_t index_base;      // added to reported request indices (chunked callers)
   unsigned long long* err;
 };

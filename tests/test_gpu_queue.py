@@ -83,3 +83,73 @@ def test_logt_predictions_and_errors(tie, mc, oracle, samples):
         q.on_prediction_batch(np.array([1], np.uint64), np.array([10.0]), np.array([5.0]))
     assert q.next_requests(5).tolist() == [1]
     assert q.next_request() is None
+
+
+# ---- fused scheduler iteration (tie_queue_step): one device round trip per step
+def _cfg(tie, q_sat=128.0, thr=0.1):
+    sc = tie.ScoreConfig()
+    sc.q_sat = q_sat
+    sc.rebuild_threshold = thr
+    return sc
+
+
+@pytest.mark.parametrize("policy,q_sat,thr", [(2, 128.0, 0.1), (2, 1e9, 0.0), (2, 64.0, 0.05),
+                                              (1, 128.0, 0.1), (0, 128.0, 0.1)])
+def test_step_equals_separate_calls(tie, mc, oracle, policy, q_sat, thr):
+    pol = [tie.Policy.FCFS, tie.Policy.SEPT, tie.Policy.TIE][policy]
+    n0, steps, per, pops = 3000, 40, 32, 8
+    tot = n0 + steps * per
+    mu, sg, mt = oracle.gen_workload(tot, seed=11)
+    ids = np.random.default_rng(5).permutation(tot * 3)[:tot].astype(np.uint64)
+    arr = np.arange(tot, dtype=np.float64) * 0.01
+    qa = tie.GpuScheduler(mc, pol, _cfg(tie, q_sat, thr), tot)
+    qb = tie.GpuScheduler(mc, pol, _cfg(tie, q_sat, thr), tot)
+    for q in (qa, qb):
+        q.on_arrival_batch(ids[:n0], arr[:n0], mt[:n0])
+        q.on_prediction_logt(ids[:n0 // 2], mu[:n0 // 2], sg[:n0 // 2], mt[:n0 // 2])
+    pending = list(range(n0 // 2, n0))  # predicted one step after they arrive
+    for s in range(steps):
+        lo, hi = n0 + s * per, n0 + (s + 1) * per
+        pa = np.array(pending[:per], np.int64)
+        got_a = qa.step(ids[lo:hi], arr[lo:hi], mt[lo:hi], ids[pa], mu[pa], sg[pa], mt[pa], pops)
+        qb.on_arrival_batch(ids[lo:hi], arr[lo:hi], mt[lo:hi])
+        qb.on_prediction_logt(ids[pa], mu[pa], sg[pa], mt[pa])
+        got_b = qb.next_requests(pops)
+        assert np.array_equal(got_a, got_b), (s, got_a, got_b)
+        popped = set(got_a.tolist())
+        pending = [p for p in pending[per:] if ids[p] not in popped] + \
+                  [p for p in range(lo, hi) if ids[p] not in popped]
+    assert qa.waiting() == qb.waiting()
+    assert np.array_equal(qa.next_requests(500), qb.next_requests(500))
+
+
+def test_step_errors_leave_reference_state(tie, mc):
+    q = tie.GpuScheduler(mc, tie.Policy.TIE, _cfg(tie), 100)
+    q.step(np.array([1, 2, 3], np.uint64), np.zeros(3), np.full(3, 512, np.uint32),
+           np.array([], np.uint64), np.array([]), np.array([]), np.array([], np.uint32), 0)
+    with pytest.raises(ValueError, match="sigma"):  # LogTParams check of prediction 1
+        q.step(np.array([4], np.uint64), np.zeros(1), np.array([64], np.uint32),
+               np.array([1, 2], np.uint64), np.array([3.0, 3.0]), np.array([0.5, -1.0]),
+               np.array([512, 512], np.uint32), 4)
+    assert q.waiting() == 4  # the arrival applied, no prediction, no pop
+    with pytest.raises(ValueError, match="not waiting"):
+        q.step(np.array([], np.uint64), np.array([]), np.array([], np.uint32),
+               np.array([9], np.uint64), np.array([3.0]), np.array([0.5]),
+               np.array([512], np.uint32), 1)
+    with pytest.raises(ValueError, match="already queued"):
+        q.step(np.array([4], np.uint64), np.zeros(1), np.array([64], np.uint32),
+               np.array([], np.uint64), np.array([]), np.array([]), np.array([], np.uint32), 1)
+    # unpredicted keys are max_tokens: 4 (64) first, then 1, 2, 3 (512) by id
+    assert q.step(np.array([], np.uint64), np.array([]), np.array([], np.uint32),
+                  np.array([], np.uint64), np.array([]), np.array([]),
+                  np.array([], np.uint32), 10).tolist() == [4, 1, 2, 3]
+
+
+def test_topb_pop_candidate_overflow_path(tie, mc):
+    """Equal keys, ids ascending with the slot: every chosen block is full of candidates, so
+    the top-B pop takes its per-pop fallback; the order is still by id."""
+    n = 20_000
+    q = tie.GpuScheduler(mc, tie.Policy.SEPT, _cfg(tie), n)
+    q.on_arrival_batch(np.arange(n, dtype=np.uint64), np.zeros(n), np.full(n, 100, np.uint32))
+    assert q.next_requests(32).tolist() == list(range(32))
+    assert q.next_requests(40).tolist() == list(range(32, 72))
