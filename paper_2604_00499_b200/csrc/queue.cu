@@ -549,6 +549,9 @@ struct tie_queue {
   uint32_t* d_out_slot = nullptr;
   uint32_t* d_out_n = nullptr;
   uint64_t stage_cap = 0;
+  void* d_out = nullptr;          // the pop output block (ensure_out)
+  uint64_t out_cap = 0;
+  void* h_out = nullptr;          // its pinned mirror
   char* h_pack = nullptr;         // pinned H2D pack of a fused step
   char* d_pack = nullptr;
   uint64_t pack_cap = 0;
@@ -568,20 +571,35 @@ double beta_at(const tie_queue* Q, uint64_t queue_len) {
 int ensure_stage(tie_queue* Q, uint64_t m) {
   if (m <= Q->stage_cap) return TIE_OK;
   cudaFree(Q->d_ids); cudaFree(Q->d_a); cudaFree(Q->d_b); cudaFree(Q->d_c);
-  cudaFree(Q->d_slots); cudaFree(Q->d_blocks); cudaFree(Q->d_out_id); cudaFree(Q->d_out_slot);
-  cudaFree(Q->d_out_n);
-  cudaFreeHost(Q->h_out_id); cudaFreeHost(Q->h_out_slot); cudaFreeHost(Q->h_out_n);
+  cudaFree(Q->d_slots); cudaFree(Q->d_blocks);
   const uint64_t cap = std::max<uint64_t>(m, 1024);
   cudaError_t e = cudaSuccess;
   if ((e = cudaMalloc(&Q->d_ids, 8 * cap)) || (e = cudaMalloc(&Q->d_a, 8 * cap)) ||
       (e = cudaMalloc(&Q->d_b, 8 * cap)) || (e = cudaMalloc(&Q->d_c, 8 * cap)) ||
-      (e = cudaMalloc(&Q->d_slots, 4 * cap)) || (e = cudaMalloc(&Q->d_blocks, 4 * cap)) ||
-      (e = cudaMalloc(&Q->d_out_id, 8 * cap)) || (e = cudaMalloc(&Q->d_out_slot, 4 * cap)) ||
-      (e = cudaMalloc(&Q->d_out_n, 4 * cap)) ||
-      (e = cudaMallocHost(&Q->h_out_id, 8 * cap)) ||
-      (e = cudaMallocHost(&Q->h_out_slot, 4 * cap)) || (e = cudaMallocHost(&Q->h_out_n, 4 * cap)))
+      (e = cudaMalloc(&Q->d_slots, 4 * cap)) || (e = cudaMalloc(&Q->d_blocks, 4 * cap)))
     return cuda_error(e, "tie_queue: staging allocation");
   Q->stage_cap = cap;
+  return TIE_OK;
+}
+
+// the pop output block, one per side so a plan's results come back in ONE small D2H:
+//   [out_n: u32 x cap | out_slot: u32 x cap | out_id: u64 x cap]   (cap >= pops, segments)
+int ensure_out(tie_queue* Q, uint64_t m) {
+  if (m <= Q->out_cap) return TIE_OK;
+  cudaFree(Q->d_out);
+  cudaFreeHost(Q->h_out);
+  Q->d_out = Q->h_out = nullptr;
+  const uint64_t cap = std::max<uint64_t>(m, 256);
+  cudaError_t e = cudaSuccess;
+  if ((e = cudaMalloc(&Q->d_out, 16 * cap)) || (e = cudaMallocHost(&Q->h_out, 16 * cap)))
+    return cuda_error(e, "tie_queue: output allocation");
+  Q->d_out_n = (uint32_t*)Q->d_out;
+  Q->d_out_slot = Q->d_out_n + cap;
+  Q->d_out_id = (uint64_t*)(Q->d_out_slot + cap);
+  Q->h_out_n = (uint32_t*)Q->h_out;
+  Q->h_out_slot = Q->h_out_n + cap;
+  Q->h_out_id = (uint64_t*)(Q->h_out_slot + cap);
+  Q->out_cap = cap;
   return TIE_OK;
 }
 
@@ -710,12 +728,9 @@ uint64_t launch_plan(tie_queue* Q, const std::vector<Seg>& plan, size_t first_se
 
 // D2H of a plan's results (issued after launch_plan)
 void fetch_plan(tie_queue* Q, size_t nseg, uint64_t total, cudaStream_t s) {
-  cudaMemcpyAsync(Q->h_out_n, Q->d_out_n, 4 * std::max<size_t>(nseg, 1), cudaMemcpyDeviceToHost,
-                  s);
-  if (total) {
-    cudaMemcpyAsync(Q->h_out_slot, Q->d_out_slot, 4 * total, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(Q->h_out_id, Q->d_out_id, 8 * total, cudaMemcpyDeviceToHost, s);
-  }
+  (void)nseg;
+  const size_t bytes = (size_t)((char*)(Q->d_out_id + total) - (char*)Q->d_out);
+  cudaMemcpyAsync(Q->h_out, Q->d_out, bytes, cudaMemcpyDeviceToHost, s);
 }
 
 // host mirror of a finished plan, segment by segment (rebuild bookkeeping, then its pops);
@@ -736,7 +751,7 @@ int execute_plan(tie_queue* Q, const std::vector<Seg>& plan, std::vector<uint64_
                  cudaStream_t s) {
   uint64_t total = 0;
   for (const Seg& g : plan) total += g.pops;
-  if (int rc = ensure_stage(Q, std::max<uint64_t>(total, plan.size() + 1))) return rc;
+  if (int rc = ensure_out(Q, std::max<uint64_t>(total, plan.size() + 1))) return rc;
   launch_plan(Q, plan, 0, 0, s, Q->ctx->d_err);
   fetch_plan(Q, plan.size(), total, s);
   const cudaError_t e = cudaStreamSynchronize(s);
@@ -781,7 +796,7 @@ int tie_queue_create(tie_ctx* ctx, int policy, int adaptive, double beta_fixed, 
       (e = cudaMalloc(&Q->q.beta, 8 * capacity)) ||
       (e = cudaMalloc(&Q->q.predicted, capacity)) || (e = cudaMalloc(&Q->q.bkey, 8 * nb)) ||
       (e = cudaMalloc(&Q->q.bid, 8 * nb)) || (e = cudaMalloc(&Q->q.bslot, 4 * nb)) ||
-      ensure_stage(Q, 1024) != TIE_OK) {
+      ensure_stage(Q, 1024) != TIE_OK || ensure_out(Q, 256) != TIE_OK) {
     tie_queue_destroy(Q);
     return cuda_error(e, "tie_queue_create");
   }
@@ -798,12 +813,9 @@ void tie_queue_destroy(tie_queue* Q) {
   for (void* p : {(void*)Q->q.key, (void*)Q->q.id, (void*)Q->q.E, (void*)Q->q.C,
                   (void*)Q->q.beta, (void*)Q->q.predicted, (void*)Q->q.bkey, (void*)Q->q.bid,
                   (void*)Q->q.bslot, (void*)Q->d_ids, (void*)Q->d_a, (void*)Q->d_b,
-                  (void*)Q->d_c, (void*)Q->d_slots, (void*)Q->d_blocks, (void*)Q->d_out_id,
-                  (void*)Q->d_out_slot, (void*)Q->d_out_n})
+                  (void*)Q->d_c, (void*)Q->d_slots, (void*)Q->d_blocks, Q->d_out})
     cudaFree(p);
-  cudaFreeHost(Q->h_out_id);
-  cudaFreeHost(Q->h_out_slot);
-  cudaFreeHost(Q->h_out_n);
+  cudaFreeHost(Q->h_out);
   cudaFreeHost(Q->h_pack);
   cudaFree(Q->d_pack);
   delete Q;
@@ -1049,10 +1061,11 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
   auto al = [](uint64_t x) { return (x + 255) & ~(uint64_t)255; };
   const uint64_t np = use_pred ? n_pred : 0;
   const uint64_t o_aid = 0, o_akey = o_aid + al(8 * n_arr), o_mu = o_akey + al(8 * n_arr),
-                 o_sg = o_mu + al(8 * np), o_E = o_sg + al(8 * np), o_C = o_E + al(8 * np),
-                 o_key = o_C + al(8 * np), o_slot = o_key + al(8 * np),
+                 o_sg = o_mu + al(8 * np), o_slot = o_sg + al(8 * np),
                  o_mt = o_slot + al(4 * np), o_blk = o_mt + al(4 * np),
-                 total = o_blk + al(4 * blocks.size());
+                 o_h2d_end = o_blk + al(4 * blocks.size()),  // host-provided up to here
+                 o_E = o_h2d_end, o_C = o_E + al(8 * np), o_key = o_C + al(8 * np),
+                 total = o_key + al(8 * np);
   if (total > Q->pack_cap) {
     cudaFreeHost(Q->h_pack);
     cudaFree(Q->d_pack);
@@ -1066,7 +1079,7 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
     }
     Q->pack_cap = cap;
   }
-  if (int rc = ensure_stage(Q, std::max<uint64_t>(planned, plan.size() + 1))) {
+  if (int rc = ensure_out(Q, std::max<uint64_t>(planned, plan.size() + 1))) {
     if (use_pred) pred_mirror(false);
     return rc;
   }
@@ -1081,9 +1094,7 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
   }
   std::memcpy(h + o_blk, blocks.data(), 4 * blocks.size());
   char* d = Q->d_pack;
-  // H2D up to E (the arrays behind mu/sigma are device scratch, then slots/mt/blocks)
-  cudaMemcpyAsync(d, h, o_E, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(d + o_slot, h + o_slot, total - o_slot, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d, h, o_h2d_end, cudaMemcpyHostToDevice, s);  // ONE H2D
   ctx->err_op = "tie_queue_step";
   const uint32_t nb = (uint32_t)((Q->n_slots + tie::dev::kBlockSlots - 1) / tie::dev::kBlockSlots);
   if (np) {
