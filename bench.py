@@ -335,12 +335,17 @@ def main():
     # DRAM traffic per launch of the dominant kernel from the committed ncu --set full capture
     # of this same configuration (profiles/ncu_traffic_r01.json), scaled to this n
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01f.json")) as f:
             tr = json.load(f)
         if dom in tr:
             roof["traffic"] = (tr[dom]["dram_read_bytes"] + tr[dom]["dram_write_bytes"]) * (
                 n_local / tr["n"])
-            roof["traffic_source"] = "profiles/ncu_traffic_r01.json: " + tr[dom]["capture"]
+            roof["traffic_source"] = "profiles/ncu_traffic_r01f.json: " + tr[dom]["capture"]
+            # what actually bounds it (ncu): the score kernel is gather-latency / L1-bound
+            roof["limiter"] = {"l1_throughput_pct": tr[dom].get("l1_throughput_pct"),
+                               "issue_active_pct": tr[dom].get("issue_active_pct"),
+                               "fp64_pipe_pct": tr[dom].get("fp64_pipe_pct"),
+                               "source": "ncu --set full, same capture"}
     except (OSError, KeyError, ValueError):
         pass
 
