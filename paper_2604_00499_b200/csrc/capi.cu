@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -501,7 +502,11 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
   if (!prep.keys) return set_error(TIE_ECUDA, "tie_score_rank_host: scratch allocation failed");
   ctx->err_op = "tie_score_rank_host";
   // pipeline: H2D of chunk c+1 (copy stream) overlaps scoring of chunk c (compute stream)
-  const int chunks = n >= (1u << 20) ? 4 : 1;
+  // 2 chunks: the second half's H2D overlaps the first half's scoring; every extra copy costs
+  // ~3 us of DMA setup, more than the finer overlap wins (tools/e2e_probe.py on B200:
+  // 1M requests, 1/2/3/8/16 chunks -> 633/626/644/698/801 us)
+  static const int max_chunks = getenv("TIE_H2D_CHUNKS") ? atoi(getenv("TIE_H2D_CHUNKS")) : 2;
+  const int chunks = std::max(1, n >= (1u << 18) ? max_chunks : 1);
   const uint64_t step = (n + chunks - 1) / chunks;
   TIE_CUDA_TRY(cudaEventRecord(ctx->ev[0], s), "tie_score_rank_host");
   TIE_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[0], 0), "tie_score_rank_host");
@@ -521,9 +526,19 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
                                                  prep.minmax, flags & TIE_SCORE_EXACT, s, lo);
     if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
   }
-  cudaError_t e = tie::dev::rank_prepared(ctx, n, d_order, s);
+  // pinned (page-locked, UVA-mapped) output: the sort's last kernel writes the dispatch
+  // order straight into host memory, so the D2H overlaps the sort instead of following it
+  cudaPointerAttributes pa{};
+  static const int zero_copy = getenv("TIE_NO_ZERO_COPY") ? 0 : 1;  // A/B switch
+  const bool mapped = zero_copy && tie::dev::rank_output_coalesced(n) &&
+                      cudaPointerGetAttributes(&pa, order) == cudaSuccess &&
+                      pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr;
+  cudaGetLastError();  // a pageable pointer is not an error here
+  cudaError_t e = tie::dev::rank_prepared(ctx, n, mapped ? (uint64_t*)pa.devicePointer : d_order,
+                                          s);
   if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
-  TIE_CUDA_TRY(cudaMemcpyAsync(order, d_order, 8 * n, cudaMemcpyDeviceToHost, s), "d2h");
+  if (!mapped)
+    TIE_CUDA_TRY(cudaMemcpyAsync(order, d_order, 8 * n, cudaMemcpyDeviceToHost, s), "d2h");
   if (score) TIE_CUDA_TRY(cudaMemcpyAsync(score, d_S, 8 * n, cudaMemcpyDeviceToHost, s), "d2h");
   return tie_sync(ctx, s);
 }

@@ -874,6 +874,7 @@ __global__ void __launch_bounds__(kPartThreads, 3) part_sort_kernel(Part q, uint
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < m; j += kPartThreads) perm[atomicAdd(&fc[sf[j]], 1u)] = (uint16_t)j;
   __syncthreads();
+  uint16_t* spos = sf;  // a key's final position in the partition replaces its fine bucket
   for (uint32_t j = threadIdx.x; j < m; j += kPartThreads) {
     const uint64_t k = sk[j];
     const uint32_t v = sv[j], fine = sf[j];
@@ -884,7 +885,18 @@ __global__ void __launch_bounds__(kPartThreads, 3) part_sort_kernel(Part q, uint
       const uint64_t kq = sk[o];
       below += (kq < k || (kq == k && sv[o] < v)) ? 1u : 0u;
     }
-    order[s0 + lo + below] = ids ? ids[v] : (uint64_t)v;
+    spos[j] = (uint16_t)(lo + below);
+  }
+  __syncthreads();
+  // place the values in partition order (the keys are no longer needed), then write the
+  // partition's slice of the dispatch order out coalesced -- also when `order` is mapped
+  // pinned host memory (the host API's zero-copy output)
+  uint32_t* outv = reinterpret_cast<uint32_t*>(sk);
+  for (uint32_t j = threadIdx.x; j < m; j += kPartThreads) outv[spos[j]] = sv[j];
+  __syncthreads();
+  for (uint32_t p = threadIdx.x; p < m; p += kPartThreads) {
+    const uint32_t v = outv[p];
+    order[s0 + p] = ids ? ids[v] : (uint64_t)v;
   }
 }
 
@@ -1146,6 +1158,8 @@ cudaError_t bucket_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_
 }  // namespace
 
 size_t rank_scratch_bytes(uint64_t n, bool with_ids) { return layout(n, with_ids).total; }
+
+bool rank_output_coalesced(uint64_t n) { return layout(n, false).part; }
 
 RankPrep rank_prepare(tie_ctx* ctx, uint64_t n, cudaStream_t s) {
   RankPrep r{nullptr, nullptr};

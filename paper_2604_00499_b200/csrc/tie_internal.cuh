@@ -236,6 +236,9 @@ cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma,
 cudaError_t launch_rank(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n,
                         uint64_t* order, cudaStream_t s);
 size_t rank_scratch_bytes(uint64_t n, bool with_ids);
+// true when the sort's last kernel writes the order in coalesced runs (partition path):
+// then a host API may hand it mapped pinned host memory as the output
+bool rank_output_coalesced(uint64_t n);
 // Fused producer path: rank_prepare() zeroes the sort metadata and returns where the
 // producer (the score kernel) writes order-preserving u64 keys and folds their range
 // (key_range_flush); rank_prepared() then bucket-sorts them and emits the order.
