@@ -484,6 +484,28 @@ def run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream):
         torch.cuda.empty_cache()
     except Exception as exc:  # never blocks the headline line
         out["config4_single_gpu"] = {"error": repr(exc)}
+    # cmd_fit's per-prompt analysis (8f #3) on the config-3 prompts: 4 families (free nu =
+    # 19 BFGS fits), KS of each, tail stats
+    try:
+        rep = torch.empty(4 * 10 * P, dtype=torch.float64, device=dev)
+        tl = torch.empty(5 * P, dtype=torch.float64, device=dev)
+        rargs = (ctx, xd.data_ptr(), P, K, 3.5, 15, rep.data_ptr(), tl.data_ptr(), sh)
+        tie.fit_report_device(*rargs)
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(stream)
+        tie.fit_report_device(*rargs)
+        b.record(stream)
+        torch.cuda.synchronize()
+        tie.sync(ctx, sh)
+        rms = a.elapsed_time(b)
+        out["fit_report"] = {
+            "metric": "prompts analysed/sec (cmd_fit: logt, logt_free_nu (19-point nu grid), "
+                      "lognormal, exponential fits + KS of each + tail stats; 1M x 16)",
+            "value": P / (rms * 1e-3), "unit": "prompts/s", "ms": rms}
+        del rep, tl
+    except Exception as exc:
+        out["fit_report"] = {"error": repr(exc)}
     out["fit"] = {"metric": "log-t fits/sec (config 3: 1M prompts x 16 lengths)",
                   "value": P / (fms * 1e-3), "unit": "fits/s", "ms": fms,
                   "e2e": {"value": P / fe2e, "unit": "fits/s", "h2d_bytes": 8 * P * K,

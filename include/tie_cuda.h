@@ -125,6 +125,18 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
                         double* score, uint64_t* order, unsigned flags);
 int tie_rank_host(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n,
                   uint64_t* order);
+/* cmd_fit's per-prompt analysis (proj/tools/main.cpp:527-562) for P prompts x K >= 5 lengths:
+ * families bitmask 1 logt (fit_logt_fixed_nu(x, nu), fit.cpp:73-178), 2 logt_free_nu
+ * (fit_logt_free_nu over default_nu_grid, fit.cpp:180-200), 4 lognormal (fit.cpp:202-230),
+ * 8 exponential (fit.cpp:232-243); each with ks_test(x, fit_cdf) (fit.cpp:245-284).
+ * fits[f][10][P] doubles, f = the family's bit index, fields mu, sigma, nu, rate,
+ * log_likelihood, iterations, converged, degenerate, ks_statistic, ks_p_value (families not
+ * requested are left as passed in); tail[5][P] = tail_stats (fit.cpp:286-324: skewness, cv,
+ * p90/p50, p99/p50, top10 share), NaN when K < 10, or tail = NULL. */
+int tie_fit_report(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
+                   unsigned families, double* fits, double* tail, void* stream);
+int tie_fit_report_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
+                        unsigned families, double* fits, double* tail);
 int tie_fit_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
                  double* mu, double* sigma, double* log_likelihood, int32_t* iterations,
                  uint8_t* converged, uint8_t* degenerate);

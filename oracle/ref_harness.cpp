@@ -208,6 +208,54 @@ int ref_fit(const double* x, uint64_t P, uint64_t K, double nu, double* mu, doub
   }
 }
 
+// cmd_fit's per-prompt analysis (tools/main.cpp:527-562) through the reference's own
+// functions: fit_* per family, ks_test(fit_cdf), tail_stats for K >= 10.  Layout as
+// tor_fit_report (oracle/tie_oracle.h).
+int ref_fit_report(const double* x, uint64_t P, uint64_t K, double nu, unsigned families,
+                   double* fits, double* tail, int threads) {
+  try {
+    parallel_for((size_t)P, threads, [&](size_t p) {
+      std::vector<double> v(x + p * K, x + (p + 1) * K);
+      const tie::FitFamily fams[4] = {tie::FitFamily::LogTFixedNu, tie::FitFamily::LogTFreeNu,
+                                      tie::FitFamily::LogNormal, tie::FitFamily::Exponential};
+      for (int f = 0; f < 4; ++f) {
+        if (!(families >> f & 1)) continue;
+        tie::FitResult fr;
+        switch (f) {
+          case 0: fr = tie::fit_logt_fixed_nu(v, nu); break;
+          case 1: fr = tie::fit_logt_free_nu(v); break;
+          case 2: fr = tie::fit_lognormal(v); break;
+          default: fr = tie::fit_exponential(v); break;
+        }
+        (void)fams;
+        tie::KsResult ks = tie::ks_test(v, [&](double t) { return tie::fit_cdf(fr, t); });
+        double* o = fits + (uint64_t)f * 10 * P;
+        const double vals[10] = {fr.mu, fr.sigma, fr.nu, fr.rate, fr.log_likelihood,
+                                 (double)fr.iterations, (double)fr.converged,
+                                 (double)fr.degenerate, ks.statistic, ks.p_value};
+        for (int j = 0; j < 10; ++j) o[(uint64_t)j * P + p] = vals[j];
+      }
+      if (tail) {
+        if (K >= 10) {
+          tie::TailStats ts = tie::tail_stats(v);
+          const double vals[5] = {ts.skewness, ts.cv, ts.p90_over_p50, ts.p99_over_p50,
+                                  ts.top10_share};
+          for (int j = 0; j < 5; ++j) tail[(uint64_t)j * P + p] = vals[j];
+        } else {
+          for (int j = 0; j < 5; ++j) tail[(uint64_t)j * P + p] = std::nan("");
+        }
+      }
+    });
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 2);
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
+}
+
 double ref_logt_loglik(const double* x, uint64_t K, double mu, double sigma, double nu) {
   return tie::logt_loglik(std::vector<double>(x, x + K), mu, sigma, nu);
 }

@@ -625,6 +625,203 @@ int tor_fit(const double* x, uint64_t P, uint64_t K, double nu, double* mu, doub
   return 0;
 }
 
+/* ---------------------------------------------------------------- fit report */
+/* cmd_fit's per-prompt analysis (main.cpp:510-585) over P prompts x K lengths: the four
+ * families (fit.cpp:73-178 fixed nu; 180-200 free nu over default_nu_grid; 202-230
+ * lognormal; 232-243 exponential), ks_test of each fit's CDF (fit.cpp:245-284) and, for
+ * K >= 10, tail_stats (fit.cpp:286-324).  Layout: fits[f][field][P] with f = 0 logt,
+ * 1 logt_free_nu, 2 lognormal, 3 exponential and field = mu, sigma, nu, rate,
+ * log_likelihood, iterations, converged, degenerate, ks_statistic, ks_p_value;
+ * tail[field][P] = skewness, cv, p90_over_p50, p99_over_p50, top10_share (NaN if K < 10). */
+enum { FR_MU, FR_SIGMA, FR_NU, FR_RATE, FR_LL, FR_ITERS, FR_CONV, FR_DEGEN, FR_KSD, FR_KSP, FR_N };
+
+static double normal_cdf(double z); /* dist.cpp:191 (defined with the lognormal family below) */
+
+typedef struct {
+  int family; /* 0..3 */
+  double mu, sigma, nu, rate, ll;
+  int iters, converged, degenerate;
+} fam_fit;
+
+static double fit_cdf(const fam_fit* f, double x) { /* fit.cpp:245-258 */
+  if (!(x > 0.0)) return 0.0;
+  switch (f->family) {
+    case 0:
+    case 1: return tor_t_cdf((log(x) - f->mu) / f->sigma, f->nu);
+    case 2: return normal_cdf((log(x) - f->mu) / f->sigma);
+    default: return -expm1(-f->rate * x);
+  }
+}
+
+/* ks_test on the sorted samples s (fit.cpp:261-284); returns 0 or the domain error */
+static int ks_sorted(const double* s, uint64_t K, const fam_fit* f, double* D, double* P) {
+  double n = (double)K, d = 0.0;
+  for (uint64_t i = 0; i < K; ++i) {
+    double F = fit_cdf(f, s[i]);
+    if (!(F >= 0.0 && F <= 1.0)) return 1;
+    double a = ((double)i + 1.0) / n - F, b = F - (double)i / n;
+    double m = a < b ? b : a;
+    d = d < m ? m : d;
+  }
+  double lambda = (sqrt(n) + 0.12 + 0.11 / sqrt(n)) * d;
+  double p = 0.0, sign = 1.0;
+  for (int j = 1; j <= 100; ++j) {
+    double term = sign * 2.0 * exp(-2.0 * j * j * lambda * lambda);
+    p += term;
+    if (fabs(term) < 1e-12) break;
+    sign = -sign;
+  }
+  p = p > 0.0 ? p : 0.0;
+  p = p < 1.0 ? p : 1.0;
+  *D = d;
+  *P = p;
+  return 0;
+}
+
+typedef struct {
+  const double* x;
+  uint64_t K, P;
+  double nu;
+  unsigned families;
+  double* fits;
+  double* tail;
+  volatile int err; /* first domain error seen (ks_test cdf outside [0,1]) */
+} report_ctx;
+
+static void report_body(void* vctx, uint64_t b, uint64_t e) {
+  report_ctx* c = (report_ctx*)vctx;
+  const uint64_t K = c->K, P = c->P;
+  double* scratch = (double*)malloc(sizeof(double) * 2 * K);
+  double* s = (double*)malloc(sizeof(double) * K);
+  for (uint64_t p = b; p < e; ++p) {
+    const double* x = c->x + p * K;
+    for (uint64_t i = 0; i < K; ++i) s[i] = x[i];
+    qsort(s, K, sizeof(double), cmp_double); /* ks_test / tail_stats sort a copy */
+    for (int f = 0; f < 4; ++f) {
+      if (!(c->families >> f & 1)) continue;
+      fam_fit r = {f, 0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0};
+      if (f == 0 || f == 1) {
+        fit_out o;
+        if (f == 0) {
+          fit_one(x, K, c->nu, scratch, &o);
+          r.nu = c->nu;
+        } else { /* fit_logt_free_nu: best log-likelihood over the grid, first on ties */
+          int have = 0;
+          for (double v = 1.0; v <= 10.0 + 1e-9; v += 0.5) {
+            fit_out t;
+            fit_one(x, K, v, scratch, &t);
+            if (!have || t.ll > o.ll) {
+              o = t;
+              r.nu = v;
+              have = 1;
+            }
+          }
+        }
+        r.mu = o.mu;
+        r.sigma = o.sigma;
+        r.ll = o.ll;
+        r.iters = o.iters;
+        r.converged = o.converged;
+        r.degenerate = o.degenerate;
+      } else if (f == 2) { /* fit_lognormal */
+        double n = (double)K, mean = 0.0, var = 0.0;
+        for (uint64_t i = 0; i < K; ++i) mean += log(x[i]);
+        mean /= n;
+        for (uint64_t i = 0; i < K; ++i) {
+          double d = log(x[i]) - mean;
+          var += d * d;
+        }
+        var /= n;
+        r.mu = mean;
+        r.sigma = sqrt(var);
+        r.converged = 1;
+        if (r.sigma < 1e-6) {
+          r.sigma = 1e-6;
+          r.degenerate = 1;
+        }
+        double ll = 0.0;
+        for (uint64_t i = 0; i < K; ++i) {
+          double z = (log(x[i]) - r.mu) / r.sigma;
+          ll += -log(r.sigma * x[i]) - 0.5 * log(2.0 * 3.14159265358979323846) - 0.5 * z * z;
+        }
+        r.ll = ll;
+      } else { /* fit_exponential */
+        double mean = 0.0;
+        for (uint64_t i = 0; i < K; ++i) mean += x[i];
+        mean /= (double)K;
+        r.rate = 1.0 / mean;
+        r.converged = 1;
+        r.ll = (double)K * log(r.rate) - r.rate * mean * (double)K;
+      }
+      double D = 0.0, Pv = 0.0;
+      if (ks_sorted(s, K, &r, &D, &Pv)) c->err = 1;
+      double* o = c->fits + (uint64_t)f * FR_N * P;
+      o[FR_MU * P + p] = r.mu;
+      o[FR_SIGMA * P + p] = r.sigma;
+      o[FR_NU * P + p] = r.nu;
+      o[FR_RATE * P + p] = r.rate;
+      o[FR_LL * P + p] = r.ll;
+      o[FR_ITERS * P + p] = (double)r.iters;
+      o[FR_CONV * P + p] = (double)r.converged;
+      o[FR_DEGEN * P + p] = (double)r.degenerate;
+      o[FR_KSD * P + p] = D;
+      o[FR_KSP * P + p] = Pv;
+    }
+    if (c->tail) {
+      double* t = c->tail;
+      if (K < 10) {
+        for (int j = 0; j < 5; ++j) t[j * P + p] = NAN;
+        continue;
+      }
+      double n = (double)K, total = 0.0, m2 = 0.0, m3 = 0.0;
+      for (uint64_t i = 0; i < K; ++i) total += s[i];
+      double mean = total / n;
+      for (uint64_t i = 0; i < K; ++i) {
+        double d = s[i] - mean;
+        m2 += d * d;
+        m3 += d * d * d;
+      }
+      m2 /= n;
+      m3 /= n;
+#define TOR_RANK(q, out)                                  \
+  do {                                                    \
+    uint64_t k_ = (uint64_t)ceil((q) * n);                \
+    if (k_ > K) k_ = K;                                   \
+    if (k_ < 1) k_ = 1;                                   \
+    out = s[k_ - 1];                                      \
+  } while (0)
+      double p50, p90, p99;
+      TOR_RANK(0.50, p50);
+      TOR_RANK(0.90, p90);
+      TOR_RANK(0.99, p99);
+#undef TOR_RANK
+      uint64_t k10 = (uint64_t)ceil(0.1 * n);
+      double top = 0.0;
+      for (uint64_t i = K - k10; i < K; ++i) top += s[i];
+      t[0 * P + p] = m2 > 0.0 ? m3 / pow(m2, 1.5) : 0.0;
+      t[1 * P + p] = mean > 0.0 ? sqrt(m2) / mean : 0.0;
+      t[2 * P + p] = p50 > 0.0 ? p90 / p50 : 1.0;
+      t[3 * P + p] = p50 > 0.0 ? p99 / p50 : 1.0;
+      t[4 * P + p] = total > 0.0 ? top / total : 0.0;
+    }
+  }
+  free(scratch);
+  free(s);
+}
+
+int tor_fit_report(const double* x, uint64_t P, uint64_t K, double nu, unsigned families,
+                   double* fits, double* tail, int threads) {
+  if (K < 5) return fail(2, "ks_test: need at least 5 samples");
+  for (uint64_t i = 0; i < P * K; ++i)
+    if (!(x[i] > 0.0) || !isfinite(x[i]))
+      return fail(1, "fit_logt_fixed_nu: samples must be finite and > 0");
+  if (!(nu > 0.0) || !isfinite(nu)) return fail(1, "fit_logt_fixed_nu: nu must be finite and > 0");
+  report_ctx c = {x, K, P, nu, families, fits, tail, 0};
+  parallel_for(P, threads, 64, report_body, &c);
+  if (c.err) return fail(1, "ks_test: cdf returned a value outside [0, 1]");
+  return 0;
+}
+
 /* ---------------------------------------------------------------- inputs */
 /* workload.cpp:37-48 + 50-78 */
 int tor_gen_workload(uint64_t n, uint64_t seed, double mu_lo, double mu_hi, double sg_lo,

@@ -58,6 +58,13 @@ int tor_fit(const double* x, uint64_t P, uint64_t K, double nu, double* mu, doub
             double* ll, int32_t* iters, uint8_t* converged, uint8_t* degenerate, int threads);
 double tor_logt_loglik(const double* x, uint64_t K, double mu, double sigma, double nu);
 
+/* cmd_fit's per-prompt analysis (main.cpp:510-585): families bitmask 1 logt (fixed nu),
+ * 2 logt_free_nu, 4 lognormal, 8 exponential; fits[f][10][P] (mu, sigma, nu, rate,
+ * log_likelihood, iterations, converged, degenerate, ks_statistic, ks_p_value) for the
+ * requested f; tail[5][P] (skewness, cv, p90/p50, p99/p50, top10_share; NaN if K < 10). */
+int tor_fit_report(const double* x, uint64_t P, uint64_t K, double nu, unsigned families,
+                   double* fits, double* tail, int threads);
+
 /* gen_logt_workload, workload.cpp:50-78 (SoA view; ids are 0..n-1) */
 int tor_gen_workload(uint64_t n, uint64_t seed, double mu_lo, double mu_hi, double sg_lo,
                      double sg_hi, double nu, uint32_t max_tokens, double rps, double* mu,

@@ -126,6 +126,8 @@ int decode_error(uint64_t word, const char* op) {
     case kDuplicateId: return set_error(TIE_EINVALID, at + "WaitingQueue::push: id already queued");
     case kSampleBad:
       return set_error(TIE_EDOMAIN, at + "fit_logt_fixed_nu: samples must be finite and > 0");
+    case kKsCdfRange:
+      return set_error(TIE_EDOMAIN, at + "ks_test: cdf returned a value outside [0, 1]");
     default: return set_error(TIE_ECUDA, at + "unknown device error");
   }
 }
@@ -558,6 +560,43 @@ int tie_rank_host(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t
   if (ids) TIE_CUDA_TRY(cudaMemcpyAsync(d_ids, ids, 8 * n, cudaMemcpyHostToDevice, s), "h2d");
   if (int rc = tie_rank(ctx, d_key, d_ids, n, d_order, s)) return rc;
   TIE_CUDA_TRY(cudaMemcpyAsync(order, d_order, 8 * n, cudaMemcpyDeviceToHost, s), "d2h");
+  return tie_sync(ctx, s);
+}
+
+// cmd_fit's per-prompt analysis (tools/main.cpp:527-562), device buffers
+int tie_fit_report(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
+                   unsigned families, double* fits, double* tail, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (K < 5) return set_error(TIE_EINVALID, "ks_test: need at least 5 samples");
+  if (!(nu > 0.0) || !std::isfinite(nu))
+    return set_error(TIE_EDOMAIN, "fit_logt_fixed_nu: nu must be finite and > 0");
+  if (families == 0 || families > 15)
+    return set_error(TIE_EINVALID, "tie_fit_report: families must be a non-empty subset of 15");
+  if (P && (!x || !fits)) return set_error(TIE_EINVALID, "tie_fit_report: null pointer");
+  DeviceGuard g(ctx->device);
+  ctx->err_op = "tie_fit_report";
+  const cudaError_t e = tie::dev::launch_fit_report(ctx, x, P, K, nu, families, fits, tail,
+                                                    as_stream(stream));
+  if (e != cudaSuccess) return cuda_error(e, "tie_fit_report");
+  return TIE_OK;
+}
+
+int tie_fit_report_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
+                        unsigned families, double* fits, double* tail) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (P == 0) return TIE_OK;
+  DeviceGuard g(ctx->device);
+  char* b = io_buffer(ctx, al(8 * P * K) + al(8 * 40 * P) + al(8 * 5 * P));
+  if (!b) return set_error(TIE_ECUDA, "tie_fit_report_host: device allocation failed");
+  double* d_x = (double*)b;
+  double* d_f = (double*)(b + al(8 * P * K));
+  double* d_t = tail ? (double*)(b + al(8 * P * K) + al(8 * 40 * P)) : nullptr;
+  cudaStream_t s = ctx->stream;
+  TIE_CUDA_TRY(cudaMemcpyAsync(d_x, x, 8 * P * K, cudaMemcpyHostToDevice, s), "h2d");
+  TIE_CUDA_TRY(cudaMemcpyAsync(d_f, fits, 8 * 40 * P, cudaMemcpyHostToDevice, s), "h2d");
+  if (int rc = tie_fit_report(ctx, d_x, P, K, nu, families, d_f, d_t, s)) return rc;
+  TIE_CUDA_TRY(cudaMemcpyAsync(fits, d_f, 8 * 40 * P, cudaMemcpyDeviceToHost, s), "d2h");
+  if (tail) TIE_CUDA_TRY(cudaMemcpyAsync(tail, d_t, 8 * 5 * P, cudaMemcpyDeviceToHost, s), "d2h");
   return tie_sync(ctx, s);
 }
 

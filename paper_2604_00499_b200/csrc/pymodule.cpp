@@ -247,6 +247,37 @@ PYBIND11_MODULE(_core, m) {
       py::arg("ctx"), py::arg("key"), py::arg("ids"), py::arg("n"), py::arg("order"),
       py::arg("stream") = 0);
   m.def(
+      "fit_report_device",
+      [](uintptr_t ctx, uintptr_t x, uint64_t P, uint64_t K, double nu, unsigned families,
+         uintptr_t fits, uintptr_t tail, uintptr_t stream) {
+        throw_code(tie_fit_report(reinterpret_cast<tie_ctx*>(ctx), (const double*)x, P, K, nu,
+                                  families, (double*)fits, (double*)tail, vp(stream)));
+      },
+      py::arg("ctx"), py::arg("x"), py::arg("P"), py::arg("K"), py::arg("nu"),
+      py::arg("families"), py::arg("fits"), py::arg("tail"), py::arg("stream") = 0,
+      "cmd_fit's per-prompt analysis on device buffers: fits[4][10][P], tail[5][P]");
+  m.def(
+      "fit_report",
+      [](carray<double> x, double nu, unsigned families) {
+        if (x.ndim() != 2) throw py::value_error("fit_report: x must be P x K");
+        const size_t P = (size_t)x.shape(0), K = (size_t)x.shape(1);
+        carray<double> fits({(py::ssize_t)4, (py::ssize_t)10, (py::ssize_t)P});
+        carray<double> tail({(py::ssize_t)5, (py::ssize_t)P});
+        std::fill(fits.mutable_data(), fits.mutable_data() + fits.size(),
+                  std::numeric_limits<double>::quiet_NaN());
+        int rc;
+        {
+          py::gil_scoped_release nogil;
+          rc = tie_fit_report_host(default_context(), x.data(), P, K, nu, families,
+                                   fits.mutable_data(), tail.mutable_data());
+        }
+        throw_code(rc);
+        return py::make_tuple(fits, tail);
+      },
+      py::arg("x"), py::arg("nu") = 3.5, py::arg("families") = 15u,
+      "cmd_fit's per-prompt analysis (tools/main.cpp:527-562) of every row of a P x K array: "
+      "(fits[4][10][P], tail[5][P])");
+  m.def(
       "score_rank_device",
       [](uintptr_t ctx, uintptr_t mu, uintptr_t sigma, uintptr_t max_tokens, uint64_t n,
          double alpha, double beta, uintptr_t E, uintptr_t C, uintptr_t S, uintptr_t order,

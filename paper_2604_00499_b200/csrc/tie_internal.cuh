@@ -26,6 +26,7 @@ enum Reason : uint32_t {
   kKeyNotFinite = 7,     // WaitingQueue::push: key must be finite        (sched.cpp:60)
   kDuplicateId = 8,      // WaitingQueue::push: id already queued         (sched.cpp:61-63)
   kSampleBad = 9,        // fit_logt_fixed_nu: samples must be finite and > 0 (fit.cpp:22-24)
+  kKsCdfRange = 10,      // ks_test: cdf returned a value outside [0, 1]  (fit.cpp:270-271)
 };
 
 __device__ __forceinline__ void report(unsigned long long* err, uint64_t index, uint32_t why) {
@@ -251,6 +252,9 @@ cudaError_t rank_prepared(tie_ctx* ctx, uint64_t n, uint64_t* order, cudaStream_
 cudaError_t launch_fit(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
                        double* mu, double* sigma, double* ll, int32_t* iters, uint8_t* conv,
                        uint8_t* degen, cudaStream_t s);
+// cmd_fit's per-prompt analysis (report.cu): fits[4][10][P], tail[5][P] (device)
+cudaError_t launch_fit_report(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
+                              unsigned families, double* fits, double* tail, cudaStream_t s);
 cudaError_t launch_loglik(tie_ctx* ctx, const double* x, uint64_t K, const double* mu,
                           const double* sigma, uint64_t P, double nu, double* ll, double* grad,
                           cudaStream_t s);

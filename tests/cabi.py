@@ -45,6 +45,7 @@ class CAbi:
         L.tie_score_rank_host.argtypes = [_p, _p, _p, _p, _u64, _d, _d, _p, _p, _u]
         L.tie_rank_host.argtypes = [_p, _p, _p, _u64, _p]
         L.tie_fit_host.argtypes = [_p, _p, _u64, _u64, _d, _p, _p, _p, _p, _p, _p]
+        L.tie_fit_report_host.argtypes = [_p, _p, _u64, _u64, _d, _u, _p, _p]
         L.tie_t_quantile.argtypes = [_d, _d]
         L.tie_t_quantile.restype = _d
         L.tie_compute_beta.argtypes = [_i, _d, _d, _d, _u64, ctypes.POINTER(_d)]
@@ -107,6 +108,15 @@ class CAbi:
                                          _ptr(it), _ptr(cv), _ptr(dg)))
         return dict(mu=mu, sigma=sg, log_likelihood=ll, iterations=it,
                     converged=cv.astype(bool), degenerate=dg.astype(bool))
+
+    def fit_report_raw(self, h, x, nu=3.5, families=15):
+        x = np.ascontiguousarray(x, np.float64)
+        P, K = x.shape
+        fits = np.full((4, 10, P), np.nan)
+        tail = np.full((5, P), np.nan)
+        self.check(self.lib.tie_fit_report_host(h, _ptr(x), P, K, nu, families, _ptr(fits),
+                                                _ptr(tail)))
+        return fits, tail
 
     def launches(self, reset=False):
         return int(self.lib.tie_launch_count(1 if reset else 0))

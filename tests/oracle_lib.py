@@ -96,6 +96,34 @@ class _Base:
                     converged=cv.astype(bool), degenerate=dg.astype(bool))
 
 
+    FIT_FAMILIES = ("logt", "logt_free_nu", "lognormal", "exponential")
+    FIT_FIELDS = ("mu", "sigma", "nu", "rate", "log_likelihood", "iterations", "converged",
+                  "degenerate", "ks_statistic", "ks_p_value")
+    TAIL_FIELDS = ("skewness", "cv", "p90_over_p50", "p99_over_p50", "top10_share")
+
+    def fit_report_raw(self, x, nu=3.5, families=15, threads=None):
+        """cmd_fit's per-prompt analysis -> (fits[4][10][P], tail[5][P]) arrays."""
+        x = np.ascontiguousarray(x, np.float64)
+        P, K = x.shape
+        fits = np.full((4, 10, P), np.nan)
+        tail = np.full((5, P), np.nan)
+        self._check(self._report(_ptr(x), P, K, nu, families, _ptr(fits), _ptr(tail),
+                                 _threads(threads)), "fit_report")
+        return fits, tail
+
+    def fit_report(self, x, nu=3.5, families=15, threads=None):
+        """-> ({family: {field: array[P]}}, {field: array[P]})."""
+        return unpack_report(*self.fit_report_raw(x, nu, families, threads), families)
+
+
+def unpack_report(fits, tail, families):
+    out = {}
+    for f, name in enumerate(_Base.FIT_FAMILIES):
+        if families >> f & 1:
+            out[name] = {k: fits[f, j] for j, k in enumerate(_Base.FIT_FIELDS)}
+    return out, {k: tail[j] for j, k in enumerate(_Base.TAIL_FIELDS)}
+
+
 class Oracle(_Base):
     """The C restatement (the parity checker)."""
 
@@ -118,6 +146,8 @@ class Oracle(_Base):
         self._beta = self._fn("compute_beta", [_i32, _d, _d, _d, _u64, ctypes.POINTER(_d)])
         self._rank = self._fn("rank", [_p, _p, _u64, _p])
         self._fit = self._fn("fit", [_p, _u64, _u64, _d, _p, _p, _p, _p, _p, _p, _i32])
+        self._report = self._fn("fit_report", [_p, _u64, _u64, _d, ctypes.c_uint, _p, _p,
+                                               _i32])
         self.logt_loglik_raw = self._fn("logt_loglik", [_p, _u64, _d, _d, _d], _d)
         self._gw = self._fn("gen_workload", [_u64, _u64, _d, _d, _d, _d, _d, ctypes.c_uint32,
                                              _d, _p, _p, _p, _p, _p, _p])
@@ -221,6 +251,8 @@ class RefLib(_Base):
         self.compute_beta_raw = self._fn("compute_beta", [_i32, _d, _d, _d, _u64], _d)
         self._rank = self._fn("rank", [_p, _p, _u64, _p])
         self._fit = self._fn("fit", [_p, _u64, _u64, _d, _p, _p, _p, _p, _p, _p, _i32])
+        self._report = self._fn("fit_report", [_p, _u64, _u64, _d, ctypes.c_uint, _p, _p,
+                                               _i32])
         self.logt_loglik_raw = self._fn("logt_loglik", [_p, _u64, _d, _d, _d], _d)
         self._gw = self._fn("gen_workload", [_u64, _u64, _d, _d, _d, _d, _d, ctypes.c_uint32,
                                              _d, _p, _p, _p, _p, _p, _p])

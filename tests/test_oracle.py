@@ -166,3 +166,29 @@ def test_sim_scores_oracle_vs_reference(oracle, predictor, family):
     E1, C1 = oracle.sim_scores(mu, sg, ids, mt, **kw)
     E2, C2 = R.sim_scores(mu, sg, ids, mt, **kw)
     assert np.array_equal(E1, E2) and np.array_equal(C1, C2)
+
+
+# ---------------------------------------------------------------- cmd_fit analysis (8f #3)
+FR_SETS = ("K16", "K5", "K12c", "K100", "degen")
+
+
+@pytest.mark.parametrize("name", FR_SETS)
+def test_fit_report_bit_exact(oracle, name):
+    """The restatement of cmd_fit's per-prompt analysis (four families, KS, tail stats)
+    equals the reference's fixtures bit for bit."""
+    g = golden("fit_report.npz")
+    fits, tail = oracle.fit_report_raw(g[f"{name}__x"])
+    np.testing.assert_array_equal(fits, g[f"{name}__fits"])
+    np.testing.assert_array_equal(tail, g[f"{name}__tail"])
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built (no /root/reference)")
+def test_fit_report_oracle_vs_reference_library(oracle):
+    R = RefLib()
+    x, _, _ = R.gen_fit_data(400, 20, seed=21)
+    for fam, nu in [(15, 3.5), (1, 2.0), (6, 3.5)]:
+        a, b = oracle.fit_report_raw(x, nu, fam), R.fit_report_raw(x, nu, fam)
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])
+    with pytest.raises(ValueError, match="at least 5"):
+        oracle.fit_report_raw(x[:, :4])
