@@ -189,6 +189,40 @@ int tie_queue_step(tie_queue* q, const uint64_t* arr_ids, const double* arr_time
 /* Scheduler::rebuild_if_drifted() (sched.cpp:152-167) */
 int tie_queue_rebuild_if_drifted(tie_queue* q, int* rebuilt);
 
+/* ---- input formats ------------------------------------------------------
+ * Request traces: JSONL, one object per request -- load_trace / save_trace
+ * (proj/src/workload.cpp:82-161).  Load fills missing arrival_s from
+ * poisson_arrivals(fill_rps, count, seed) (fill_rps <= 0: such records are an error) and
+ * stable-sorts by arrival; mu / sigma are NaN where a record has none.  Host-only calls. */
+typedef struct tie_trace tie_trace;
+int tie_trace_load(const char* path, double fill_rps, uint64_t seed, tie_trace** out);
+uint64_t tie_trace_size(const tie_trace* t);
+const uint64_t* tie_trace_ids(const tie_trace* t);
+const double* tie_trace_arrival(const tie_trace* t);
+const uint32_t* tie_trace_prompt_tokens(const tie_trace* t);
+const uint32_t* tie_trace_output_tokens(const tie_trace* t);
+const uint32_t* tie_trace_max_tokens(const tie_trace* t);
+const double* tie_trace_mu(const tie_trace* t);
+const double* tie_trace_sigma(const tie_trace* t);
+void tie_trace_free(tie_trace* t);
+int tie_trace_save(const char* path, uint64_t n, const uint64_t* ids, const double* arrival,
+                   const uint32_t* prompt_tokens, const uint32_t* output_tokens,
+                   const uint32_t* max_tokens, const double* mu, const double* sigma);
+/* Fit inputs of `tie fit` (proj/tools/main.cpp:432-495): "*.csv" with header
+ * prompt_id,length, else JSONL {"prompt_id": str, "lengths": [int >= 1]}.  Prompt p's
+ * samples are lengths[offsets[p] .. offsets[p+1]). */
+typedef struct tie_fit_input tie_fit_input;
+int tie_fit_input_load(const char* path, tie_fit_input** out);
+uint64_t tie_fit_input_count(const tie_fit_input* f);
+const char* tie_fit_input_prompt_id(const tie_fit_input* f, uint64_t i);
+const uint64_t* tie_fit_input_offsets(const tie_fit_input* f);
+const double* tie_fit_input_lengths(const tie_fit_input* f);
+void tie_fit_input_free(tie_fit_input* f);
+/* tie_fit_report over ragged prompts (grouped by sample count, one GPU batch per group) */
+int tie_fit_report_ragged_host(tie_ctx* ctx, const double* lengths, const uint64_t* offsets,
+                               uint64_t P, double nu, unsigned families, double* fits,
+                               double* tail);
+
 /* ---- diagnostics ------------------------------------------------------------------------
  * Kernel-level profiling: with tie_profile(ctx, 1) every kernel launched by this context is
  * bracketed by a CUDA event pair on its stream; tie_profile_report() synchronises and

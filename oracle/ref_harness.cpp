@@ -25,6 +25,7 @@
 #include <exception>
 #include <string>
 #include <thread>
+#include <optional>
 #include <vector>
 
 #include "tiesched/dist.hpp"
@@ -251,6 +252,55 @@ int ref_fit_report(const double* x, uint64_t P, uint64_t K, double nu, unsigned 
     return fail(e, 1);
   } catch (const std::invalid_argument& e) {
     return fail(e, 2);
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
+}
+
+// save_trace / load_trace (workload.cpp:82-161) through the reference itself
+int ref_save_trace(const char* path, uint64_t n, const uint64_t* ids, const double* arrival,
+                   const uint32_t* prompt, const uint32_t* output, const uint32_t* max_tokens,
+                   const double* mu, const double* sigma) {
+  try {
+    std::vector<tie::Request> reqs(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      tie::Request& r = reqs[i];
+      r.id = ids[i];
+      r.arrival_s = arrival[i];
+      r.prompt_tokens = prompt[i];
+      r.true_output_tokens = output[i];
+      r.max_tokens = max_tokens[i];
+      if (mu && !std::isnan(mu[i])) r.true_mu = mu[i];
+      if (sigma && !std::isnan(sigma[i])) r.true_sigma = sigma[i];
+    }
+    tie::save_trace(reqs, path);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
+}
+
+int ref_load_trace(const char* path, double fill_rps, uint64_t seed, uint64_t cap, uint64_t* ids,
+                   double* arrival, uint32_t* prompt, uint32_t* output, uint32_t* max_tokens,
+                   double* mu, double* sigma, uint64_t* n_out) {
+  try {
+    std::optional<double> rps;
+    if (fill_rps > 0.0) rps = fill_rps;
+    std::vector<tie::Request> reqs = tie::load_trace(path, rps, seed);
+    *n_out = reqs.size();
+    for (uint64_t i = 0; i < reqs.size() && i < cap; ++i) {
+      const tie::Request& r = reqs[i];
+      ids[i] = r.id;
+      arrival[i] = r.arrival_s;
+      prompt[i] = r.prompt_tokens;
+      output[i] = r.true_output_tokens;
+      max_tokens[i] = r.max_tokens;
+      mu[i] = r.true_mu ? *r.true_mu : std::nan("");
+      sigma[i] = r.true_sigma ? *r.true_sigma : std::nan("");
+    }
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
   } catch (const std::exception& e) {
     return fail(e, 3);
   }

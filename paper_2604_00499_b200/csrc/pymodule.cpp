@@ -277,6 +277,78 @@ PYBIND11_MODULE(_core, m) {
       py::arg("x"), py::arg("nu") = 3.5, py::arg("families") = 15u,
       "cmd_fit's per-prompt analysis (tools/main.cpp:527-562) of every row of a P x K array: "
       "(fits[4][10][P], tail[5][P])");
+  // ---- input formats
+  m.def(
+      "load_trace",
+      [](const std::string& path, double fill_rps, uint64_t seed) {
+        tie_trace* t = nullptr;
+        throw_code(tie_trace_load(path.c_str(), fill_rps, seed, &t));
+        const size_t n = tie_trace_size(t);
+        py::dict d;
+        d["id"] = carray<uint64_t>((py::ssize_t)n, tie_trace_ids(t));
+        d["arrival_s"] = carray<double>((py::ssize_t)n, tie_trace_arrival(t));
+        d["prompt_tokens"] = carray<uint32_t>((py::ssize_t)n, tie_trace_prompt_tokens(t));
+        d["output_tokens"] = carray<uint32_t>((py::ssize_t)n, tie_trace_output_tokens(t));
+        d["max_tokens"] = carray<uint32_t>((py::ssize_t)n, tie_trace_max_tokens(t));
+        d["mu"] = carray<double>((py::ssize_t)n, tie_trace_mu(t));
+        d["sigma"] = carray<double>((py::ssize_t)n, tie_trace_sigma(t));
+        tie_trace_free(t);
+        return d;
+      },
+      py::arg("path"), py::arg("fill_rps") = 0.0, py::arg("seed") = 0,
+      "load_trace (workload.cpp:106-161) -> dict of arrays (mu / sigma NaN where absent)");
+  m.def(
+      "save_trace",
+      [](const std::string& path, carray<uint64_t> id, carray<double> arrival_s,
+         carray<uint32_t> prompt_tokens, carray<uint32_t> output_tokens,
+         carray<uint32_t> max_tokens, py::object mu, py::object sigma) {
+        const size_t n = (size_t)id.size();
+        carray<double> m = mu.is_none() ? carray<double>() : mu.cast<carray<double>>();
+        carray<double> s = sigma.is_none() ? carray<double>() : sigma.cast<carray<double>>();
+        throw_code(tie_trace_save(path.c_str(), n, id.data(), arrival_s.data(),
+                                  prompt_tokens.data(), output_tokens.data(), max_tokens.data(),
+                                  mu.is_none() ? nullptr : m.data(),
+                                  sigma.is_none() ? nullptr : s.data()));
+      },
+      py::arg("path"), py::arg("id"), py::arg("arrival_s"), py::arg("prompt_tokens"),
+      py::arg("output_tokens"), py::arg("max_tokens"), py::arg("mu") = py::none(),
+      py::arg("sigma") = py::none(), "save_trace (workload.cpp:94-104)");
+  m.def(
+      "load_fit_input",
+      [](const std::string& path) {
+        tie_fit_input* f = nullptr;
+        throw_code(tie_fit_input_load(path.c_str(), &f));
+        const size_t n = tie_fit_input_count(f);
+        py::list ids;
+        for (size_t i = 0; i < n; ++i) ids.append(py::str(tie_fit_input_prompt_id(f, i)));
+        const uint64_t* off = tie_fit_input_offsets(f);
+        auto offsets = carray<uint64_t>((py::ssize_t)(n + 1), off);
+        auto lengths = carray<double>((py::ssize_t)off[n], tie_fit_input_lengths(f));
+        tie_fit_input_free(f);
+        return py::make_tuple(ids, offsets, lengths);
+      },
+      py::arg("path"),
+      "`tie fit` input (main.cpp:432-495): (prompt_ids, offsets[P+1], lengths)");
+  m.def(
+      "fit_report_ragged",
+      [](carray<double> lengths, carray<uint64_t> offsets, double nu, unsigned families) {
+        const size_t P = (size_t)offsets.size() - 1;
+        carray<double> fits({(py::ssize_t)4, (py::ssize_t)10, (py::ssize_t)P});
+        carray<double> tail({(py::ssize_t)5, (py::ssize_t)P});
+        std::fill(fits.mutable_data(), fits.mutable_data() + fits.size(),
+                  std::numeric_limits<double>::quiet_NaN());
+        int rc;
+        {
+          py::gil_scoped_release nogil;
+          rc = tie_fit_report_ragged_host(default_context(), lengths.data(), offsets.data(), P,
+                                          nu, families, fits.mutable_data(),
+                                          tail.mutable_data());
+        }
+        throw_code(rc);
+        return py::make_tuple(fits, tail);
+      },
+      py::arg("lengths"), py::arg("offsets"), py::arg("nu") = 3.5, py::arg("families") = 15u,
+      "fit_report over ragged prompts (grouped by sample count on the host)");
   m.def(
       "score_rank_device",
       [](uintptr_t ctx, uintptr_t mu, uintptr_t sigma, uintptr_t max_tokens, uint64_t n,

@@ -46,6 +46,7 @@ class CAbi:
         L.tie_rank_host.argtypes = [_p, _p, _p, _u64, _p]
         L.tie_fit_host.argtypes = [_p, _p, _u64, _u64, _d, _p, _p, _p, _p, _p, _p]
         L.tie_fit_report_host.argtypes = [_p, _p, _u64, _u64, _d, _u, _p, _p]
+        L.tie_fit_report_ragged_host.argtypes = [_p, _p, _p, _u64, _d, _u, _p, _p]
         L.tie_t_quantile.argtypes = [_d, _d]
         L.tie_t_quantile.restype = _d
         L.tie_compute_beta.argtypes = [_i, _d, _d, _d, _u64, ctypes.POINTER(_d)]
@@ -116,6 +117,16 @@ class CAbi:
         tail = np.full((5, P), np.nan)
         self.check(self.lib.tie_fit_report_host(h, _ptr(x), P, K, nu, families, _ptr(fits),
                                                 _ptr(tail)))
+        return fits, tail
+
+    def fit_report_ragged_raw(self, h, lengths, offsets, nu=3.5, families=15):
+        lengths = np.ascontiguousarray(lengths, np.float64)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        P = len(offsets) - 1
+        fits = np.full((4, 10, P), np.nan)
+        tail = np.full((5, P), np.nan)
+        self.check(self.lib.tie_fit_report_ragged_host(h, _ptr(lengths), _ptr(offsets), P, nu,
+                                                       families, _ptr(fits), _ptr(tail)))
         return fits, tail
 
     def launches(self, reset=False):

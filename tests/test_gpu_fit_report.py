@@ -77,3 +77,17 @@ def test_fit_report_errors(abi, h):
     x[1, 2] = -1.0
     with pytest.raises(TieError, match="finite and > 0"):
         abi.fit_report_raw(h, x)
+
+
+def test_fit_report_ragged_prompts(abi, h, oracle):
+    """`tie fit` inputs are ragged: prompts with 5..40 samples, grouped by count on the host,
+    one GPU batch per group; each prompt equals the oracle's report of its own row."""
+    rng = np.random.default_rng(12)
+    Ks = rng.integers(5, 41, 700)
+    rows = [oracle.gen_fit_data(1, int(k), seed=100 + i)[0][0] for i, k in enumerate(Ks)]
+    offsets = np.r_[0, np.cumsum(Ks)].astype(np.uint64)
+    fits, tail = abi.fit_report_ragged_raw(h, np.concatenate(rows), offsets)
+    for k in np.unique(Ks):
+        sel = np.flatnonzero(Ks == k)
+        rf, rt = oracle.fit_report_raw(np.stack([rows[i] for i in sel]))
+        check(fits[:, :, sel], rf, tail[:, sel], rt)
