@@ -235,6 +235,7 @@ void tie_ctx_destroy(tie_ctx* ctx) {
   cudaFree(ctx->d_table);
   cudaFree(ctx->d_tail);
   cudaFree(ctx->d_bins);
+  cudaFree(ctx->d_ka_table);
   cudaFree(ctx->d_err);
   cudaFree(ctx->scratch);
   cudaFree(ctx->io);

@@ -460,8 +460,7 @@ __device__ __forceinline__ void stage_rows_async(const double* myrow, double* sl
       const unsigned dst =
           (unsigned)__cvta_generic_to_shared(slab + r * kSlabStride + 2 * sub);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
-                   "l"(reinterpret_cast<const double2*>(rp) + sub)
-                   : "memory");
+                   "l"(reinterpret_cast<const double2*>(rp) + sub));
     }
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
@@ -543,13 +542,24 @@ __global__ void __launch_bounds__(256, kMinBlocks) score_coop_kernel(const __gri
   double* slab = slab_all[wib];
   const double** ptrs = ptr_all[wib];
   const bool ka_smem = p.ka_smem && p.G <= kKaMaxG && p.k_alpha > 0;
-  if (ka_smem) {
-    for (int c = threadIdx.x; c < p.G * (kMoments / 2); c += blockDim.x) {
-      const int g = c / (kMoments / 2), sub = c % (kMoments / 2);
-      const double2 v = __ldg(reinterpret_cast<const double2*>(
-                                  p.table + ((size_t)g * (p.N + 1) + p.k_alpha) * kMoments) +
-                              sub);
-      *reinterpret_cast<double2*>(ka_rows + g * kSlabStride + 2 * sub) = v;
+  if (ka_smem) {  // the per-alpha k_alpha rows are one contiguous table: coalesced loads,
+                  // all in flight before the first store
+    constexpr int kU = 8;  // 8 x 256 x 16 B = 32 KB >= G_max(320) x 96 B
+    const int nc = p.G * (kMoments / 2);
+    double2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int c = threadIdx.x + u * 256;
+      v[u] = c < nc ? __ldg(reinterpret_cast<const double2*>(p.ka_table) + c)
+                    : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int c = threadIdx.x + u * 256;
+      if (c < nc) {
+        const int g = c / (kMoments / 2), sub = c % (kMoments / 2);
+        *reinterpret_cast<double2*>(ka_rows + g * kSlabStride + 2 * sub) = v[u];
+      }
     }
   }
   __syncthreads();
@@ -558,22 +568,25 @@ __global__ void __launch_bounds__(256, kMinBlocks) score_coop_kernel(const __gri
   const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   uint64_t base = warp0 * 32;
-  double nm = 0.0, nsig = 1.0, nxm = 1.0;
+  // the next iteration's inputs are prefetched raw (converted only when used, so the
+  // conversion does not wait on the load)
+  double nm = 0.0, nsig = 1.0;
+  XT nxm = (XT)1;
   if (base + lane < n) {
     nm = mu[base + lane];
     nsig = sigma[base + lane];
-    nxm = (double)xmax[base + lane];
+    nxm = xmax[base + lane];
   }
   for (; base < n; base += nwarps * 32) {  // warp-uniform loop
     const uint64_t i = base + lane;
     const bool active = i < n;
-    const double m = nm, sig = nsig, xm = nxm;
+    const double m = nm, sig = nsig, xm = (double)nxm;
     {  // prefetch the next iteration's inputs
       const uint64_t j = i + nwarps * 32;
       if (j < n) {
         nm = mu[j];
         nsig = sigma[j];
-        nxm = (double)xmax[j];
+        nxm = xmax[j];
       }
     }
     // LogTParams / CensoredLogT validation (dist.cpp:108-120)
@@ -659,6 +672,16 @@ __global__ void __launch_bounds__(256, kMinBlocks) score_coop_kernel(const __gri
     }
   }
   if (minmax) key_range_flush(minmax, kmin, kmax);
+}
+
+// k_alpha rows of every grid point into one contiguous [G][kMoments] table (once per alpha)
+__global__ void gather_ka_rows_kernel(const double* __restrict__ table, int G, int N,
+                                      uint32_t k_alpha, double* __restrict__ out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < G * kMoments;
+       c += gridDim.x * blockDim.x) {
+    const int g = c / kMoments, m = c % kMoments;
+    out[c] = table[((size_t)g * (N + 1) + k_alpha) * kMoments + m];
+  }
 }
 
 int sm_count(int device) {
@@ -841,6 +864,18 @@ cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, co
     ctx->ka_k = k;
   }
   p.k_alpha = ctx->ka_k;
+  if (ctx->ka_table_k != ctx->ka_k || !ctx->d_ka_table) {  // contiguous k_alpha rows
+    if (!ctx->d_ka_table) {
+      const cudaError_t e = cudaMalloc(&ctx->d_ka_table, sizeof(double) * kMoments *
+                                                             std::max(ctx->G, 1));
+      if (e != cudaSuccess) return e;
+    }
+    if (ctx->G > 0)
+      gather_ka_rows_kernel<<<(ctx->G * kMoments + 255) / 256, 256, 0, s>>>(
+          ctx->d_table, ctx->G, ctx->N, ctx->ka_k, ctx->d_ka_table);
+    ctx->ka_table_k = ctx->ka_k;
+  }
+  p.ka_table = ctx->d_ka_table;
   const int sms = sm_count(ctx->device);
   const uint64_t blocks_needed = (n + 255) / 256;
   ProfScope prof(ctx, exact ? "score.exact" : "score.moment", s);

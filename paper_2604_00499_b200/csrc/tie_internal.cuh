@@ -147,6 +147,7 @@ struct ScoreParams {
   int N;
   int G;                    // grid points in the table (0 => no table)
   uint32_t k_alpha;         // upper_bound(Y, t_quantile(alpha, nu)); 0 when alpha == 0
+  const double* ka_table;   // [G][kMoments] the k_alpha row of every grid point
   double alpha, beta;
   int raw;                  // TIE_SCORE_RAW: skip max(C,E) and compute_score
   int ka_smem;              // stage the k_alpha rows of every grid point in shared memory
@@ -188,6 +189,8 @@ struct tie_ctx {
   // cached k_alpha = upper_bound(Y, t_quantile(alpha, nu)) of the last alpha seen
   double ka_alpha = -1.0;
   uint32_t ka_k = 0;
+  double* d_ka_table = nullptr;          // [G][kMoments] rows at k = ka_table_k
+  uint32_t ka_table_k = 0xffffffffu;
   // pinned host staging for the *_host entry points
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
