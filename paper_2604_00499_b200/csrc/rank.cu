@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "tie_internal.cuh"
 
@@ -558,6 +559,33 @@ __device__ __forceinline__ uint32_t scan_block_excl(uint32_t v, uint32_t* sh) {
   return r;
 }
 
+template <int kT>
+__device__ __forceinline__ uint32_t block_excl_scan_t(uint32_t v, uint32_t* sh) {
+  constexpr int kW = kT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < kW ? sh[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < kW) sh[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t r = x - v + (warp ? sh[warp - 1] : 0u);
+  __syncthreads();
+  return r;
+}
+
 __global__ void __launch_bounds__(kScanThreads) bucket_scan_a_kernel(Bucket b) {
   __shared__ uint32_t sh[32];
   const uint32_t i0 = blockIdx.x * kScanChunk + threadIdx.x * kScanPer;
@@ -763,20 +791,25 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(Part q, uint64
     const uint32_t c = h[p];
     q.cta_off[(uint64_t)blockIdx.x * q.P + p] = c ? atomicAdd(q.pcount + p, c) : 0u;
   }
-}
-
-__global__ void __launch_bounds__(kScanThreads) part_scan_kernel(Part q, uint64_t n) {
+  // the last CTA to finish turns the partition counts into bases (no separate scan launch)
+  __shared__ uint32_t ticket;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(q.pcount + q.P, 1u);
+  __syncthreads();
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  constexpr int kPer = kPartMaxP / kPartThreads;
   __shared__ uint32_t sh[32];
-  constexpr int kPer = kPartMaxP / kScanThreads;
   uint32_t c[kPer], t = 0;
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const uint32_t p = threadIdx.x * kPer + j;
-    c[j] = p < q.P ? q.pcount[p] : 0u;
+    c[j] = p < q.P ? __ldcg(q.pcount + p) : 0u;
     t += c[j];
     if (c[j] > kPartCap) *q.overflow = 1;
   }
-  uint32_t v = scan_block_excl(t, sh);
+  uint32_t v = block_excl_scan_t<kPartThreads>(t, sh);
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const uint32_t p = threadIdx.x * kPer + j;
@@ -817,7 +850,8 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(Part q, uint
   }
 }
 
-__global__ void __launch_bounds__(kPartThreads, 3) part_sort_kernel(Part q, uint64_t n,
+template <int kT>
+__global__ void __launch_bounds__(kT, 1536 / kT) part_sort_kernel(Part q, uint64_t n,
                                                                    const uint64_t* __restrict__ ids,
                                                                    uint64_t* __restrict__ order,
                                                                    Fallback f) {
@@ -837,10 +871,10 @@ __global__ void __launch_bounds__(kPartThreads, 3) part_sort_kernel(Part q, uint
   uint32_t* fc = fb + (1u << kPartMaxFineLog2) + 1;              // [nf] counts / cursors
   __shared__ uint32_t sh[32];
   const uint32_t nf = 1u << q.fine_log2, fmask = nf - 1u;
-  for (uint32_t j = threadIdx.x; j < nf; j += kPartThreads) fc[j] = 0;
+  for (uint32_t j = threadIdx.x; j < nf; j += kT) fc[j] = 0;
   __syncthreads();
   const KeyRange r = key_range(q.mm, q.p_log2 + q.fine_log2);
-  for (uint32_t j = threadIdx.x; j < m; j += kPartThreads) {
+  for (uint32_t j = threadIdx.x; j < m; j += kT) {
     const uint64_t k = q.tk[s0 + j];
     sk[j] = k;
     sv[j] = q.tv[s0 + j];
@@ -850,7 +884,7 @@ __global__ void __launch_bounds__(kPartThreads, 3) part_sort_kernel(Part q, uint
   }
   __syncthreads();
   {  // exclusive scan of the nf (<= 1024) fine counts, 4 per thread
-    constexpr int kPer = (1 << kPartMaxFineLog2) / kPartThreads;
+    constexpr int kPer = (1 << kPartMaxFineLog2) / kT;
     uint32_t c[kPer], t = 0;
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
@@ -858,7 +892,7 @@ __global__ void __launch_bounds__(kPartThreads, 3) part_sort_kernel(Part q, uint
       c[u] = j < nf ? fc[j] : 0u;
       t += c[u];
     }
-    uint32_t v = block_excl_scan_256(t, sh);
+    uint32_t v = block_excl_scan_t<kT>(t, sh);
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
@@ -872,10 +906,10 @@ __global__ void __launch_bounds__(kPartThreads, 3) part_sort_kernel(Part q, uint
     if (threadIdx.x == 0) fb[nf] = m;
   }
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < m; j += kPartThreads) perm[atomicAdd(&fc[sf[j]], 1u)] = (uint16_t)j;
+  for (uint32_t j = threadIdx.x; j < m; j += kT) perm[atomicAdd(&fc[sf[j]], 1u)] = (uint16_t)j;
   __syncthreads();
   uint16_t* spos = sf;  // a key's final position in the partition replaces its fine bucket
-  for (uint32_t j = threadIdx.x; j < m; j += kPartThreads) {
+  for (uint32_t j = threadIdx.x; j < m; j += kT) {
     const uint64_t k = sk[j];
     const uint32_t v = sv[j], fine = sf[j];
     const uint32_t lo = fb[fine], hi = fb[fine + 1];
@@ -892,9 +926,9 @@ __global__ void __launch_bounds__(kPartThreads, 3) part_sort_kernel(Part q, uint
   // partition's slice of the dispatch order out coalesced -- also when `order` is mapped
   // pinned host memory (the host API's zero-copy output)
   uint32_t* outv = reinterpret_cast<uint32_t*>(sk);
-  for (uint32_t j = threadIdx.x; j < m; j += kPartThreads) outv[spos[j]] = sv[j];
+  for (uint32_t j = threadIdx.x; j < m; j += kT) outv[spos[j]] = sv[j];
   __syncthreads();
-  for (uint32_t p = threadIdx.x; p < m; p += kPartThreads) {
+  for (uint32_t p = threadIdx.x; p < m; p += kT) {
     const uint32_t v = outv[p];
     order[s0 + p] = ids ? ids[v] : (uint64_t)v;
   }
@@ -962,7 +996,7 @@ Layout layout(uint64_t n, bool with_ids) {
       kPartMaxFineLog2);
   L.bzero_begin = off;
   if (L.part) {
-    L.pcount = off; off += align_up(4ull << L.p_log2);
+    L.pcount = off; off += align_up(4 * ((1ull << L.p_log2) + 1));  // + the count ticket
   } else {
     L.count = off; off += align_up(4 * nb);
   }
@@ -1073,7 +1107,9 @@ cudaError_t part_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_t*
   const size_t smem = (size_t)kPartCap * (8 + 4 + 2 + 2) +
                       4 * (2 * (1u << kPartMaxFineLog2) + 1);
   if (!attr) {
-    cudaFuncSetAttribute(part_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(part_sort_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(part_sort_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = true;
   }
@@ -1097,18 +1133,18 @@ cudaError_t part_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_t*
     part_count_kernel<<<q.ctas, kPartThreads, 0, s>>>(q, n);
   }
   {
-    ProfScope p(ctx, "rank.scan", s);
-    part_scan_kernel<<<1, kScanThreads, 0, s>>>(q, n);
-  }
-  {
     ProfScope p(ctx, "rank.scatter", s);
     part_scatter_kernel<<<q.ctas, kPartThreads, 0, s>>>(q, n);
   }
   {
     ProfScope p(ctx, "rank.local", s);
-    part_sort_kernel<<<q.P, kPartThreads, smem, s>>>(q, n, ids, order, f);
+    static const int threads = getenv("TIE_PART_SORT_THREADS") ? atoi(getenv("TIE_PART_SORT_THREADS")) : 512;
+    if (threads == 256)
+      part_sort_kernel<256><<<q.P, 256, smem, s>>>(q, n, ids, order, f);
+    else
+      part_sort_kernel<512><<<q.P, 512, smem, s>>>(q, n, ids, order, f);
   }
-  capi::count_launch(4);
+  capi::count_launch(3);
   return cudaGetLastError();
 }
 
