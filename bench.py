@@ -491,6 +491,43 @@ def run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream):
             "metric": "requests scored+ranked/sec, 64M-request queue on ONE B200 (config 4 size)",
             "value": n4 / (ms4 * 1e-3), "unit": "requests/s", "ms_per_step": ms4,
             "note": "inputs resident in HBM (1.3 GB, larger than L2); large-queue bucket sort"}
+        # rank 0's final step at G = 8 weak scaling (8 x 1M sorted (score, id) runs, as after
+        # the NCCL all-gather): k-way merge vs a stable re-sort of the concatenation
+        from paper_2604_00499_b200.dist import DeviceOps
+
+        G, L = 8, 1_000_000
+        ops = DeviceOps(tie.McContext(3.5, 10000, 12, dev.index or 0), ALPHA)
+        rk = torch.empty((G, L), dtype=torch.float64, device=dev)
+        ri = torch.empty((G, L), dtype=torch.int64, device=dev)
+        for g in range(G):
+            sc = S4[g * L:(g + 1) * L]
+            loc = ops.stable_sort(sc)
+            rk[g] = sc[loc]
+            ri[g] = loc + g * L
+        torch.cuda.synchronize()
+
+        def timed(f, reps=5):
+            f()
+            torch.cuda.synchronize()
+            a, b = ev(), ev()
+            a.record(stream)
+            for _ in range(reps):
+                f()
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / reps
+
+        res = {}
+        for g in (2, 4, 8):
+            flat = rk[:g].reshape(-1)
+            ms_merge = timed(lambda: ops.merge_runs(rk[:g], ri[:g], [L] * g))
+            ms_sort = timed(lambda: ops.stable_sort(flat))
+            res[f"G{g}"] = {"kmerge_ms": ms_merge, "stable_resort_ms": ms_sort}
+        ops.sync()
+        out["rank0_merge"] = {
+            "metric": "rank-0 final step of G x 1M sorted (score, id) runs (weak scaling): "
+                      "k-way merge vs stable re-sort of the concatenation", **res}
+        del rk, ri, flat
         del mu4, sg4, mt4, S4, o4
         torch.cuda.empty_cache()
     except Exception as exc:  # never blocks the headline line

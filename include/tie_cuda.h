@@ -125,6 +125,12 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
                         double* score, uint64_t* order, unsigned flags);
 int tie_rank_host(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n,
                   uint64_t* order);
+/* Sharded score+rank's final k-way merge: G runs on the device, run g =
+ * keys/ids[g*stride .. g*stride + lens[g]) (lens: HOST array), each sorted by (score asc, id
+ * asc) -- the reference heap's order (sched.cpp:28-31).  out_ids: the sum(lens) merged ids.
+ * Replaces the merge implied by one global WaitingQueue over all shards. */
+int tie_merge_runs(tie_ctx* ctx, const double* keys, const uint64_t* ids, int G,
+                   uint64_t stride, const uint64_t* lens, uint64_t* out_ids, void* stream);
 /* cmd_fit's per-prompt analysis (proj/tools/main.cpp:527-562) for P prompts x K >= 5 lengths:
  * families bitmask 1 logt (fit_logt_fixed_nu(x, nu), fit.cpp:73-178), 2 logt_free_nu
  * (fit_logt_free_nu over default_nu_grid, fit.cpp:180-200), 4 lognormal (fit.cpp:202-230),

@@ -564,6 +564,23 @@ int tie_rank_host(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t
   return tie_sync(ctx, s);
 }
 
+// final step of the sharded score+rank: merge G runs sorted by (score, id) (device buffers)
+int tie_merge_runs(tie_ctx* ctx, const double* keys, const uint64_t* ids, int G,
+                   uint64_t stride, const uint64_t* lens, uint64_t* out_ids, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (G < 0 || G > 128) return set_error(TIE_EINVALID, "tie_merge_runs: G must be in [0, 128]");
+  if (G && (!keys || !ids || !lens || !out_ids))
+    return set_error(TIE_EINVALID, "tie_merge_runs: null pointer");
+  for (int g = 0; g < G; ++g)
+    if (lens[g] > stride) return set_error(TIE_EINVALID, "tie_merge_runs: run longer than stride");
+  DeviceGuard dg(ctx->device);
+  ctx->err_op = "tie_merge_runs";
+  const cudaError_t e = tie::dev::launch_merge_runs(ctx, keys, ids, G, stride, lens, out_ids,
+                                                    as_stream(stream));
+  if (e != cudaSuccess) return cuda_error(e, "tie_merge_runs");
+  return TIE_OK;
+}
+
 // cmd_fit's per-prompt analysis (tools/main.cpp:527-562), device buffers
 int tie_fit_report(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
                    unsigned families, double* fits, double* tail, void* stream) {

@@ -247,6 +247,17 @@ PYBIND11_MODULE(_core, m) {
       py::arg("ctx"), py::arg("key"), py::arg("ids"), py::arg("n"), py::arg("order"),
       py::arg("stream") = 0);
   m.def(
+      "merge_runs_device",
+      [](uintptr_t ctx, uintptr_t keys, uintptr_t ids, uint64_t stride,
+         std::vector<uint64_t> lens, uintptr_t out_ids, uintptr_t stream) {
+        throw_code(tie_merge_runs(reinterpret_cast<tie_ctx*>(ctx), (const double*)keys,
+                                  (const uint64_t*)ids, (int)lens.size(), stride, lens.data(),
+                                  (uint64_t*)out_ids, vp(stream)));
+      },
+      py::arg("ctx"), py::arg("keys"), py::arg("ids"), py::arg("stride"), py::arg("lens"),
+      py::arg("out_ids"), py::arg("stream") = 0,
+      "k-way merge of G device runs sorted by (score, id): the sharded rank's final step");
+  m.def(
       "fit_report_device",
       [](uintptr_t ctx, uintptr_t x, uint64_t P, uint64_t K, double nu, unsigned families,
          uintptr_t fits, uintptr_t tail, uintptr_t stream) {

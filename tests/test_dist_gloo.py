@@ -38,6 +38,14 @@ class OracleOps:
         order = self.o.rank(S).astype(np.int64)
         return torch.from_numpy(S), torch.from_numpy(order)
 
+    def merge_runs(self, keys, ids, lens):
+        """reference semantics of the k-way merge: (key, id) order of the valid prefixes"""
+        import torch
+
+        k = np.concatenate([keys[g, :L].numpy() for g, L in enumerate(lens)])
+        i = np.concatenate([ids[g, :L].numpy() for g, L in enumerate(lens)])
+        return torch.from_numpy(i[np.lexsort((i, k))])
+
     def stable_sort(self, keys):
         return torch.from_numpy(np.argsort(keys.numpy(), kind="stable").astype(np.int64))
 
@@ -64,12 +72,12 @@ def _worker(rank, world, port, n_global, case, out_q):
         lo, hi = shard_bounds(n_global, world, rank)
         beta = o.compute_beta(True, 0.1, 0.5, 128.0, n_global)  # GLOBAL queue length
         ops = OracleOps()
-        for merge_on in ("root", "all"):
-            res = ShardedScoreRank(ops, beta, merge_on=merge_on)(
+        for merge_on, kway in (("root", "auto"), ("all", "auto"), ("root", "never")):
+            res = ShardedScoreRank(ops, beta, merge_on=merge_on, kway=kway)(
                 torch.from_numpy(mu[lo:hi].copy()), torch.from_numpy(sg[lo:hi].copy()),
                 torch.from_numpy(mt[lo:hi].copy()), n_global)
             if res.global_order is not None:
-                out_q.put((rank, merge_on, res.global_order.numpy().tolist()))
+                out_q.put((rank, merge_on + "/" + kway, res.global_order.numpy().tolist()))
     finally:
         dist.destroy_process_group()
 
@@ -85,7 +93,8 @@ def test_two_rank_order_matches_single_queue(n_global, case, oracle):
     for p in procs:
         p.join(timeout=180)
         assert p.exitcode == 0
-    got = [q.get(timeout=5) for _ in range(3)]  # root-merge on rank 0, all-merge on both
+    # k-way root merge and re-sort root merge on rank 0, all-merge on both ranks
+    got = [q.get(timeout=5) for _ in range(4)]
     # the reference: one queue, one heap
     if case == "workload":
         mu, sg, mt = oracle.gen_workload(n_global, seed=1)
