@@ -17,12 +17,15 @@
 //     no separate upsweep / scan kernels, keys read once and written once per pass;
 //   * digit runs are written out coalesced from the shared-memory-sorted tile; the LAST
 //     active pass writes the u64 dispatch order (ids[value]) directly instead of keys+values.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdlib>
 
 #include "tie_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace tie {
 namespace dev {
@@ -850,19 +853,14 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(Part q, uint
   }
 }
 
+// Sort partition p's m keys (already grouped at tk/tv[s0..s0+m)) and write its slice of the
+// dispatch order: fine-bucket counting sort in shared memory, each key ranked inside its fine
+// bucket (~1-2 keys) by (key, index), values placed in order, written out coalesced.
 template <int kT>
-__global__ void __launch_bounds__(kT, 1536 / kT) part_sort_kernel(Part q, uint64_t n,
-                                                                   const uint64_t* __restrict__ ids,
-                                                                   uint64_t* __restrict__ order,
-                                                                   Fallback f) {
-  if (*(volatile int*)q.overflow) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) lsd_tail_launch(f, q.keys, n, ids, order);
-    return;
-  }
-  const uint32_t p = blockIdx.x;
-  const uint32_t s0 = q.pbase[p], m = q.pbase[p + 1] - s0;  // m <= kPartCap
-  if (m == 0) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void sort_partition(const Part& q, uint32_t s0, uint32_t m,
+                                               const uint64_t* __restrict__ ids,
+                                               uint64_t* __restrict__ order,
+                                               unsigned char* smem_raw) {
   uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
   uint32_t* sv = reinterpret_cast<uint32_t*>(sk + kPartCap);
   uint16_t* sf = reinterpret_cast<uint16_t*>(sv + kPartCap);    // fine bucket of key j
@@ -932,6 +930,107 @@ __global__ void __launch_bounds__(kT, 1536 / kT) part_sort_kernel(Part q, uint64
     const uint32_t v = outv[p];
     order[s0 + p] = ids ? ids[v] : (uint64_t)v;
   }
+}
+
+template <int kT>
+__global__ void __launch_bounds__(kT, 1536 / kT) part_sort_kernel(Part q, uint64_t n,
+                                                                   const uint64_t* __restrict__ ids,
+                                                                   uint64_t* __restrict__ order,
+                                                                   Fallback f) {
+  if (*(volatile int*)q.overflow) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) lsd_tail_launch(f, q.keys, n, ids, order);
+    return;
+  }
+  const uint32_t p = blockIdx.x;
+  const uint32_t s0 = q.pbase[p], m = q.pbase[p + 1] - s0;  // m <= kPartCap
+  if (m == 0) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  sort_partition<kT>(q, s0, m, ids, order, smem_raw);
+}
+
+// The partition path in ONE cooperative launch: count (keys of the CTA's chunk staged in
+// shared memory, one atomic per (CTA, partition) reservation) -> grid sync -> every CTA scans
+// the partition counts itself and scatters its staged keys (no second read of the keys) ->
+// grid sync -> the CTAs sort the partitions round-robin.  An overflowing partition leaves
+// everything to part_fallback_kernel (the device-side LSD path).
+constexpr int kFusedThreads = 512;
+
+__global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
+    Part q, uint64_t n, const uint64_t* __restrict__ ids, uint64_t* __restrict__ order) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t pb[kPartMaxP + 1];  // partition bases (every CTA keeps its own copy)
+  __shared__ uint32_t sh[32];
+  __shared__ int over;
+  const uint32_t P = q.P;
+  uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);   // [P] chunk histogram -> cursors
+  uint64_t* ck = reinterpret_cast<uint64_t*>(h + kPartMaxP);  // the chunk's keys
+  for (uint32_t p = threadIdx.x; p < P; p += kFusedThreads) h[p] = 0;
+  __syncthreads();
+  const KeyRange r = key_range(q.mm, q.p_log2 + q.fine_log2);
+  const uint64_t lo = (uint64_t)blockIdx.x * q.chunk;
+  const uint64_t hi = min(n, lo + q.chunk);
+  const uint32_t cn = hi > lo ? (uint32_t)(hi - lo) : 0u;
+  for (uint32_t j = threadIdx.x; j < cn; j += kFusedThreads) {
+    const uint64_t k = q.keys[lo + j];
+    ck[j] = k;
+    atomicAdd(&h[part_bucket(q, r, k) >> q.fine_log2], 1u);
+  }
+  __syncthreads();
+  for (uint32_t p = threadIdx.x; p < P; p += kFusedThreads) {
+    const uint32_t c = h[p];
+    h[p] = c ? atomicAdd(q.pcount + p, c) : 0u;  // this CTA's offset inside partition p
+  }
+  grid.sync();
+  // partition bases from the final counts (each CTA scans the <= 2048 counts itself)
+  {
+    constexpr int kPer = kPartMaxP / kFusedThreads;
+    uint32_t c[kPer], t = 0;
+    int big = 0;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t p = threadIdx.x * kPer + u;
+      c[u] = p < P ? __ldcg(q.pcount + p) : 0u;
+      t += c[u];
+      big |= c[u] > kPartCap;
+    }
+    if (threadIdx.x == 0) over = 0;
+    __syncthreads();
+    if (big) over = 1;
+    uint32_t v = block_excl_scan_t<kFusedThreads>(t, sh);
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t p = threadIdx.x * kPer + u;
+      if (p < P) pb[p] = v;
+      v += c[u];
+    }
+    if (threadIdx.x == 0) pb[P] = (uint32_t)n;
+    __syncthreads();
+  }
+  if (over) {  // identical decision in every CTA (same counts): hand over to the LSD path
+    if (blockIdx.x == 0 && threadIdx.x == 0) *q.overflow = 1;
+    return;
+  }
+  for (uint32_t p = threadIdx.x; p < P; p += kFusedThreads) h[p] += pb[p];
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < cn; j += kFusedThreads) {
+    const uint64_t k = ck[j];
+    const uint32_t pos = atomicAdd(&h[part_bucket(q, r, k) >> q.fine_log2], 1u);
+    q.tk[pos] = k;
+    q.tv[pos] = (uint32_t)(lo + j);
+  }
+  grid.sync();
+  for (uint32_t p = blockIdx.x; p < P; p += gridDim.x) {
+    const uint32_t s0 = pb[p], m = pb[p + 1] - s0;
+    if (m) sort_partition<kFusedThreads>(q, s0, m, ids, order, smem_raw);
+    __syncthreads();
+  }
+}
+
+// after the fused kernel: the LSD fallback when a partition overflowed
+__global__ void part_fallback_kernel(Part q, uint64_t n, const uint64_t* ids, uint64_t* order,
+                                     Fallback f) {
+  if (*(volatile int*)q.overflow) lsd_tail_launch(f, q.keys, n, ids, order);
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -1128,6 +1227,34 @@ cudaError_t part_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_t*
   q.ctas = (uint32_t)std::min<uint64_t>(
       std::min<uint64_t>((uint64_t)sms * 2, kPartMaxCtas), (n + 1023) / 1024);
   q.chunk = (n + q.ctas - 1) / q.ctas;
+  // default: the whole path as one cooperative launch (count -> scatter -> sort)
+  static const int fused = getenv("TIE_PART_UNFUSED") ? 0 : 1;  // A/B switch
+  if (fused) {
+    static bool fattr = false;
+    static int bpsm = 0;
+    if (!fattr) {
+      cudaFuncSetAttribute(part_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, part_fused_kernel, kFusedThreads,
+                                                    smem);
+      fattr = true;
+    }
+    const uint64_t co = (uint64_t)std::max(bpsm, 0) * sms;  // co-resident CTAs
+    Part qf = q;
+    qf.ctas = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(co, kPartMaxCtas),
+                                           (n + 1023) / 1024);
+    if (qf.ctas > 0) qf.chunk = (n + qf.ctas - 1) / qf.ctas;
+    if (qf.ctas > 0 && 4 * kPartMaxP + 8 * qf.chunk <= smem) {
+      ProfScope p(ctx, "rank.fused", s);
+      void* args[] = {(void*)&qf, (void*)&n, (void*)&ids, (void*)&order};
+      cudaError_t e = cudaLaunchCooperativeKernel((const void*)part_fused_kernel, qf.ctas,
+                                                  kFusedThreads, args, smem, s);
+      if (e != cudaSuccess) return e;
+      part_fallback_kernel<<<1, 1, 0, s>>>(qf, n, ids, order, f);
+      capi::count_launch(2);
+      return cudaGetLastError();
+    }
+  }
   {
     ProfScope p(ctx, "rank.count", s);
     part_count_kernel<<<q.ctas, kPartThreads, 0, s>>>(q, n);
