@@ -43,20 +43,21 @@ def _ref():
     return L
 
 
-def run(tie, mc, sizes=(1000, 10_000, 100_000, 1_000_000), steps=120, per_step=32, pops=8,
+def run(tie, mc, sizes=(1000, 10_000, 100_000, 1_000_000, 10_000_000, 64 * 2 ** 20), steps=120,
+        per_step=32, pops=8,
         variants=("steady", "rekey"), cpu=True, cpu_max_n=1_000_000):
     ptr = lambda a: a.ctypes.data
     L = _ref() if cpu else None
-    out = {}
-    for variant in variants:
-        q_sat = 128.0 if variant == "steady" else 1e9
-        thr = 0.1 if variant == "steady" else 0.0
-        res = {}
-        for n in sizes:
-            tot = n + steps * per_step
-            w = tie.gen_logt_workload_soa(tot, 7)
-            mu, sg, mt = w["mu"], w["sigma"], w["max_tokens"]
-            ids = np.arange(tot, dtype=np.uint64)
+    out = {v: {} for v in variants}
+    for n in sizes:  # one workload per queue size, shared by the variants
+        tot = n + steps * per_step
+        w = tie.gen_logt_workload_soa(tot, 7)
+        mu, sg, mt = w["mu"], w["sigma"], w["max_tokens"]
+        ids = np.arange(tot, dtype=np.uint64)
+        for variant in variants:
+            q_sat = 128.0 if variant == "steady" else 1e9
+            thr = 0.1 if variant == "steady" else 0.0
+            res = out[variant]
             cfg = tie.ScoreConfig()
             cfg.q_sat = q_sat
             cfg.rebuild_threshold = thr
@@ -80,7 +81,8 @@ def run(tie, mc, sizes=(1000, 10_000, 100_000, 1_000_000), steps=120, per_step=3
             r = {"gpu_p50_us": 1e6 * float(np.median(lat)),
                  "gpu_p90_us": 1e6 * float(np.percentile(lat, 90)), "steps": steps}
             if L is not None and n <= cpu_max_n:
-                cpu_steps = steps if (variant == "steady" or n <= 100_000) else max(20, steps // 6)
+                cpu_steps = (steps if (variant == "steady" or n <= 100_000)
+                             else max(20, steps // 6))
                 secs = np.empty(cpu_steps)
                 pop_ref = np.empty(cpu_steps * pops, np.uint64)
                 npop = ctypes.c_uint64(0)
@@ -100,7 +102,6 @@ def run(tie, mc, sizes=(1000, 10_000, 100_000, 1_000_000), steps=120, per_step=3
                               "pops_identical": bool(np.array_equal(ref_pop[:m], gpu_pop[:m])),
                               "pops_compared": int(m)})
             res[str(n)] = r
-        out[variant] = res
     return out
 
 
