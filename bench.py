@@ -35,6 +35,7 @@ N_CONFIG2 = 1_000_000
 ALPHA = 0.9
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0
+TRAFFIC_FILE = "ncu_traffic_r01h.json"
 
 
 def parse():
@@ -324,37 +325,60 @@ def main():
     active = sum(1 for p in range(8)
                  if len(np.unique(((bits >> np.uint64(8 * p)) & np.uint64(255))[:200000])) > 1)
     dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
-    roof = None
-    if dom in ("rank.downsweep", "rank.onesweep"):
-        bytes_per_launch = 24.0 * n_local  # read + write one (8 B key, 4 B id) record per key
-        t_launch = kern[dom]["ms_per_step"] * 1e-3 / max(active, 1)
-        ach = bytes_per_launch / t_launch / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "traffic": None, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": bytes_per_launch, "active_passes": active,
-                "launch_ms": t_launch * 1e3}
-    else:
-        bytes_per_launch = 28.0 * n_local  # mu, sigma (16 B) + max_tokens (4 B) in, key (8 B) out
-        t_launch = kern[dom]["ms_per_step"] * 1e-3 / max(kern[dom]["launches"], 1)
-        ach = bytes_per_launch / t_launch / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "traffic": None, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": bytes_per_launch, "launch_ms": t_launch * 1e3}
+    # algorithmic bytes per launch: the score kernel reads mu, sigma (16 B) + max_tokens (4 B)
+    # and writes the u64 key (8 B); a sort reads each key (8 B) and writes the order (8 B); an
+    # LSD digit pass reads and writes one (8 B key, 4 B value) record per key
+    algo = {"score.moment": 28.0, "rank.fused": 16.0, "rank.local": 16.0,
+            "rank.onesweep": 24.0, "rank.downsweep": 24.0}
 
-    # DRAM traffic per launch of the dominant kernel from the committed ncu --set full capture
-    # of this same configuration (profiles/ncu_traffic_r01.json), scaled to this n
+    def roofline(k):
+        per = algo.get(k, 28.0)
+        launches = max(active, 1) if k in ("rank.onesweep", "rank.downsweep") else \
+            max(kern[k]["launches"], 1)
+        t_launch = kern[k]["ms_per_step"] * 1e-3 / launches
+        ach = per * n_local / t_launch / 1e9
+        return {"kernel": k, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": per * n_local,
+                "algorithmic_bytes_per_unit": per, "launch_ms": t_launch * 1e3}
+
+    roof = roofline(dom)
+    others = {k: roofline(k) for k in kern if k != dom and k in algo}
+
+    # the score kernel against the FP64 roofline SURVEY.md 8d defines for it: one sample-term
+    # exp(mu + sigma Y_i) = 32 FP64 flops, k_max(r) = #{Y_i <= y_max(r)} terms per request;
+    # the moment tables evaluate O(1) work per request instead, so the per-term rate is an
+    # EFFECTIVE figure (the reference's arithmetic it replaces), the executed FP64-pipe share
+    # comes from ncu
+    score_roof = roof if dom == "score.moment" else others.get("score.moment")
+    if score_roof is not None and n_local == N_CONFIG2:
+        Ys = np.asarray(mc.samples)
+        y_max = (np.log(mt_h.astype(np.float64)) - mu_h) / sg_h
+        terms = float(np.searchsorted(Ys, y_max, side="right").sum())
+        t_k = kern["score.moment"]["ms_per_step"] * 1e-3 / max(kern["score.moment"]["launches"], 1)
+        score_roof["fp64_effective"] = {
+            "sample_terms_per_launch": terms, "flops_per_term": 32,
+            "effective_tflops": 32.0 * terms / t_k / 1e12,
+            "fp64_peak_tflops_nominal": 148 * 64 * 2 * 1.965e9 / 1e12,
+            "note": "reference arithmetic replaced per second; not executed flops"}
+
+    # DRAM traffic per launch from the committed ncu --set full capture of this same
+    # configuration (profiles/ncu_traffic_r01h.json), scaled to this n, and what bounds the
+    # kernel according to that capture
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01f.json")) as f:
+        with open(os.path.join(ROOT, "profiles", TRAFFIC_FILE)) as f:
             tr = json.load(f)
-        if dom in tr:
-            roof["traffic"] = (tr[dom]["dram_read_bytes"] + tr[dom]["dram_write_bytes"]) * (
-                n_local / tr["n"])
-            roof["traffic_source"] = "profiles/ncu_traffic_r01f.json: " + tr[dom]["capture"]
-            # what actually bounds it (ncu): the score kernel is gather-latency / L1-bound
-            roof["limiter"] = {"l1_throughput_pct": tr[dom].get("l1_throughput_pct"),
-                               "issue_active_pct": tr[dom].get("issue_active_pct"),
-                               "fp64_pipe_pct": tr[dom].get("fp64_pipe_pct"),
-                               "source": "ncu --set full, same capture"}
+        for r in [roof] + list(others.values()):
+            k = r["kernel"]
+            if k in tr:
+                r["traffic"] = (tr[k]["dram_read_bytes"] + tr[k]["dram_write_bytes"]) * (
+                    n_local / tr["n"])
+                r["traffic_source"] = f"profiles/{TRAFFIC_FILE}: " + tr[k]["capture"]
+                r["limiter"] = {"l1_throughput_pct": tr[k].get("l1_throughput_pct"),
+                                "issue_active_pct": tr[k].get("issue_active_pct"),
+                                "fp64_pipe_pct": tr[k].get("fp64_pipe_pct"),
+                                "top_stalls": tr[k].get("top_stalls"),
+                                "source": "ncu --set full, same capture"}
     except (OSError, KeyError, ValueError):
         pass
 
@@ -392,7 +416,8 @@ def main():
                     "statistic": f"median of {len(e2e_ts)} wall-clocked calls",
                     "api": "tie_score_rank_host (C-ABI), pinned",
                     "order_matches_device_path": e2e_order_ok},
-            "gpu_launches": launches, "roofline": roof, "clocks": clk,
+            "gpu_launches": launches, "roofline": roof, "roofline_other_kernels": others,
+            "clocks": clk,
             "kernels_ms_per_step": {k: round(v["ms_per_step"], 5) for k, v in kern.items()},
             "sorted_check": sorted_ok}
     line.update(extras)
