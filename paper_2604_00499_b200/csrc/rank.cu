@@ -1027,7 +1027,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
   }
 }
 
-// after the fused kernel: the LSD fallback when a partition overflowed
+// after the fused kernel: the LSD fallback when a partition overflowed (a cooperative launch
+// may not contain device-side launches -- cudaErrorNotPermitted -- so this is its own kernel)
 __global__ void part_fallback_kernel(Part q, uint64_t n, const uint64_t* ids, uint64_t* order,
                                      Fallback f) {
   if (*(volatile int*)q.overflow) lsd_tail_launch(f, q.keys, n, ids, order);
