@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "tie_internal.cuh"
@@ -767,6 +768,13 @@ struct Part {
   int* overflow;
   uint32_t p_log2, P, fine_log2, ctas;
   uint64_t chunk;
+  uint32_t low_bits;    // bits below the level-1 partition index (fine, or level-2 + fine)
+  uint32_t total_bits;  // B: bucket bits of (k - kmin) >> shift
+  uint32_t cap1;        // level-1 partition capacity (kPartCap; unbounded with level 2)
+  // level 2 (two-level path): P2 sub-partitions per level-1 partition, regrouped keys
+  uint32_t p2_log2;
+  uint64_t* tk2;
+  uint32_t* tv2;
 };
 
 __device__ __forceinline__ uint32_t part_bucket(const Part& q, const KeyRange& r, uint64_t k) {
@@ -777,7 +785,7 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(Part q, uint64
   __shared__ uint32_t h[kPartMaxP];
   for (uint32_t p = threadIdx.x; p < q.P; p += kPartThreads) h[p] = 0;
   __syncthreads();
-  const KeyRange r = key_range(q.mm, q.p_log2 + q.fine_log2);
+  const KeyRange r = key_range(q.mm, q.total_bits);
   const uint64_t lo = (uint64_t)blockIdx.x * q.chunk;
   const uint64_t hi = min(n, lo + q.chunk);
   uint64_t i = lo + threadIdx.x;
@@ -786,9 +794,9 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(Part q, uint64
 #pragma unroll
     for (int u = 0; u < 4; ++u) k[u] = q.keys[i + u * kPartThreads];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) atomicAdd(&h[part_bucket(q, r, k[u]) >> q.fine_log2], 1u);
+    for (int u = 0; u < 4; ++u) atomicAdd(&h[part_bucket(q, r, k[u]) >> q.low_bits], 1u);
   }
-  for (; i < hi; i += kPartThreads) atomicAdd(&h[part_bucket(q, r, q.keys[i]) >> q.fine_log2], 1u);
+  for (; i < hi; i += kPartThreads) atomicAdd(&h[part_bucket(q, r, q.keys[i]) >> q.low_bits], 1u);
   __syncthreads();
   for (uint32_t p = threadIdx.x; p < q.P; p += kPartThreads) {
     const uint32_t c = h[p];
@@ -810,7 +818,7 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(Part q, uint64
     const uint32_t p = threadIdx.x * kPer + j;
     c[j] = p < q.P ? __ldcg(q.pcount + p) : 0u;
     t += c[j];
-    if (c[j] > kPartCap) *q.overflow = 1;
+    if (c[j] > q.cap1) *q.overflow = 1;
   }
   uint32_t v = block_excl_scan_t<kPartThreads>(t, sh);
 #pragma unroll
@@ -828,7 +836,7 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(Part q, uint
   for (uint32_t p = threadIdx.x; p < q.P; p += kPartThreads)
     cur[p] = q.pbase[p] + q.cta_off[(uint64_t)blockIdx.x * q.P + p];
   __syncthreads();
-  const KeyRange r = key_range(q.mm, q.p_log2 + q.fine_log2);
+  const KeyRange r = key_range(q.mm, q.total_bits);
   const uint64_t lo = (uint64_t)blockIdx.x * q.chunk;
   const uint64_t hi = min(n, lo + q.chunk);
   uint64_t i = lo + threadIdx.x;
@@ -838,7 +846,7 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(Part q, uint
 #pragma unroll
     for (int u = 0; u < 4; ++u) k[u] = q.keys[i + u * kPartThreads];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) pos[u] = atomicAdd(&cur[part_bucket(q, r, k[u]) >> q.fine_log2], 1u);
+    for (int u = 0; u < 4; ++u) pos[u] = atomicAdd(&cur[part_bucket(q, r, k[u]) >> q.low_bits], 1u);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       q.tk[pos[u]] = k[u];
@@ -847,7 +855,7 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(Part q, uint
   }
   for (; i < hi; i += kPartThreads) {
     const uint64_t k = q.keys[i];
-    const uint32_t pos = atomicAdd(&cur[part_bucket(q, r, k) >> q.fine_log2], 1u);
+    const uint32_t pos = atomicAdd(&cur[part_bucket(q, r, k) >> q.low_bits], 1u);
     q.tk[pos] = k;
     q.tv[pos] = (uint32_t)i;
   }
@@ -871,7 +879,7 @@ __device__ __forceinline__ void sort_partition(const Part& q, uint32_t s0, uint3
   const uint32_t nf = 1u << q.fine_log2, fmask = nf - 1u;
   for (uint32_t j = threadIdx.x; j < nf; j += kT) fc[j] = 0;
   __syncthreads();
-  const KeyRange r = key_range(q.mm, q.p_log2 + q.fine_log2);
+  const KeyRange r = key_range(q.mm, q.total_bits);
   for (uint32_t j = threadIdx.x; j < m; j += kT) {
     const uint64_t k = q.tk[s0 + j];
     sk[j] = k;
@@ -967,14 +975,14 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
   uint64_t* ck = reinterpret_cast<uint64_t*>(h + kPartMaxP);  // the chunk's keys
   for (uint32_t p = threadIdx.x; p < P; p += kFusedThreads) h[p] = 0;
   __syncthreads();
-  const KeyRange r = key_range(q.mm, q.p_log2 + q.fine_log2);
+  const KeyRange r = key_range(q.mm, q.total_bits);
   const uint64_t lo = (uint64_t)blockIdx.x * q.chunk;
   const uint64_t hi = min(n, lo + q.chunk);
   const uint32_t cn = hi > lo ? (uint32_t)(hi - lo) : 0u;
   for (uint32_t j = threadIdx.x; j < cn; j += kFusedThreads) {
     const uint64_t k = q.keys[lo + j];
     ck[j] = k;
-    atomicAdd(&h[part_bucket(q, r, k) >> q.fine_log2], 1u);
+    atomicAdd(&h[part_bucket(q, r, k) >> q.low_bits], 1u);
   }
   __syncthreads();
   for (uint32_t p = threadIdx.x; p < P; p += kFusedThreads) {
@@ -992,7 +1000,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
       const uint32_t p = threadIdx.x * kPer + u;
       c[u] = p < P ? __ldcg(q.pcount + p) : 0u;
       t += c[u];
-      big |= c[u] > kPartCap;
+      big |= c[u] > q.cap1;
     }
     if (threadIdx.x == 0) over = 0;
     __syncthreads();
@@ -1015,7 +1023,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < cn; j += kFusedThreads) {
     const uint64_t k = ck[j];
-    const uint32_t pos = atomicAdd(&h[part_bucket(q, r, k) >> q.fine_log2], 1u);
+    const uint32_t pos = atomicAdd(&h[part_bucket(q, r, k) >> q.low_bits], 1u);
     q.tk[pos] = k;
     q.tv[pos] = (uint32_t)(lo + j);
   }
@@ -1034,6 +1042,83 @@ __global__ void part_fallback_kernel(Part q, uint64_t n, const uint64_t* ids, ui
   if (*(volatile int*)q.overflow) lsd_tail_launch(f, q.keys, n, ids, order);
 }
 
+// Level 2 of the two-level partition path (n > kPartMaxN): one CTA per level-1 partition
+// (~n/2048 keys, in global memory) histograms its keys over P2 sub-partitions (the next
+// p2_log2 bucket bits), regroups them into tk2 / tv2 and sorts every sub-partition (~1k keys)
+// in shared memory with sort_partition.  A sub-partition above kPartCap (massive ties) only
+// raises the overflow flag; part_fallback_kernel, launched after this grid, then runs the
+// stable LSD path, which rewrites the whole order.
+constexpr uint32_t kL2MaxP = 1024;
+
+__global__ void __launch_bounds__(kFusedThreads, 2) part_l2_kernel(
+    Part q, uint64_t n, const uint64_t* __restrict__ ids, uint64_t* __restrict__ order) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int skip;
+  // another CTA of THIS grid may raise the flag at any moment: read it once per CTA so the
+  // whole CTA leaves (or stays) together -- a per-thread read let part of a CTA return and
+  // the rest run its barriers short-handed
+  if (threadIdx.x == 0) skip = *(volatile int*)q.overflow;
+  __syncthreads();
+  if (skip) return;
+  __shared__ uint32_t sb[kL2MaxP + 1];  // sub-partition bases
+  __shared__ uint32_t cur[kL2MaxP];
+  __shared__ uint32_t sh[32];
+  __shared__ int big;
+  const uint32_t p = blockIdx.x;
+  const uint32_t s0 = q.pbase[p], m1 = q.pbase[p + 1] - s0;
+  if (m1 == 0) return;
+  const uint32_t P2 = 1u << q.p2_log2, mask2 = P2 - 1;
+  const KeyRange r = key_range(q.mm, q.total_bits);
+  for (uint32_t j = threadIdx.x; j < P2; j += kFusedThreads) cur[j] = 0;
+  if (threadIdx.x == 0) big = 0;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < m1; j += kFusedThreads)
+    atomicAdd(&cur[(part_bucket(q, r, q.tk[s0 + j]) >> q.fine_log2) & mask2], 1u);
+  __syncthreads();
+  {
+    constexpr int kPer = kL2MaxP / kFusedThreads;
+    uint32_t c[kPer], t = 0;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t j = threadIdx.x * kPer + u;
+      c[u] = j < P2 ? cur[j] : 0u;
+      t += c[u];
+      if (c[u] > kPartCap) big = 1;
+    }
+    uint32_t v = block_excl_scan_t<kFusedThreads>(t, sh);
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t j = threadIdx.x * kPer + u;
+      if (j < P2) {
+        sb[j] = v;
+        cur[j] = v;
+      }
+      v += c[u];
+    }
+    if (threadIdx.x == 0) sb[P2] = m1;
+  }
+  __syncthreads();
+  if (big) {
+    if (threadIdx.x == 0) atomicExch(q.overflow, 1);
+    return;
+  }
+  for (uint32_t j = threadIdx.x; j < m1; j += kFusedThreads) {
+    const uint64_t k = q.tk[s0 + j];
+    const uint32_t pos = atomicAdd(&cur[(part_bucket(q, r, k) >> q.fine_log2) & mask2], 1u);
+    q.tk2[s0 + pos] = k;
+    q.tv2[s0 + pos] = q.tv[s0 + j];
+  }
+  __syncthreads();  // this CTA's global writes are visible to it after the barrier
+  Part q2 = q;
+  q2.tk = q.tk2;
+  q2.tv = q.tv2;
+  for (uint32_t b = 0; b < P2; ++b) {
+    const uint32_t m = sb[b + 1] - sb[b];
+    if (m) sort_partition<kFusedThreads>(q2, s0 + sb[b], m, ids, order, smem_raw);
+    __syncthreads();
+  }
+}
+
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 int items_for(uint64_t) { return 16; }
@@ -1044,10 +1129,10 @@ struct Layout {
   // bucket / partition path: [bzero_begin, bzero_end) = count (bucket path) or pcount
   // (partition path), mm, overflow -- zeroed once per sort
   size_t count, mm, overflow, base, cursor, partial, seg, bzero_begin, bzero_end;
-  size_t pcount, pbase, cta_off;
+  size_t pcount, pbase, cta_off, tk2, tv2;
   uint32_t tiles, nb_log2, nseg;
-  bool part;
-  uint32_t p_log2, fine_log2;
+  bool part, part2;  // one-level (n <= kPartMaxN) / two-level partition path
+  uint32_t p_log2, p2_log2, fine_log2;
 };
 
 constexpr uint32_t kPartMaxCtas = 512;
@@ -1089,11 +1174,22 @@ Layout layout(uint64_t n, bool with_ids) {
   L.meta_end = off;
   L.plan = off; off += align_up(sizeof(Plan));
   L.flag = off; off += align_up(sizeof(int));
+  static const int two_level = getenv("TIE_NO_TWO_LEVEL") ? 0 : 1;  // A/B switch
   L.part = n <= kPartMaxN;
+  // two levels pay off from ~6M keys (B200: 8M 0.32 vs 0.37 ms bucket path; 4M 0.18 vs 0.15)
+  L.part2 = !L.part && two_level && n >= (6ull << 20) && n < (1ull << 32);
   L.p_log2 = std::min<uint32_t>(std::max<uint32_t>(ceil_log2((n + 1023) / 1024), 6u), 11u);
+  // two-level: 2048 level-1 partitions of P2 ~1k-key sub-partitions each
+  L.p2_log2 = L.part2 ? std::min<uint32_t>(std::max<uint32_t>(
+                            ceil_log2((n + (1024ull << L.p_log2) - 1) >> (L.p_log2 + 10)), 1u),
+                        10u)
+                      : 0u;
   L.fine_log2 = std::min<uint32_t>(
-      std::max<uint32_t>(ceil_log2((n + (1ull << L.p_log2) - 1) >> L.p_log2), 1u),
+      std::max<uint32_t>(ceil_log2((n + (1ull << (L.p_log2 + L.p2_log2)) - 1) >>
+                                   (L.p_log2 + L.p2_log2)),
+                         1u),
       kPartMaxFineLog2);
+  L.part = L.part || L.part2;  // both share the level-1 buffers below
   L.bzero_begin = off;
   if (L.part) {
     L.pcount = off; off += align_up(4 * ((1ull << L.p_log2) + 1));  // + the count ticket
@@ -1111,6 +1207,10 @@ Layout layout(uint64_t n, bool with_ids) {
   if (L.part) {
     L.pbase = off; off += align_up(4 * ((1ull << L.p_log2) + 1));
     L.cta_off = off; off += align_up(4ull * kPartMaxCtas << L.p_log2);
+  }
+  if (L.part2) {  // level-2 regrouped (key, index) -- separate from the LSD buffers
+    L.tk2 = off; off += align_up(8 * n);
+    L.tv2 = off; off += align_up(4 * n);
   }
   L.k2 = off; off += with_ids ? align_up(8 * n) : 0;  // transformed keys (id path)
   L.k3 = off; off += with_ids ? align_up(8 * n) : 0;  // keys gathered into id order
@@ -1225,11 +1325,41 @@ cudaError_t part_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_t*
   q.p_log2 = L.p_log2;
   q.P = 1u << L.p_log2;
   q.fine_log2 = L.fine_log2;
+  q.p2_log2 = L.p2_log2;
+  q.low_bits = L.p2_log2 + L.fine_log2;
+  q.total_bits = L.p_log2 + q.low_bits;
+  q.cap1 = L.part2 ? 0xffffffffu : kPartCap;
+
+  q.tk2 = L.part2 ? (uint64_t*)(base + L.tk2) : nullptr;
+  q.tv2 = L.part2 ? (uint32_t*)(base + L.tv2) : nullptr;
   q.ctas = (uint32_t)std::min<uint64_t>(
       std::min<uint64_t>((uint64_t)sms * 2, kPartMaxCtas), (n + 1023) / 1024);
   q.chunk = (n + q.ctas - 1) / q.ctas;
   // default: the whole path as one cooperative launch (count -> scatter -> sort)
   static const int fused = getenv("TIE_PART_UNFUSED") ? 0 : 1;  // A/B switch
+  if (L.part2) {  // level 1 (count, scatter), then level 2 per level-1 partition
+    static bool l2attr = false;
+    if (!l2attr) {
+      cudaFuncSetAttribute(part_l2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      l2attr = true;
+    }
+    {
+      ProfScope p(ctx, "rank.count", s);
+      part_count_kernel<<<q.ctas, kPartThreads, 0, s>>>(q, n);
+    }
+    {
+      ProfScope p(ctx, "rank.scatter", s);
+      part_scatter_kernel<<<q.ctas, kPartThreads, 0, s>>>(q, n);
+    }
+    {
+      ProfScope p(ctx, "rank.local", s);
+      part_l2_kernel<<<q.P, kFusedThreads, smem, s>>>(q, n, ids, order);
+      part_fallback_kernel<<<1, 1, 0, s>>>(q, n, ids, order, f);
+    }
+    capi::count_launch(4);
+    return cudaGetLastError();
+  }
   if (fused) {
     static bool fattr = false;
     static int bpsm = 0;

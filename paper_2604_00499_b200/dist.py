@@ -148,11 +148,11 @@ class ShardedScoreRank:
         if self.merge_on == "all" or self.rank == 0:
             lens = [b - a for a, b in (shard_bounds(n_global, self.world, g)
                                        for g in range(self.world))]
-            # k-way merge of the sorted runs where it is the faster final step: measured on one
-            # B200 for G x 1M runs (bench.py "rank0_merge"): G=2 68 vs 76 us re-sort, G=4 209
-            # vs 149, G=8 483 vs 373 -- the re-sort's partition / bucket sort wins beyond two
-            # runs, so the merge tree is used for G <= 2 (both give the identical order)
-            use_kway = self.kway == "always" or (self.kway == "auto" and self.world <= 2)
+            # k-way merge of the sorted runs, or a re-sort of the concatenation: both give the
+            # identical order; measured on one B200 for G x 1M runs (bench.py "rank0_merge"):
+            # G=2 73 vs 71 us re-sort, G=4 213 vs 179, G=8 490 vs 322 -- the range-partition
+            # sort is at least as fast, so "auto" re-sorts and the merge tree is opt-in
+            use_kway = self.kway == "always"
             if hasattr(self.ops, "merge_runs") and use_kway:
                 merged = self.ops.merge_runs(torch.stack(gk), torch.stack(gi), lens)
             else:  # stable re-sort of the concatenation (sentinels sort last)

@@ -72,7 +72,7 @@ def _worker(rank, world, port, n_global, case, out_q):
         lo, hi = shard_bounds(n_global, world, rank)
         beta = o.compute_beta(True, 0.1, 0.5, 128.0, n_global)  # GLOBAL queue length
         ops = OracleOps()
-        for merge_on, kway in (("root", "auto"), ("all", "auto"), ("root", "never")):
+        for merge_on, kway in (("root", "auto"), ("all", "auto"), ("root", "always")):
             res = ShardedScoreRank(ops, beta, merge_on=merge_on, kway=kway)(
                 torch.from_numpy(mu[lo:hi].copy()), torch.from_numpy(sg[lo:hi].copy()),
                 torch.from_numpy(mt[lo:hi].copy()), n_global)

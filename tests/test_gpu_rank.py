@@ -110,3 +110,20 @@ def test_bucket_extreme_range(abi, h, oracle):
     n = 100_000
     key = rng.standard_normal(n) * np.exp(rng.uniform(-600, 600, n))  # span of all exponents
     assert np.array_equal(abi.rank(h, key), oracle.rank(key))
+
+
+@pytest.mark.parametrize("distinct", [1, 3])
+def test_two_level_path_overflow_falls_back_exactly(abi, h, oracle, distinct):
+    """n > 2^21 takes the two-level partition path; massive ties overflow a sub-partition and
+    the device-side LSD fallback must still give the heap's order."""
+    rng = np.random.default_rng(distinct + 50)
+    n = 2_500_000
+    key = rng.integers(0, distinct, n).astype(np.float64) * 3.5 + 10.0
+    assert np.array_equal(abi.rank(h, key), oracle.rank(key))
+
+
+def test_two_level_path_moderate_ties(abi, h, oracle):
+    rng = np.random.default_rng(77)
+    n = 4_200_000
+    key = np.round(rng.lognormal(5.0, 0.7, n), 1)  # many small tie groups, no overflow
+    assert np.array_equal(abi.rank(h, key), oracle.rank(key))
