@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -419,6 +420,16 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
   }
 }
 
+// the fused step's completion record: the error word, then (after a system fence) the
+// step's sequence number, which the host polls instead of synchronising the stream
+__global__ void step_finish_kernel(const unsigned long long* err,
+                                   unsigned long long* status_err,
+                                   volatile uint32_t* status_seq, uint32_t seq) {
+  *status_err = *(const volatile unsigned long long*)err;
+  __threadfence_system();
+  *status_seq = seq;
+}
+
 __global__ void __launch_bounds__(1024) pop_topb_kernel(QDev q, uint32_t nblocks,
                                                         uint64_t n_slots, uint32_t pops,
                                                         uint64_t* out_id, uint32_t* out_slot,
@@ -435,7 +446,8 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
     const uint32_t* slots, uint64_t np, const double* E, double* C, double beta,
     const uint32_t* blocks, uint32_t nblk, uint32_t n_uncond, uint32_t nblocks, uint64_t n_slots,
     uint32_t pops, uint64_t* out_id, uint32_t* out_slot, uint32_t* out_n,
-    unsigned long long* err) {
+    unsigned long long* err, unsigned long long* status_err = nullptr,
+    volatile uint32_t* status_seq = nullptr, uint32_t seq = 0) {
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
@@ -507,9 +519,18 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
   __syncthreads();
   if (skip || pops == 0) {
     if (threadIdx.x == 0) *out_n = 0;
-    return;
+  } else {
+    pop_topb(q, nblocks, n_slots, pops, out_id, out_slot, out_n);
   }
-  pop_topb(q, nblocks, n_slots, pops, out_id, out_slot, out_n);
+  if (status_seq) {  // the step's last kernel: publish the completion record (step_finish)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      *status_err = *(const volatile unsigned long long*)err;
+      __threadfence_system();
+      *status_seq = seq;
+    }
+  }
 }
 
 }  // namespace
@@ -549,9 +570,14 @@ struct tie_queue {
   uint32_t* d_out_slot = nullptr;
   uint32_t* d_out_n = nullptr;
   uint64_t stage_cap = 0;
-  void* d_out = nullptr;          // the pop output block (ensure_out)
   uint64_t out_cap = 0;
-  void* h_out = nullptr;          // its pinned mirror
+  void* h_out = nullptr;          // the pop output block (ensure_out), mapped pinned
+  // completion record of a fused step, mapped pinned: written by the step's last kernel
+  struct Status {
+    unsigned long long err;
+    volatile uint32_t seq;
+  }* status = nullptr;
+  uint32_t seq = 0;
   char* h_pack = nullptr;         // pinned H2D pack of a fused step
   char* d_pack = nullptr;
   uint64_t pack_cap = 0;
@@ -582,23 +608,22 @@ int ensure_stage(tie_queue* Q, uint64_t m) {
   return TIE_OK;
 }
 
-// the pop output block, one per side so a plan's results come back in ONE small D2H:
-//   [out_n: u32 x cap | out_slot: u32 x cap | out_id: u64 x cap]   (cap >= pops, segments)
+// the pop output block: [out_n: u32 x cap | out_slot: u32 x cap | out_id: u64 x cap] in
+// mapped pinned host memory -- the pop kernels write their results straight into it, so no
+// D2H copy follows them (UVA: the host pointer is the device pointer)
 int ensure_out(tie_queue* Q, uint64_t m) {
   if (m <= Q->out_cap) return TIE_OK;
-  cudaFree(Q->d_out);
   cudaFreeHost(Q->h_out);
-  Q->d_out = Q->h_out = nullptr;
+  Q->h_out = nullptr;
   const uint64_t cap = std::max<uint64_t>(m, 256);
-  cudaError_t e = cudaSuccess;
-  if ((e = cudaMalloc(&Q->d_out, 16 * cap)) || (e = cudaMallocHost(&Q->h_out, 16 * cap)))
-    return cuda_error(e, "tie_queue: output allocation");
-  Q->d_out_n = (uint32_t*)Q->d_out;
-  Q->d_out_slot = Q->d_out_n + cap;
-  Q->d_out_id = (uint64_t*)(Q->d_out_slot + cap);
+  cudaError_t e = cudaHostAlloc(&Q->h_out, 16 * cap, cudaHostAllocMapped);
+  if (e != cudaSuccess) return cuda_error(e, "tie_queue: output allocation");
   Q->h_out_n = (uint32_t*)Q->h_out;
   Q->h_out_slot = Q->h_out_n + cap;
   Q->h_out_id = (uint64_t*)(Q->h_out_slot + cap);
+  Q->d_out_n = Q->h_out_n;
+  Q->d_out_slot = Q->h_out_slot;
+  Q->d_out_id = Q->h_out_id;
   Q->out_cap = cap;
   return TIE_OK;
 }
@@ -727,11 +752,7 @@ uint64_t launch_plan(tie_queue* Q, const std::vector<Seg>& plan, size_t first_se
 }
 
 // D2H of a plan's results (issued after launch_plan)
-void fetch_plan(tie_queue* Q, size_t nseg, uint64_t total, cudaStream_t s) {
-  (void)nseg;
-  const size_t bytes = (size_t)((char*)(Q->d_out_id + total) - (char*)Q->d_out);
-  cudaMemcpyAsync(Q->h_out, Q->d_out, bytes, cudaMemcpyDeviceToHost, s);
-}
+void fetch_plan(tie_queue*, size_t, uint64_t, cudaStream_t) {}  // results are written to host
 
 // host mirror of a finished plan, segment by segment (rebuild bookkeeping, then its pops);
 // returns false when the queue ran dry
@@ -796,10 +817,13 @@ int tie_queue_create(tie_ctx* ctx, int policy, int adaptive, double beta_fixed, 
       (e = cudaMalloc(&Q->q.beta, 8 * capacity)) ||
       (e = cudaMalloc(&Q->q.predicted, capacity)) || (e = cudaMalloc(&Q->q.bkey, 8 * nb)) ||
       (e = cudaMalloc(&Q->q.bid, 8 * nb)) || (e = cudaMalloc(&Q->q.bslot, 4 * nb)) ||
-      ensure_stage(Q, 1024) != TIE_OK || ensure_out(Q, 256) != TIE_OK) {
+      ensure_stage(Q, 1024) != TIE_OK || ensure_out(Q, 256) != TIE_OK ||
+      (e = cudaHostAlloc((void**)&Q->status, sizeof(*Q->status), cudaHostAllocMapped))) {
     tie_queue_destroy(Q);
     return cuda_error(e, "tie_queue_create");
   }
+  Q->status->err = ~0ull;
+  Q->status->seq = 0;
   cudaMemset(Q->q.key, 0xff, 8 * capacity);
   cudaMemset(Q->q.bkey, 0xff, 8 * nb);
   cudaMemset(Q->q.bid, 0xff, 8 * nb);
@@ -813,9 +837,10 @@ void tie_queue_destroy(tie_queue* Q) {
   for (void* p : {(void*)Q->q.key, (void*)Q->q.id, (void*)Q->q.E, (void*)Q->q.C,
                   (void*)Q->q.beta, (void*)Q->q.predicted, (void*)Q->q.bkey, (void*)Q->q.bid,
                   (void*)Q->q.bslot, (void*)Q->d_ids, (void*)Q->d_a, (void*)Q->d_b,
-                  (void*)Q->d_c, (void*)Q->d_slots, (void*)Q->d_blocks, Q->d_out})
+                  (void*)Q->d_c, (void*)Q->d_slots, (void*)Q->d_blocks})
     cudaFree(p);
   cudaFreeHost(Q->h_out);
+  cudaFreeHost(Q->status);
   cudaFreeHost(Q->h_pack);
   cudaFree(Q->d_pack);
   delete Q;
@@ -1094,12 +1119,16 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
   }
   std::memcpy(h + o_blk, blocks.data(), 4 * blocks.size());
   char* d = Q->d_pack;
-  cudaMemcpyAsync(d, h, o_h2d_end, cudaMemcpyHostToDevice, s);  // ONE H2D
+  const bool small = n_arr <= 16384 && np <= 16384 && blocks.size() <= 4096;
+  // small steps: the kernels read the pack straight from pinned host memory (no H2D copy);
+  // the device pack keeps the scratch (E, C, key)
+  const char* in = small ? h : d;
+  if (!small) cudaMemcpyAsync(d, h, o_h2d_end, cudaMemcpyHostToDevice, s);  // ONE H2D
   ctx->err_op = "tie_queue_step";
   const uint32_t nb = (uint32_t)((Q->n_slots + tie::dev::kBlockSlots - 1) / tie::dev::kBlockSlots);
   if (np) {
     const cudaError_t e = tie::dev::launch_score(
-        ctx, (const double*)(d + o_mu), (const double*)(d + o_sg), d + o_mt, true, np, Q->alpha,
+        ctx, (const double*)(in + o_mu), (const double*)(in + o_sg), in + o_mt, true, np, Q->alpha,
         0.0, (double*)(d + o_E), (double*)(d + o_C), nullptr, nullptr, nullptr, TIE_SCORE_RAW,
         s);
     if (e != cudaSuccess) {
@@ -1108,13 +1137,16 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
     }
   }
   uint32_t* seg0_n = Q->d_out_n + (seg0_fused ? 0 : plan.size());  // unused slot if not fused
-  const bool small = n_arr <= 16384 && np <= 16384 && blocks.size() <= 4096;
+  const uint32_t seq = ++Q->seq;
+  // the apply kernel is the step's last kernel when no further plan segments follow it
+  const bool apply_last = small && plan.size() <= (seg0_fused ? 1u : 0u);
   if (small) {  // everything after the scoring in one single-CTA kernel
     tie::dev::step_apply_kernel<<<1, 1024, 0, s>>>(
-        Q->q, first, n_arr, (const uint64_t*)(d + o_aid), (const double*)(d + o_akey),
-        (const uint32_t*)(d + o_slot), np, (const double*)(d + o_E), (double*)(d + o_C), beta,
-        (const uint32_t*)(d + o_blk), (uint32_t)blocks.size(), n_uncond, nb, Q->n_slots,
-        fused_pops, Q->d_out_id, Q->d_out_slot, seg0_n, ctx->d_err);
+        Q->q, first, n_arr, (const uint64_t*)(in + o_aid), (const double*)(in + o_akey),
+        (const uint32_t*)(in + o_slot), np, (const double*)(d + o_E), (double*)(d + o_C), beta,
+        (const uint32_t*)(in + o_blk), (uint32_t)blocks.size(), n_uncond, nb, Q->n_slots,
+        fused_pops, Q->d_out_id, Q->d_out_slot, seg0_n, ctx->d_err,
+        apply_last ? &Q->status->err : nullptr, apply_last ? &Q->status->seq : nullptr, seq);
     tie::capi::count_launch(1);
   } else {
     if (n_arr)
@@ -1142,11 +1174,38 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
                             (fused_pops ? 1 : 0));
   }
   launch_plan(Q, plan, seg0_fused ? 1 : 0, fused_pops, s, ctx->d_err);
-  fetch_plan(Q, plan.size(), planned, s);
-  // the error word (tie_sync decodes + resets it); arrivals stay applied like the reference's
-  if (int rc = tie_sync(ctx, s)) {
+  // completion: the last kernel publishes the error word and the step's sequence number in
+  // mapped host memory; the host polls it (a stream synchronisation costs more than the
+  // whole small step) and falls back to synchronising after 20 ms
+  if (!apply_last) {
+    tie::dev::step_finish_kernel<<<1, 1, 0, s>>>(ctx->d_err, &Q->status->err, &Q->status->seq,
+                                                 seq);
+    tie::capi::count_launch();
+  }
+  cudaError_t le = cudaGetLastError();
+  if (le != cudaSuccess) {
     if (use_pred) pred_mirror(false);
-    return rc;
+    return cuda_error(le, "tie_queue_step");
+  }
+  {
+    const auto t0 = std::chrono::steady_clock::now();
+    while (Q->status->seq != seq) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(20)) {
+        const cudaError_t se = cudaStreamSynchronize(s);
+        if (se != cudaSuccess) {
+          if (use_pred) pred_mirror(false);
+          return cuda_error(se, "tie_queue_step");
+        }
+        break;
+      }
+    }
+  }
+  // the error word (tie_sync decodes + resets it); arrivals stay applied like the reference's
+  if (Q->status->err != ~0ull) {
+    if (int rc = tie_sync(ctx, s)) {
+      if (use_pred) pred_mirror(false);
+      return rc;
+    }
   }
   std::vector<uint64_t> got;
   const bool dry = !replay_plan(Q, plan, got);
