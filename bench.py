@@ -10,8 +10,9 @@ alpha=0.9, adaptive beta from the global queue length -> 0.5) -- one fused score
 radix-sort dispatch order, inputs resident in HBM.  The 20 MB inputs fit in L2, so L2 is
 flushed (256 MB write) between timed steps; each step is bracketed by CUDA events on the
 launching stream and the K step times are summed.  N>1 (weak scaling): 1M requests per rank,
-global queue N x 1M, each rank scores + sorts its shard, then the sorted (score, id) runs are
-all-gathered over NCCL and merged on rank 0 into the global dispatch order.
+global queue N x 1M, each rank scores + sorts its shard, then G-1 (score, id) splitters are
+chosen from an all-gathered regular sample and one NCCL all-to-all sends every rank its score
+range, which it orders locally (dist.py merge_on="range").
 
 e2e: the same metric through the public C-ABI host-buffer call tie_score_rank_host (pinned
 host inputs -> H2D -> score -> rank -> D2H of the u64 dispatch order), wall-clocked per call.
@@ -225,14 +226,15 @@ def main():
     if world > 1:
         from paper_2604_00499_b200.dist import DeviceOps, ShardedScoreRank
 
-        sharded = ShardedScoreRank(DeviceOps(mc, ALPHA), beta)
+        # splitter all-to-all: each rank ends with its score range of the global order
+        sharded = ShardedScoreRank(DeviceOps(mc, ALPHA), beta, merge_on="range")
 
     def step():
         if world == 1:
             tie.score_rank_device(ctx, mu.data_ptr(), sg.data_ptr(), mt.data_ptr(), n_local,
                                   ALPHA, beta, 0, 0, S.data_ptr(), order.data_ptr(), 0, sh)
         else:
-            # local K1+K2 -> NCCL all-gather of sorted (score, id) runs -> merge on rank 0
+            # local K1+K2 -> splitters -> NCCL all-to-all of (score, id) pieces -> local order
             res = sharded(mu, sg, mt, n_global)
             S.copy_(res.scores)
             order.copy_(res.local_order)
@@ -404,7 +406,8 @@ def main():
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "config2: 1M-request queue score+rank per GPU"
-                       if world == 1 else f"{world} x 1M-request shards, NCCL all-gather merge",
+                       if world == 1
+                       else f"{world} x 1M-request shards, splitter all-to-all (range-owned order)",
                        "n_requests_per_gpu": n_local, "n_requests_global": n_global,
                        "nu": 3.5, "alpha": ALPHA, "beta": beta, "mc_samples": 10000,
                        "score_path": "moment tables (TIE_SCORE_MOMENT)",

@@ -15,6 +15,14 @@ exactly across shards:
    concatenation: runs are concatenated in rank order over contiguous ascending id ranges,
    so among equal scores the concatenation order IS ascending id order.
 
+``merge_on="range"`` replaces steps 4-5 by a splitter exchange (the preferred
+alternative for scaling): every rank contributes a regular sample of its sorted run, all ranks
+pick the same G-1 (score, id) splitters from the gathered sample, cut their run at the
+splitters (lexicographic binary search), and one variable-size all-to-all sends cut j to rank
+j.  Rank j then orders the G pieces it received and owns global positions
+[offset_j, offset_j + len_j): the global order is the concatenation over ranks, and no rank
+receives more than its range (no redundant all-gather, no single-rank merge).
+
 Device work is behind ``DeviceOps`` (the C-ABI through ``_core``); tests substitute
 reference-semantics NumPy ops to exercise the sharding / padding / gather / merge logic on
 CPU with the gloo backend.
@@ -102,6 +110,8 @@ class ShardResult:
     scores: object            # this rank's scores, queue order (device tensor)
     local_order: object       # this rank's sorted local indices
     global_order: object      # rank 0 (or every rank with merge_on="all"): global ids; else None
+                              # merge_on="range": this rank's slice of the global order
+    offset: int = 0           # merge_on="range": global position of global_order[0]
 
 
 class ShardedScoreRank:
@@ -117,12 +127,14 @@ class ShardedScoreRank:
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        if merge_on not in ("root", "all"):
-            raise ValueError("merge_on must be 'root' or 'all'")
+        if merge_on not in ("root", "all", "range"):
+            raise ValueError("merge_on must be 'root', 'all' or 'range'")
         self.merge_on = merge_on
         if kway not in ("auto", "always", "never"):
             raise ValueError("kway must be 'auto', 'always' or 'never'")
         self.kway = kway
+
+    oversample = 32  # regular-sample points per rank and destination range
 
     def __call__(self, mu, sigma, max_tokens, n_global: int) -> ShardResult:
         import torch
@@ -134,6 +146,8 @@ class ShardedScoreRank:
         S, order = self.ops.score_sort(mu, sigma, max_tokens, self.beta)
         if self.world == 1:
             return ShardResult(S, order, order)
+        if self.merge_on == "range":
+            return self._range_exchange(S, order, lo, hi)
         width = shard_bounds(n_global, self.world, 0)[1]  # the longest shard
         run_k = torch.full((width,), SENTINEL, dtype=torch.float64, device=S.device)
         run_i = torch.full((width,), -1, dtype=torch.int64, device=S.device)
@@ -161,3 +175,85 @@ class ShardedScoreRank:
                 perm = self.ops.stable_sort(keys)
                 merged = ids[perm][:n_global]
         return ShardResult(S, order, merged)
+
+    def _splitters(self, keys, ids):
+        """G-1 (score, id) splitters, identical on every rank: a regular sample of each sorted
+        run is all-gathered (padded with sentinels) and cut at equal sample counts."""
+        import torch
+
+        G, m = self.world, keys.numel()
+        s = self.oversample * G
+        take = min(m, s)
+        pos = (torch.arange(take, dtype=torch.float64) + 0.5) * (m / max(take, 1))
+        pos = pos.to(torch.int64).clamp_(max=max(m - 1, 0)).to(keys.device)
+        sk = torch.full((s,), SENTINEL, dtype=torch.float64, device=keys.device)
+        si = torch.full((s,), -1, dtype=torch.int64, device=keys.device)
+        sk[:take] = keys[pos]
+        si[:take] = ids[pos]
+        gk = [torch.empty_like(sk) for _ in range(G)]
+        gi = [torch.empty_like(si) for _ in range(G)]
+        self.dist.all_gather(gk, sk, group=self.group)
+        self.dist.all_gather(gi, si, group=self.group)
+        ak = torch.cat(gk).cpu().numpy()
+        ai = torch.cat(gi).cpu().numpy()
+        valid = ai >= 0
+        ak, ai = ak[valid], ai[valid]
+        o = np.lexsort((ai, ak))
+        ak, ai = ak[o], ai[o]
+        t = len(ak)
+        cut = [(j * t) // G for j in range(1, G)]
+        return ([float(ak[c]) if c < t else SENTINEL for c in cut],
+                [int(ai[c]) if c < t else 2 ** 62 for c in cut])
+
+    def _range_exchange(self, S, order, lo, hi):
+        import torch
+
+        G = self.world
+        keys = S[order].contiguous()
+        ids = (order + lo).contiguous()
+        spk, spi = self._splitters(keys, ids)
+        # lexicographic cut: #{(k, i) < (spk, spi)} in the run sorted by (k, i)
+        tk = torch.tensor(spk, dtype=torch.float64, device=keys.device)
+        left = torch.searchsorted(keys, tk, side="left").cpu().tolist()
+        right = torch.searchsorted(keys, tk, side="right").cpu().tolist()
+        cuts = [0]
+        for j in range(G - 1):
+            c = left[j]
+            if right[j] > left[j]:  # equal scores: ids ascending inside the tie run
+                tie = ids[left[j]:right[j]]
+                c += int(torch.searchsorted(tie, torch.tensor([spi[j]], dtype=torch.int64,
+                                                              device=ids.device)).item())
+            cuts.append(max(c, cuts[-1]))
+        cuts.append(keys.numel())
+        send = [cuts[j + 1] - cuts[j] for j in range(G)]
+        dev = keys.device  # NCCL exchanges device tensors only (counts included)
+        recv_t = torch.empty(G, dtype=torch.int64, device=dev)
+        self.dist.all_to_all_single(recv_t, torch.tensor(send, dtype=torch.int64, device=dev),
+                                    group=self.group)
+        recv = recv_t.tolist()
+        total = int(sum(recv))
+        rk = torch.empty(total, dtype=torch.float64, device=keys.device)
+        ri = torch.empty(total, dtype=torch.int64, device=keys.device)
+        self.dist.all_to_all_single(rk, keys, recv, send, group=self.group)
+        self.dist.all_to_all_single(ri, ids, recv, send, group=self.group)
+        # pieces arrive in source-rank order = ascending id ranges, each sorted by (k, i):
+        # a stable sort by k alone (or the k-way merge) yields the (k, i) order
+        if hasattr(self.ops, "merge_runs") and self.kway == "always" and total:
+            width = max(recv)
+            pk = torch.full((G, width), SENTINEL, dtype=torch.float64, device=keys.device)
+            pi = torch.full((G, width), -1, dtype=torch.int64, device=keys.device)
+            o = 0
+            for g in range(G):
+                pk[g, :recv[g]] = rk[o:o + recv[g]]
+                pi[g, :recv[g]] = ri[o:o + recv[g]]
+                o += recv[g]
+            mine = self.ops.merge_runs(pk, pi, recv)
+        elif total:
+            mine = ri[self.ops.stable_sort(rk)]
+        else:
+            mine = ri
+        sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(G)]
+        self.dist.all_gather(sizes, torch.tensor([total], dtype=torch.int64, device=dev),
+                             group=self.group)
+        offset = int(sum(int(x.item()) for x in sizes[:self.rank]))
+        return ShardResult(S, order, mine, offset)

@@ -72,11 +72,15 @@ def _worker(rank, world, port, n_global, case, out_q):
         lo, hi = shard_bounds(n_global, world, rank)
         beta = o.compute_beta(True, 0.1, 0.5, 128.0, n_global)  # GLOBAL queue length
         ops = OracleOps()
-        for merge_on, kway in (("root", "auto"), ("all", "auto"), ("root", "always")):
+        for merge_on, kway in (("root", "auto"), ("all", "auto"), ("root", "always"),
+                               ("range", "auto"), ("range", "always")):
             res = ShardedScoreRank(ops, beta, merge_on=merge_on, kway=kway)(
                 torch.from_numpy(mu[lo:hi].copy()), torch.from_numpy(sg[lo:hi].copy()),
                 torch.from_numpy(mt[lo:hi].copy()), n_global)
-            if res.global_order is not None:
+            if merge_on == "range":  # this rank's slice of the global order
+                out_q.put((rank, merge_on + "/" + kway,
+                           (res.offset, res.global_order.numpy().tolist())))
+            elif res.global_order is not None:
                 out_q.put((rank, merge_on + "/" + kway, res.global_order.numpy().tolist()))
     finally:
         dist.destroy_process_group()
@@ -93,8 +97,9 @@ def test_two_rank_order_matches_single_queue(n_global, case, oracle):
     for p in procs:
         p.join(timeout=180)
         assert p.exitcode == 0
-    # k-way root merge and re-sort root merge on rank 0, all-merge on both ranks
-    got = [q.get(timeout=5) for _ in range(4)]
+    # k-way root merge and re-sort root merge on rank 0, all-merge on both ranks, and the
+    # splitter exchange's two slices per variant
+    got = [q.get(timeout=5) for _ in range(8)]
     # the reference: one queue, one heap
     if case == "workload":
         mu, sg, mt = oracle.gen_workload(n_global, seed=1)
@@ -104,8 +109,19 @@ def test_two_rank_order_matches_single_queue(n_global, case, oracle):
     _, _, S = oracle.score(oracle.mc_samples(), mu, sg, np.asarray(mt, float), alpha=0.9,
                            beta=beta)
     ref = oracle.rank(S).tolist()
+    slices = {}
     for rank, merge_on, order in got:
+        if merge_on.startswith("range"):
+            slices.setdefault(merge_on, []).append(order)
+            continue
         assert order == ref, (rank, merge_on)
+    assert len(slices) == 2
+    for variant, parts in slices.items():
+        parts.sort()
+        assert parts[0][0] == 0 and parts[1][0] == len(parts[0][1]), variant
+        assert parts[0][1] + parts[1][1] == ref, variant
+        if n_global > 100:  # the regular sample balances the ranges
+            assert min(len(p[1]) for p in parts) > n_global // 4, variant
     if case == "ties":
         assert ref == list(range(n_global))
 
