@@ -194,6 +194,19 @@ int tie_queue_step(tie_queue* q, const uint64_t* arr_ids, const double* arr_time
                    uint64_t n_pred, uint64_t max_pops, uint64_t* out_ids, uint64_t* n_out);
 /* Scheduler::rebuild_if_drifted() (sched.cpp:152-167) */
 int tie_queue_rebuild_if_drifted(tie_queue* q, int* rebuilt);
+/* Shard-level primitives for a scheduler sharded by request (coordinated by
+ * paper_2604_00499_b200/dist.py ShardedScheduler so the shards together behave as ONE
+ * reference Scheduler):
+ *  - set_peer_waiting: compute_beta's queue length becomes waiting() + peers (sched.cpp:9-17
+ *    is called with the GLOBAL queue size, sched.cpp:136, 154);
+ *  - beta_range: betas_in_use_ (sched.hpp:88) extremes and size (n_in_use 0: empty);
+ *  - rebuild_at: rebuild_if_drifted's re-key (sched.cpp:156-166) at a beta decided globally;
+ *  - peek: the next min(k, waiting) pops under the current keys (order-preserving u64 keys
+ *    + ids, comparable across shards), leaving the queue unchanged and doing no rebuild. */
+int tie_queue_set_peer_waiting(tie_queue* q, uint64_t peers);
+int tie_queue_beta_range(const tie_queue* q, double* lo, double* hi, uint64_t* n_in_use);
+int tie_queue_rebuild_at(tie_queue* q, double beta);
+int tie_queue_peek(tie_queue* q, uint64_t k, uint64_t* keys, uint64_t* ids, uint64_t* n_out);
 
 /* ---- input formats ------------------------------------------------------
  * Request traces: JSONL, one object per request -- load_trace / save_trace

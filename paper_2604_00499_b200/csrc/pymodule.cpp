@@ -535,6 +535,29 @@ PYBIND11_MODULE(_core, m) {
              throw_code(tie_queue_rebuild_if_drifted(g.q, &r));
              return r != 0;
            })
+      .def("set_peer_waiting",
+           [](GpuQueue& g, uint64_t peers) { throw_code(tie_queue_set_peer_waiting(g.q, peers)); },
+           py::arg("peers"), "beta's queue length = waiting() + peers (sharded scheduler)")
+      .def("beta_range",
+           [](const GpuQueue& g) {
+             double lo = 0, hi = 0;
+             uint64_t n = 0;
+             throw_code(tie_queue_beta_range(g.q, &lo, &hi, &n));
+             return py::make_tuple(lo, hi, n);
+           },
+           "(min beta, max beta, count) of betas_in_use_; count 0 = empty")
+      .def("rebuild_at",
+           [](GpuQueue& g, double beta) { throw_code(tie_queue_rebuild_at(g.q, beta)); },
+           py::arg("beta"), "re-key every predicted entry at `beta` (a global rebuild)")
+      .def("peek",
+           [](GpuQueue& g, uint64_t k) {
+             std::vector<uint64_t> keys(k), ids(k);
+             uint64_t n = 0;
+             throw_code(tie_queue_peek(g.q, k, keys.data(), ids.data(), &n));
+             return py::make_tuple(carray<uint64_t>((py::ssize_t)n, keys.data()),
+                                   carray<uint64_t>((py::ssize_t)n, ids.data()));
+           },
+           py::arg("k"), "(keys, ids) of the next k pops under the current keys, not popped")
       .def("waiting", [](const GpuQueue& g) { return tie_queue_size(g.q); })
       .def("current_beta", [](const GpuQueue& g) { return tie_queue_current_beta(g.q); });
 

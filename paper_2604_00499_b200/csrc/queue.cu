@@ -311,7 +311,7 @@ constexpr int kTopB = 32;            // pops per launch
 constexpr int kCandCap = 2048;       // candidates held in shared memory
 __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64_t n_slots,
                                          uint32_t pops, uint64_t* out_id, uint32_t* out_slot,
-                                         uint32_t* out_n) {
+                                         uint32_t* out_n, uint64_t* out_key = nullptr) {
   __shared__ uint64_t sk[32], si[32];
   __shared__ uint32_t ss[32];
   __shared__ uint32_t chosen[kTopB];
@@ -411,6 +411,7 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
       if (threadIdx.x == 0) {
         out_id[done] = i;
         out_slot[done] = s;
+        if (out_key) out_key[done] = k;
         q.key[s] = kDead;
       }
       __syncthreads();
@@ -427,6 +428,7 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
     if (rank < npop) {
       out_id[rank] = ci[c];
       out_slot[rank] = cs[c];
+      if (out_key) out_key[rank] = ck[c];
       q.key[cs[c]] = kDead;
     }
   }
@@ -460,8 +462,30 @@ __global__ void step_finish_kernel(const unsigned long long* err,
 __global__ void __launch_bounds__(1024) pop_topb_kernel(QDev q, uint32_t nblocks,
                                                         uint64_t n_slots, uint32_t pops,
                                                         uint64_t* out_id, uint32_t* out_slot,
-                                                        uint32_t* out_n) {
-  pop_topb(q, nblocks, n_slots, pops, out_id, out_slot, out_n);
+                                                        uint32_t* out_n,
+                                                        uint64_t* out_key = nullptr) {
+  pop_topb(q, nblocks, n_slots, pops, out_id, out_slot, out_n, out_key);
+}
+
+// undo a peek's pops (one CTA): restore the popped slots' keys, then refresh their blocks
+// (one warp per popped slot; a block popped twice is refreshed twice, identically)
+__global__ void __launch_bounds__(1024) unpop_kernel(QDev q, const uint32_t* slots,
+                                                     const uint64_t* keys, uint32_t n,
+                                                     uint64_t n_slots) {
+  for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) q.key[slots[t]] = keys[t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t t = warp; t < n; t += blockDim.x >> 5) {
+    const uint32_t blk = slots[t] / kBlockSlots;
+    uint64_t k, i;
+    uint32_t s;
+    warp_block_min(q, blk, n_slots, lane, k, i, s);
+    if (lane == 0) {
+      q.bkey[blk] = k;
+      q.bid[blk] = i;
+      q.bslot[blk] = s;
+    }
+  }
 }
 
 // A small scheduler iteration in ONE kernel (one CTA): write the arrivals' slots; check the
@@ -587,6 +611,9 @@ struct tie_queue {
   char* h_pack = nullptr;         // pinned H2D pack of a fused step
   char* d_pack = nullptr;
   uint64_t pack_cap = 0;
+  uint64_t peers = 0;             // waiting requests held by other shards (beta's queue length)
+  uint64_t* h_peek_key = nullptr; // mapped pinned: keys of a peek's (undone) pops
+  uint64_t peek_cap = 0;
   uint64_t* h_out_id = nullptr;   // pinned
   uint32_t* h_out_slot = nullptr;
   uint32_t* h_out_n = nullptr;
@@ -708,7 +735,7 @@ std::vector<Seg> plan_pops(const tie_queue* Q, uint64_t left) {
     bool rebuild = false;
     double now = 0.0;
     if (tie_policy && !empty) {
-      now = beta_at(Q, Q->size - j);
+      now = beta_at(Q, Q->size + Q->peers - j);
       const double d = std::max(std::fabs(now - lo), std::fabs(now - hi));
       if (d > Q->threshold) {
         if (!(exact && Q->n_predicted > j)) break;  // uncertain: stop here
@@ -846,6 +873,7 @@ void tie_queue_destroy(tie_queue* Q) {
                   (void*)Q->d_c, (void*)Q->d_slots, (void*)Q->d_blocks})
     cudaFree(p);
   cudaFreeHost(Q->h_out);
+  cudaFreeHost(Q->h_peek_key);
   cudaFreeHost(Q->status);
   cudaFreeHost(Q->h_pack);
   cudaFree(Q->d_pack);
@@ -854,7 +882,7 @@ void tie_queue_destroy(tie_queue* Q) {
 
 uint64_t tie_queue_size(const tie_queue* Q) { return Q ? Q->size : 0; }
 
-double tie_queue_current_beta(const tie_queue* Q) { return Q ? beta_at(Q, Q->size) : 0.0; }
+double tie_queue_current_beta(const tie_queue* Q) { return Q ? beta_at(Q, Q->size + Q->peers) : 0.0; }
 
 // Scheduler::on_arrival x m (sched.cpp:125-132): key = FCFS ? arrival_s : max_tokens.
 int tie_queue_arrive(tie_queue* Q, const uint64_t* ids, const double* arrival_s,
@@ -909,7 +937,7 @@ int tie_queue_predict(tie_queue* Q, const uint64_t* ids, const double* E, const 
     slots[t] = it->second;
   }
   if (Q->policy == 0) return TIE_OK;  // FCFS: arrival order is the schedule
-  const double beta = Q->policy == 1 ? 0.0 : beta_at(Q, Q->size);
+  const double beta = Q->policy == 1 ? 0.0 : beta_at(Q, Q->size + Q->peers);
   for (uint64_t t = 0; t < m; ++t) {
     if (Q->predicted[slots[t]])
       return set_error(TIE_EINVALID, "Scheduler::on_prediction: id " + std::to_string(ids[t]) +
@@ -974,7 +1002,7 @@ int tie_queue_next(tie_queue* Q, uint64_t max_pops, uint64_t* out_ids, uint64_t*
   while (left > 0) {
     std::vector<Seg> plan = plan_pops(Q, left);
     if (plan.empty()) {  // the very first decision is uncertain only if... never: j = 0 exact
-      const double now = beta_at(Q, Q->size);
+      const double now = beta_at(Q, Q->size + Q->peers);
       plan.push_back({true, now, 1});
     }
     const size_t before = got.size();
@@ -1047,7 +1075,7 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
                                          std::to_string(pred_ids[t]) + " not waiting");
     slots[t] = it->second;
   }
-  const double beta = Q->policy == 1 ? 0.0 : beta_at(Q, Q->size);
+  const double beta = Q->policy == 1 ? 0.0 : beta_at(Q, Q->size + Q->peers);
   if (use_pred) {
     std::vector<uint32_t> srt(slots);
     std::sort(srt.begin(), srt.end());
@@ -1226,11 +1254,93 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
   return TIE_OK;
 }
 
+// ---- shard-level primitives (the scheduler sharded by request) ------------
+// A sharded scheduler keeps each request's (E, CVaR) on its owner GPU and reproduces ONE
+// reference Scheduler over the union of the shards; these expose what the coordinating layer
+// (paper_2604_00499_b200/dist.py ShardedScheduler) needs to make the global decisions.
+
+// beta's queue length is this shard's waiting count plus `peers` (compute_beta over the
+// GLOBAL queue, sched.cpp:9-17, 136, 154)
+int tie_queue_set_peer_waiting(tie_queue* Q, uint64_t peers) {
+  if (!Q) return set_error(TIE_EINVALID, "tie_queue: null queue");
+  Q->peers = peers;
+  return TIE_OK;
+}
+
+// betas_in_use_ of this shard (sched.hpp:88): its extremes and size (0: empty)
+int tie_queue_beta_range(const tie_queue* Q, double* lo, double* hi, uint64_t* n_in_use) {
+  if (!Q || !lo || !hi || !n_in_use) return set_error(TIE_EINVALID, "tie_queue: null argument");
+  *n_in_use = 0;
+  *lo = *hi = 0.0;
+  if (Q->betas.empty()) return TIE_OK;
+  *lo = Q->betas.begin()->first;
+  *hi = Q->betas.rbegin()->first;
+  for (const auto& kv : Q->betas) *n_in_use += kv.second;
+  return TIE_OK;
+}
+
+// the rebuild of rebuild_if_drifted (sched.cpp:156-166) at a beta decided elsewhere: every
+// predicted entry of this shard is re-keyed with `beta` (no-op when it has none)
+int tie_queue_rebuild_at(tie_queue* Q, double beta) {
+  if (!Q) return set_error(TIE_EINVALID, "tie_queue: null queue");
+  if (Q->policy != 2 || Q->betas.empty()) return TIE_OK;
+  if (int rc = rebuild_all(Q, beta, Q->ctx->stream)) return rc;
+  const cudaError_t e = cudaStreamSynchronize(Q->ctx->stream);
+  return e == cudaSuccess ? TIE_OK : cuda_error(e, "tie_queue_rebuild_at");
+}
+
+// the next min(k, waiting) entries in pop order under the CURRENT keys -- (key, id) with the
+// key's order-preserving u64 bits, comparable across shards -- without popping them and
+// without any drift rebuild: pops on the device, then the popped keys restored
+int tie_queue_peek(tie_queue* Q, uint64_t k, uint64_t* keys, uint64_t* ids, uint64_t* n_out) {
+  if (!Q || !n_out || (k && (!keys || !ids)))
+    return set_error(TIE_EINVALID, "tie_queue: null argument");
+  *n_out = 0;
+  k = std::min<uint64_t>(k, Q->size);
+  if (!k) return TIE_OK;
+  const uint64_t nseg = (k + tie::dev::kTopB - 1) / tie::dev::kTopB;
+  if (int rc = ensure_out(Q, std::max<uint64_t>(k, nseg + 1))) return rc;
+  if (k > Q->peek_cap) {
+    cudaFreeHost(Q->h_peek_key);
+    Q->h_peek_key = nullptr;
+    Q->peek_cap = 0;
+    const cudaError_t e = cudaHostAlloc((void**)&Q->h_peek_key, 8 * std::max<uint64_t>(k, 256),
+                                        cudaHostAllocMapped);
+    if (e != cudaSuccess) return cuda_error(e, "tie_queue_peek: allocation");
+    Q->peek_cap = std::max<uint64_t>(k, 256);
+  }
+  cudaStream_t s = Q->ctx->stream;
+  const uint32_t nb = (uint32_t)((Q->n_slots + tie::dev::kBlockSlots - 1) / tie::dev::kBlockSlots);
+  uint64_t off = 0;
+  for (uint64_t g = 0; g < nseg; ++g) {
+    const uint32_t cnt = (uint32_t)std::min<uint64_t>(tie::dev::kTopB, k - off);
+    tie::dev::pop_topb_kernel<<<1, 1024, 0, s>>>(Q->q, nb, Q->n_slots, cnt, Q->d_out_id + off,
+                                                 Q->d_out_slot + off, Q->d_out_n + g,
+                                                 Q->h_peek_key + off);
+    off += cnt;
+  }
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_error(e, "tie_queue_peek");
+  uint64_t got = 0;
+  for (uint64_t g = 0; g < nseg; ++g) got += Q->h_out_n[g];  // == k: k <= waiting
+  tie::dev::unpop_kernel<<<1, 1024, 0, s>>>(Q->q, Q->d_out_slot, Q->h_peek_key, (uint32_t)got,
+                                            Q->n_slots);
+  tie::capi::count_launch(nseg + 1);
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_error(e, "tie_queue_peek");
+  for (uint64_t j = 0; j < got; ++j) {
+    keys[j] = Q->h_peek_key[j];
+    ids[j] = Q->h_out_id[j];
+  }
+  *n_out = got;
+  return TIE_OK;
+}
+
 int tie_queue_rebuild_if_drifted(tie_queue* Q, int* rebuilt) {
   if (!Q) return set_error(TIE_EINVALID, "tie_queue: null queue");
   if (rebuilt) *rebuilt = 0;
   if (Q->policy != 2 || Q->betas.empty()) return TIE_OK;
-  const double now = beta_at(Q, Q->size);
+  const double now = beta_at(Q, Q->size + Q->peers);
   if (!(drift(Q, now) > Q->threshold)) return TIE_OK;
   if (int rc = rebuild_all(Q, now, Q->ctx->stream)) return rc;
   if (rebuilt) *rebuilt = 1;

@@ -257,3 +257,158 @@ class ShardedScoreRank:
                              group=self.group)
         offset = int(sum(int(x.item()) for x in sizes[:self.rank]))
         return ShardResult(S, order, mine, offset)
+
+
+U64_MAX = np.iinfo(np.uint64).max
+
+
+class ShardedScheduler:
+    """ONE reference Scheduler (sched.cpp:125-175) over requests sharded across ranks
+    ("queue-resident scheduler"): each rank's ``local`` queue (a
+    ``GpuScheduler``) holds the (E, CVaR, key) of the requests it owns, and every method is a
+    collective that all ranks call with their own slice of the events.  The shards together
+    pop exactly the reference's sequence:
+
+    * beta at a prediction or pop is compute_beta of the GLOBAL waiting count (sched.cpp:136,
+      154): each rank tells its queue how many requests the others hold
+      (``set_peer_waiting``) after one all-gather of the shard sizes;
+    * rebuild_if_drifted (sched.cpp:152-167) is a global decision: drift is taken over the
+      union of the shards' betas_in_use_, whose extremes are the extremes of the per-shard
+      extremes (``beta_range``), and a rebuild re-keys every shard at the same beta
+      (``rebuild_at``);
+    * pops: the multiset only loses entries as pops proceed, so its range only shrinks; the
+      pops for which no rebuild is possible under the current range are selected in ONE
+      exchange -- every rank peeks its next L (key, id) entries, one all-gather of G x L
+      candidates, the L smallest in (key, id) order are the next L global pops, and shard g
+      pops its share with ``next_requests`` (its own top entries, in order).  A rebuild that
+      must fire is applied on every shard and the exchange repeats.
+
+    Every rank returns the same global pop sequence.  ``beta_fn(queue_len)`` is compute_beta
+    for the queue's ScoreConfig; ``policy`` 0 FCFS / 1 SEPT / 2 TIE."""
+
+    def __init__(self, local, policy: int, beta_fn, rebuild_threshold: float, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.local = local
+        self.policy = int(policy)
+        self.beta_fn = beta_fn
+        self.threshold = float(rebuild_threshold)
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.exchanges = 0  # all-gathers issued (diagnostics)
+
+    # ---- collectives over small host arrays (device tensors under NCCL)
+    def _gather(self, arr):
+        import torch
+
+        a = np.ascontiguousarray(arr)
+        wire = a.view(np.int64) if a.dtype == np.uint64 else a
+        dev = "cpu"
+        if self.dist.get_backend(self.group) == "nccl":
+            dev = torch.device("cuda", torch.cuda.current_device())
+        t = torch.from_numpy(wire.copy()).to(dev)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        self.exchanges += 1
+        res = np.stack([o.cpu().numpy() for o in out])
+        return res.view(np.uint64) if a.dtype == np.uint64 else res
+
+    def _collective(self, fn):
+        """run the local part, then agree on success: a failure on any rank raises on all"""
+        err = None
+        try:
+            out = fn()
+        except Exception as e:  # noqa: BLE001 -- re-raised below
+            err, out = e, None
+        flags = self._gather(np.array([0 if err is None else 1], np.int64))
+        if err is not None:
+            raise err
+        if flags.any():
+            bad = [int(r) for r in np.nonzero(flags[:, 0])[0]]
+            raise RuntimeError(f"ShardedScheduler: the event batch failed on rank(s) {bad}")
+        return out
+
+    def _sync_sizes(self, extra: int = 0) -> int:
+        """global waiting count (after this rank adds ``extra``); sets the peer count"""
+        mine = self.local.waiting() + int(extra)
+        sizes = self._gather(np.array([mine], np.int64))[:, 0]
+        total = int(sizes.sum())
+        self.local.set_peer_waiting(total - mine)
+        return total
+
+    # ---- Scheduler entry points (each a collective)
+    def waiting(self) -> int:
+        return int(self._gather(np.array([self.local.waiting()], np.int64)).sum())
+
+    def on_arrival_batch(self, ids, arrival_s, max_tokens):
+        self._collective(lambda: self.local.on_arrival_batch(ids, arrival_s, max_tokens))
+
+    def on_prediction_batch(self, ids, expectation, cvar):
+        self._sync_sizes()
+        self._collective(lambda: self.local.on_prediction_batch(ids, expectation, cvar))
+
+    def on_prediction_logt(self, ids, mu, sigma, max_tokens):
+        self._sync_sizes()
+        self._collective(lambda: self.local.on_prediction_logt(ids, mu, sigma, max_tokens))
+
+    def step(self, arr_ids, arrival_s, arr_max_tokens, pred_ids, mu, sigma, pred_max_tokens,
+             k: int):
+        """one iteration: every rank's arrivals, then every rank's predictions (beta of the
+        global queue after all arrivals), then k global pops"""
+        self._sync_sizes(extra=len(arr_ids))
+        self._collective(lambda: self.local.step(arr_ids, arrival_s, arr_max_tokens, pred_ids,
+                                                 mu, sigma, pred_max_tokens, 0))
+        return self.next_requests(k)
+
+    def next_requests(self, k: int):
+        """next_request() x k over the union of the shards -> global pop ids (uint64)"""
+        out = []
+        while len(out) < k:
+            mine = self.local.waiting()
+            lo, hi, n_in_use = self.local.beta_range()
+            st = self._gather(np.array([mine, lo, hi, n_in_use], np.float64))
+            sizes = st[:, 0].astype(np.int64)
+            Q = int(sizes.sum())
+            if Q == 0:
+                break
+            left = min(k - len(out), Q)
+            used = st[:, 3] > 0
+            pred = self.policy == 2 and bool(used.any())
+            if pred:
+                glo, ghi = float(st[used, 1].min()), float(st[used, 2].max())
+            # pops with no possible rebuild before them: the range only shrinks as pops go
+            L = 0
+            while L < left:
+                if pred:
+                    now = self.beta_fn(Q - L)
+                    if max(abs(now - glo), abs(now - ghi)) > self.threshold:
+                        break
+                L += 1
+            if L == 0:  # the range is exact now: this rebuild fires (sched.cpp:156-166)
+                now = self.beta_fn(Q)
+                self.local.set_peer_waiting(Q - mine)
+                self._collective(lambda: self.local.rebuild_at(now))
+                continue
+            keys, ids = self.local.peek(L)
+            ck = np.full(L, U64_MAX, np.uint64)
+            ci = np.full(L, U64_MAX, np.uint64)
+            ck[:len(keys)] = keys
+            ci[:len(ids)] = ids
+            g = self._gather(np.stack([ck, ci]))  # [G, 2, L]: one exchange
+            owner = np.repeat(np.arange(self.world), L)
+            fk, fi = g[:, 0].reshape(-1), g[:, 1].reshape(-1)
+            o = np.lexsort((fi, fk))[:L]
+            win_ids, win_owner = fi[o], owner[o]
+            take = int((win_owner == self.rank).sum())
+            self.local.set_peer_waiting(Q - mine)
+            got = np.asarray(self.local.next_requests(take), np.uint64) if take else \
+                np.empty(0, np.uint64)
+            if not np.array_equal(got, win_ids[win_owner == self.rank]):
+                raise RuntimeError(f"ShardedScheduler: rank {self.rank} popped {got.tolist()}, "
+                                   f"expected {win_ids[win_owner == self.rank].tolist()}")
+            out.extend(int(x) for x in win_ids)
+            # peers after this batch: (Q - L) global, (mine - take) here
+            self.local.set_peer_waiting((Q - L) - (mine - take))
+        return np.array(out, np.uint64)
