@@ -31,6 +31,9 @@
 #include "../../include/tie_cuda.h"
 #include "tie_internal.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace tie {
 namespace dev {
 namespace {
@@ -43,7 +46,6 @@ struct QDev {
   uint64_t* id;
   double* E;
   double* C;
-  double* beta;
   uint8_t* predicted;
   uint64_t* bkey;  // per block: min key
   uint64_t* bid;   // per block: id of that min
@@ -200,7 +202,6 @@ __global__ void write_predictions_kernel(QDev q, const uint32_t* slots, uint64_t
   q.key[s] = order_bits(key[t]);
   q.E[s] = E[t];
   q.C[s] = C[t];
-  q.beta[s] = beta;
   q.predicted[s] = 1;
 }
 
@@ -234,7 +235,6 @@ __global__ void write_predictions_checked_kernel(QDev q, const uint32_t* slots, 
   q.key[s] = order_bits(key[t]);
   q.E[s] = E[t];
   q.C[s] = C[t];
-  q.beta[s] = beta;
   q.predicted[s] = 1;
 }
 
@@ -273,7 +273,6 @@ __global__ void __launch_bounds__(256) rekey_refresh_kernel(QDev q, uint32_t nb,
       if (kk != kDead && q.predicted[slot]) {
         kk = order_bits(__dadd_rn(q.E[slot], __dmul_rn(beta_now, q.C[slot])));
         q.key[slot] = kk;
-        q.beta[slot] = beta_now;
       }
       const uint64_t ii = q.id[slot];
       if (less_kv(kk, ii, k, i)) {
@@ -291,13 +290,115 @@ __global__ void __launch_bounds__(256) rekey_refresh_kernel(QDev q, uint32_t nb,
   }
 }
 
-// drift rebuild: re-key every live predicted entry with beta_now (sched.cpp:159-164)
-__global__ void rekey_kernel(QDev q, uint64_t n_slots, double beta_now) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_slots; s += stride) {
-    if (!q.predicted[s] || q.key[s] == kDead) continue;
-    q.key[s] = order_bits(__dadd_rn(q.E[s], __dmul_rn(beta_now, q.C[s])));
-    q.beta[s] = beta_now;
+
+// A run of drift-rebuild + single-pop segments (the threshold-0 regime: beta moves with
+// every pop, so the reference re-keys the whole queue before each next_request(),
+// sched.cpp:152-175) in ONE cooperative launch instead of two kernels per pop.  Segment g:
+// every CTA re-keys its blocks at betas[g] and recomputes their minima (skipping -- killing --
+// the slot popped by segment g-1, which every CTA knows), posts its CTA minimum, grid sync;
+// every CTA then reduces the <= gridDim.x CTA minima itself (double-buffered by segment
+// parity, so no second grid sync), CTA 0 records the pop.  The last popped slot's owner
+// kills it and refreshes its block at the end.  A failed fused step (err set) skips all.
+struct SegBetas {
+  double b[32];
+};
+constexpr int kRekeyThreads = 256;
+
+__global__ void __launch_bounds__(kRekeyThreads) rekey_pop_seq_kernel(
+    QDev q, uint32_t nb, uint64_t n_slots, SegBetas betas, uint32_t nseg, uint64_t* out_id,
+    uint32_t* out_slot, uint32_t* out_n, uint64_t* cmin, const unsigned long long* err) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint64_t sk[32], si[32];
+  __shared__ uint32_t ss[32];
+  __shared__ int skip;
+  if (threadIdx.x == 0) skip = err && *(const volatile unsigned long long*)err != ~0ull;
+  __syncthreads();
+  if (skip) return;  // the same decision in every CTA: err is final before this launch
+  const uint32_t G = gridDim.x;
+  uint64_t killed = ~0ull;
+  for (uint32_t g = 0; g < nseg; ++g) {
+    const double beta = betas.b[g];
+    uint64_t ck = kDead, ci = kDead;
+    uint32_t cs = 0;
+    for (uint32_t b = blockIdx.x; b < nb; b += G) {
+      uint64_t k = kDead, i = kDead;
+      uint32_t s = 0;
+      constexpr int kU = kBlockSlots / kRekeyThreads;
+      uint64_t kk[kU], ii[kU];
+      double ee[kU], cc[kU];
+      uint8_t pr[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {  // all loads in flight first (E, C too: no second trip)
+        const uint64_t slot = (uint64_t)b * kBlockSlots + threadIdx.x + u * kRekeyThreads;
+        const bool in = slot < n_slots;
+        kk[u] = in ? q.key[slot] : kDead;
+        ii[u] = in ? q.id[slot] : kDead;
+        pr[u] = in ? q.predicted[slot] : 0;
+        ee[u] = in ? q.E[slot] : 0.0;
+        cc[u] = in ? q.C[slot] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint64_t slot = (uint64_t)b * kBlockSlots + threadIdx.x + u * kRekeyThreads;
+        if (slot == killed) {
+          kk[u] = kDead;
+          q.key[slot] = kDead;
+        } else if (kk[u] != kDead && pr[u]) {
+          kk[u] = order_bits(__dadd_rn(ee[u], __dmul_rn(beta, cc[u])));
+          q.key[slot] = kk[u];
+        }
+        if (less_kv(kk[u], ii[u], k, i)) {
+          k = kk[u];
+          i = ii[u];
+          s = (uint32_t)slot;
+        }
+      }
+      block_argmin(k, i, s, sk, si, ss);
+      if (threadIdx.x == 0) {
+        q.bkey[b] = k;
+        q.bid[b] = i;
+        q.bslot[b] = s;
+      }
+      if (less_kv(k, i, ck, ci)) {
+        ck = k;
+        ci = i;
+        cs = s;
+      }
+    }
+    uint64_t* buf = cmin + (size_t)(g & 1) * 3 * G;
+    if (threadIdx.x == 0) {
+      buf[blockIdx.x] = ck;
+      buf[G + blockIdx.x] = ci;
+      buf[2 * G + blockIdx.x] = cs;
+    }
+    grid.sync();
+    uint64_t k = kDead, i = kDead;
+    uint32_t s = 0;
+    for (uint32_t c = threadIdx.x; c < G; c += kRekeyThreads) {
+      const uint64_t k2 = __ldcg(buf + c), i2 = __ldcg(buf + G + c);
+      if (less_kv(k2, i2, k, i)) {
+        k = k2;
+        i = i2;
+        s = (uint32_t)__ldcg(buf + 2 * G + c);
+      }
+    }
+    block_argmin(k, i, s, sk, si, ss);
+    if (k == kDead) {  // the queue ran dry (same decision in every CTA)
+      if (blockIdx.x == 0 && threadIdx.x == 0) out_n[g] = 0;
+      killed = ~0ull;
+      break;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      out_id[g] = i;
+      out_slot[g] = s;
+      out_n[g] = 1;
+    }
+    killed = s;
+  }
+  if (killed != ~0ull && (uint32_t)(killed / kBlockSlots) % G == blockIdx.x) {
+    if (threadIdx.x == 0) q.key[killed] = kDead;
+    __syncthreads();
+    refresh_block(q, (uint32_t)(killed / kBlockSlots), n_slots, sk, si, ss);
   }
 }
 
@@ -377,17 +478,26 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
       kk[u] = sl[u] < n_slots ? q.key[sl[u]] : kDead;
       ii[u] = sl[u] < n_slots ? q.id[sl[u]] : kDead;
     }
+    // warp-aggregated appends (one shared atomic per warp and item; the loop is warp-uniform:
+    // nchosen * kBlockSlots is a multiple of 32)
+    const uint32_t lane = threadIdx.x & 31;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      if (kk[u] == kDead) continue;
-      if (less_kv(vB_k, vB_i, kk[u], ii[u])) continue;  // > v_B
-      const uint32_t c = atomicAdd(&ncand, 1u);
-      if (c < kCandCap) {
-        ck[c] = kk[u];
-        ci[c] = ii[u];
-        cs[c] = (uint32_t)sl[u];
-      } else {
-        overflow = 1;
+      const bool take = kk[u] != kDead && !less_kv(vB_k, vB_i, kk[u], ii[u]);  // <= v_B
+      const unsigned m = __ballot_sync(0xffffffffu, take);
+      if (!m) continue;
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&ncand, (uint32_t)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (take) {
+        const uint32_t c = base + __popc(m & ((1u << lane) - 1u));
+        if (c < kCandCap) {
+          ck[c] = kk[u];
+          ci[c] = ii[u];
+          cs[c] = (uint32_t)sl[u];
+        } else {
+          overflow = 1;
+        }
       }
     }
   }
@@ -423,8 +533,12 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
   // 3. rank the candidates; the first min(pops, nc) in (key, id) order are the pops
   const uint32_t npop = min(pops, nc);
   for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
+    // only ranks < npop matter: stop counting once a candidate is known to rank lower (all
+    // candidates of a single live block compete when the queue holds < pops blocks)
     uint32_t rank = 0;
-    for (uint32_t d = 0; d < nc; ++d) rank += less_kv(ck[d], ci[d], ck[c], ci[c]) ? 1u : 0u;
+    const uint64_t kc = ck[c], ic = ci[c];
+    for (uint32_t d = 0; d < nc && rank < npop; ++d)
+      rank += less_kv(ck[d], ci[d], kc, ic) ? 1u : 0u;
     if (rank < npop) {
       out_id[rank] = ci[c];
       out_slot[rank] = cs[c];
@@ -530,8 +644,7 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
       q.key[s] = order_bits(__dadd_rn(E[t], __dmul_rn(beta, C[t])));
       q.E[s] = E[t];
       q.C[s] = C[t];
-      q.beta[s] = beta;
-      q.predicted[s] = 1;
+          q.predicted[s] = 1;
     }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -569,6 +682,8 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
 
 using tie::capi::cuda_error;
 using tie::capi::set_error;
+
+constexpr uint32_t kCminCtas = 4096;  // grid cap of the cooperative re-key + pop kernel
 
 struct tie_queue {
   tie_ctx* ctx = nullptr;
@@ -612,6 +727,7 @@ struct tie_queue {
   char* d_pack = nullptr;
   uint64_t pack_cap = 0;
   uint64_t peers = 0;             // waiting requests held by other shards (beta's queue length)
+  uint64_t* d_cmin = nullptr;     // [2][3][kCminCtas] CTA minima of the re-key + pop kernel
   uint64_t* h_peek_key = nullptr; // mapped pinned: keys of a peek's (undone) pops
   uint64_t peek_cap = 0;
   uint64_t* h_out_id = nullptr;   // pinned
@@ -770,17 +886,62 @@ void apply_pops(tie_queue* Q, uint32_t off, uint32_t cnt, std::vector<uint64_t>&
 
 // launch a plan's kernels: segment g = [rebuild][pops -> d_out_*[off..], d_out_n[g]]; a set
 // error word (a failed fused step) makes every kernel skip
+// cooperative launch arguments (addresses handed to cudaLaunchCooperativeKernel)
+struct QDevArgs {
+  tie::dev::QDev q;
+  uint32_t nb;
+  uint64_t n_slots;
+  tie::dev::SegBetas sb;
+  uint32_t nseg;
+  uint64_t* out_id;
+  uint32_t* out_slot;
+  uint32_t* out_n;
+  uint64_t* cmin;
+  const unsigned long long* err;
+};
+
 uint64_t launch_plan(tie_queue* Q, const std::vector<Seg>& plan, size_t first_seg,
                      uint32_t off, cudaStream_t s, unsigned long long* err) {
   const uint32_t nb = (uint32_t)((Q->n_slots + tie::dev::kBlockSlots - 1) / tie::dev::kBlockSlots);
-  for (size_t g = first_seg; g < plan.size(); ++g) {
+  static int rekey_ctas = -1;  // co-resident CTAs of the cooperative re-key + pop kernel
+  if (rekey_ctas < 0) {
+    int bpsm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, tie::dev::rekey_pop_seq_kernel,
+                                                  tie::dev::kRekeyThreads, 0);
+    if (const char* v = getenv("TIE_REKEY_CTAS_PER_SM")) bpsm = std::min(bpsm, atoi(v));
+    rekey_ctas = std::min(bpsm * sms, (int)kCminCtas);
+    if (getenv("TIE_NO_REKEY_SEQ")) rekey_ctas = 0;  // A/B switch
+  }
+  auto single_rebuild_pop = [&](size_t g) { return plan[g].rebuild && plan[g].pops == 1; };
+  size_t g = first_seg;
+  while (g < plan.size()) {
+    size_t e = g;  // [g, e): a run of (rebuild, 1 pop) segments for one cooperative launch
+    while (e < plan.size() && e - g < 32 && single_rebuild_pop(e)) ++e;
+    if (e - g >= 2 && rekey_ctas > 0 && nb > 0) {
+      tie::dev::SegBetas sb{};
+      for (size_t j = g; j < e; ++j) sb.b[j - g] = plan[j].beta;
+      QDevArgs a{Q->q, nb, Q->n_slots, sb, (uint32_t)(e - g), Q->d_out_id + off,
+                 Q->d_out_slot + off, Q->d_out_n + g, Q->d_cmin, err};
+      const uint32_t grid = std::min<uint32_t>(nb, (uint32_t)rekey_ctas);
+      void* args[] = {&a.q, &a.nb, &a.n_slots, &a.sb, &a.nseg, &a.out_id, &a.out_slot,
+                      &a.out_n, &a.cmin, &a.err};
+      cudaLaunchCooperativeKernel((const void*)tie::dev::rekey_pop_seq_kernel, grid,
+                                  tie::dev::kRekeyThreads, args, 0, s);
+      tie::capi::count_launch(1);
+      off += (uint32_t)(e - g);
+      g = e;
+      continue;
+    }
     if (plan[g].rebuild) rebuild_launch(Q, plan[g].beta, s, err);
     tie::dev::step_apply_kernel<<<1, 1024, 0, s>>>(
         Q->q, 0, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0.0, nullptr, 0, 0, nb,
         Q->n_slots, plan[g].pops, Q->d_out_id + off, Q->d_out_slot + off, Q->d_out_n + g, err);
     off += plan[g].pops;
+    tie::capi::count_launch(1);
+    ++g;
   }
-  tie::capi::count_launch(plan.size() - first_seg);
   return off;
 }
 
@@ -847,8 +1008,8 @@ int tie_queue_create(tie_ctx* ctx, int policy, int adaptive, double beta_fixed, 
   cudaError_t e;
   if ((e = cudaMalloc(&Q->q.key, 8 * capacity)) || (e = cudaMalloc(&Q->q.id, 8 * capacity)) ||
       (e = cudaMalloc(&Q->q.E, 8 * capacity)) || (e = cudaMalloc(&Q->q.C, 8 * capacity)) ||
-      (e = cudaMalloc(&Q->q.beta, 8 * capacity)) ||
       (e = cudaMalloc(&Q->q.predicted, capacity)) || (e = cudaMalloc(&Q->q.bkey, 8 * nb)) ||
+      (e = cudaMalloc(&Q->d_cmin, 8 * 6 * kCminCtas)) ||
       (e = cudaMalloc(&Q->q.bid, 8 * nb)) || (e = cudaMalloc(&Q->q.bslot, 4 * nb)) ||
       ensure_stage(Q, 1024) != TIE_OK || ensure_out(Q, 256) != TIE_OK ||
       (e = cudaHostAlloc((void**)&Q->status, sizeof(*Q->status), cudaHostAllocMapped))) {
@@ -868,9 +1029,9 @@ void tie_queue_destroy(tie_queue* Q) {
   if (!Q) return;
   cudaDeviceSynchronize();
   for (void* p : {(void*)Q->q.key, (void*)Q->q.id, (void*)Q->q.E, (void*)Q->q.C,
-                  (void*)Q->q.beta, (void*)Q->q.predicted, (void*)Q->q.bkey, (void*)Q->q.bid,
+                  (void*)Q->q.predicted, (void*)Q->q.bkey, (void*)Q->q.bid,
                   (void*)Q->q.bslot, (void*)Q->d_ids, (void*)Q->d_a, (void*)Q->d_b,
-                  (void*)Q->d_c, (void*)Q->d_slots, (void*)Q->d_blocks})
+                  (void*)Q->d_c, (void*)Q->d_slots, (void*)Q->d_blocks, (void*)Q->d_cmin})
     cudaFree(p);
   cudaFreeHost(Q->h_out);
   cudaFreeHost(Q->h_peek_key);

@@ -4,7 +4,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2604_00499_b200 as tie
 
-n, steps, per = 1_000_000, 200, 32
+n, steps, per = (int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000), 200, 32
 mc = tie.McContext(3.5)
 w = tie.gen_logt_workload_soa(n + steps * per * 4, 7)
 mu, sg, mt = w["mu"], w["sigma"], w["max_tokens"]
