@@ -400,10 +400,28 @@ struct LaneRow {
   static constexpr bool kStatic = true;
   double lx;       // this lane's log-sample (lanes >= KT hold 0)
   unsigned mask;   // the prompt's lanes
-  double t[KT];    // gathered copy for the median / MAD sorts
   __device__ __forceinline__ int size() const { return KT; }
-  __device__ __forceinline__ double& Tm(int i) { return t[i]; }
 };
+
+// median_sorted (fit.cpp:27-30) of the KT lane values v (lane j < KT) without sorting: each
+// lane's position in the sorted order is its rank by (value, lane) -- equal values share the
+// value, so the element at sorted position q is exactly the value of the lane ranked q.
+// Replaces two unrolled KT-round sorting networks (~3.5k instructions of kernel code, whose
+// i-cache misses dominated the kernel's stalls) by KT shuffles per median.
+template <int KT, int W>
+__device__ __forceinline__ double lane_median(double v, int j, int grp, unsigned mask) {
+  uint32_t rank = 0;
+#pragma unroll
+  for (int i = 0; i < KT; ++i) {
+    const double u = __shfl_sync(mask, v, i, W);
+    rank += (u < v || (u == v && i < j)) ? 1u : 0u;
+  }
+  auto at = [&](uint32_t q) {
+    const unsigned b = __ballot_sync(mask, j < KT && rank == q);
+    return __shfl_sync(mask, v, (__ffs(b) - 1) - grp * W, W);
+  };
+  return (KT % 2) ? at(KT / 2) : 0.5 * (at(KT / 2 - 1) + at(KT / 2));
+}
 
 template <int KT, int W>
 __device__ __noinline__ double loglik(LaneRow<KT, W>& r, const FitConst& c, double mu,
@@ -456,19 +474,13 @@ __global__ void __launch_bounds__(128) fit_lanes_kernel(const FitArgs a) {
       }
       continue;
     }
-#pragma unroll
-    for (int i = 0; i < KT; ++i) r.t[i] = __shfl_sync(r.mask, r.lx, i, W);
-    // fit_init on the gathered copy (identical sorts in every lane)
+    // fit_init (fit.cpp:78-100): median and MAD by lane ranks (the same values in every lane)
     FitOut o;
     Bfgs st;
     bool live;
     {
-      sort_scratch(r);
-      const double mu0 = median_scratch(r);
-#pragma unroll
-      for (int i = 0; i < KT; ++i) r.t[i] = fabs(r.t[i] - mu0);
-      sort_scratch(r);
-      const double sigma0 = 1.4826 * median_scratch(r);
+      const double mu0 = lane_median<KT, W>(r.lx, j, grp, r.mask);
+      const double sigma0 = 1.4826 * lane_median<KT, W>(fabs(r.lx - mu0), j, grp, r.mask);
       o.degenerate = false;
       o.iters = 0;
       live = !(sigma0 < kSigmaFloor);
