@@ -36,7 +36,7 @@ N_CONFIG2 = 1_000_000
 ALPHA = 0.9
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0
-TRAFFIC_FILE = "ncu_traffic_r01h.json"
+TRAFFIC_FILE = "ncu_traffic_r01j.json"
 
 
 def parse():
@@ -518,7 +518,7 @@ def run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream):
         out["config4_single_gpu"] = {
             "metric": "requests scored+ranked/sec, 64M-request queue on ONE B200 (config 4 size)",
             "value": n4 / (ms4 * 1e-3), "unit": "requests/s", "ms_per_step": ms4,
-            "note": "inputs resident in HBM (1.3 GB, larger than L2); large-queue bucket sort"}
+            "note": "inputs resident in HBM (1.3 GB, larger than L2); two-level partition sort"}
         # rank 0's final step at G = 8 weak scaling (8 x 1M sorted (score, id) runs, as after
         # the NCCL all-gather): k-way merge vs a stable re-sort of the concatenation
         from paper_2604_00499_b200.dist import DeviceOps

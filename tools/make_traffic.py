@@ -25,7 +25,7 @@ def main(src, dst, n):
                            "issue_active_pct": round(k.get("issue_active_pct", 0), 1),
                            "fp64_pipe_pct": round(k.get("fp64_pipe_pct", 0), 1),
                            "top_stalls": k.get("top_stalls_cycles_per_issue"),
-                           "capture": f"{src} id {k['id']}"}
+                           "capture": f"{src} id {k['id']}" + (f" ({k['report']})" if "report" in k else "")}
     json.dump(out, open(dst, "w"), indent=1)
 
 

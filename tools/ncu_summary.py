@@ -8,6 +8,8 @@ import subprocess
 import sys
 
 UNIT = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,  # -> us
+        "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6,
+        "B": 1.0, "KB": 1e3, "MB": 1e6, "GB": 1e9,
         "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}                 # -> bytes
 METRICS = {
     "duration_us": ("gpu__time_duration.sum", 1),
