@@ -979,10 +979,22 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
   const uint64_t lo = (uint64_t)blockIdx.x * q.chunk;
   const uint64_t hi = min(n, lo + q.chunk);
   const uint32_t cn = hi > lo ? (uint32_t)(hi - lo) : 0u;
-  for (uint32_t j = threadIdx.x; j < cn; j += kFusedThreads) {
-    const uint64_t k = q.keys[lo + j];
-    ck[j] = k;
-    atomicAdd(&h[part_bucket(q, r, k) >> q.low_bits], 1u);
+  constexpr int kLd = 8;  // key loads in flight per thread before the first use
+  for (uint32_t j0 = threadIdx.x; j0 < cn; j0 += kLd * kFusedThreads) {
+    uint64_t kk[kLd];
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const uint32_t j = j0 + u * kFusedThreads;
+      kk[u] = j < cn ? q.keys[lo + j] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const uint32_t j = j0 + u * kFusedThreads;
+      if (j < cn) {
+        ck[j] = kk[u];
+        atomicAdd(&h[part_bucket(q, r, kk[u]) >> q.low_bits], 1u);
+      }
+    }
   }
   __syncthreads();
   for (uint32_t p = threadIdx.x; p < P; p += kFusedThreads) {
