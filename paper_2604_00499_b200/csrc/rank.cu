@@ -771,6 +771,7 @@ struct Part {
   uint32_t low_bits;    // bits below the level-1 partition index (fine, or level-2 + fine)
   uint32_t total_bits;  // B: bucket bits of (k - kmin) >> shift
   uint32_t cap1;        // level-1 partition capacity (kPartCap; unbounded with level 2)
+  uint32_t local_scatter;  // fused kernel: group the chunk by partition before scattering
   // level 2 (two-level path): P2 sub-partitions per level-1 partition, regrouped keys
   uint32_t p2_log2;
   uint64_t* tk2;
@@ -972,7 +973,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
   __shared__ int over;
   const uint32_t P = q.P;
   uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);   // [P] chunk histogram -> cursors
-  uint64_t* ck = reinterpret_cast<uint64_t*>(h + kPartMaxP);  // the chunk's keys
+  // the chunk's keys (after the local bases / cursors when the chunk is grouped locally)
+  uint64_t* ck = reinterpret_cast<uint64_t*>(h + (q.local_scatter ? 3 : 1) * kPartMaxP);
   for (uint32_t p = threadIdx.x; p < P; p += kFusedThreads) h[p] = 0;
   __syncthreads();
   const KeyRange r = key_range(q.mm, q.total_bits);
@@ -997,9 +999,41 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
     }
   }
   __syncthreads();
+  // local grouping (before the grid sync, so it overlaps the other CTAs' staging): the
+  // chunk's keys ordered by partition in shared memory (lb: local partition bases, srt: key
+  // index per local position), so the scatter below writes each partition's run with
+  // consecutive threads instead of one scattered store per key
+  uint32_t* lb = h + kPartMaxP;                                   // [P] local bases
+  uint32_t* cur = lb + kPartMaxP;                                 // [P] local cursors
+  uint16_t* srt = reinterpret_cast<uint16_t*>(ck + q.chunk);      // [chunk]
+  if (q.local_scatter) {
+    constexpr int kPer = kPartMaxP / kFusedThreads;
+    uint32_t c[kPer], t = 0;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t p = threadIdx.x * kPer + u;
+      c[u] = p < P ? h[p] : 0u;
+      t += c[u];
+    }
+    uint32_t v = block_excl_scan_t<kFusedThreads>(t, sh);
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t p = threadIdx.x * kPer + u;
+      if (p < P) {
+        lb[p] = v;
+        cur[p] = v;
+      }
+      v += c[u];
+    }
+  }
   for (uint32_t p = threadIdx.x; p < P; p += kFusedThreads) {
     const uint32_t c = h[p];
     h[p] = c ? atomicAdd(q.pcount + p, c) : 0u;  // this CTA's offset inside partition p
+  }
+  if (q.local_scatter) {
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < cn; j += kFusedThreads)
+      srt[atomicAdd(&cur[part_bucket(q, r, ck[j]) >> q.low_bits], 1u)] = (uint16_t)j;
   }
   grid.sync();
   // partition bases from the final counts (each CTA scans the <= 2048 counts itself)
@@ -1033,11 +1067,22 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
   }
   for (uint32_t p = threadIdx.x; p < P; p += kFusedThreads) h[p] += pb[p];
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < cn; j += kFusedThreads) {
-    const uint64_t k = ck[j];
-    const uint32_t pos = atomicAdd(&h[part_bucket(q, r, k) >> q.low_bits], 1u);
-    q.tk[pos] = k;
-    q.tv[pos] = (uint32_t)(lo + j);
+  if (q.local_scatter) {
+    for (uint32_t t = threadIdx.x; t < cn; t += kFusedThreads) {
+      const uint32_t j = srt[t];
+      const uint64_t k = ck[j];
+      const uint32_t p = part_bucket(q, r, k) >> q.low_bits;
+      const uint32_t pos = h[p] + (t - lb[p]);
+      q.tk[pos] = k;
+      q.tv[pos] = (uint32_t)(lo + j);
+    }
+  } else {
+    for (uint32_t j = threadIdx.x; j < cn; j += kFusedThreads) {
+      const uint64_t k = ck[j];
+      const uint32_t pos = atomicAdd(&h[part_bucket(q, r, k) >> q.low_bits], 1u);
+      q.tk[pos] = k;
+      q.tv[pos] = (uint32_t)(lo + j);
+    }
   }
   grid.sync();
   for (uint32_t p = blockIdx.x; p < P; p += gridDim.x) {
@@ -1342,6 +1387,7 @@ cudaError_t part_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_t*
   q.low_bits = L.p2_log2 + L.fine_log2;
   q.total_bits = L.p_log2 + q.low_bits;
   q.cap1 = L.part2 ? 0xffffffffu : kPartCap;
+  q.local_scatter = 0;
 
   q.tk2 = L.part2 ? (uint64_t*)(base + L.tk2) : nullptr;
   q.tv2 = L.part2 ? (uint32_t*)(base + L.tv2) : nullptr;
@@ -1385,9 +1431,12 @@ cudaError_t part_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_t*
     }
     const uint64_t co = (uint64_t)std::max(bpsm, 0) * sms;  // co-resident CTAs
     Part qf = q;
+    static const int local_scatter = getenv("TIE_NO_LOCAL_SCATTER") ? 0 : 1;  // A/B switch
     qf.ctas = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(co, kPartMaxCtas),
                                            (n + 1023) / 1024);
     if (qf.ctas > 0) qf.chunk = (n + qf.ctas - 1) / qf.ctas;
+    qf.local_scatter =
+        local_scatter && 4 * 3 * kPartMaxP + 10 * qf.chunk + 16 <= smem && qf.chunk < 65536;
     if (qf.ctas > 0 && 4 * kPartMaxP + 8 * qf.chunk <= smem) {
       ProfScope p(ctx, "rank.fused", s);
       void* args[] = {(void*)&qf, (void*)&n, (void*)&ids, (void*)&order};
