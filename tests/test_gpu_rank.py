@@ -112,18 +112,27 @@ def test_bucket_extreme_range(abi, h, oracle):
     assert np.array_equal(abi.rank(h, key), oracle.rank(key))
 
 
+@pytest.mark.parametrize("n", [2_500_000, 6_600_000])  # bucket path | two-level path
 @pytest.mark.parametrize("distinct", [1, 3])
-def test_two_level_path_overflow_falls_back_exactly(abi, h, oracle, distinct):
-    """n > 2^21 takes the two-level partition path; massive ties overflow a sub-partition and
-    the device-side LSD fallback must still give the heap's order."""
+def test_large_n_overflow_falls_back_exactly(abi, h, oracle, distinct, n):
+    """2^21 < n < 6M takes the bucket path, n >= 6M the two-level partition path (tiled
+    level-1 scatter); massive ties overflow a bucket / sub-partition and the device-side LSD
+    fallback must still give the heap's order."""
     rng = np.random.default_rng(distinct + 50)
-    n = 2_500_000
     key = rng.integers(0, distinct, n).astype(np.float64) * 3.5 + 10.0
     assert np.array_equal(abi.rank(h, key), oracle.rank(key))
 
 
-def test_two_level_path_moderate_ties(abi, h, oracle):
+@pytest.mark.parametrize("n", [4_200_000, 6_600_000, 9_000_001])
+def test_large_n_moderate_ties(abi, h, oracle, n):
     rng = np.random.default_rng(77)
-    n = 4_200_000
     key = np.round(rng.lognormal(5.0, 0.7, n), 1)  # many small tie groups, no overflow
+    assert np.array_equal(abi.rank(h, key), oracle.rank(key))
+
+
+def test_two_level_path_continuous_keys(abi, h, oracle):
+    """two-level path with score-like keys: skewed partition sizes, tiles ending mid-chunk"""
+    rng = np.random.default_rng(123)
+    n = 7_000_003
+    key = rng.lognormal(5.0, 0.6, n) + 50.0
     assert np.array_equal(abi.rank(h, key), oracle.rank(key))
