@@ -489,9 +489,15 @@ def run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream):
     xp = torch.from_numpy(x).pin_memory()
     hb = [torch.empty(P, dtype=t).pin_memory() for t in
           (torch.float64, torch.float64, torch.float64, torch.int32, torch.uint8, torch.uint8)]
-    t0 = time.perf_counter()
-    tie.fit_host_ptr(ctx, xp.data_ptr(), P, K, 3.5, *[t.data_ptr() for t in hb])
-    fe2e = time.perf_counter() - t0
+    fit_host = lambda: tie.fit_host_ptr(ctx, xp.data_ptr(), P, K, 3.5,
+                                        *[t.data_ptr() for t in hb])
+    fit_host()  # first call allocates the staging buffers
+    fts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        fit_host()
+        fts.append(time.perf_counter() - t0)
+    fe2e = float(np.median(fts))
     # config 4 on one GPU: the 64M-request queue (the multi-GPU config's full size), resident
     try:
         n4 = 64 * 2 ** 20

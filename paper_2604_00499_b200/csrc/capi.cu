@@ -625,8 +625,12 @@ int tie_fit_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double n
   if (K < 3)
     return set_error(TIE_EINVALID, "fit_logt_fixed_nu: need at least 3 samples, got " +
                                        std::to_string(K));
+  if (!(nu > 0.0) || !std::isfinite(nu))
+    return set_error(TIE_EDOMAIN, "fit_logt_fixed_nu: nu must be finite and > 0");
+  if (P && (!x || !mu || !sigma)) return set_error(TIE_EINVALID, "tie_fit_host: null pointer");
   if (P == 0) return TIE_OK;
   DeviceGuard g(ctx->device);
+  ctx->err_op = "tie_fit";
   char* b = io_buffer(ctx, al(8 * P * K) + 3 * al(8 * P) + al(4 * P) + 2 * al(P));
   if (!b) return set_error(TIE_ECUDA, "tie_fit_host: device allocation failed");
   size_t off = 0;
@@ -637,18 +641,53 @@ int tie_fit_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double n
   int32_t* d_it = (int32_t*)(b + off); off += al(4 * P);
   uint8_t* d_cv = (uint8_t*)(b + off); off += al(P);
   uint8_t* d_dg = (uint8_t*)(b + off);
-  cudaStream_t s = ctx->stream;
-  TIE_CUDA_TRY(cudaMemcpyAsync(d_x, x, 8 * P * K, cudaMemcpyHostToDevice, s), "h2d");
-  if (int rc = tie_fit(ctx, d_x, P, K, nu, d_mu, d_sg, d_ll, d_it, d_cv, d_dg, s)) return rc;
-  TIE_CUDA_TRY(cudaMemcpyAsync(mu, d_mu, 8 * P, cudaMemcpyDeviceToHost, s), "d2h");
-  TIE_CUDA_TRY(cudaMemcpyAsync(sigma, d_sg, 8 * P, cudaMemcpyDeviceToHost, s), "d2h");
-  if (log_likelihood)
-    TIE_CUDA_TRY(cudaMemcpyAsync(log_likelihood, d_ll, 8 * P, cudaMemcpyDeviceToHost, s), "d2h");
-  if (iterations)
-    TIE_CUDA_TRY(cudaMemcpyAsync(iterations, d_it, 4 * P, cudaMemcpyDeviceToHost, s), "d2h");
-  if (converged) TIE_CUDA_TRY(cudaMemcpyAsync(converged, d_cv, P, cudaMemcpyDeviceToHost, s), "d2h");
-  if (degenerate)
-    TIE_CUDA_TRY(cudaMemcpyAsync(degenerate, d_dg, P, cudaMemcpyDeviceToHost, s), "d2h");
+  cudaStream_t s = ctx->stream, cs = ctx->copy_stream;
+  // pipeline over prompt chunks (fits are independent per prompt): all H2D copies queued on
+  // the copy stream, chunk c's fit waits for its copy, its results go back on the copy
+  // stream behind the H2Ds -- copies in both directions overlap the fits
+  const int chunks = P >= (1u << 18) ? 4 : 1;
+  const uint64_t step = (P + chunks - 1) / chunks;
+  cudaEvent_t* evH = ctx->ev + 1;                                       // ev[1..4]
+  cudaEvent_t evF[4] = {ctx->ev[5], ctx->ev[6], ctx->ev[7], ctx->ev[0]};  // after ev[0]'s wait
+  TIE_CUDA_TRY(cudaEventRecord(ctx->ev[0], s), "tie_fit_host");
+  TIE_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[0], 0), "tie_fit_host");
+  for (int c = 0; c < chunks; ++c) {
+    const uint64_t lo = std::min<uint64_t>(P, c * step), m = std::min<uint64_t>(P, lo + step) - lo;
+    TIE_CUDA_TRY(cudaMemcpyAsync(d_x + lo * K, x + lo * K, 8 * m * K, cudaMemcpyHostToDevice, cs),
+                 "h2d");
+    TIE_CUDA_TRY(cudaEventRecord(evH[c], cs), "tie_fit_host");
+  }
+  for (int c = 0; c < chunks; ++c) {
+    const uint64_t lo = std::min<uint64_t>(P, c * step), m = std::min<uint64_t>(P, lo + step) - lo;
+    TIE_CUDA_TRY(cudaStreamWaitEvent(s, evH[c], 0), "tie_fit_host");
+    if (m) {
+      const cudaError_t e = tie::dev::launch_fit(ctx, d_x + lo * K, m, K, nu, d_mu + lo,
+                                                 d_sg + lo, d_ll + lo, d_it + lo, d_cv + lo,
+                                                 d_dg + lo, s, lo);
+      if (e != cudaSuccess) return cuda_error(e, "tie_fit_host");
+    }
+    TIE_CUDA_TRY(cudaEventRecord(evF[c], s), "tie_fit_host");
+  }
+  for (int c = 0; c < chunks; ++c) {
+    const uint64_t lo = std::min<uint64_t>(P, c * step), m = std::min<uint64_t>(P, lo + step) - lo;
+    TIE_CUDA_TRY(cudaStreamWaitEvent(cs, evF[c], 0), "tie_fit_host");
+    if (!m) continue;
+    TIE_CUDA_TRY(cudaMemcpyAsync(mu + lo, d_mu + lo, 8 * m, cudaMemcpyDeviceToHost, cs), "d2h");
+    TIE_CUDA_TRY(cudaMemcpyAsync(sigma + lo, d_sg + lo, 8 * m, cudaMemcpyDeviceToHost, cs), "d2h");
+    if (log_likelihood)
+      TIE_CUDA_TRY(cudaMemcpyAsync(log_likelihood + lo, d_ll + lo, 8 * m, cudaMemcpyDeviceToHost, cs),
+                   "d2h");
+    if (iterations)
+      TIE_CUDA_TRY(cudaMemcpyAsync(iterations + lo, d_it + lo, 4 * m, cudaMemcpyDeviceToHost, cs),
+                   "d2h");
+    if (converged)
+      TIE_CUDA_TRY(cudaMemcpyAsync(converged + lo, d_cv + lo, m, cudaMemcpyDeviceToHost, cs), "d2h");
+    if (degenerate)
+      TIE_CUDA_TRY(cudaMemcpyAsync(degenerate + lo, d_dg + lo, m, cudaMemcpyDeviceToHost, cs),
+                   "d2h");
+  }
+  TIE_CUDA_TRY(cudaEventRecord(evF[0], cs), "tie_fit_host");
+  TIE_CUDA_TRY(cudaStreamWaitEvent(s, evF[0], 0), "tie_fit_host");
   return tie_sync(ctx, s);
 }
 

@@ -298,6 +298,7 @@ struct FitArgs {
   uint8_t* conv;
   uint8_t* degen;
   unsigned long long* err;
+  uint64_t index_base;  // added to reported prompt indices (chunked callers)
   // stragglers: prompts still iterating after kPhase1Iters are handed to warp-per-prompt
   // phase 2 (bounded by spill_cap; beyond it a thread simply finishes the prompt itself)
   FitSpill* spill;
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(128) fit_kernel_static(const FitArgs a) {
       r.lx[i] = log(v);
     }
     if (!ok) {  // check_samples (fit.cpp:18-25)
-      report(a.err, p, kSampleBad);
+      report(a.err, a.index_base + p, kSampleBad);
       store_nan(a, p);
       continue;
     }
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(128) fit_kernel_generic(const FitArgs a) {
       r.lx[i] = log(v);
     }
     if (!ok) {
-      report(a.err, p, kSampleBad);
+      report(a.err, a.index_base + p, kSampleBad);
       store_nan(a, p);
       continue;
     }
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(128) fit_lanes_kernel(const FitArgs a) {
     r.lx = j < KT ? log(v) : 0.0;
     if (__ballot_sync(r.mask, bad)) {  // check_samples (fit.cpp:18-25)
       if (j == 0) {
-        report(a.err, p, kSampleBad);
+        report(a.err, a.index_base + p, kSampleBad);
         store_nan(a, p);
       }
       continue;
@@ -615,7 +616,7 @@ int sm_count(int device) {
 
 cudaError_t launch_fit(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
                        double* mu, double* sigma, double* ll, int32_t* iters, uint8_t* conv,
-                       uint8_t* degen, cudaStream_t s) {
+                       uint8_t* degen, cudaStream_t s, uint64_t index_base) {
   if (P == 0) return cudaSuccess;
   FitArgs a;
   a.c = make_const(nu);
@@ -630,6 +631,7 @@ cudaError_t launch_fit(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, do
   a.conv = conv;
   a.degen = degen;
   a.err = ctx->d_err;
+  a.index_base = index_base;
   const int sms = sm_count(ctx->device);
   const unsigned grid = (unsigned)std::min<uint64_t>((P + 127) / 128, (uint64_t)sms * 16);
   // scratch: [log-samples (generic K only)][straggler spill buffer][spill counter]

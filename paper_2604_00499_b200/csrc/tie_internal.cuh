@@ -254,7 +254,7 @@ RankPrep rank_prepare(tie_ctx* ctx, uint64_t n, cudaStream_t s);
 cudaError_t rank_prepared(tie_ctx* ctx, uint64_t n, uint64_t* order, cudaStream_t s);
 cudaError_t launch_fit(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
                        double* mu, double* sigma, double* ll, int32_t* iters, uint8_t* conv,
-                       uint8_t* degen, cudaStream_t s);
+                       uint8_t* degen, cudaStream_t s, uint64_t index_base = 0);
 // k-way merge of sorted (score, id) runs (merge.cu): keys/ids [G][stride], lens host array
 cudaError_t launch_merge_runs(tie_ctx* ctx, const double* keys, const uint64_t* ids, int G,
                               uint64_t stride, const uint64_t* lens, uint64_t* out_ids,

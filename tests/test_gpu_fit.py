@@ -104,3 +104,15 @@ def test_errors(abi, h):
     with pytest.raises(TieError) as ei:
         abi.fit(h, np.full((2, 5), 3.0), nu=-1.0)
     assert ei.value.code == 1
+
+
+def test_chunked_host_pipeline(abi, h, oracle):
+    """tie_fit_host pipelines >= 2^18 prompts in 4 chunks (H2D / fit / D2H overlapped):
+    results equal the one-shot device fits and errors name the global prompt index."""
+    x, _, _ = oracle.gen_fit_data(300_001, 16, seed=4)
+    got = abi.fit(h, x)
+    _compare(got, oracle.fit(x), "chunked-300k")
+    x[290_000, 7] = 0.0
+    with pytest.raises(TieError) as ei:
+        abi.fit(h, x)
+    assert ei.value.code == 1 and "item 290000" in str(ei.value)
