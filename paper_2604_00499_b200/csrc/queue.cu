@@ -927,12 +927,14 @@ uint64_t launch_plan(tie_queue* Q, const std::vector<Seg>& plan, size_t first_se
       const uint32_t grid = std::min<uint32_t>(nb, (uint32_t)rekey_ctas);
       void* args[] = {&a.q, &a.nb, &a.n_slots, &a.sb, &a.nseg, &a.out_id, &a.out_slot,
                       &a.out_n, &a.cmin, &a.err};
-      cudaLaunchCooperativeKernel((const void*)tie::dev::rekey_pop_seq_kernel, grid,
-                                  tie::dev::kRekeyThreads, args, 0, s);
-      tie::capi::count_launch(1);
-      off += (uint32_t)(e - g);
-      g = e;
-      continue;
+      if (cudaLaunchCooperativeKernel((const void*)tie::dev::rekey_pop_seq_kernel, grid,
+                                      tie::dev::kRekeyThreads, args, 0, s) == cudaSuccess) {
+        tie::capi::count_launch(1);
+        off += (uint32_t)(e - g);
+        g = e;
+        continue;
+      }
+      cudaGetLastError();  // not launchable here (e.g. co-residency): per-segment kernels
     }
     if (plan[g].rebuild) rebuild_launch(Q, plan[g].beta, s, err);
     tie::dev::step_apply_kernel<<<1, 1024, 0, s>>>(
