@@ -971,6 +971,8 @@ int execute_plan(tie_queue* Q, const std::vector<Seg>& plan, std::vector<uint64_
   if (int rc = ensure_out(Q, std::max<uint64_t>(total, plan.size() + 1))) return rc;
   launch_plan(Q, plan, 0, 0, s, Q->ctx->d_err);
   fetch_plan(Q, plan.size(), total, s);
+  if (const cudaError_t le = cudaGetLastError(); le != cudaSuccess)
+    return cuda_error(le, "tie_queue_next");
   const cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_error(e, "tie_queue_next");
   replay_plan(Q, plan, out);
