@@ -412,3 +412,77 @@ class ShardedScheduler:
             # peers after this batch: (Q - L) global, (mine - take) here
             self.local.set_peer_waiting((Q - L) - (mine - take))
         return np.array(out, np.uint64)
+
+
+FIT_FIELDS = ("mu", "sigma", "log_likelihood", "iterations", "converged", "degenerate")
+
+
+class DeviceFitOps:
+    """K3 (fit_logt_fixed_nu per prompt) on this rank's GPU through the C-ABI."""
+
+    def __init__(self, mc, nu: float = 3.5):
+        import torch
+
+        from . import _core
+
+        self.torch, self.core, self.mc, self.nu = torch, _core, mc, nu
+
+    def fit(self, x):
+        """x: [P, K] float64 device tensor -> dict of device tensors (FIT_FIELDS)"""
+        torch = self.torch
+        P, K = x.shape
+        dev = x.device
+        out = {"mu": torch.empty(P, dtype=torch.float64, device=dev),
+               "sigma": torch.empty(P, dtype=torch.float64, device=dev),
+               "log_likelihood": torch.empty(P, dtype=torch.float64, device=dev),
+               "iterations": torch.empty(P, dtype=torch.int32, device=dev),
+               "converged": torch.empty(P, dtype=torch.uint8, device=dev),
+               "degenerate": torch.empty(P, dtype=torch.uint8, device=dev)}
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        self.core.fit_device(self.mc.handle, x.contiguous().data_ptr(), P, K, self.nu,
+                             *[out[f].data_ptr() for f in FIT_FIELDS], stream)
+        self.core.sync(self.mc.handle, stream)
+        return out
+
+
+class ShardedFit:
+    """Config 3 over the ranks of ``group`` ("Fit K3: embarrassingly parallel
+    by prompt"): prompts are sharded contiguously (``shard_bounds``), every rank fits its own
+    shard, and the only collective is the optional result gather -- ``gather="root"`` (rank
+    0) or ``"all"`` returns the fits of every prompt in global order, ``"none"`` only the
+    local ones."""
+
+    def __init__(self, ops, group=None, gather: str = "none"):
+        import torch.distributed as dist
+
+        if gather not in ("none", "root", "all"):
+            raise ValueError("gather must be 'none', 'root' or 'all'")
+        self.dist, self.ops, self.group, self.gather = dist, ops, group, gather
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+
+    def __call__(self, x_local, P_global: int):
+        import torch
+
+        lo, hi = shard_bounds(P_global, self.world, self.rank)
+        if x_local.shape[0] != hi - lo:
+            raise ValueError(f"rank {self.rank}: shard holds {x_local.shape[0]} prompts, "
+                             f"expected {hi - lo} (prompts [{lo}, {hi}))")
+        local = self.ops.fit(x_local)
+        if self.gather == "none" or self.world == 1:
+            return local, (local if self.gather != "none" else None)
+        lens = [b - a for a, b in (shard_bounds(P_global, self.world, g)
+                                   for g in range(self.world))]
+        width = lens[0]
+        glob = {}
+        for f in FIT_FIELDS:
+            t = local[f]
+            wire = t.to(torch.int32) if t.dtype == torch.uint8 else t  # gloo / NCCL friendly
+            pad = torch.zeros(width, dtype=wire.dtype, device=wire.device)
+            pad[:wire.numel()] = wire
+            parts = [torch.empty_like(pad) for _ in range(self.world)]
+            self.dist.all_gather(parts, pad, group=self.group)
+            if self.gather == "all" or self.rank == 0:
+                cat = torch.cat([p[:L] for p, L in zip(parts, lens)])
+                glob[f] = cat.to(t.dtype)
+        return local, (glob if glob else None)

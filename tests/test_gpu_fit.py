@@ -116,3 +116,18 @@ def test_chunked_host_pipeline(abi, h, oracle):
     with pytest.raises(TieError) as ei:
         abi.fit(h, x)
     assert ei.value.code == 1 and "item 290000" in str(ei.value)
+
+
+def test_device_fit_ops_for_sharded_fit(tie, mc, oracle):
+    """dist.DeviceFitOps (the per-rank op of dist.ShardedFit) on the GPU vs the reference"""
+    import torch
+
+    from paper_2604_00499_b200.dist import FIT_FIELDS, DeviceFitOps, ShardedFit
+
+    x, _, _ = oracle.gen_fit_data(5000, 16, seed=8)
+    local, glob = ShardedFit(DeviceFitOps(mc), gather="all")(torch.from_numpy(x).cuda(), 5000)
+    got = {f: local[f].cpu().numpy() for f in FIT_FIELDS}
+    got["converged"] = got["converged"].astype(bool)
+    got["degenerate"] = got["degenerate"].astype(bool)
+    _compare(got, oracle.fit(x), "device-fit-ops")
+    assert glob is local  # one rank: the gathered result is the local one
