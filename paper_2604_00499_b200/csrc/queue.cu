@@ -410,6 +410,81 @@ __global__ void __launch_bounds__(kRekeyThreads) rekey_pop_seq_kernel(
 // per block).  *skip != 0 (an invalid prediction in the same fused step): pop nothing.
 constexpr int kTopB = 32;            // pops per launch
 constexpr int kCandCap = 2048;       // candidates held in shared memory
+// The `pops` smallest live entries of <= 8 chosen blocks, for a 1024-thread CTA: each thread
+// holds its <= 8 slots (slot threadIdx.x of chosen block u) sorted in registers, and `pops`
+// CTA argmin rounds over the threads' heads pop them in order; then the blocks are refreshed.
+// Used when the queue has fewer live blocks than pops (all their entries compete, which
+// would overflow the general path's candidate list).
+__device__ __forceinline__ void pop_from_blocks_regs(const QDev& q, const uint32_t* chosen,
+                                                  uint32_t nchosen, uint64_t n_slots,
+                                                  uint32_t pops, uint64_t* out_id,
+                                                  uint32_t* out_slot, uint32_t* out_n,
+                                                  uint64_t* out_key, uint64_t* sk,
+                                                  uint64_t* si, uint32_t* ss) {
+  constexpr int kF = 8;
+  uint64_t fk[kF], fi[kF];
+  uint32_t fs[kF];
+#pragma unroll
+  for (int u = 0; u < kF; ++u) {
+    const uint64_t slot =
+        u < (int)nchosen ? (uint64_t)chosen[u] * kBlockSlots + threadIdx.x : n_slots;
+    fk[u] = slot < n_slots ? q.key[slot] : kDead;
+    fi[u] = slot < n_slots ? q.id[slot] : kDead;
+    fs[u] = (uint32_t)slot;
+  }
+#pragma unroll
+  for (int a = 1; a < kF; ++a)  // insertion sort, unrolled (compile-time indices)
+#pragma unroll
+    for (int b = a; b > 0; --b)
+      if (less_kv(fk[b], fi[b], fk[b - 1], fi[b - 1])) {
+        const uint64_t tk = fk[b], ti = fi[b];
+        const uint32_t ts = fs[b];
+        fk[b] = fk[b - 1];
+        fi[b] = fi[b - 1];
+        fs[b] = fs[b - 1];
+        fk[b - 1] = tk;
+        fi[b - 1] = ti;
+        fs[b - 1] = ts;
+      }
+  uint32_t done = 0;
+  for (; done < pops; ++done) {
+    uint64_t k = fk[0], i = fi[0];
+    uint32_t s = fs[0];
+    block_argmin(k, i, s, sk, si, ss);
+    if (k == kDead) break;
+    if (threadIdx.x == 0) {
+      out_id[done] = i;
+      out_slot[done] = s;
+      if (out_key) out_key[done] = k;
+      q.key[s] = kDead;
+    }
+    if (fk[0] != kDead && fs[0] == s) {  // the winner advances to its next entry
+#pragma unroll
+      for (int u = 0; u + 1 < kF; ++u) {
+        fk[u] = fk[u + 1];
+        fi[u] = fi[u + 1];
+        fs[u] = fs[u + 1];
+      }
+      fk[kF - 1] = kDead;
+      fi[kF - 1] = kDead;
+    }
+  }
+  if (threadIdx.x == 0) *out_n = done;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t e = warp; e < nchosen; e += blockDim.x >> 5) {
+    const uint32_t blk = chosen[e];
+    uint64_t k, i;
+    uint32_t s;
+    warp_block_min(q, blk, n_slots, lane, k, i, s);
+    if (lane == 0) {
+      q.bkey[blk] = k;
+      q.bid[blk] = i;
+      q.bslot[blk] = s;
+    }
+  }
+}
+
 __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64_t n_slots,
                                          uint32_t pops, uint64_t* out_id, uint32_t* out_slot,
                                          uint32_t* out_n, uint64_t* out_key = nullptr) {
@@ -460,6 +535,12 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
   }
   if (nchosen == 0) {
     if (threadIdx.x == 0) *out_n = 0;
+    return;
+  }
+  if (nchosen < pops && nchosen <= 8 && blockDim.x == 1024) {
+    // every live block is chosen (a small queue): select among all their entries directly
+    pop_from_blocks_regs(q, chosen, nchosen, n_slots, pops, out_id, out_slot, out_n, out_key,
+                         sk, si, ss);
     return;
   }
   if (nchosen < pops) {  // every live block is chosen: all their live entries are candidates
