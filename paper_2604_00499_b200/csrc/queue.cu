@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(256) rekey_refresh_kernel(QDev q, uint32_t nb,
 // kills it and refreshes its block at the end.  A failed fused step (err set) skips all.
 struct SegBetas {
   double b[32];
+  int eager;  // A/B: store keys and block minima in every segment
 };
 constexpr int kRekeyThreads = 256;
 
@@ -318,6 +319,9 @@ __global__ void __launch_bounds__(kRekeyThreads) rekey_pop_seq_kernel(
   uint64_t killed = ~0ull;
   for (uint32_t g = 0; g < nseg; ++g) {
     const double beta = betas.b[g];
+    // keys and block minima are stored by the last segment only (earlier passes keep them in
+    // registers; a popped slot's death is stored at once)
+    const bool last = g + 1 == nseg || betas.eager;
     uint64_t ck = kDead, ci = kDead;
     uint32_t cs = 0;
     for (uint32_t b = blockIdx.x; b < nb; b += G) {
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(kRekeyThreads) rekey_pop_seq_kernel(
           q.key[slot] = kDead;
         } else if (kk[u] != kDead && pr[u]) {
           kk[u] = order_bits(__dadd_rn(ee[u], __dmul_rn(beta, cc[u])));
-          q.key[slot] = kk[u];
+          if (last) q.key[slot] = kk[u];
         }
         if (less_kv(kk[u], ii[u], k, i)) {
           k = kk[u];
@@ -354,7 +358,7 @@ __global__ void __launch_bounds__(kRekeyThreads) rekey_pop_seq_kernel(
         }
       }
       block_argmin(k, i, s, sk, si, ss);
-      if (threadIdx.x == 0) {
+      if (last && threadIdx.x == 0) {
         q.bkey[b] = k;
         q.bid[b] = i;
         q.bslot[b] = s;
@@ -383,8 +387,13 @@ __global__ void __launch_bounds__(kRekeyThreads) rekey_pop_seq_kernel(
       }
     }
     block_argmin(k, i, s, sk, si, ss);
-    if (k == kDead) {  // the queue ran dry (same decision in every CTA)
+    if (k == kDead) {  // the queue ran dry (same decision in every CTA): every block is empty
       if (blockIdx.x == 0 && threadIdx.x == 0) out_n[g] = 0;
+      if (threadIdx.x == 0)
+        for (uint32_t b = blockIdx.x; b < nb; b += G) {
+          q.bkey[b] = kDead;
+          q.bid[b] = kDead;
+        }
       killed = ~0ull;
       break;
     }
@@ -1003,6 +1012,8 @@ uint64_t launch_plan(tie_queue* Q, const std::vector<Seg>& plan, size_t first_se
     if (e - g >= 2 && rekey_ctas > 0 && nb > 0) {
       tie::dev::SegBetas sb{};
       for (size_t j = g; j < e; ++j) sb.b[j - g] = plan[j].beta;
+      static const int eager = getenv("TIE_REKEY_EAGER") ? 1 : 0;
+      sb.eager = eager;
       QDevArgs a{Q->q, nb, Q->n_slots, sb, (uint32_t)(e - g), Q->d_out_id + off,
                  Q->d_out_slot + off, Q->d_out_n + g, Q->d_cmin, err};
       const uint32_t grid = std::min<uint32_t>(nb, (uint32_t)rekey_ctas);
