@@ -392,7 +392,8 @@ def main():
 
     extras = {}
     if rank == 0 and not args.no_extras:
-        extras = run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream)
+        extras = run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream,
+                        (fit_xp, fit_hb))
         # second half of the metric: p50 schedule-step latency vs queue size (bench_sched.py)
         try:
             import bench_sched
@@ -447,7 +448,7 @@ def main():
         dist.destroy_process_group()
 
 
-def run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream):
+def run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream, fit_bufs):
     """Secondary numbers on rank 0: exact-mode score+rank, and config-3 fits/s."""
     out = {}
     sh = stream.cuda_stream
@@ -492,9 +493,8 @@ def run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream):
     fms = a.elapsed_time(b) / reps
     iters = fit_it.cpu().numpy()
     # e2e fits through the C-ABI host call (pinned)
-    xp = fit_xp
+    xp, hb = fit_bufs  # pinned up front (see main)
     xp.copy_(torch.from_numpy(x))
-    hb = fit_hb
     fit_host = lambda: tie.fit_host_ptr(ctx, xp.data_ptr(), P, K, 3.5,
                                         *[t.data_ptr() for t in hb])
     fit_host()  # first call allocates the staging buffers
