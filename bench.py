@@ -36,7 +36,7 @@ N_CONFIG2 = 1_000_000
 ALPHA = 0.9
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0
-TRAFFIC_FILE = "ncu_traffic_r01l.json"
+TRAFFIC_FILE = "ncu_traffic_r01n.json"
 
 
 def parse():
@@ -392,8 +392,11 @@ def main():
 
     extras = {}
     if rank == 0 and not args.no_extras:
-        extras = run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream,
-                        (fit_xp, fit_hb))
+        try:  # the extras never block the headline line
+            extras = run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta,
+                                stream, (fit_xp, fit_hb))
+        except Exception as exc:  # noqa: BLE001
+            extras = {"extras_error": repr(exc)}
         # second half of the metric: p50 schedule-step latency vs queue size (bench_sched.py)
         try:
             import bench_sched

@@ -494,6 +494,10 @@ __device__ __forceinline__ void pop_from_blocks_regs(const QDev& q, const uint32
   }
 }
 
+// kSmallPath: include the register path for queues with fewer live blocks than pops (kept
+// out of the fused apply kernel, whose instruction footprint it would grow: the host sends
+// small queues' pops to pop_topb_kernel instead)
+template <bool kSmallPath>
 __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64_t n_slots,
                                          uint32_t pops, uint64_t* out_id, uint32_t* out_slot,
                                          uint32_t* out_n, uint64_t* out_key = nullptr) {
@@ -546,7 +550,7 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
     if (threadIdx.x == 0) *out_n = 0;
     return;
   }
-  if (nchosen < pops && nchosen <= 8 && blockDim.x == 1024) {
+  if (kSmallPath && nchosen < pops && nchosen <= 8 && blockDim.x == 1024) {
     // every live block is chosen (a small queue): select among all their entries directly
     pop_from_blocks_regs(q, chosen, nchosen, n_slots, pops, out_id, out_slot, out_n, out_key,
                          sk, si, ss);
@@ -667,8 +671,13 @@ __global__ void __launch_bounds__(1024) pop_topb_kernel(QDev q, uint32_t nblocks
                                                         uint64_t n_slots, uint32_t pops,
                                                         uint64_t* out_id, uint32_t* out_slot,
                                                         uint32_t* out_n,
-                                                        uint64_t* out_key = nullptr) {
-  pop_topb(q, nblocks, n_slots, pops, out_id, out_slot, out_n, out_key);
+                                                        uint64_t* out_key = nullptr,
+                                                        const unsigned long long* err = nullptr) {
+  __shared__ int skip;
+  if (threadIdx.x == 0) skip = err && *(const volatile unsigned long long*)err != ~0ull;
+  __syncthreads();
+  if (skip) return;  // a failed fused step pops nothing
+  pop_topb<true>(q, nblocks, n_slots, pops, out_id, out_slot, out_n, out_key);
 }
 
 // undo a peek's pops (one CTA): restore the popped slots' keys, then refresh their blocks
@@ -753,7 +762,7 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
   if (skip || pops == 0) {
     if (threadIdx.x == 0) *out_n = 0;
   } else {
-    pop_topb(q, nblocks, n_slots, pops, out_id, out_slot, out_n);
+    pop_topb<false>(q, nblocks, n_slots, pops, out_id, out_slot, out_n);
   }
   if (status_seq) {  // the step's last kernel: publish the completion record (step_finish)
     __syncthreads();
@@ -976,6 +985,10 @@ void apply_pops(tie_queue* Q, uint32_t off, uint32_t cnt, std::vector<uint64_t>&
 
 // launch a plan's kernels: segment g = [rebuild][pops -> d_out_*[off..], d_out_n[g]]; a set
 // error word (a failed fused step) makes every kernel skip
+// pops of a queue this small may come from fewer live blocks than pops: they go through
+// pop_topb_kernel (which has the register path for that case), not the fused apply kernel
+bool small_queue(const tie_queue* Q) { return Q->size < 8 * (uint64_t)tie::dev::kBlockSlots; }
+
 // cooperative launch arguments (addresses handed to cudaLaunchCooperativeKernel)
 struct QDevArgs {
   tie::dev::QDev q;
@@ -1029,9 +1042,15 @@ uint64_t launch_plan(tie_queue* Q, const std::vector<Seg>& plan, size_t first_se
       cudaGetLastError();  // not launchable here (e.g. co-residency): per-segment kernels
     }
     if (plan[g].rebuild) rebuild_launch(Q, plan[g].beta, s, err);
-    tie::dev::step_apply_kernel<<<1, 1024, 0, s>>>(
-        Q->q, 0, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0.0, nullptr, 0, 0, nb,
-        Q->n_slots, plan[g].pops, Q->d_out_id + off, Q->d_out_slot + off, Q->d_out_n + g, err);
+    if (small_queue(Q))
+      tie::dev::pop_topb_kernel<<<1, 1024, 0, s>>>(Q->q, nb, Q->n_slots, plan[g].pops,
+                                                   Q->d_out_id + off, Q->d_out_slot + off,
+                                                   Q->d_out_n + g, nullptr, err);
+    else
+      tie::dev::step_apply_kernel<<<1, 1024, 0, s>>>(
+          Q->q, 0, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0.0, nullptr, 0, 0, nb,
+          Q->n_slots, plan[g].pops, Q->d_out_id + off, Q->d_out_slot + off, Q->d_out_n + g,
+          err);
     off += plan[g].pops;
     tie::capi::count_launch(1);
     ++g;
@@ -1370,7 +1389,7 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
   uint64_t planned = 0;
   for (const Seg& g : plan) planned += g.pops;
   // segment 0's pops ride in the apply kernel unless a rebuild must precede them
-  const bool seg0_fused = !plan.empty() && !plan[0].rebuild;
+  const bool seg0_fused = !plan.empty() && !plan[0].rebuild && !small_queue(Q);
   const uint32_t fused_pops = seg0_fused ? plan[0].pops : 0;
   // ---- pack: [arr ids | arr keys | mu | sigma | E | C | key | pred slots | pred max_tokens |
   //            blocks]  (E, C, key: device-only scratch)
