@@ -563,7 +563,9 @@ __device__ __forceinline__ uint32_t scan_block_excl(uint32_t v, uint32_t* sh) {
   return r;
 }
 
-template <int kT>
+// kTrail = false: no trailing barrier protecting `sh` -- for callers whose next use of `sh`
+// (and of whatever they read before the scan) is separated from this one by other barriers
+template <int kT, bool kTrail = true>
 __device__ __forceinline__ uint32_t block_excl_scan_t(uint32_t v, uint32_t* sh) {
   constexpr int kW = kT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -586,7 +588,7 @@ __device__ __forceinline__ uint32_t block_excl_scan_t(uint32_t v, uint32_t* sh) 
   }
   __syncthreads();
   const uint32_t r = x - v + (warp ? sh[warp - 1] : 0u);
-  __syncthreads();
+  if (kTrail) __syncthreads();
   return r;
 }
 
@@ -1039,8 +1041,9 @@ __device__ __forceinline__ void sort_partition(const Part& q, uint32_t s0, uint3
       c[u] = j < nf ? fc[j] : 0u;
       t += c[u];
     }
-    uint32_t v = block_excl_scan_t<kT>(t, sh);
-    __syncthreads();
+    // every thread read its counts before the scan's first barrier, and the next use of sh
+    // is a partition away: no barriers around the scan beyond its own two
+    uint32_t v = block_excl_scan_t<kT, false>(t, sh);
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const uint32_t j = threadIdx.x * kPer + u;
