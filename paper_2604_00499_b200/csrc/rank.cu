@@ -563,9 +563,7 @@ __device__ __forceinline__ uint32_t scan_block_excl(uint32_t v, uint32_t* sh) {
   return r;
 }
 
-// kTrail = false: no trailing barrier protecting `sh` -- for callers whose next use of `sh`
-// (and of whatever they read before the scan) is separated from this one by other barriers
-template <int kT, bool kTrail = true>
+template <int kT>
 __device__ __forceinline__ uint32_t block_excl_scan_t(uint32_t v, uint32_t* sh) {
   constexpr int kW = kT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -588,7 +586,7 @@ __device__ __forceinline__ uint32_t block_excl_scan_t(uint32_t v, uint32_t* sh) 
   }
   __syncthreads();
   const uint32_t r = x - v + (warp ? sh[warp - 1] : 0u);
-  if (kTrail) __syncthreads();
+  __syncthreads();
   return r;
 }
 
@@ -974,13 +972,6 @@ __global__ void __launch_bounds__(kScatThreads) part_scatter_tiled_kernel(Part q
 // Sort partition p's m keys (already grouped at tk/tv[s0..s0+m)) and write its slice of the
 // dispatch order: fine-bucket counting sort in shared memory, each key ranked inside its fine
 // bucket (~1-2 keys) by (key, index), values placed in order, written out coalesced.
-// sort_partition's fine-bucket counters in the dynamic shared memory (prefetching callers
-// zero them once before their first partition; each call re-zeroes them for the next)
-__device__ __forceinline__ uint32_t* sort_fc(unsigned char* smem_raw) {
-  return reinterpret_cast<uint32_t*>(smem_raw + (size_t)kPartCap * (8 + 4 + 2 + 2)) +
-         (1u << kPartMaxFineLog2) + 1;
-}
-
 // kPF > 0: the first kPF x kT keys / values arrive prefetched in pk / pv, and once they are
 // in shared memory the next partition's [ns0, ns0 + nm) first kPF x kT are loaded into pk /
 // pv, so that load's latency overlaps this partition's ranking.
@@ -999,10 +990,8 @@ __device__ __forceinline__ void sort_partition(const Part& q, uint32_t s0, uint3
   uint32_t* fc = fb + (1u << kPartMaxFineLog2) + 1;              // [nf] counts / cursors
   __shared__ uint32_t sh[32];
   const uint32_t nf = 1u << q.fine_log2, fmask = nf - 1u;
-  if (kPF == 0) {  // prefetching callers keep fc zeroed between partitions (see below)
-    for (uint32_t j = threadIdx.x; j < nf; j += kT) fc[j] = 0;
-    __syncthreads();
-  }
+  for (uint32_t j = threadIdx.x; j < nf; j += kT) fc[j] = 0;
+  __syncthreads();
   const KeyRange r = key_range(q.mm, q.total_bits);
   if (kPF > 0) {
 #pragma unroll
@@ -1041,9 +1030,8 @@ __device__ __forceinline__ void sort_partition(const Part& q, uint32_t s0, uint3
       c[u] = j < nf ? fc[j] : 0u;
       t += c[u];
     }
-    // every thread read its counts before the scan's first barrier, and the next use of sh
-    // is a partition away: no barriers around the scan beyond its own two
-    uint32_t v = block_excl_scan_t<kT, false>(t, sh);
+    uint32_t v = block_excl_scan_t<kT>(t, sh);
+    __syncthreads();
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const uint32_t j = threadIdx.x * kPer + u;
@@ -1058,8 +1046,6 @@ __device__ __forceinline__ void sort_partition(const Part& q, uint32_t s0, uint3
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < m; j += kT) perm[atomicAdd(&fc[sf[j]], 1u)] = (uint16_t)j;
   __syncthreads();
-  if (kPF > 0)  // the cursors are spent: zero them for the next partition (barriers follow)
-    for (uint32_t j = threadIdx.x; j < nf; j += kT) fc[j] = 0;
   uint16_t* spos = sf;  // a key's final position in the partition replaces its fine bucket
   for (uint32_t j = threadIdx.x; j < m; j += kT) {
     const uint64_t k = sk[j];
@@ -1229,11 +1215,6 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
       q.tv[pos] = (uint32_t)(lo + j);
     }
   }
-  __syncthreads();  // the scatter's staging reads are done: the counters may reuse the space
-  {
-    uint32_t* fc = sort_fc(smem_raw);
-    for (uint32_t j = threadIdx.x; j < (1u << q.fine_log2); j += kFusedThreads) fc[j] = 0;
-  }
   grid.sync();
   // the CTA's partitions in turn, each one's head prefetched while the previous one is ranked
   constexpr int kPF = 2;
@@ -1367,11 +1348,6 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_l2_kernel(
   Part q2 = q;
   q2.tk = q.tk2;
   q2.tv = q.tv2;
-  {
-    uint32_t* fc = sort_fc(smem_raw);
-    for (uint32_t j = threadIdx.x; j < (1u << q.fine_log2); j += kFusedThreads) fc[j] = 0;
-  }
-  __syncthreads();
   // the sub-partitions in turn, each one's head prefetched while the previous one is ranked
   constexpr int kPF = 2;
   uint64_t pk[kPF];

@@ -1,0 +1,6 @@
+# Same-box A/B of the in-tree build against a second build under _ab_old/ (development tool:
+# copy the package to _ab_old/, put the variant's sources in, make there, copy tools/kernel_ab.py)
+for i in 1 2 3; do
+  echo "new"; timeout 300 python tools/kernel_ab.py 2>&1 | grep score_rank_us_median
+  echo "old"; timeout 300 python _ab_old/tools/kernel_ab.py 2>&1 | grep score_rank_us_median
+done
