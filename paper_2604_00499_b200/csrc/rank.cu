@@ -972,16 +972,11 @@ __global__ void __launch_bounds__(kScatThreads) part_scatter_tiled_kernel(Part q
 // Sort partition p's m keys (already grouped at tk/tv[s0..s0+m)) and write its slice of the
 // dispatch order: fine-bucket counting sort in shared memory, each key ranked inside its fine
 // bucket (~1-2 keys) by (key, index), values placed in order, written out coalesced.
-// kPF > 0: the first kPF x kT keys / values arrive prefetched in pk / pv, and once they are
-// in shared memory the next partition's [ns0, ns0 + nm) first kPF x kT are loaded into pk /
-// pv, so that load's latency overlaps this partition's ranking.
-template <int kT, int kPF = 0>
+template <int kT>
 __device__ __forceinline__ void sort_partition(const Part& q, uint32_t s0, uint32_t m,
                                                const uint64_t* __restrict__ ids,
                                                uint64_t* __restrict__ order,
-                                               unsigned char* smem_raw,
-                                               uint64_t* pk = nullptr, uint32_t* pv = nullptr,
-                                               uint32_t ns0 = 0, uint32_t nm = 0) {
+                                               unsigned char* smem_raw) {
   uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
   uint32_t* sv = reinterpret_cast<uint32_t*>(sk + kPartCap);
   uint16_t* sf = reinterpret_cast<uint16_t*>(sv + kPartCap);    // fine bucket of key j
@@ -993,26 +988,7 @@ __device__ __forceinline__ void sort_partition(const Part& q, uint32_t s0, uint3
   for (uint32_t j = threadIdx.x; j < nf; j += kT) fc[j] = 0;
   __syncthreads();
   const KeyRange r = key_range(q.mm, q.total_bits);
-  if (kPF > 0) {
-#pragma unroll
-    for (int u = 0; u < (kPF > 0 ? kPF : 1); ++u) {
-      const uint32_t j = threadIdx.x + u * kT;
-      if (j < m) {
-        sk[j] = pk[u];
-        sv[j] = pv[u];
-        const uint32_t fine = part_bucket(q, r, pk[u]) & fmask;
-        sf[j] = (uint16_t)fine;
-        atomicAdd(&fc[fine], 1u);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < (kPF > 0 ? kPF : 1); ++u) {  // the next partition's head, in flight
-      const uint32_t j = threadIdx.x + u * kT;
-      pk[u] = j < nm ? q.tk[ns0 + j] : 0ull;
-      pv[u] = j < nm ? q.tv[ns0 + j] : 0u;
-    }
-  }
-  for (uint32_t j = threadIdx.x + kPF * kT; j < m; j += kT) {
+  for (uint32_t j = threadIdx.x; j < m; j += kT) {
     const uint64_t k = q.tk[s0 + j];
     sk[j] = k;
     sv[j] = q.tv[s0 + j];
@@ -1216,32 +1192,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
     }
   }
   grid.sync();
-  // the CTA's partitions in turn, each one's head prefetched while the previous one is ranked
-  constexpr int kPF = 2;
-  uint64_t pk[kPF];
-  uint32_t pv[kPF];
-  uint32_t p = blockIdx.x;
-#pragma unroll
-  for (int u = 0; u < kPF; ++u) {
-    const uint32_t j = threadIdx.x + u * kFusedThreads;
-    const bool in = p < P && j < pb[p + 1] - pb[p];
-    pk[u] = in ? q.tk[pb[p] + j] : 0ull;
-    pv[u] = in ? q.tv[pb[p] + j] : 0u;
-  }
-  for (; p < P; p += gridDim.x) {
+  for (uint32_t p = blockIdx.x; p < P; p += gridDim.x) {
     const uint32_t s0 = pb[p], m = pb[p + 1] - s0;
-    const uint32_t np = p + gridDim.x;
-    const uint32_t ns0 = np < P ? pb[np] : 0u, nm = np < P ? pb[np + 1] - pb[np] : 0u;
-    if (m) {
-      sort_partition<kFusedThreads, kPF>(q, s0, m, ids, order, smem_raw, pk, pv, ns0, nm);
-    } else {
-#pragma unroll
-      for (int u = 0; u < kPF; ++u) {  // nothing to sort: load the next head directly
-        const uint32_t j = threadIdx.x + u * kFusedThreads;
-        pk[u] = j < nm ? q.tk[ns0 + j] : 0ull;
-        pv[u] = j < nm ? q.tv[ns0 + j] : 0u;
-      }
-    }
+    if (m) sort_partition<kFusedThreads>(q, s0, m, ids, order, smem_raw);
     __syncthreads();
   }
 }
@@ -1284,19 +1237,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_l2_kernel(
   for (uint32_t j = threadIdx.x; j < P2; j += kFusedThreads) cur[j] = 0;
   if (threadIdx.x == 0) big = 0;
   __syncthreads();
-  constexpr int kLd = 8;  // loads in flight per thread before the first use
-  for (uint32_t j0 = threadIdx.x; j0 < m1; j0 += kLd * kFusedThreads) {
-    uint64_t kk[kLd];
-#pragma unroll
-    for (int u = 0; u < kLd; ++u) {
-      const uint32_t j = j0 + u * kFusedThreads;
-      kk[u] = j < m1 ? q.tk[s0 + j] : 0ull;
-    }
-#pragma unroll
-    for (int u = 0; u < kLd; ++u)
-      if (j0 + u * kFusedThreads < m1)
-        atomicAdd(&cur[(part_bucket(q, r, kk[u]) >> q.fine_log2) & mask2], 1u);
-  }
+  for (uint32_t j = threadIdx.x; j < m1; j += kFusedThreads)
+    atomicAdd(&cur[(part_bucket(q, r, q.tk[s0 + j]) >> q.fine_log2) & mask2], 1u);
   __syncthreads();
   {
     constexpr int kPer = kL2MaxP / kFusedThreads;
@@ -1325,51 +1267,20 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_l2_kernel(
     if (threadIdx.x == 0) atomicExch(q.overflow, 1);
     return;
   }
-  for (uint32_t j0 = threadIdx.x; j0 < m1; j0 += kLd * kFusedThreads) {
-    uint64_t kk[kLd];
-    uint32_t vv[kLd];
-#pragma unroll
-    for (int u = 0; u < kLd; ++u) {
-      const uint32_t j = j0 + u * kFusedThreads;
-      kk[u] = j < m1 ? q.tk[s0 + j] : 0ull;
-      vv[u] = j < m1 ? q.tv[s0 + j] : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < kLd; ++u) {
-      if (j0 + u * kFusedThreads < m1) {
-        const uint32_t pos =
-            atomicAdd(&cur[(part_bucket(q, r, kk[u]) >> q.fine_log2) & mask2], 1u);
-        q.tk2[s0 + pos] = kk[u];
-        q.tv2[s0 + pos] = vv[u];
-      }
-    }
+  for (uint32_t j = threadIdx.x; j < m1; j += kFusedThreads) {
+    const uint64_t k = q.tk[s0 + j];
+    const uint32_t pos = atomicAdd(&cur[(part_bucket(q, r, k) >> q.fine_log2) & mask2], 1u);
+    q.tk2[s0 + pos] = k;
+    q.tv2[s0 + pos] = q.tv[s0 + j];
   }
   __syncthreads();  // this CTA's global writes are visible to it after the barrier
   Part q2 = q;
   q2.tk = q.tk2;
   q2.tv = q.tv2;
-  // the sub-partitions in turn, each one's head prefetched while the previous one is ranked
-  constexpr int kPF = 2;
-  uint64_t pk[kPF];
-  uint32_t pv[kPF];
-  uint32_t b = 0;
-  while (b < P2 && sb[b + 1] == sb[b]) ++b;
-#pragma unroll
-  for (int u = 0; u < kPF; ++u) {
-    const uint32_t j = threadIdx.x + u * kFusedThreads;
-    const bool in = b < P2 && j < sb[b + 1] - sb[b];
-    pk[u] = in ? q2.tk[s0 + sb[b] + j] : 0ull;
-    pv[u] = in ? q2.tv[s0 + sb[b] + j] : 0u;
-  }
-  while (b < P2) {
-    uint32_t nb = b + 1;
-    while (nb < P2 && sb[nb + 1] == sb[nb]) ++nb;
+  for (uint32_t b = 0; b < P2; ++b) {
     const uint32_t m = sb[b + 1] - sb[b];
-    const uint32_t nm = nb < P2 ? sb[nb + 1] - sb[nb] : 0u;
-    sort_partition<kFusedThreads, kPF>(q2, s0 + sb[b], m, ids, order, smem_raw, pk, pv,
-                                       nb < P2 ? s0 + sb[nb] : 0u, nm);
+    if (m) sort_partition<kFusedThreads>(q2, s0 + sb[b], m, ids, order, smem_raw);
     __syncthreads();
-    b = nb;
   }
 }
 
