@@ -36,7 +36,7 @@ N_CONFIG2 = 1_000_000
 ALPHA = 0.9
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0
-TRAFFIC_FILE = "ncu_traffic_r01o.json"
+TRAFFIC_FILE = "ncu_traffic_r01p.json"
 
 
 def parse():
