@@ -473,12 +473,16 @@ PYBIND11_MODULE(_core, m) {
       .def("on_arrival_batch",
            [](GpuQueue& g, carray<uint64_t> ids, carray<double> arrival_s,
               carray<uint32_t> max_tokens) {
+             if (arrival_s.size() != ids.size() || max_tokens.size() != ids.size())
+               throw py::value_error("on_arrival_batch: array lengths differ");
              throw_code(tie_queue_arrive(g.q, ids.data(), arrival_s.data(), max_tokens.data(),
                                          (uint64_t)ids.size()));
            },
            py::arg("ids"), py::arg("arrival_s"), py::arg("max_tokens"))
       .def("on_prediction_batch",
            [](GpuQueue& g, carray<uint64_t> ids, carray<double> E, carray<double> C) {
+             if (E.size() != ids.size() || C.size() != ids.size())
+               throw py::value_error("on_prediction_batch: array lengths differ");
              throw_code(tie_queue_predict(g.q, ids.data(), E.data(), C.data(),
                                           (uint64_t)ids.size()));
            },
@@ -486,6 +490,9 @@ PYBIND11_MODULE(_core, m) {
       .def("on_prediction_logt",
            [](GpuQueue& g, carray<uint64_t> ids, carray<double> mu, carray<double> sigma,
               carray<uint32_t> max_tokens) {
+             if (mu.size() != ids.size() || sigma.size() != ids.size() ||
+                 max_tokens.size() != ids.size())
+               throw py::value_error("on_prediction_logt: array lengths differ");
              throw_code(tie_queue_predict_logt(g.q, ids.data(), mu.data(), sigma.data(),
                                                max_tokens.data(), (uint64_t)ids.size()));
            },

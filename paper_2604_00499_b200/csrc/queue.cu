@@ -842,6 +842,91 @@ double beta_at(const tie_queue* Q, uint64_t queue_len) {
   return b;
 }
 
+// the beta of Scheduler::on_prediction (sched.cpp:139): SEPT 0, TIE compute_beta -- which
+// throws std::domain_error on an invalid ScoreConfig (sched.cpp:10-15), reported here
+int prediction_beta(const tie_queue* Q, double* beta) {
+  *beta = 0.0;
+  if (Q->policy != 2) return TIE_OK;
+  return tie_compute_beta(Q->adaptive, Q->beta_fixed, Q->beta_max, Q->q_sat,
+                          Q->size + Q->peers, beta);
+}
+
+// index of the first element of ids[0..m) whose id occurred earlier in the batch (m if none)
+uint64_t first_batch_duplicate(const uint64_t* ids, uint64_t m) {
+  std::vector<std::pair<uint64_t, uint64_t>> srt(m);
+  for (uint64_t t = 0; t < m; ++t) srt[t] = {ids[t], t};
+  std::sort(srt.begin(), srt.end());
+  uint64_t first = m;
+  for (uint64_t t = 1; t < m; ++t)
+    if (srt[t].first == srt[t - 1].first) first = std::min(first, srt[t].second);
+  return first;
+}
+
+// Scheduler::on_arrival x m validation (sched.cpp:125-132 -> WaitingQueue::push, 59-63): the
+// error of the first failing request, as the reference's per-item loop raises it; fills the
+// keys.  Changes nothing.
+int check_arrivals(const tie_queue* Q, const uint64_t* ids, const double* arrival_s,
+                   const uint32_t* max_tokens, uint64_t m, std::vector<double>& keys) {
+  if (Q->n_slots + m > Q->capacity)
+    return set_error(TIE_EINVALID, "tie_queue_arrive: capacity exceeded");
+  keys.resize(m);
+  const uint64_t dup = first_batch_duplicate(ids, m);
+  for (uint64_t t = 0; t < m; ++t) {
+    keys[t] = Q->policy == 0 ? arrival_s[t] : (double)max_tokens[t];
+    if (!std::isfinite(keys[t]))
+      return set_error(TIE_EDOMAIN, "WaitingQueue::push: key must be finite");
+    if (t == dup || Q->slot_of.count(ids[t]))
+      return set_error(TIE_EINVALID, "WaitingQueue::push: id " + std::to_string(ids[t]) +
+                                         " already queued");
+  }
+  return TIE_OK;
+}
+
+// Scheduler::on_prediction x m validation up to the compute_score checks (sched.cpp:134-145):
+// "not waiting", the policy's beta, "already predicted" (also for an id repeated inside the
+// batch) -- the first failing request's error.  `pending` (may be null) holds ids of arrivals
+// of the same step, not yet in slot_of, at slots first_pending + index.  Fills the slots and
+// beta.  Changes nothing.
+int check_predictions(const tie_queue* Q, const uint64_t* ids, uint64_t m,
+                      const uint64_t* pending, uint64_t n_pending, uint64_t first_pending,
+                      std::vector<uint32_t>& slots, double* beta, const double* E = nullptr,
+                      const double* C = nullptr) {
+  slots.resize(m);
+  std::unordered_map<uint64_t, uint32_t> pend;
+  for (uint64_t t = 0; t < n_pending; ++t) pend.emplace(pending[t], (uint32_t)(first_pending + t));
+  const uint64_t dup = Q->policy == 0 ? m : first_batch_duplicate(ids, m);
+  *beta = 0.0;
+  bool have_beta = false;
+  for (uint64_t t = 0; t < m; ++t) {
+    auto it = Q->slot_of.find(ids[t]);
+    if (it != Q->slot_of.end()) {
+      slots[t] = it->second;
+    } else if (auto p = pend.find(ids[t]); p != pend.end()) {
+      slots[t] = p->second;
+    } else {
+      return set_error(TIE_EINVALID, "Scheduler::on_prediction: id " + std::to_string(ids[t]) +
+                                         " not waiting");
+    }
+    if (Q->policy == 0) continue;  // FCFS: arrival order is the schedule (sched.cpp:138)
+    if (!have_beta) {  // the first waiting prediction evaluates compute_beta
+      if (int rc = prediction_beta(Q, beta)) return rc;
+      have_beta = true;
+    }
+    if (t == dup || Q->predicted[slots[t]])
+      return set_error(TIE_EINVALID, "Scheduler::on_prediction: id " + std::to_string(ids[t]) +
+                                         " already predicted");
+    if (!E) continue;  // (E, CVaR) computed on the device: checked there
+    const double e = E[t], c = C[t];  // compute_score checks (sched.cpp:19-26)
+    if (!std::isfinite(e) || !std::isfinite(c) || !std::isfinite(*beta))
+      return set_error(TIE_EDOMAIN, "compute_score: arguments must be finite");
+    if (!(e > 0.0)) return set_error(TIE_EDOMAIN, "compute_score: expectation must be > 0");
+    if (c < e)
+      return set_error(TIE_EINVALID,
+                       "compute_score: cvar below expectation violates the invariant");
+  }
+  return TIE_OK;
+}
+
 int ensure_stage(tie_queue* Q, uint64_t m) {
   if (m <= Q->stage_cap) return TIE_OK;
   cudaFree(Q->d_ids); cudaFree(Q->d_a); cudaFree(Q->d_b); cudaFree(Q->d_c);
@@ -1165,22 +1250,11 @@ int tie_queue_arrive(tie_queue* Q, const uint64_t* ids, const double* arrival_s,
                      const uint32_t* max_tokens, uint64_t m) {
   if (!Q) return set_error(TIE_EINVALID, "tie_queue: null queue");
   if (m == 0) return TIE_OK;
-  if (Q->n_slots + m > Q->capacity)
-    return set_error(TIE_EINVALID, "tie_queue_arrive: capacity exceeded");
-  std::vector<double> keys(m);
-  for (uint64_t t = 0; t < m; ++t) {
-    keys[t] = Q->policy == 0 ? arrival_s[t] : (double)max_tokens[t];
-    if (!std::isfinite(keys[t]))
-      return set_error(TIE_EDOMAIN, "WaitingQueue::push: key must be finite");
-    if (Q->slot_of.count(ids[t]))
-      return set_error(TIE_EINVALID, "WaitingQueue::push: id " + std::to_string(ids[t]) +
-                                         " already queued");
-    Q->slot_of.emplace(ids[t], (uint32_t)(Q->n_slots + t));  // rejects in-batch duplicates next
-  }
-  if (Q->slot_of.size() != Q->size + m) {  // duplicate inside the batch
-    for (uint64_t t = 0; t < m; ++t) Q->slot_of.erase(ids[t]);
-    return set_error(TIE_EINVALID, "WaitingQueue::push: id already queued");
-  }
+  // validate the whole batch before any host state changes (a rejected batch leaves the
+  // queue untouched)
+  std::vector<double> keys;
+  if (int rc = check_arrivals(Q, ids, arrival_s, max_tokens, m, keys)) return rc;
+  for (uint64_t t = 0; t < m; ++t) Q->slot_of.emplace(ids[t], (uint32_t)(Q->n_slots + t));
   cudaStream_t s = Q->ctx->stream;
   if (int rc = ensure_stage(Q, m)) return rc;
   cudaMemcpyAsync(Q->d_ids, ids, 8 * m, cudaMemcpyHostToDevice, s);
@@ -1204,33 +1278,10 @@ int tie_queue_predict(tie_queue* Q, const uint64_t* ids, const double* E, const 
                       uint64_t m) {
   if (!Q) return set_error(TIE_EINVALID, "tie_queue: null queue");
   if (m == 0) return TIE_OK;
-  std::vector<uint32_t> slots(m);
-  for (uint64_t t = 0; t < m; ++t) {
-    auto it = Q->slot_of.find(ids[t]);
-    if (it == Q->slot_of.end())
-      return set_error(TIE_EINVALID, "Scheduler::on_prediction: id " + std::to_string(ids[t]) +
-                                         " not waiting");
-    slots[t] = it->second;
-  }
+  std::vector<uint32_t> slots;
+  double beta = 0.0;
+  if (int rc = check_predictions(Q, ids, m, nullptr, 0, 0, slots, &beta, E, C)) return rc;
   if (Q->policy == 0) return TIE_OK;  // FCFS: arrival order is the schedule
-  const double beta = Q->policy == 1 ? 0.0 : beta_at(Q, Q->size + Q->peers);
-  for (uint64_t t = 0; t < m; ++t) {
-    if (Q->predicted[slots[t]])
-      return set_error(TIE_EINVALID, "Scheduler::on_prediction: id " + std::to_string(ids[t]) +
-                                         " already predicted");
-    const double e = E[t], c = C[t];  // compute_score checks (sched.cpp:19-26)
-    if (!std::isfinite(e) || !std::isfinite(c) || !std::isfinite(beta))
-      return set_error(TIE_EDOMAIN, "compute_score: arguments must be finite");
-    if (!(e > 0.0)) return set_error(TIE_EDOMAIN, "compute_score: expectation must be > 0");
-    if (c < e)
-      return set_error(TIE_EINVALID,
-                       "compute_score: cvar below expectation violates the invariant");
-  }
-  for (uint64_t t = 0; t + 1 < m; ++t)  // duplicate ids inside one batch
-    for (uint64_t u = t + 1; u < m && u < t + 64; ++u)
-      if (slots[u] == slots[t])
-        return set_error(TIE_EINVALID, "Scheduler::on_prediction: id " + std::to_string(ids[t]) +
-                                           " already predicted");
   cudaStream_t s = Q->ctx->stream;
   if (int rc = ensure_stage(Q, m)) return rc;
   cudaMemcpyAsync(Q->d_slots, slots.data(), 4 * m, cudaMemcpyHostToDevice, s);
@@ -1307,25 +1358,27 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
   *n_out = 0;
   tie_ctx* ctx = Q->ctx;
   cudaStream_t s = ctx->stream;
-  // ---- arrivals: host validation (tie_queue_arrive)
-  if (Q->n_slots + n_arr > Q->capacity)
-    return set_error(TIE_EINVALID, "tie_queue_arrive: capacity exceeded");
-  std::vector<double> akeys(n_arr);
-  for (uint64_t t = 0; t < n_arr; ++t) {
-    akeys[t] = Q->policy == 0 ? arr_time[t] : (double)arr_max_tokens[t];
-    if (!std::isfinite(akeys[t]))
-      return set_error(TIE_EDOMAIN, "WaitingQueue::push: key must be finite");
-    if (Q->slot_of.count(arr_ids[t]))
-      return set_error(TIE_EINVALID, "WaitingQueue::push: id " + std::to_string(arr_ids[t]) +
-                                         " already queued");
-  }
-  {
-    std::vector<uint64_t> srt(arr_ids, arr_ids + n_arr);
-    std::sort(srt.begin(), srt.end());
-    if (std::adjacent_find(srt.begin(), srt.end()) != srt.end())
-      return set_error(TIE_EINVALID, "WaitingQueue::push: id already queued");
-  }
+  // ---- host validation of the whole step before any host state changes: the arrivals
+  // (tie_queue_arrive), then the predictions with this step's arrivals counted as waiting
+  // (tie_queue_predict).  A prediction error leaves the arrivals applied, as the reference's
+  // on_arrival calls stay applied when a later on_prediction throws.
+  std::vector<double> akeys;
+  if (int rc = check_arrivals(Q, arr_ids, arr_time, arr_max_tokens, n_arr, akeys)) return rc;
   const uint64_t first = Q->n_slots;
+  std::vector<uint32_t> slots;
+  double beta = 0.0;
+  {
+    // predictions see the queue length after this step's arrivals (compute_beta at
+    // on_prediction time, sched.cpp:139)
+    Q->size += n_arr;
+    const int rc = check_predictions(Q, pred_ids, n_pred, arr_ids, n_arr, first, slots, &beta);
+    Q->size -= n_arr;
+    if (rc) {
+      const std::string msg = tie_last_error();
+      if (int rc2 = tie_queue_arrive(Q, arr_ids, arr_time, arr_max_tokens, n_arr)) return rc2;
+      return set_error(rc, msg);
+    }
+  }
   for (uint64_t t = 0; t < n_arr; ++t) {
     Q->slot_of.emplace(arr_ids[t], (uint32_t)(first + t));
     Q->alive[first + t] = 1;
@@ -1341,24 +1394,9 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
     blocks.erase(std::unique(blocks.begin(), blocks.end()), blocks.end());
   }
   const uint32_t n_uncond = (uint32_t)blocks.size();
-  // ---- predictions: host validation (tie_queue_predict); FCFS ignores them
+  // FCFS ignores predictions
   const bool use_pred = n_pred > 0 && Q->policy != 0;
-  std::vector<uint32_t> slots(n_pred);
-  for (uint64_t t = 0; t < n_pred; ++t) {
-    auto it = Q->slot_of.find(pred_ids[t]);
-    if (it == Q->slot_of.end())
-      return set_error(TIE_EINVALID, "Scheduler::on_prediction: id " +
-                                         std::to_string(pred_ids[t]) + " not waiting");
-    slots[t] = it->second;
-  }
-  const double beta = Q->policy == 1 ? 0.0 : beta_at(Q, Q->size + Q->peers);
   if (use_pred) {
-    std::vector<uint32_t> srt(slots);
-    std::sort(srt.begin(), srt.end());
-    for (uint64_t t = 0; t < n_pred; ++t)
-      if (Q->predicted[slots[t]] || (t + 1 < n_pred && srt[t] == srt[t + 1]))
-        return set_error(TIE_EINVALID, "Scheduler::on_prediction: id " +
-                                           std::to_string(pred_ids[t]) + " already predicted");
     std::vector<uint32_t> pb;
     for (uint32_t sl : slots) pb.push_back(sl / tie::dev::kBlockSlots);
     std::sort(pb.begin(), pb.end());

@@ -153,3 +153,100 @@ def test_topb_pop_candidate_overflow_path(tie, mc):
     q.on_arrival_batch(np.arange(n, dtype=np.uint64), np.zeros(n), np.full(n, 100, np.uint32))
     assert q.next_requests(32).tolist() == list(range(32))
     assert q.next_requests(40).tolist() == list(range(32, 72))
+
+
+def _empty_step_args():
+    return (np.array([], np.uint64), np.array([]), np.array([], np.uint32))
+
+
+def test_step_prediction_error_keeps_arrivals_poppable(tie, mc):
+    """a prediction-validation error in a fused step leaves the step's
+    arrivals applied ON THE DEVICE too (reference: on_arrival calls stay applied when a later
+    on_prediction throws), so they pop with their ids and a later prediction re-keys them."""
+    for bad in ("not waiting", "already predicted"):
+        q = tie.GpuScheduler(mc, tie.Policy.TIE, _cfg(tie), 100)
+        q.on_arrival_batch(np.array([1], np.uint64), np.zeros(1), np.array([512], np.uint32))
+        q.on_prediction_batch(np.array([1], np.uint64), np.array([50.0]), np.array([80.0]))
+        pid = np.array([99], np.uint64) if bad == "not waiting" else np.array([1], np.uint64)
+        with pytest.raises(ValueError, match=bad):
+            q.step(np.array([5, 6], np.uint64), np.zeros(2), np.array([300, 200], np.uint32),
+                   pid, np.array([3.0]), np.array([0.5]), np.array([512], np.uint32), 3)
+        assert q.waiting() == 3
+        # the arrival 6 (key 200) gets a prediction now: key 10 + beta * 20 < 50 + beta * 80
+        q.on_prediction_batch(np.array([6], np.uint64), np.array([10.0]), np.array([20.0]))
+        assert q.next_requests(3).tolist() == [6, 1, 5]
+
+
+def test_step_prediction_of_same_step_arrival(tie, mc):
+    """A prediction may name an arrival of the same step (it is waiting by then)."""
+    q = tie.GpuScheduler(mc, tie.Policy.TIE, _cfg(tie), 100)
+    got = q.step(np.array([7, 8], np.uint64), np.zeros(2), np.array([512, 512], np.uint32),
+                 np.array([8], np.uint64), np.array([3.0]), np.array([0.5]),
+                 np.array([512], np.uint32), 1)
+    assert got.tolist() == [8]
+
+
+def test_arrive_rejected_batch_leaves_queue_usable(tie, mc):
+    """a batch rejected part-way (non-finite key / duplicate) changes nothing, so
+    later arrivals are accepted and every id pops exactly once."""
+    q = tie.GpuScheduler(mc, tie.Policy.FCFS, _cfg(tie), 100)
+    with pytest.raises(ValueError, match="finite"):
+        q.on_arrival_batch(np.array([1, 2, 3], np.uint64), np.array([0.1, 0.2, np.inf]),
+                           np.full(3, 512, np.uint32))
+    with pytest.raises(ValueError, match="id 2 already queued"):
+        q.on_arrival_batch(np.array([1, 2, 2], np.uint64), np.array([0.1, 0.2, 0.3]),
+                           np.full(3, 512, np.uint32))
+    assert q.waiting() == 0
+    q.on_arrival_batch(np.array([1, 2, 3], np.uint64), np.array([0.3, 0.2, 0.1]),
+                       np.full(3, 512, np.uint32))
+    assert q.next_requests(5).tolist() == [3, 2, 1]
+
+
+def test_predict_duplicate_far_apart_rejected(tie, mc):
+    """an id repeated anywhere in one prediction batch is 'already predicted'
+    (the reference's second on_prediction throws), and the queue is unchanged."""
+    n = 200
+    q = tie.GpuScheduler(mc, tie.Policy.TIE, _cfg(tie), n)
+    q.on_arrival_batch(np.arange(n, dtype=np.uint64), np.zeros(n), np.full(n, 512, np.uint32))
+    ids = np.arange(100, dtype=np.uint64)
+    ids[99] = 3  # 96 positions after the first 3
+    with pytest.raises(ValueError, match="id 3 already predicted"):
+        q.on_prediction_batch(ids, np.full(100, 10.0), np.full(100, 20.0))
+    assert q.beta_range()[2] == 0  # betas_in_use_ untouched
+    q.on_prediction_batch(np.array([150], np.uint64), np.array([10.0]), np.array([20.0]))
+    assert q.next_requests(2).tolist() == [150, 0]
+
+
+def test_invalid_beta_config_raises_domain_error(tie, mc):
+    """ADVICE r1: compute_beta's std::domain_error on an invalid ScoreConfig surfaces at
+    on_prediction (sched.cpp:10-15, 139) instead of running with beta = 0."""
+    for field, val in [("q_sat", 0.0), ("beta_max", -1.0)]:
+        sc = _cfg(tie)
+        setattr(sc, field, val)
+        q = tie.GpuScheduler(mc, tie.Policy.TIE, sc, 10)
+        q.on_arrival_batch(np.array([1], np.uint64), np.zeros(1), np.array([512], np.uint32))
+        with pytest.raises(ValueError, match="compute_beta"):
+            q.on_prediction_batch(np.array([1], np.uint64), np.array([10.0]), np.array([20.0]))
+        with pytest.raises(ValueError, match="compute_beta"):
+            q.step(*_empty_step_args(), np.array([1], np.uint64), np.array([3.0]),
+                   np.array([0.5]), np.array([512], np.uint32), 0)
+        assert q.next_requests(1).tolist() == [1]
+    sc = _cfg(tie)
+    sc.beta_mode = tie.BetaMode.Fixed
+    sc.beta_fixed = -0.5
+    q = tie.GpuScheduler(mc, tie.Policy.TIE, sc, 10)
+    q.on_arrival_batch(np.array([1], np.uint64), np.zeros(1), np.array([512], np.uint32))
+    with pytest.raises(ValueError, match="beta_fixed"):
+        q.on_prediction_batch(np.array([1], np.uint64), np.array([10.0]), np.array([20.0]))
+
+
+def test_batch_length_mismatch_is_value_error(tie, mc):
+    q = tie.GpuScheduler(mc, tie.Policy.TIE, _cfg(tie), 10)
+    with pytest.raises(ValueError, match="lengths"):
+        q.on_arrival_batch(np.array([1, 2], np.uint64), np.zeros(1), np.full(2, 5, np.uint32))
+    q.on_arrival_batch(np.array([1, 2], np.uint64), np.zeros(2), np.full(2, 5, np.uint32))
+    with pytest.raises(ValueError, match="lengths"):
+        q.on_prediction_batch(np.array([1, 2], np.uint64), np.array([1.0, 2.0]), np.ones(1))
+    with pytest.raises(ValueError, match="lengths"):
+        q.on_prediction_logt(np.array([1, 2], np.uint64), np.ones(2), np.ones(1),
+                             np.full(2, 5, np.uint32))
