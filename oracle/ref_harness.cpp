@@ -310,6 +310,13 @@ double ref_logt_loglik(const double* x, uint64_t K, double mu, double sigma, dou
   return tie::logt_loglik(std::vector<double>(x, x + K), mu, sigma, nu);
 }
 
+void ref_logt_loglik_grad(const double* x, uint64_t K, double mu, double sigma, double nu,
+                          double* grad) {
+  const auto g = tie::logt_loglik_grad(std::vector<double>(x, x + K), mu, sigma, nu);
+  grad[0] = g[0];
+  grad[1] = g[1];
+}
+
 // Config-3 prompt generator (following main.cpp:841-845): truths drawn
 // sequentially from Rng(seed); samples sample_logt(LogTParams(mu,sigma,nu), K,
 // mix64(seed, p)); integerised max(1, llround(x)) with a u32 ceiling (the reference's

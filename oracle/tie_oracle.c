@@ -476,6 +476,12 @@ static void logt_grad(const double* x, uint64_t K, double mu, double sigma, doub
   *gsig = b;
 }
 
+/* logt_loglik_grad (fit.cpp:58-71), exported for the device loglik/grad parity test */
+void tor_logt_loglik_grad(const double* x, uint64_t K, double mu, double sigma, double nu,
+                          double* grad) {
+  logt_grad(x, K, mu, sigma, nu, &grad[0], &grad[1]);
+}
+
 static double median_sorted(const double* v, uint64_t n) {
   return n % 2 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
 }

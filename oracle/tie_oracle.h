@@ -57,6 +57,8 @@ int tor_rank(const double* key, const uint64_t* ids, uint64_t n, uint64_t* order
 int tor_fit(const double* x, uint64_t P, uint64_t K, double nu, double* mu, double* sigma,
             double* ll, int32_t* iters, uint8_t* converged, uint8_t* degenerate, int threads);
 double tor_logt_loglik(const double* x, uint64_t K, double mu, double sigma, double nu);
+void tor_logt_loglik_grad(const double* x, uint64_t K, double mu, double sigma, double nu,
+                          double* grad);
 
 /* cmd_fit's per-prompt analysis (main.cpp:510-585): families bitmask 1 logt (fixed nu),
  * 2 logt_free_nu, 4 lognormal, 8 exponential; fits[f][10][P] (mu, sigma, nu, rate,

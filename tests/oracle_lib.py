@@ -227,6 +227,13 @@ class Oracle(_Base):
         x = np.ascontiguousarray(x, np.float64)
         return self.logt_loglik_raw(_ptr(x), len(x), mu, sigma, nu)
 
+    def logt_loglik_grad(self, x, mu, sigma, nu):
+        f = self._fn("logt_loglik_grad", [_p, _u64, _d, _d, _d, _p], None)
+        x = np.ascontiguousarray(x, np.float64)
+        g = np.empty(2)
+        f(_ptr(x), len(x), mu, sigma, nu, _ptr(g))
+        return g
+
 
 def ref_available():
     return os.path.exists(REF_SO)
@@ -288,6 +295,13 @@ class RefLib(_Base):
     def logt_loglik(self, x, mu, sigma, nu):
         x = np.ascontiguousarray(x, np.float64)
         return self.logt_loglik_raw(_ptr(x), len(x), mu, sigma, nu)
+
+    def logt_loglik_grad(self, x, mu, sigma, nu):
+        f = self._fn("logt_loglik_grad", [_p, _u64, _d, _d, _d, _p], None)
+        x = np.ascontiguousarray(x, np.float64)
+        g = np.empty(2)
+        f(_ptr(x), len(x), mu, sigma, nu, _ptr(g))
+        return g
 
     def sim_scores(self, mu, sigma, ids, max_tokens, predictor=0, mu_sd=0.0, ls_sd=0.0,
                    seed=0, family=0, alpha=0.9, threads=None):

@@ -131,3 +131,110 @@ def test_device_fit_ops_for_sharded_fit(tie, mc, oracle):
     got["degenerate"] = got["degenerate"].astype(bool)
     _compare(got, oracle.fit(x), "device-fit-ops")
     assert glob is local  # one rank: the gathered result is the local one
+
+
+def _dev_loglik(abi, h, x, mu, sigma, nu=3.5):
+    """tie_logt_loglik (the device F2/F3 entry point) over P parameter points, device buffers."""
+    import ctypes
+
+    import torch
+
+    L = abi.lib
+    L.tie_logt_loglik.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                  ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_void_p]
+    dx = torch.from_numpy(np.ascontiguousarray(x, np.float64)).cuda()
+    dm = torch.from_numpy(np.ascontiguousarray(mu, np.float64)).cuda()
+    ds = torch.from_numpy(np.ascontiguousarray(sigma, np.float64)).cuda()
+    P = dm.numel()
+    ll = torch.empty(P, dtype=torch.float64, device="cuda")
+    g = torch.empty(2 * P, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    abi.check(L.tie_logt_loglik(h, dx.data_ptr(), dx.numel(), dm.data_ptr(), ds.data_ptr(), P,
+                                nu, ll.data_ptr(), g.data_ptr(), None))
+    abi.check(L.tie_sync(h, None))
+    return ll.cpu().numpy(), g.cpu().numpy().reshape(P, 2)
+
+
+def test_device_loglik_grad_vs_reference(abi, h, oracle):
+    """F2/F3 (fit.cpp:44-71) through the device entry point: log-likelihood and gradient at
+    1e-12 relative of the reference's (oracle restatement pinned bit-exact in
+    test_oracle.py) over a grid of parameter points and sample sizes."""
+    rng = np.random.default_rng(11)
+    for K, seed in [(1, 3), (16, 5), (60, 123), (1000, 9)]:
+        x = oracle.sample_logt(4.0, 0.8, 3.5, K, seed)
+        mu = rng.uniform(1.0, 7.0, 257)
+        sg = np.exp(rng.uniform(np.log(0.05), np.log(5.0), 257))
+        ll, g = _dev_loglik(abi, h, x, mu, sg)
+        ll_ref = np.array([oracle.logt_loglik(x, m, s, 3.5) for m, s in zip(mu, sg)])
+        g_ref = np.array([oracle.logt_loglik_grad(x, m, s, 3.5) for m, s in zip(mu, sg)])
+        assert (np.abs(ll - ll_ref) / np.maximum(1.0, np.abs(ll_ref))).max() <= 1e-12, K
+        assert (np.abs(g - g_ref) / np.maximum(1.0, np.abs(g_ref))).max() <= 1e-12, K
+    gold = golden("loglik.npz")  # values from the compiled reference itself
+    for K in (1, 16, 60, 1000):
+        ll, g = _dev_loglik(abi, h, gold[f"K{K}__x"], gold[f"K{K}__mu"], gold[f"K{K}__sigma"])
+        ll_ref, g_ref = gold[f"K{K}__ll"], gold[f"K{K}__grad"]
+        assert (np.abs(ll - ll_ref) / np.maximum(1.0, np.abs(ll_ref))).max() <= 1e-12, K
+        assert (np.abs(g - g_ref) / np.maximum(1.0, np.abs(g_ref))).max() <= 1e-12, K
+
+
+def test_device_loglik_grad_reference_unit_cases(abi, h, oracle):
+    """proj/tests/test_fit.cpp:25-60 on the device entry point: single-sample closed form,
+    symmetric pair (d/dmu = 0), unimodality in mu, and central finite differences (h = 1e-5,
+    oracles.hpp:121-126) within 1e-5 across mu in {3.2, 4.0, 4.9} x sigma in {0.4, 0.8, 1.7}."""
+    from math import exp, lgamma, log, pi
+
+    nu = 3.5
+    t0 = lgamma(0.5 * (nu + 1)) - lgamma(0.5 * nu) - 0.5 * log(nu * pi)  # ln t_nu(0)
+    ll, _ = _dev_loglik(abi, h, [exp(5.0)], [5.0], [1.0])
+    assert abs(ll[0] - (t0 - 5.0)) <= 1e-12 * abs(t0 - 5.0)
+    sym = [exp(1.3), exp(2.7)]
+    _, g = _dev_loglik(abi, h, sym, [2.0], [0.9])
+    assert abs(g[0, 0]) <= 1e-12
+    ll, _ = _dev_loglik(abi, h, [exp(1.0), exp(3.0)], [2.0, 1.0, 3.0], [1.0, 1.0, 1.0])
+    assert ll[0] > ll[1] and ll[0] > ll[2]
+    x = oracle.sample_logt(4.0, 0.8, 3.5, 60, 123)
+    hh = 1e-5
+    for mu in (3.2, 4.0, 4.9):
+        for sg in (0.4, 0.8, 1.7):
+            pts_m = [mu, mu + hh, mu - hh, mu, mu]
+            pts_s = [sg, sg, sg, sg + hh, sg - hh]
+            ll, g = _dev_loglik(abi, h, x, pts_m, pts_s)
+            fd = ((ll[1] - ll[2]) / (2 * hh), (ll[3] - ll[4]) / (2 * hh))
+            assert abs(g[0, 0] - fd[0]) / max(1.0, abs(fd[0])) < 1e-5
+            assert abs(g[0, 1] - fd[1]) / max(1.0, abs(fd[1])) < 1e-5
+
+
+def test_per_item_loglik_grad_api(tie, oracle):
+    """The reference-named per-item calls (module.cpp:80-82) route to the device kernel."""
+    x = oracle.sample_logt(5.0, 0.7, 3.5, 100, 77).tolist()
+    for mu, sg in [(5.0, 0.7), (4.1, 1.3), (6.0, 0.2)]:
+        ref = oracle.logt_loglik(np.array(x), mu, sg, 3.5)
+        assert abs(tie.logt_loglik(x, mu, sg, 3.5) - ref) <= 1e-12 * abs(ref)
+        gr = oracle.logt_loglik_grad(np.array(x), mu, sg, 3.5)
+        g = tie.logt_loglik_grad(x, mu, sg, 3.5)
+        assert np.allclose(g, gr, rtol=1e-12, atol=1e-12)
+    with pytest.raises(ValueError):
+        tie.logt_loglik([-1.0], 0.0, 1.0, 3.5)
+    with pytest.raises(ValueError):
+        tie.logt_loglik([], 0.0, 1.0, 3.5)
+    with pytest.raises(ValueError):
+        tie.logt_loglik([1.0], 0.0, 0.0, 3.5)
+
+
+def test_config3_full_1m_vs_oracle(abi, h, oracle):
+    """Config 3 at its full size: 1M prompts x 16, every fit vs the oracle."""
+    x, _, _ = oracle.gen_fit_data(1_000_000, 16, seed=1)
+    _compare(abi.fit(h, x), oracle.fit(x), "config3-1M")
+
+
+@pytest.mark.slow
+def test_north_star_10m_fits_vs_oracle(abi, h, oracle):
+    """The north star's fitting target on one GPU: 10M prompts x 16 samples (1.28 GB of
+    samples), every fit vs the oracle (threaded over the host cores)."""
+    P = 10_000_000
+    x, _, _ = oracle.gen_fit_data(P, 16, seed=1)
+    got = abi.fit(h, x)
+    mism = _compare(got, oracle.fit(x), "north-star-10M")
+    assert mism <= P // 10

@@ -192,3 +192,14 @@ def test_fit_report_oracle_vs_reference_library(oracle):
         np.testing.assert_array_equal(a[1], b[1])
     with pytest.raises(ValueError, match="at least 5"):
         oracle.fit_report_raw(x[:, :4])
+
+
+def test_loglik_grad_bit_exact(oracle):
+    """F2/F3 restatement vs the reference's own logt_loglik / logt_loglik_grad values."""
+    g = golden("loglik.npz")
+    for K in (1, 16, 60, 1000):
+        x, mu, sg = g[f"K{K}__x"], g[f"K{K}__mu"], g[f"K{K}__sigma"]
+        ll = np.array([oracle.logt_loglik(x, m, s, 3.5) for m, s in zip(mu, sg)])
+        gr = np.array([oracle.logt_loglik_grad(x, m, s, 3.5) for m, s in zip(mu, sg)])
+        assert np.array_equal(ll, g[f"K{K}__ll"]), K
+        assert np.array_equal(gr, g[f"K{K}__grad"]), K
