@@ -73,6 +73,33 @@ int tie_compute_beta(int adaptive, double beta_fixed, double beta_max, double q_
 double tie_t_quantile(double p, double nu);
 double tie_t_cdf(double y, double nu);
 
+/* ---- per-item distribution functions (GPU, batched) ----------------------------------------
+ * The reference's per-item public functions (proj/include/tiesched/dist.hpp:47-88; pybind
+ * proj/bindings/module.cpp:48-60) over n items.  HOST buffers; inputs are validated in the
+ * reference's per-item order first (the first failing item returns its error), then one
+ * kernel evaluates every item.  Arguments per op (param is nu or alpha):
+ *   TIE_EVAL_PSI             a=y  b=mu  c=sigma, param=nu (must equal the context's nu)
+ *                            psi(y, LogTParams(mu, sigma, nu), mc)           dist.cpp:149-156
+ *   TIE_EVAL_INCBETA         a=a  b=b   c=x   regularized_incomplete_beta     dist.cpp:52-63
+ *   TIE_EVAL_T_PDF / T_CDF   a=y, param=nu    t_pdf / t_cdf (any nu)          dist.cpp:65-81
+ *   TIE_EVAL_LOGT_PDF / CDF  a=x  b=mu  c=sigma, param=nu                     dist.cpp:131-140
+ *   TIE_EVAL_NORMAL_CDF      a=z                                              dist.cpp:191
+ *   TIE_EVAL_NORMAL_QUANTILE a=p                                              dist.cpp:193-225
+ *   TIE_EVAL_LOGNORMAL_E     a=mu b=sigma c=x_max                             dist.cpp:227-236
+ *   TIE_EVAL_LOGNORMAL_CVAR  a=mu b=sigma c=x_max, param=alpha                dist.cpp:238-249 */
+#define TIE_EVAL_PSI 1
+#define TIE_EVAL_INCBETA 2
+#define TIE_EVAL_T_PDF 3
+#define TIE_EVAL_T_CDF 4
+#define TIE_EVAL_LOGT_PDF 5
+#define TIE_EVAL_LOGT_CDF 6
+#define TIE_EVAL_NORMAL_CDF 7
+#define TIE_EVAL_NORMAL_QUANTILE 8
+#define TIE_EVAL_LOGNORMAL_E 9
+#define TIE_EVAL_LOGNORMAL_CVAR 10
+int tie_eval_host(tie_ctx* ctx, int op, const double* a, const double* b, const double* c,
+                  uint64_t n, double param, double* out);
+
 /* ---- K1 score -------------------------------------------------------------------------
  * Batched replacement for, per request i,
  *   CensoredLogT cl(LogTParams(mu[i], sigma[i], nu), x_max[i]);      dist.cpp:108-120
@@ -143,6 +170,12 @@ int tie_fit_report(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double
                    unsigned families, double* fits, double* tail, void* stream);
 int tie_fit_report_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
                         unsigned families, double* fits, double* tail);
+/* ks_test(x, fit_cdf(fit, .)) (fit.cpp:245-284) against ONE caller-given fit (the pybind
+ * ks_test_fit, module.cpp:117-123): family 0 LogTFixedNu, 1 LogTFreeNu (t CDF at `nu`),
+ * 2 LogNormal (mu, sigma), 3 Exponential (rate).  K >= 5. */
+int tie_ks_test_fit_host(tie_ctx* ctx, const double* x, uint64_t K, int family, double mu,
+                         double sigma, double nu, double rate, double* statistic,
+                         double* p_value);
 int tie_fit_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double nu,
                  double* mu, double* sigma, double* log_likelihood, int32_t* iterations,
                  uint8_t* converged, uint8_t* degenerate);
@@ -207,6 +240,46 @@ int tie_queue_set_peer_waiting(tie_queue* q, uint64_t peers);
 int tie_queue_beta_range(const tie_queue* q, double* lo, double* hi, uint64_t* n_in_use);
 int tie_queue_rebuild_at(tie_queue* q, double beta);
 int tie_queue_peek(tie_queue* q, uint64_t k, uint64_t* keys, uint64_t* ids, uint64_t* n_out);
+
+/* ---- WaitingQueue (proj/include/tiesched/sched.hpp:32-68, proj/src/sched.cpp:28-123) -------
+ * policy TIE_QUEUE_RAW in tie_queue_create makes a bare WaitingQueue: entries carry caller-
+ * given keys, pops are pop_min() in (key asc, req_id asc) order, and there is no Scheduler
+ * rule (no policy keys, no beta, no drift rebuild).  The entry fields of QueueEntry
+ * (sched.hpp:32-39) -- predicted, expectation, cvar, beta_at_update -- ride along.  Slots
+ * are managed automatically: a queue grows (or compacts its popped slots) as needed.
+ *  - push:        WaitingQueue::push x m (sched.cpp:59-67); predicted/E/C/beta may be NULL
+ *  - update:      WaitingQueue::update x m (sched.cpp:69-79); a repeated id: last write wins
+ *  - set_entries: write back edited entries (keys + fields) -- entries()/at() edits followed
+ *                 by rebuild() (sched.cpp:110-114)
+ *  - pop:         pop_min() x max_pops with the popped entries (sched.cpp:81-94)
+ * and for any queue (a Scheduler's too):
+ *  - contains / get (WaitingQueue::at, sched.cpp:96-108) / entries (slot order) / validate
+ *    (sched.cpp:116-123: host index consistency + every device block minimum rescanned). */
+#define TIE_QUEUE_FCFS 0
+#define TIE_QUEUE_SEPT 1
+#define TIE_QUEUE_TIE 2
+#define TIE_QUEUE_RAW 3
+int tie_queue_contains(const tie_queue* q, uint64_t id); /* 1 waiting, 0 not */
+int tie_queue_push(tie_queue* q, const uint64_t* ids, const double* keys,
+                   const uint8_t* predicted, const double* E, const double* C,
+                   const double* beta_at_update, uint64_t m);
+int tie_queue_update(tie_queue* q, const uint64_t* ids, const double* keys, uint64_t m);
+int tie_queue_set_entries(tie_queue* q, const uint64_t* ids, const double* keys,
+                          const uint8_t* predicted, const double* E, const double* C,
+                          const double* beta_at_update, uint64_t m);
+int tie_queue_pop(tie_queue* q, uint64_t max_pops, uint64_t* ids, double* keys,
+                  uint8_t* predicted, double* E, double* C, double* beta_at_update,
+                  uint64_t* n_out);
+int tie_queue_get(tie_queue* q, const uint64_t* ids, uint64_t m, double* keys,
+                  uint8_t* predicted, double* E, double* C, double* beta_at_update);
+int tie_queue_entries(tie_queue* q, uint64_t cap, uint64_t* ids, double* keys,
+                      uint8_t* predicted, double* E, double* C, double* beta_at_update,
+                      uint64_t* n_out);
+int tie_queue_validate(tie_queue* q, int* ok);
+/* slot management: relayout the live entries into `capacity` slots (>= waiting, < 2^32) */
+int tie_queue_reserve(tie_queue* q, uint64_t capacity);
+uint64_t tie_queue_capacity(const tie_queue* q);
+uint64_t tie_queue_slots_used(const tie_queue* q);
 
 /* ---- input formats ------------------------------------------------------
  * Request traces: JSONL, one object per request -- load_trace / save_trace

@@ -493,3 +493,122 @@ int ref_sched_bench(int policy, int adaptive, double beta_max, double q_sat, dou
 }
 
 }  // extern "C"
+
+// ---- per-item distribution functions (dist.hpp:47-88), n items, same op codes as
+// include/tie_cuda.h TIE_EVAL_* (1 psi, 2 incbeta, 3 t_pdf, 4 t_cdf, 5 logt_pdf, 6 logt_cdf,
+// 7 normal_cdf, 8 normal_quantile, 9 lognormal E, 10 lognormal CVaR)
+extern "C" int ref_eval(int op, const double* a, const double* b, const double* c, uint64_t n,
+                        double param, double* out) {
+  try {
+    std::optional<tie::McContext> mc;
+    if (op == 1) mc.emplace(param);
+    for (uint64_t i = 0; i < n; ++i) {
+      switch (op) {
+        case 1: out[i] = tie::psi(a[i], tie::LogTParams(b[i], c[i], param), *mc); break;
+        case 2: out[i] = tie::regularized_incomplete_beta(a[i], b[i], c[i]); break;
+        case 3: out[i] = tie::t_pdf(a[i], param); break;
+        case 4: out[i] = tie::t_cdf(a[i], param); break;
+        case 5: out[i] = tie::logt_pdf(a[i], tie::LogTParams(b[i], c[i], param)); break;
+        case 6: out[i] = tie::logt_cdf(a[i], tie::LogTParams(b[i], c[i], param)); break;
+        case 7: out[i] = tie::normal_cdf(a[i]); break;
+        case 8: out[i] = tie::normal_quantile(a[i]); break;
+        case 9: out[i] = tie::lognormal_censored_expectation(a[i], b[i], c[i]); break;
+        case 10: out[i] = tie::lognormal_censored_cvar(a[i], b[i], c[i], param); break;
+        default: throw std::invalid_argument("ref_eval: unknown op");
+      }
+    }
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
+  } catch (const std::exception& e) {
+    return fail(e, 2);
+  }
+}
+
+// ks_test(x, fit_cdf(fit, .)) for one given fit (module.cpp:117-123)
+extern "C" int ref_ks_test_fit(const double* x, uint64_t K, int family, double mu, double sigma,
+                               double nu, double rate, double* stat, double* p) {
+  try {
+    tie::FitResult f;
+    f.family = (tie::FitFamily)family;
+    f.mu = mu;
+    f.sigma = sigma;
+    f.nu = nu;
+    f.rate = rate;
+    std::vector<double> v(x, x + K);
+    const tie::KsResult r = tie::ks_test(v, [&](double t) { return tie::fit_cdf(f, t); });
+    *stat = r.statistic;
+    *p = r.p_value;
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
+  } catch (const std::exception& e) {
+    return fail(e, 2);
+  }
+}
+
+// run_sim (sim.cpp:39-185) on the reference's own workload: gen_logt_workload(spec, wseed)
+// then run_sim(policy, ScoreConfig{alpha, adaptive, beta_fixed, beta_max, q_sat, threshold},
+// EngineConfig{slots, c0, c1, c2}, PredictorConfig{kind, family, noise, batched}, seed).
+// Outputs per event (id order): arrival, predict_ready (NaN if none), admit, first_token,
+// completion, emitted; metrics[4] = ttft_avg, ttft_p90, ptla_avg, ptla_p90; and the wall
+// seconds of run_sim itself.
+extern "C" int ref_run_sim(uint64_t n, double rps, double mu_lo, double mu_hi, double sg_lo,
+                           double sg_hi, uint32_t prompt_lo, uint32_t prompt_hi,
+                           uint32_t max_tokens, uint64_t wseed, int policy, double alpha,
+                           int adaptive, double beta_fixed, double beta_max, double q_sat,
+                           double threshold, int slots, double c0, double c1, double c2,
+                           int kind, int family, double mu_sd, double ls_sd, int batched,
+                           uint64_t seed, double* arrival, double* ready, double* admit,
+                           double* first, double* done, uint32_t* emitted, double* metrics,
+                           double* seconds) {
+  try {
+    tie::WorkloadSpec ws;
+    ws.n_requests = n;
+    ws.rps = rps;
+    ws.mu_range = {mu_lo, mu_hi};
+    ws.sigma_range = {sg_lo, sg_hi};
+    ws.prompt_range = {prompt_lo, prompt_hi};
+    ws.max_tokens = max_tokens;
+    const std::vector<tie::Request> w = tie::gen_logt_workload(ws, wseed);
+    tie::ScoreConfig sc;
+    sc.alpha = alpha;
+    sc.beta_mode = adaptive ? tie::BetaMode::AdaptiveLinear : tie::BetaMode::Fixed;
+    sc.beta_fixed = beta_fixed;
+    sc.beta_max = beta_max;
+    sc.q_sat = q_sat;
+    sc.rebuild_threshold = threshold;
+    tie::EngineConfig ec;
+    ec.batch_slots = slots;
+    ec.c0 = c0;
+    ec.c1 = c1;
+    ec.c2 = c2;
+    tie::PredictorConfig pc;
+    pc.kind = (tie::PredictorKind)kind;
+    pc.family = (tie::ScoreFamily)family;
+    pc.noise.mu_sd = mu_sd;
+    pc.noise.log_sigma_sd = ls_sd;
+    pc.batched = batched != 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    const tie::SimReport r = tie::run_sim(w, (tie::Policy)policy, sc, ec, pc, seed);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (size_t i = 0; i < r.events.size(); ++i) {
+      const tie::RequestEvent& e = r.events[i];
+      arrival[i] = e.arrival_s;
+      ready[i] = e.predict_ready_s ? *e.predict_ready_s : std::nan("");
+      admit[i] = e.admit_s;
+      first[i] = e.first_token_s;
+      done[i] = e.completion_s;
+      emitted[i] = e.emitted_tokens;
+    }
+    metrics[0] = r.metrics.ttft_avg;
+    metrics[1] = r.metrics.ttft_p90;
+    metrics[2] = r.metrics.ptla_avg;
+    metrics[3] = r.metrics.ptla_p90;
+    return 0;
+  } catch (const std::domain_error& e) {
+    return fail(e, 1);
+  } catch (const std::exception& e) {
+    return fail(e, 2);
+  }
+}

@@ -6,6 +6,9 @@
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
+#include <cmath>
+#include <optional>
+
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -37,9 +40,12 @@ const T* ptr_or_null(const py::object& o) {
 
 void* vp(uintptr_t p) { return reinterpret_cast<void*>(p); }
 
-// sim.hpp:24-28 (the simulator's own enums; only the scoring-relevant values)
-enum class PredictorKindPy { Oracle = 0, Noisy = 1 };
-enum class ScoreFamilyPy { LogT = 0, LogNormal = 1 };
+struct KsResultPy {  // fit.hpp:43-47
+  double statistic = 0.0;
+  double p_value = 0.0;
+  int n = 0;
+};
+
 
 }  // namespace
 
@@ -74,7 +80,7 @@ PYBIND11_MODULE(_core, m) {
       .def_property_readonly("samples",
                              [](const McContext& mc) {
                                return carray<double>((py::ssize_t)mc.n_samples(),
-                                                     mc.samples().data());
+                                                     mc.samples.data());
                              })
       .def_property_readonly("handle",
                              [](const McContext& mc) { return (uintptr_t)mc.handle(); });
@@ -85,6 +91,49 @@ PYBIND11_MODULE(_core, m) {
   m.def("sample_logt", &sample_logt, py::arg("params"), py::arg("n"), py::arg("seed"));
   m.def("censored_expectation", &censored_expectation, py::arg("censored"), py::arg("mc"));
   m.def("censored_cvar", &censored_cvar, py::arg("censored"), py::arg("mc"), py::arg("alpha"));
+  m.def("psi", &psi, py::arg("y"), py::arg("params"), py::arg("mc"));
+  m.def("regularized_incomplete_beta", &regularized_incomplete_beta, py::arg("a"), py::arg("b"),
+        py::arg("x"));
+  m.def("logt_pdf", &logt_pdf, py::arg("x"), py::arg("params"));
+  m.def("logt_cdf", &logt_cdf, py::arg("x"), py::arg("params"));
+  m.def("normal_cdf", &normal_cdf, py::arg("z"));
+  m.def("normal_quantile", &normal_quantile, py::arg("p"));
+  m.def("lognormal_censored_expectation", &lognormal_censored_expectation, py::arg("mu"),
+        py::arg("sigma"), py::arg("x_max"));
+  m.def("lognormal_censored_cvar", &lognormal_censored_cvar, py::arg("mu"), py::arg("sigma"),
+        py::arg("x_max"), py::arg("alpha"));
+  m.def(
+      "dist_eval",
+      [](const std::string& fn, carray<double> a, py::object b, py::object c, double param,
+         const McContext* mc) {
+        static const std::pair<const char*, int> ops[] = {
+            {"psi", TIE_EVAL_PSI}, {"regularized_incomplete_beta", TIE_EVAL_INCBETA},
+            {"t_pdf", TIE_EVAL_T_PDF}, {"t_cdf", TIE_EVAL_T_CDF},
+            {"logt_pdf", TIE_EVAL_LOGT_PDF}, {"logt_cdf", TIE_EVAL_LOGT_CDF},
+            {"normal_cdf", TIE_EVAL_NORMAL_CDF}, {"normal_quantile", TIE_EVAL_NORMAL_QUANTILE},
+            {"lognormal_censored_expectation", TIE_EVAL_LOGNORMAL_E},
+            {"lognormal_censored_cvar", TIE_EVAL_LOGNORMAL_CVAR}};
+        int op = 0;
+        for (const auto& o : ops)
+          if (fn == o.first) op = o.second;
+        if (!op) throw py::value_error("dist_eval: unknown function " + fn);
+        const size_t n = (size_t)a.size();
+        carray<double> bb = b.is_none() ? carray<double>(n) : b.cast<carray<double>>();
+        carray<double> cc = c.is_none() ? carray<double>(n) : c.cast<carray<double>>();
+        if ((size_t)bb.size() != n || (size_t)cc.size() != n)
+          throw py::value_error("dist_eval: array lengths differ");
+        std::vector<double> out;
+        {
+          py::gil_scoped_release nogil;
+          out = eval_batch(op, a.data(), bb.data(), cc.data(), n, param, mc);
+        }
+        return carray<double>((py::ssize_t)n, out.data());
+      },
+      py::arg("fn"), py::arg("a"), py::arg("b") = py::none(), py::arg("c") = py::none(),
+      py::arg("param") = 0.0, py::arg("mc") = nullptr,
+      "batched per-item distribution function on the GPU: fn(a[i], b[i], c[i]; param) with the "
+      "reference's argument order (psi: y, mu, sigma, param=nu, mc; logt_*: x, mu, sigma, "
+      "param=nu; t_*: y, param=nu; lognormal_*: mu, sigma, x_max, param=alpha)");
 
   // ------------------------------------------------------------- scoring / policy
   py::enum_<Policy>(m, "Policy")
@@ -94,6 +143,13 @@ PYBIND11_MODULE(_core, m) {
   py::enum_<BetaMode>(m, "BetaMode")
       .value("Fixed", BetaMode::Fixed)
       .value("AdaptiveLinear", BetaMode::AdaptiveLinear);
+  py::enum_<PredictorKind>(m, "PredictorKind")
+      .value("NoPredictor", PredictorKind::None)
+      .value("Oracle", PredictorKind::Oracle)
+      .value("Noisy", PredictorKind::Noisy);
+  py::enum_<ScoreFamily>(m, "ScoreFamily")
+      .value("LogT", ScoreFamily::LogT)
+      .value("LogNormal", ScoreFamily::LogNormal);
   py::class_<ScoreConfig>(m, "ScoreConfig")
       .def(py::init<>())
       .def_readwrite("alpha", &ScoreConfig::alpha)
@@ -290,7 +346,7 @@ PYBIND11_MODULE(_core, m) {
       "(fits[4][10][P], tail[5][P])");
   // ---- input formats
   m.def(
-      "load_trace",
+      "load_trace_soa",
       [](const std::string& path, double fill_rps, uint64_t seed) {
         tie_trace* t = nullptr;
         throw_code(tie_trace_load(path.c_str(), fill_rps, seed, &t));
@@ -309,7 +365,7 @@ PYBIND11_MODULE(_core, m) {
       py::arg("path"), py::arg("fill_rps") = 0.0, py::arg("seed") = 0,
       "load_trace (workload.cpp:106-161) -> dict of arrays (mu / sigma NaN where absent)");
   m.def(
-      "save_trace",
+      "save_trace_soa",
       [](const std::string& path, carray<uint64_t> id, carray<double> arrival_s,
          carray<uint32_t> prompt_tokens, carray<uint32_t> output_tokens,
          carray<uint32_t> max_tokens, py::object mu, py::object sigma) {
@@ -568,34 +624,300 @@ PYBIND11_MODULE(_core, m) {
       .def("waiting", [](const GpuQueue& g) { return tie_queue_size(g.q); })
       .def("current_beta", [](const GpuQueue& g) { return tie_queue_current_beta(g.q); });
 
-  py::enum_<PredictorKindPy>(m, "PredictorKind")
-      .value("Oracle", PredictorKindPy::Oracle)
-      .value("Noisy", PredictorKindPy::Noisy);
-  py::enum_<ScoreFamilyPy>(m, "ScoreFamily")
-      .value("LogT", ScoreFamilyPy::LogT)
-      .value("LogNormal", ScoreFamilyPy::LogNormal);
   m.def(
       "sim_scores",
       [](carray<double> mu, carray<double> sigma, carray<uint64_t> ids,
-         carray<uint32_t> max_tokens, const McContext& mc, PredictorKindPy predictor,
-         double mu_sd, double log_sigma_sd, uint64_t seed, ScoreFamilyPy family, double alpha) {
+         carray<uint32_t> max_tokens, const McContext& mc, PredictorKind predictor,
+         double mu_sd, double log_sigma_sd, uint64_t seed, ScoreFamily family, double alpha) {
         const size_t n = (size_t)mu.size();
         carray<double> E(n), C(n);
         int rc;
         {
           py::gil_scoped_release nogil;
           rc = tie_sim_scores_host(mc.handle(), mu.data(), sigma.data(), ids.data(),
-                                   max_tokens.data(), n, (int)predictor, mu_sd, log_sigma_sd,
-                                   seed, (int)family, alpha, E.mutable_data(), C.mutable_data());
+                                   max_tokens.data(), n,
+                                   predictor == PredictorKind::Noisy ? 1 : 0, mu_sd,
+                                   log_sigma_sd, seed, family == ScoreFamily::LogNormal ? 1 : 0,
+                                   alpha, E.mutable_data(), C.mutable_data());
         }
         throw_code(rc);
         return py::make_tuple(E, C);
       },
       py::arg("mu"), py::arg("sigma"), py::arg("ids"), py::arg("max_tokens"), py::arg("mc"),
-      py::arg("predictor") = PredictorKindPy::Oracle, py::arg("mu_sd") = 0.0,
+      py::arg("predictor") = PredictorKind::Oracle, py::arg("mu_sd") = 0.0,
       py::arg("log_sigma_sd") = 0.0, py::arg("seed") = 0,
-      py::arg("family") = ScoreFamilyPy::LogT, py::arg("alpha") = 0.9,
+      py::arg("family") = ScoreFamily::LogT, py::arg("alpha") = 0.9,
       "run_sim's scoring precompute (sim.cpp:77-96) on the GPU: (E, max(CVaR, E)) per request");
+
+  // ------------------------------------------------------------- goodness of fit
+  py::class_<KsResultPy>(m, "KsResult")
+      .def_readonly("statistic", &KsResultPy::statistic)
+      .def_readonly("p_value", &KsResultPy::p_value)
+      .def_readonly("n", &KsResultPy::n);
+  m.def(
+      "ks_test_fit",
+      [](const std::vector<double>& samples, const FitResult& f) {
+        KsResultPy r;
+        throw_code(tie_ks_test_fit_host(default_context(), samples.data(), samples.size(),
+                                        (int)f.family, f.mu, f.sigma, f.nu, f.rate,
+                                        &r.statistic, &r.p_value));
+        r.n = (int)samples.size();
+        return r;
+      },
+      py::arg("samples"), py::arg("fit"),
+      "KS test of samples against a fitted family's CDF (GPU; fit.cpp:245-284)");
+  m.def(
+      "ks_test_fit_raw",
+      [](carray<double> x, int family, double mu, double sigma, double nu, double rate) {
+        double st = 0.0, p = 0.0;
+        throw_code(tie_ks_test_fit_host(default_context(), x.data(), (uint64_t)x.size(), family,
+                                        mu, sigma, nu, rate, &st, &p));
+        return py::make_tuple(st, p);
+      },
+      py::arg("samples"), py::arg("family"), py::arg("mu") = 0.0, py::arg("sigma") = 0.0,
+      py::arg("nu") = 0.0, py::arg("rate") = 0.0,
+      "(statistic, p_value) of ks_test against family 0 logt / 1 logt free-nu / 2 lognormal / "
+      "3 exponential with the given parameters");
+
+  // ------------------------------------------------------------- workload (workload.hpp)
+  py::class_<Request>(m, "Request")
+      .def(py::init<>())
+      .def_readwrite("id", &Request::id)
+      .def_readwrite("arrival_s", &Request::arrival_s)
+      .def_readwrite("prompt_tokens", &Request::prompt_tokens)
+      .def_readwrite("true_output_tokens", &Request::true_output_tokens)
+      .def_readwrite("max_tokens", &Request::max_tokens)
+      .def_readwrite("true_mu", &Request::true_mu)
+      .def_readwrite("true_sigma", &Request::true_sigma);
+  py::class_<WorkloadSpec>(m, "WorkloadSpec")
+      .def(py::init<>())
+      .def_readwrite("n_requests", &WorkloadSpec::n_requests)
+      .def_readwrite("rps", &WorkloadSpec::rps)
+      .def_readwrite("mu_range", &WorkloadSpec::mu_range)
+      .def_readwrite("sigma_range", &WorkloadSpec::sigma_range)
+      .def_readwrite("nu", &WorkloadSpec::nu)
+      .def_readwrite("prompt_range", &WorkloadSpec::prompt_range)
+      .def_readwrite("max_tokens", &WorkloadSpec::max_tokens);
+  m.def("gen_logt_workload", &gen_logt_workload, py::arg("spec"), py::arg("seed"));
+  m.def("poisson_arrivals", &poisson_arrivals, py::arg("rps"), py::arg("n"), py::arg("seed"));
+  m.def(
+      "load_trace",
+      [](const std::string& path, std::optional<double> fill_rps, uint64_t seed) {
+        tie_trace* t = nullptr;
+        throw_code(tie_trace_load(path.c_str(), fill_rps ? *fill_rps : 0.0, seed, &t));
+        const size_t n = tie_trace_size(t);
+        std::vector<Request> out(n);
+        for (size_t i = 0; i < n; ++i) {
+          Request& r = out[i];
+          r.id = tie_trace_ids(t)[i];
+          r.arrival_s = tie_trace_arrival(t)[i];
+          r.prompt_tokens = tie_trace_prompt_tokens(t)[i];
+          r.true_output_tokens = tie_trace_output_tokens(t)[i];
+          r.max_tokens = tie_trace_max_tokens(t)[i];
+          const double mu = tie_trace_mu(t)[i], sg = tie_trace_sigma(t)[i];
+          if (!std::isnan(mu)) r.true_mu = mu;
+          if (!std::isnan(sg)) r.true_sigma = sg;
+        }
+        tie_trace_free(t);
+        return out;
+      },
+      py::arg("path"), py::arg("fill_rps") = std::optional<double>{}, py::arg("seed") = 0,
+      "load_trace (workload.cpp:106-161)");
+  m.def(
+      "save_trace",
+      [](const std::vector<Request>& reqs, const std::string& path) {
+        const size_t n = reqs.size();
+        std::vector<uint64_t> id(n);
+        std::vector<double> arr(n), mu(n), sg(n);
+        std::vector<uint32_t> pt(n), ot(n), mt(n);
+        for (size_t i = 0; i < n; ++i) {
+          id[i] = reqs[i].id;
+          arr[i] = reqs[i].arrival_s;
+          pt[i] = reqs[i].prompt_tokens;
+          ot[i] = reqs[i].true_output_tokens;
+          mt[i] = reqs[i].max_tokens;
+          mu[i] = reqs[i].true_mu ? *reqs[i].true_mu : std::nan("");
+          sg[i] = reqs[i].true_sigma ? *reqs[i].true_sigma : std::nan("");
+        }
+        throw_code(tie_trace_save(path.c_str(), n, id.data(), arr.data(), pt.data(), ot.data(),
+                                  mt.data(), mu.data(), sg.data()));
+      },
+      py::arg("requests"), py::arg("path"), "save_trace (workload.cpp:94-104)");
+
+  // ------------------------------------------------------------- WaitingQueue / Scheduler
+  py::class_<QueueEntry>(m, "QueueEntry")
+      .def(py::init<>())
+      .def(py::init([](uint64_t id, double key, bool predicted, double e, double c, double b) {
+             return QueueEntry{id, key, predicted, e, c, b};
+           }),
+           py::arg("req_id"), py::arg("key"), py::arg("predicted") = false,
+           py::arg("expectation") = 0.0, py::arg("cvar") = 0.0, py::arg("beta_at_update") = 0.0)
+      .def_readwrite("req_id", &QueueEntry::req_id)
+      .def_readwrite("key", &QueueEntry::key)
+      .def_readwrite("predicted", &QueueEntry::predicted)
+      .def_readwrite("expectation", &QueueEntry::expectation)
+      .def_readwrite("cvar", &QueueEntry::cvar)
+      .def_readwrite("beta_at_update", &QueueEntry::beta_at_update);
+  py::class_<WaitingQueue>(m, "WaitingQueue")
+      .def(py::init<const McContext*, size_t>(), py::arg("mc") = nullptr,
+           py::arg("initial_capacity") = 1024, py::keep_alive<1, 2>())
+      .def("push", &WaitingQueue::push, py::arg("entry"))
+      .def("update", &WaitingQueue::update, py::arg("req_id"), py::arg("key"))
+      .def("pop_min", &WaitingQueue::pop_min)
+      .def("contains", &WaitingQueue::contains, py::arg("req_id"))
+      .def("size", &WaitingQueue::size)
+      .def("empty", &WaitingQueue::empty)
+      .def("__len__", &WaitingQueue::size)
+      .def("at", [](const WaitingQueue& q, uint64_t id) { return q.at(id); }, py::arg("req_id"),
+           "a copy of the entry (use update() to re-key)")
+      .def("entries", [](const WaitingQueue& q) { return q.entries(); },
+           "copies of every waiting entry (slot order)")
+      .def("validate", &WaitingQueue::validate)
+      .def("push_batch",
+           [](WaitingQueue& q, carray<uint64_t> ids, carray<double> keys) {
+             if (keys.size() != ids.size()) throw py::value_error("push_batch: lengths differ");
+             std::vector<QueueEntry> e((size_t)ids.size());
+             for (size_t j = 0; j < e.size(); ++j) e[j] = QueueEntry{ids.data()[j], keys.data()[j]};
+             q.push_batch(e.data(), e.size());
+           },
+           py::arg("ids"), py::arg("keys"))
+      .def("update_batch",
+           [](WaitingQueue& q, carray<uint64_t> ids, carray<double> keys) {
+             if (keys.size() != ids.size()) throw py::value_error("update_batch: lengths differ");
+             q.update_batch(ids.data(), keys.data(), (size_t)ids.size());
+           },
+           py::arg("ids"), py::arg("keys"))
+      .def("pop_batch",
+           [](WaitingQueue& q, size_t k) {
+             const std::vector<QueueEntry> v = q.pop_batch(k);
+             carray<uint64_t> ids((py::ssize_t)v.size());
+             carray<double> keys((py::ssize_t)v.size());
+             for (size_t j = 0; j < v.size(); ++j) {
+               ids.mutable_data()[j] = v[j].req_id;
+               keys.mutable_data()[j] = v[j].key;
+             }
+             return py::make_tuple(ids, keys);
+           },
+           py::arg("max_pops"), "(ids, keys) of up to max_pops pop_min() calls");
+  py::class_<Scheduler>(m, "Scheduler")
+      .def(py::init<Policy, ScoreConfig, const McContext*, size_t>(), py::arg("policy"),
+           py::arg("config"), py::arg("mc") = nullptr, py::arg("initial_capacity") = 1024,
+           py::keep_alive<1, 4>())
+      .def("on_arrival", &Scheduler::on_arrival, py::arg("request"))
+      .def("on_prediction", &Scheduler::on_prediction, py::arg("req_id"), py::arg("expectation"),
+           py::arg("cvar"))
+      .def("rebuild_if_drifted", &Scheduler::rebuild_if_drifted)
+      .def("next_request", &Scheduler::next_request)
+      .def("waiting_on", &Scheduler::waiting_on, py::arg("req_id"))
+      .def("waiting", &Scheduler::waiting)
+      .def("current_beta", &Scheduler::current_beta)
+      .def("policy", &Scheduler::policy)
+      .def("queue", &Scheduler::queue, py::return_value_policy::reference_internal)
+      .def("on_arrival_batch",
+           [](Scheduler& s, const std::vector<Request>& reqs) {
+             s.on_arrival_batch(reqs.data(), reqs.size());
+           },
+           py::arg("requests"))
+      .def("on_prediction_batch",
+           [](Scheduler& s, carray<uint64_t> ids, carray<double> E, carray<double> C) {
+             if (E.size() != ids.size() || C.size() != ids.size())
+               throw py::value_error("on_prediction_batch: array lengths differ");
+             s.on_prediction_batch(ids.data(), E.data(), C.data(), (size_t)ids.size());
+           },
+           py::arg("ids"), py::arg("expectation"), py::arg("cvar"))
+      .def("next_requests",
+           [](Scheduler& s, size_t k) {
+             const std::vector<uint64_t> v = s.next_requests(k);
+             return carray<uint64_t>((py::ssize_t)v.size(), v.data());
+           },
+           py::arg("k"));
+
+  // ------------------------------------------------------------- predictor (predictor.hpp)
+  py::class_<PredictedDist>(m, "PredictedDist")
+      .def_readonly("mu_hat", &PredictedDist::mu_hat)
+      .def_readonly("sigma_hat", &PredictedDist::sigma_hat);
+  py::class_<NoiseSpec>(m, "NoiseSpec")
+      .def(py::init<>())
+      .def_readwrite("mu_sd", &NoiseSpec::mu_sd)
+      .def_readwrite("log_sigma_sd", &NoiseSpec::log_sigma_sd);
+  py::class_<BatcherConfig>(m, "BatcherConfig")
+      .def(py::init<>())
+      .def_readwrite("timeout_s", &BatcherConfig::timeout_s)
+      .def_readwrite("max_batch", &BatcherConfig::max_batch)
+      .def_readwrite("latency_base_s", &BatcherConfig::latency_base_s)
+      .def_readwrite("latency_per_item_s", &BatcherConfig::latency_per_item_s);
+  m.def("oracle_predict", &oracle_predict, py::arg("request"));
+  m.def("noisy_predict", &noisy_predict, py::arg("request"), py::arg("noise"), py::arg("seed"));
+  m.def("point_predict", &point_predict, py::arg("request"), py::arg("noise"), py::arg("seed"),
+        py::arg("mc"));
+  py::class_<Submission>(m, "Submission")
+      .def(py::init<uint64_t, double>(), py::arg("req_id"), py::arg("submit_s"))
+      .def_readonly("req_id", &Submission::req_id)
+      .def_readonly("submit_s", &Submission::submit_s);
+  py::class_<PredictionReady>(m, "PredictionReady")
+      .def_readonly("req_id", &PredictionReady::req_id)
+      .def_readonly("ready_s", &PredictionReady::ready_s);
+  m.def("batch_schedule", &batch_schedule, py::arg("submissions"), py::arg("config"));
+
+  // ------------------------------------------------------------- simulator (sim.hpp)
+  py::class_<EngineConfig>(m, "EngineConfig")
+      .def(py::init<>())
+      .def_readwrite("batch_slots", &EngineConfig::batch_slots)
+      .def_readwrite("c0", &EngineConfig::c0)
+      .def_readwrite("c1", &EngineConfig::c1)
+      .def_readwrite("c2", &EngineConfig::c2);
+  py::class_<PredictorConfig>(m, "PredictorConfig")
+      .def(py::init<>())
+      .def_readwrite("kind", &PredictorConfig::kind)
+      .def_readwrite("family", &PredictorConfig::family)
+      .def_readwrite("noise", &PredictorConfig::noise)
+      .def_readwrite("batched", &PredictorConfig::batched)
+      .def_readwrite("batcher", &PredictorConfig::batcher)
+      .def_readwrite("nu", &PredictorConfig::nu)
+      .def_readwrite("mc_samples", &PredictorConfig::mc_samples)
+      .def_readwrite("mc_seed", &PredictorConfig::mc_seed);
+  py::class_<RequestEvent>(m, "RequestEvent")
+      .def_readonly("req_id", &RequestEvent::req_id)
+      .def_readonly("arrival_s", &RequestEvent::arrival_s)
+      .def_readonly("predict_ready_s", &RequestEvent::predict_ready_s)
+      .def_readonly("admit_s", &RequestEvent::admit_s)
+      .def_readonly("first_token_s", &RequestEvent::first_token_s)
+      .def_readonly("completion_s", &RequestEvent::completion_s)
+      .def_readonly("emitted_tokens", &RequestEvent::emitted_tokens);
+  py::class_<Metrics>(m, "Metrics")
+      .def_readonly("ttft_avg", &Metrics::ttft_avg)
+      .def_readonly("ttft_p90", &Metrics::ttft_p90)
+      .def_readonly("ptla_avg", &Metrics::ptla_avg)
+      .def_readonly("ptla_p90", &Metrics::ptla_p90)
+      .def_readonly("time_at_k", &Metrics::time_at_k)
+      .def_readonly("throughput_at_w", &Metrics::throughput_at_w);
+  py::class_<HeatmapSpec>(m, "HeatmapSpec")
+      .def(py::init<>())
+      .def_readwrite("time_bins", &HeatmapSpec::time_bins)
+      .def_readwrite("len_bins", &HeatmapSpec::len_bins)
+      .def_readwrite("time_max", &HeatmapSpec::time_max)
+      .def_readwrite("len_max", &HeatmapSpec::len_max);
+  py::class_<Heatmap>(m, "Heatmap")
+      .def_readonly("spec", &Heatmap::spec)
+      .def_readonly("counts", &Heatmap::counts);
+  py::class_<SimReport>(m, "SimReport")
+      .def_readonly("seed", &SimReport::seed)
+      .def_readonly("policy", &SimReport::policy)
+      .def_readonly("events", &SimReport::events)
+      .def_readonly("metrics", &SimReport::metrics);
+  m.def(
+      "run_sim",
+      [](const std::vector<Request>& w, Policy policy, const ScoreConfig& sc,
+         const EngineConfig& ec, const PredictorConfig& pc, uint64_t seed,
+         const std::vector<uint64_t>& ks, const std::vector<double>& ws, int device) {
+        py::gil_scoped_release nogil;
+        return run_sim(w, policy, sc, ec, pc, seed, ks, ws, device);
+      },
+      py::arg("workload"), py::arg("policy"), py::arg("score_config"), py::arg("engine_config"),
+      py::arg("predictor_config"), py::arg("seed"), py::arg("ks") = std::vector<uint64_t>{},
+      py::arg("ws") = std::vector<double>{}, py::arg("device") = 0);
+  m.def("summarize", &summarize, py::arg("events"), py::arg("ks"), py::arg("ws"));
+  m.def("heatmap", &heatmap, py::arg("events"), py::arg("spec"));
 
   m.def("default_context", []() { return (uintptr_t)default_context(); });
   m.def("launch_count", [](bool reset) { return tie_launch_count(reset ? 1 : 0); },

@@ -775,6 +775,95 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
   }
 }
 
+// ---- WaitingQueue-level primitives (sched.cpp:59-123) ------------------------------------
+
+__device__ __forceinline__ double key_of_bits(uint64_t u) {  // inverse of order_bits
+  return __longlong_as_double((long long)((u >> 63) ? (u & 0x7fffffffffffffffull) : ~u));
+}
+
+// WaitingQueue::push x m: slots first..first+m with caller-given keys and entry fields
+__global__ void push_slots_kernel(QDev q, uint64_t first, uint64_t m, const uint64_t* ids,
+                                  const double* keys, const double* E, const double* C,
+                                  const uint8_t* predicted) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const uint64_t s = first + t;
+  q.key[s] = order_bits(keys[t]);
+  q.id[s] = ids[t];
+  q.E[s] = E ? E[t] : 0.0;
+  q.C[s] = C ? C[t] : 0.0;
+  q.predicted[s] = predicted ? predicted[t] : 0;
+}
+
+// WaitingQueue::update x m (and the entry write-back of rebuild): keys (and optionally the
+// entry fields) of existing slots
+__global__ void set_slots_kernel(QDev q, const uint32_t* slots, uint64_t m, const double* keys,
+                                 const double* E, const double* C, const uint8_t* predicted) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const uint32_t s = slots[t];
+  q.key[s] = order_bits(keys[t]);
+  if (E) q.E[s] = E[t];
+  if (C) q.C[s] = C[t];
+  if (predicted) q.predicted[s] = predicted[t];
+}
+
+// entries of the listed slots: key (decoded), E, C, predicted
+__global__ void gather_slots_kernel(QDev q, const uint32_t* slots, uint64_t m, double* key,
+                                    double* E, double* C, uint8_t* predicted) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const uint32_t s = slots[t];
+  key[t] = key_of_bits(q.key[s]);
+  E[t] = q.E[s];
+  C[t] = q.C[s];
+  predicted[t] = q.predicted[s];
+}
+
+// compaction / growth: new slot j <- old slot src[j] (j < m), dead beyond m up to cap
+__global__ void relayout_kernel(QDev dst, QDev src, const uint32_t* from, uint64_t m,
+                                uint64_t cap) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cap;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    if (j < m) {
+      const uint32_t s = from[j];
+      dst.key[j] = src.key[s];
+      dst.id[j] = src.id[s];
+      dst.E[j] = src.E[s];
+      dst.C[j] = src.C[s];
+      dst.predicted[j] = src.predicted[s];
+    } else {
+      dst.key[j] = kDead;
+      dst.id[j] = kDead;
+      dst.predicted[j] = 0;
+    }
+  }
+}
+
+// WaitingQueue::validate's device half: every block minimum equals a full rescan of its
+// block; bad[0] counts mismatching blocks
+__global__ void __launch_bounds__(256) validate_blocks_kernel(QDev q, uint32_t nb,
+                                                              uint64_t n_slots,
+                                                              unsigned int* bad) {
+  __shared__ uint64_t sk[32], si[32];
+  __shared__ uint32_t ss[32];
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    uint64_t k = kDead, i = kDead;
+    uint32_t s = 0;
+    for (uint32_t t = threadIdx.x; t < kBlockSlots; t += blockDim.x) {
+      const uint64_t slot = (uint64_t)b * kBlockSlots + t;
+      if (slot < n_slots && less_kv(q.key[slot], q.id[slot], k, i)) {
+        k = q.key[slot];
+        i = q.id[slot];
+        s = (uint32_t)slot;
+      }
+    }
+    block_argmin(k, i, s, sk, si, ss);
+    if (threadIdx.x == 0 && (q.bkey[b] != k || q.bid[b] != i || (k != kDead && q.bslot[b] != s)))
+      atomicAdd(bad, 1u);
+  }
+}
+
 }  // namespace
 }  // namespace dev
 }  // namespace tie
@@ -834,6 +923,8 @@ struct tie_queue {
   uint32_t* h_out_n = nullptr;
 };
 
+constexpr int kPolicyRaw = 3;  // a bare WaitingQueue: caller-given keys, no Scheduler rules
+
 namespace {
 
 double beta_at(const tie_queue* Q, uint64_t queue_len) {
@@ -868,7 +959,7 @@ uint64_t first_batch_duplicate(const uint64_t* ids, uint64_t m) {
 int check_arrivals(const tie_queue* Q, const uint64_t* ids, const double* arrival_s,
                    const uint32_t* max_tokens, uint64_t m, std::vector<double>& keys) {
   if (Q->n_slots + m > Q->capacity)
-    return set_error(TIE_EINVALID, "tie_queue_arrive: capacity exceeded");
+    return set_error(TIE_EINVALID, "tie_queue_arrive: capacity exceeded");  // see ensure_capacity
   keys.resize(m);
   const uint64_t dup = first_batch_duplicate(ids, m);
   for (uint64_t t = 0; t < m; ++t) {
@@ -976,6 +1067,81 @@ int refresh(tie_queue* Q, const std::vector<uint32_t>& slots, cudaStream_t s) {
                                                      Q->n_slots);
   tie::capi::count_launch();
   return TIE_OK;
+}
+
+// Slots are append-only, so a long-lived queue (the simulator, a server) periodically needs
+// a new layout: the live slots are gathered, in slot order, into arrays of `new_cap` slots --
+// a compaction when popped slots dominate, else a growth.  The pop order is unaffected (it
+// depends on (key, id) only); the host index is remapped and every block minimum rebuilt.
+int relayout(tie_queue* Q, uint64_t new_cap) {
+  namespace d = tie::dev;
+  cudaStream_t s = Q->ctx->stream;
+  std::vector<uint32_t> live;
+  live.reserve(Q->size);
+  for (uint64_t sl = 0; sl < Q->n_slots; ++sl)
+    if (Q->alive[sl]) live.push_back((uint32_t)sl);
+  const uint64_t m = live.size();
+  const uint64_t nb = (new_cap + d::kBlockSlots - 1) / d::kBlockSlots;
+  d::QDev nq{};
+  uint32_t* d_from = nullptr;
+  cudaError_t e;
+  if ((e = cudaMalloc(&nq.key, 8 * new_cap)) || (e = cudaMalloc(&nq.id, 8 * new_cap)) ||
+      (e = cudaMalloc(&nq.E, 8 * new_cap)) || (e = cudaMalloc(&nq.C, 8 * new_cap)) ||
+      (e = cudaMalloc(&nq.predicted, new_cap)) || (e = cudaMalloc(&nq.bkey, 8 * nb)) ||
+      (e = cudaMalloc(&nq.bid, 8 * nb)) || (e = cudaMalloc(&nq.bslot, 4 * nb)) ||
+      (e = cudaMalloc(&d_from, 4 * std::max<uint64_t>(m, 1)))) {
+    for (void* p : {(void*)nq.key, (void*)nq.id, (void*)nq.E, (void*)nq.C, (void*)nq.predicted,
+                    (void*)nq.bkey, (void*)nq.bid, (void*)nq.bslot, (void*)d_from})
+      cudaFree(p);
+    return cuda_error(e, "tie_queue: relayout allocation");
+  }
+  if (m) cudaMemcpyAsync(d_from, live.data(), 4 * m, cudaMemcpyHostToDevice, s);
+  d::relayout_kernel<<<(unsigned)std::min<uint64_t>((new_cap + 255) / 256, 148 * 16), 256, 0,
+                       s>>>(nq, Q->q, d_from, m, new_cap);
+  cudaMemsetAsync(nq.bkey, 0xff, 8 * nb, s);
+  cudaMemsetAsync(nq.bid, 0xff, 8 * nb, s);
+  const uint32_t used_nb = (uint32_t)((m + d::kBlockSlots - 1) / d::kBlockSlots);
+  if (used_nb)
+    d::refresh_blocks_kernel<<<std::min<uint32_t>(used_nb, 4096), 256, 0, s>>>(nq, nullptr,
+                                                                             used_nb, m);
+  tie::capi::count_launch(used_nb ? 2 : 1);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_error(e, "tie_queue: relayout");
+  cudaFree(d_from);
+  for (void* p : {(void*)Q->q.key, (void*)Q->q.id, (void*)Q->q.E, (void*)Q->q.C,
+                  (void*)Q->q.predicted, (void*)Q->q.bkey, (void*)Q->q.bid, (void*)Q->q.bslot})
+    cudaFree(p);
+  Q->q = nq;
+  // host mirror, remapped
+  std::vector<uint32_t> newpos(Q->n_slots, 0);
+  for (uint64_t j = 0; j < m; ++j) newpos[live[j]] = (uint32_t)j;
+  for (auto& kv : Q->slot_of) kv.second = newpos[kv.second];
+  std::vector<uint8_t> alive(new_cap, 0), pred(new_cap, 0);
+  std::vector<double> pbeta(new_cap, 0.0);
+  std::vector<uint32_t> pepoch(new_cap, 0);
+  for (uint64_t j = 0; j < m; ++j) {
+    alive[j] = 1;
+    pred[j] = Q->predicted[live[j]];
+    pbeta[j] = Q->pred_beta[live[j]];
+    pepoch[j] = Q->pred_epoch[live[j]];
+  }
+  Q->alive.swap(alive);
+  Q->predicted.swap(pred);
+  Q->pred_beta.swap(pbeta);
+  Q->pred_epoch.swap(pepoch);
+  Q->n_slots = m;
+  Q->capacity = new_cap;
+  return TIE_OK;
+}
+
+// room for m more slots: compact when at most half the capacity is live afterwards, else grow
+int ensure_capacity(tie_queue* Q, uint64_t m) {
+  if (Q->n_slots + m <= Q->capacity) return TIE_OK;
+  const uint64_t need = Q->size + m;
+  uint64_t cap = Q->capacity;
+  if (need > cap / 2) cap = std::max<uint64_t>(2 * cap, need + need / 2);
+  cap = std::min<uint64_t>(cap, (1ull << 32) - 1);
+  if (need > cap) return set_error(TIE_EINVALID, "tie_queue: more than 2^32 - 1 waiting entries");
+  return relayout(Q, cap);
 }
 
 void rebuild_launch(tie_queue* Q, double now, cudaStream_t s,
@@ -1183,7 +1349,8 @@ int tie_queue_create(tie_ctx* ctx, int policy, int adaptive, double beta_fixed, 
                      double q_sat, double rebuild_threshold, double alpha, uint64_t capacity,
                      tie_queue** out) {
   if (!ctx || !out) return set_error(TIE_EINVALID, "tie_queue_create: null argument");
-  if (policy < 0 || policy > 2) return set_error(TIE_EINVALID, "tie_queue_create: bad policy");
+  if (policy < 0 || policy > kPolicyRaw)
+    return set_error(TIE_EINVALID, "tie_queue_create: bad policy");
   if (!(alpha >= 0.0 && alpha < 1.0))
     return set_error(TIE_EDOMAIN, "censored_cvar: alpha must lie in [0, 1)");
   if (capacity == 0 || capacity >= (1ull << 32))
@@ -1249,9 +1416,12 @@ double tie_queue_current_beta(const tie_queue* Q) { return Q ? beta_at(Q, Q->siz
 int tie_queue_arrive(tie_queue* Q, const uint64_t* ids, const double* arrival_s,
                      const uint32_t* max_tokens, uint64_t m) {
   if (!Q) return set_error(TIE_EINVALID, "tie_queue: null queue");
+  if (Q->policy == kPolicyRaw)
+    return set_error(TIE_EINVALID, "tie_queue: a WaitingQueue has no Scheduler operations");
   if (m == 0) return TIE_OK;
   // validate the whole batch before any host state changes (a rejected batch leaves the
   // queue untouched)
+  if (int rc = ensure_capacity(Q, m)) return rc;
   std::vector<double> keys;
   if (int rc = check_arrivals(Q, ids, arrival_s, max_tokens, m, keys)) return rc;
   for (uint64_t t = 0; t < m; ++t) Q->slot_of.emplace(ids[t], (uint32_t)(Q->n_slots + t));
@@ -1277,6 +1447,8 @@ int tie_queue_arrive(tie_queue* Q, const uint64_t* ids, const double* arrival_s,
 int tie_queue_predict(tie_queue* Q, const uint64_t* ids, const double* E, const double* C,
                       uint64_t m) {
   if (!Q) return set_error(TIE_EINVALID, "tie_queue: null queue");
+  if (Q->policy == kPolicyRaw)
+    return set_error(TIE_EINVALID, "tie_queue: a WaitingQueue has no Scheduler operations");
   if (m == 0) return TIE_OK;
   std::vector<uint32_t> slots;
   double beta = 0.0;
@@ -1356,12 +1528,15 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
                    uint64_t n_pred, uint64_t max_pops, uint64_t* out_ids, uint64_t* n_out) {
   if (!Q || !n_out) return set_error(TIE_EINVALID, "tie_queue: null argument");
   *n_out = 0;
+  if (Q->policy == kPolicyRaw)
+    return set_error(TIE_EINVALID, "tie_queue: a WaitingQueue has no Scheduler operations");
   tie_ctx* ctx = Q->ctx;
   cudaStream_t s = ctx->stream;
   // ---- host validation of the whole step before any host state changes: the arrivals
   // (tie_queue_arrive), then the predictions with this step's arrivals counted as waiting
   // (tie_queue_predict).  A prediction error leaves the arrivals applied, as the reference's
   // on_arrival calls stay applied when a later on_prediction throws.
+  if (int rc = ensure_capacity(Q, n_arr)) return rc;
   std::vector<double> akeys;
   if (int rc = check_arrivals(Q, arr_ids, arr_time, arr_max_tokens, n_arr, akeys)) return rc;
   const uint64_t first = Q->n_slots;
@@ -1661,5 +1836,321 @@ int tie_queue_rebuild_if_drifted(tie_queue* Q, int* rebuilt) {
   const cudaError_t e = cudaStreamSynchronize(Q->ctx->stream);
   return e == cudaSuccess ? TIE_OK : cuda_error(e, "tie_queue_rebuild_if_drifted");
 }
+
+// ---- WaitingQueue (sched.hpp:43-68, sched.cpp:28-123) ------------------------------------
+
+int tie_queue_contains(const tie_queue* Q, uint64_t id) {
+  return Q && Q->slot_of.count(id) ? 1 : 0;
+}
+
+// WaitingQueue::push x m (sched.cpp:59-67); predicted / E / C / beta_at_update may be NULL
+int tie_queue_push(tie_queue* Q, const uint64_t* ids, const double* keys,
+                   const uint8_t* predicted, const double* E, const double* C,
+                   const double* beta_at_update, uint64_t m) {
+  if (!Q) return set_error(TIE_EINVALID, "tie_queue: null queue");
+  if (Q->policy != kPolicyRaw)
+    return set_error(TIE_EINVALID, "tie_queue_push: a Scheduler's queue is keyed by its policy");
+  if (m == 0) return TIE_OK;
+  if (!ids || !keys) return set_error(TIE_EINVALID, "tie_queue_push: null argument");
+  if (int rc = ensure_capacity(Q, m)) return rc;
+  const uint64_t dup = first_batch_duplicate(ids, m);
+  for (uint64_t t = 0; t < m; ++t) {
+    if (!std::isfinite(keys[t]))
+      return set_error(TIE_EDOMAIN, "WaitingQueue::push: key must be finite");
+    if (t == dup || Q->slot_of.count(ids[t]))
+      return set_error(TIE_EINVALID, "WaitingQueue::push: id " + std::to_string(ids[t]) +
+                                         " already queued");
+  }
+  cudaStream_t s = Q->ctx->stream;
+  if (int rc = ensure_stage(Q, m)) return rc;
+  const uint64_t first = Q->n_slots;
+  // staging: ids | keys | E | C | predicted (u8 packed into d_slots' bytes)
+  cudaMemcpyAsync(Q->d_ids, ids, 8 * m, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(Q->d_a, keys, 8 * m, cudaMemcpyHostToDevice, s);
+  if (E) cudaMemcpyAsync(Q->d_b, E, 8 * m, cudaMemcpyHostToDevice, s);
+  if (C) cudaMemcpyAsync(Q->d_c, C, 8 * m, cudaMemcpyHostToDevice, s);
+  if (predicted) cudaMemcpyAsync(Q->d_slots, predicted, m, cudaMemcpyHostToDevice, s);
+  tie::dev::push_slots_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(
+      Q->q, first, m, Q->d_ids, Q->d_a, E ? Q->d_b : nullptr, C ? Q->d_c : nullptr,
+      predicted ? (const uint8_t*)Q->d_slots : nullptr);
+  tie::capi::count_launch();
+  std::vector<uint32_t> touched;
+  for (uint64_t t = 0; t < m; ++t) {
+    const uint32_t sl = (uint32_t)(first + t);
+    Q->slot_of.emplace(ids[t], sl);
+    Q->alive[sl] = 1;
+    Q->predicted[sl] = predicted && predicted[t] ? 1 : 0;
+    Q->pred_beta[sl] = beta_at_update ? beta_at_update[t] : 0.0;
+    Q->pred_epoch[sl] = Q->epoch;
+    if (Q->predicted[sl]) ++Q->n_predicted;
+  }
+  for (uint64_t t = 0; t < m; t += tie::dev::kBlockSlots) touched.push_back((uint32_t)(first + t));
+  touched.push_back((uint32_t)(first + m - 1));
+  Q->n_slots += m;
+  Q->size += m;
+  if (int rc = refresh(Q, touched, s)) return rc;
+  const cudaError_t e = cudaStreamSynchronize(s);
+  return e == cudaSuccess ? TIE_OK : cuda_error(e, "tie_queue_push");
+}
+
+namespace {
+
+// write keys (and, when given, entry fields) of waiting entries; `who` names the reference
+// operation for the error messages.  Repeated ids: the last write wins, as sequential calls.
+int write_entries(tie_queue* Q, const uint64_t* ids, const double* keys, const uint8_t* pred,
+                  const double* E, const double* C, const double* beta, uint64_t m,
+                  const char* who) {
+  if (!Q) return set_error(TIE_EINVALID, "tie_queue: null queue");
+  if (Q->policy != kPolicyRaw)
+    return set_error(TIE_EINVALID, std::string(who) + ": a Scheduler's queue is keyed by its policy");
+  if (m == 0) return TIE_OK;
+  if (!ids || !keys) return set_error(TIE_EINVALID, std::string(who) + ": null argument");
+  std::vector<uint32_t> slots(m);
+  for (uint64_t t = 0; t < m; ++t) {  // update(): finiteness, then the id (sched.cpp:69-74)
+    if (!std::isfinite(keys[t]))
+      return set_error(TIE_EDOMAIN, std::string(who) + ": key must be finite");
+    auto it = Q->slot_of.find(ids[t]);
+    if (it == Q->slot_of.end())
+      return set_error(TIE_EINVALID, std::string(who) + ": id " + std::to_string(ids[t]) +
+                                         " not queued");
+    slots[t] = it->second;
+  }
+  // keep the last occurrence of each slot
+  std::vector<uint64_t> keep;
+  {
+    std::unordered_map<uint32_t, uint64_t> last;
+    for (uint64_t t = 0; t < m; ++t) last[slots[t]] = t;
+    keep.reserve(last.size());
+    for (uint64_t t = 0; t < m; ++t)
+      if (last[slots[t]] == t) keep.push_back(t);
+  }
+  const uint64_t k = keep.size();
+  std::vector<uint32_t> ks(k);
+  std::vector<double> kk(k), ke, kc;
+  std::vector<uint8_t> kp;
+  if (E) ke.resize(k);
+  if (C) kc.resize(k);
+  if (pred) kp.resize(k);
+  for (uint64_t j = 0; j < k; ++j) {
+    const uint64_t t = keep[j];
+    ks[j] = slots[t];
+    kk[j] = keys[t];
+    if (E) ke[j] = E[t];
+    if (C) kc[j] = C[t];
+    if (pred) kp[j] = pred[t] ? 1 : 0;
+  }
+  cudaStream_t s = Q->ctx->stream;
+  if (int rc = ensure_stage(Q, k)) return rc;
+  cudaMemcpyAsync(Q->d_slots, ks.data(), 4 * k, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(Q->d_a, kk.data(), 8 * k, cudaMemcpyHostToDevice, s);
+  if (E) cudaMemcpyAsync(Q->d_b, ke.data(), 8 * k, cudaMemcpyHostToDevice, s);
+  if (C) cudaMemcpyAsync(Q->d_c, kc.data(), 8 * k, cudaMemcpyHostToDevice, s);
+  if (pred) cudaMemcpyAsync(Q->d_ids, kp.data(), k, cudaMemcpyHostToDevice, s);
+  tie::dev::set_slots_kernel<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(
+      Q->q, Q->d_slots, k, Q->d_a, E ? Q->d_b : nullptr, C ? Q->d_c : nullptr,
+      pred ? (const uint8_t*)Q->d_ids : nullptr);
+  tie::capi::count_launch();
+  for (uint64_t j = 0; j < k; ++j) {
+    const uint32_t sl = ks[j];
+    if (pred) {
+      if (Q->predicted[sl] && !kp[j]) --Q->n_predicted;
+      if (!Q->predicted[sl] && kp[j]) ++Q->n_predicted;
+      Q->predicted[sl] = kp[j];
+    }
+    if (beta) {
+      Q->pred_beta[sl] = beta[keep[j]];
+      Q->pred_epoch[sl] = Q->epoch;
+    }
+  }
+  if (int rc = refresh(Q, ks, s)) return rc;
+  const cudaError_t e = cudaStreamSynchronize(s);
+  return e == cudaSuccess ? TIE_OK : cuda_error(e, who);
+}
+
+}  // namespace
+
+// WaitingQueue::update x m (sched.cpp:69-79)
+int tie_queue_update(tie_queue* Q, const uint64_t* ids, const double* keys, uint64_t m) {
+  return write_entries(Q, ids, keys, nullptr, nullptr, nullptr, nullptr, m,
+                       "WaitingQueue::update");
+}
+
+// entry write-back (the edits WaitingQueue::entries() / at() hand out, then rebuild(),
+// sched.cpp:110-114)
+int tie_queue_set_entries(tie_queue* Q, const uint64_t* ids, const double* keys,
+                          const uint8_t* predicted, const double* E, const double* C,
+                          const double* beta_at_update, uint64_t m) {
+  return write_entries(Q, ids, keys, predicted, E, C, beta_at_update, m, "WaitingQueue::rebuild");
+}
+
+namespace {
+
+int gather_entries(tie_queue* Q, const std::vector<uint32_t>& slots, uint64_t* ids,
+                   double* keys, uint8_t* predicted, double* E, double* C, double* beta) {
+  const uint64_t m = slots.size();
+  if (m == 0) return TIE_OK;
+  cudaStream_t s = Q->ctx->stream;
+  if (int rc = ensure_stage(Q, m)) return rc;
+  std::vector<double> k(m), e(m), c(m);
+  std::vector<uint8_t> p(m);
+  std::vector<uint64_t> id(m);
+  cudaMemcpyAsync(Q->d_slots, slots.data(), 4 * m, cudaMemcpyHostToDevice, s);
+  tie::dev::gather_slots_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(
+      Q->q, Q->d_slots, m, Q->d_a, Q->d_b, Q->d_c, (uint8_t*)Q->d_blocks);
+  tie::capi::count_launch();
+  cudaMemcpyAsync(k.data(), Q->d_a, 8 * m, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(e.data(), Q->d_b, 8 * m, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(c.data(), Q->d_c, 8 * m, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(p.data(), Q->d_blocks, m, cudaMemcpyDeviceToHost, s);
+  const cudaError_t err = cudaStreamSynchronize(s);
+  if (err != cudaSuccess) return cuda_error(err, "tie_queue: entry read");
+  for (uint64_t t = 0; t < m; ++t) {
+    if (keys) keys[t] = k[t];
+    if (E) E[t] = e[t];
+    if (C) C[t] = c[t];
+    if (predicted) predicted[t] = p[t];
+    if (beta) {  // a Scheduler's unpredicted entries keep QueueEntry's default 0
+      const uint32_t sl = slots[t];
+      beta[t] = Q->policy == kPolicyRaw ? Q->pred_beta[sl]
+                                         : (Q->predicted[sl] ? Q->beta_of(sl) : 0.0);
+    }
+  }
+  (void)ids;
+  return TIE_OK;
+}
+
+}  // namespace
+
+// WaitingQueue::at x m (sched.cpp:96-108): the entries of waiting ids; any output may be NULL
+int tie_queue_get(tie_queue* Q, const uint64_t* ids, uint64_t m, double* keys,
+                  uint8_t* predicted, double* E, double* C, double* beta_at_update) {
+  if (!Q) return set_error(TIE_EINVALID, "tie_queue: null queue");
+  std::vector<uint32_t> slots(m);
+  for (uint64_t t = 0; t < m; ++t) {
+    auto it = Q->slot_of.find(ids[t]);
+    if (it == Q->slot_of.end())
+      return set_error(TIE_EINVALID, "WaitingQueue::at: id " + std::to_string(ids[t]) +
+                                         " not queued");
+    slots[t] = it->second;
+  }
+  return gather_entries(Q, slots, nullptr, keys, predicted, E, C, beta_at_update);
+}
+
+// WaitingQueue::entries() (sched.hpp:60-61): every waiting entry, in slot (arrival) order --
+// the reference hands out its heap array, whose order is unspecified as well
+int tie_queue_entries(tie_queue* Q, uint64_t cap, uint64_t* ids, double* keys,
+                      uint8_t* predicted, double* E, double* C, double* beta_at_update,
+                      uint64_t* n_out) {
+  if (!Q || !n_out) return set_error(TIE_EINVALID, "tie_queue: null argument");
+  *n_out = 0;
+  std::vector<std::pair<uint32_t, uint64_t>> live;
+  live.reserve(Q->size);
+  for (const auto& kv : Q->slot_of) live.push_back({kv.second, kv.first});
+  std::sort(live.begin(), live.end());
+  if (live.size() > cap) return set_error(TIE_EINVALID, "tie_queue_entries: buffer too small");
+  std::vector<uint32_t> slots(live.size());
+  for (size_t j = 0; j < live.size(); ++j) {
+    slots[j] = live[j].first;
+    if (ids) ids[j] = live[j].second;
+  }
+  if (int rc = gather_entries(Q, slots, nullptr, keys, predicted, E, C, beta_at_update)) return rc;
+  *n_out = live.size();
+  return TIE_OK;
+}
+
+// WaitingQueue::pop_min() x max_pops (sched.cpp:81-94) with the popped entries (raw queues;
+// a Scheduler pops through tie_queue_next).  Any output but ids / n_out may be NULL.
+int tie_queue_pop(tie_queue* Q, uint64_t max_pops, uint64_t* ids, double* keys,
+                  uint8_t* predicted, double* E, double* C, double* beta_at_update,
+                  uint64_t* n_out) {
+  if (!Q || !n_out) return set_error(TIE_EINVALID, "tie_queue: null argument");
+  *n_out = 0;
+  if (Q->policy != kPolicyRaw)
+    return set_error(TIE_EINVALID, "tie_queue_pop: a Scheduler pops through next_request");
+  const uint64_t k = std::min<uint64_t>(max_pops, Q->size);
+  if (!k) return TIE_OK;
+  const uint64_t nseg = (k + tie::dev::kTopB - 1) / tie::dev::kTopB;
+  if (int rc = ensure_out(Q, std::max<uint64_t>(k, nseg + 1))) return rc;
+  if (k > Q->peek_cap) {
+    cudaFreeHost(Q->h_peek_key);
+    Q->h_peek_key = nullptr;
+    Q->peek_cap = 0;
+    const cudaError_t e = cudaHostAlloc((void**)&Q->h_peek_key, 8 * std::max<uint64_t>(k, 256),
+                                        cudaHostAllocMapped);
+    if (e != cudaSuccess) return cuda_error(e, "tie_queue_pop: allocation");
+    Q->peek_cap = std::max<uint64_t>(k, 256);
+  }
+  cudaStream_t s = Q->ctx->stream;
+  const uint32_t nb = (uint32_t)((Q->n_slots + tie::dev::kBlockSlots - 1) / tie::dev::kBlockSlots);
+  uint64_t off = 0;
+  for (uint64_t g = 0; g < nseg; ++g) {
+    const uint32_t cnt = (uint32_t)std::min<uint64_t>(tie::dev::kTopB, k - off);
+    tie::dev::pop_topb_kernel<<<1, 1024, 0, s>>>(Q->q, nb, Q->n_slots, cnt, Q->d_out_id + off,
+                                                 Q->d_out_slot + off, Q->d_out_n + g,
+                                                 Q->h_peek_key + off);
+    off += cnt;
+  }
+  tie::capi::count_launch(nseg);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_error(e, "tie_queue_pop");
+  std::vector<uint32_t> slots(k);
+  for (uint64_t j = 0; j < k; ++j) slots[j] = Q->h_out_slot[j];
+  std::vector<double> pk(k);
+  for (uint64_t j = 0; j < k; ++j) {
+    const uint64_t u = Q->h_peek_key[j];  // order_bits image of the popped key
+    const uint64_t b = (u >> 63) ? (u & 0x7fffffffffffffffull) : ~u;
+    std::memcpy(&pk[j], &b, 8);
+  }
+  // entry fields survive the pop on the device (only the key slot is killed)
+  if (int rc = gather_entries(Q, slots, nullptr, nullptr, predicted, E, C, beta_at_update))
+    return rc;
+  std::vector<uint64_t> got;
+  apply_pops(Q, 0, (uint32_t)k, got);
+  for (uint64_t j = 0; j < k; ++j) {
+    ids[j] = got[j];
+    if (keys) keys[j] = pk[j];
+  }
+  *n_out = k;
+  return TIE_OK;
+}
+
+// WaitingQueue::validate() (sched.cpp:116-123): host index consistency (the id -> slot map
+// covers exactly the live slots) and every device block minimum equal to a rescan
+int tie_queue_validate(tie_queue* Q, int* ok) {
+  if (!Q || !ok) return set_error(TIE_EINVALID, "tie_queue: null argument");
+  *ok = 0;
+  uint64_t live = 0;
+  for (uint64_t sl = 0; sl < Q->n_slots; ++sl) live += Q->alive[sl];
+  if (live != Q->size || Q->slot_of.size() != Q->size) return TIE_OK;
+  for (const auto& kv : Q->slot_of)
+    if (kv.second >= Q->n_slots || !Q->alive[kv.second]) return TIE_OK;
+  const uint32_t nb = (uint32_t)((Q->n_slots + tie::dev::kBlockSlots - 1) / tie::dev::kBlockSlots);
+  if (nb) {
+    cudaStream_t s = Q->ctx->stream;
+    if (int rc = ensure_stage(Q, 1)) return rc;
+    unsigned int bad = 0;
+    cudaMemsetAsync(Q->d_blocks, 0, 4, s);
+    tie::dev::validate_blocks_kernel<<<std::min<uint32_t>(nb, 4096), 256, 0, s>>>(
+        Q->q, nb, Q->n_slots, Q->d_blocks);
+    tie::capi::count_launch();
+    cudaMemcpyAsync(&bad, Q->d_blocks, 4, cudaMemcpyDeviceToHost, s);
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_error(e, "tie_queue_validate");
+    if (bad) return TIE_OK;
+  }
+  *ok = 1;
+  return TIE_OK;
+}
+
+// slot-count management: compact the live entries into `capacity` slots (>= waiting)
+int tie_queue_reserve(tie_queue* Q, uint64_t capacity) {
+  if (!Q) return set_error(TIE_EINVALID, "tie_queue: null queue");
+  if (capacity < Q->size || capacity == 0 || capacity >= (1ull << 32))
+    return set_error(TIE_EINVALID, "tie_queue_reserve: capacity must be in [waiting, 2^32)");
+  return relayout(Q, capacity);
+}
+
+uint64_t tie_queue_capacity(const tie_queue* Q) { return Q ? Q->capacity : 0; }
+uint64_t tie_queue_slots_used(const tie_queue* Q) { return Q ? Q->n_slots : 0; }
 
 }  // extern "C"

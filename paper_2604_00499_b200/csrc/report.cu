@@ -21,6 +21,7 @@
 #include <cmath>
 #include <vector>
 
+#include "../../include/tie_cuda.h"
 #include "tdist.cuh"
 #include "tie_internal.cuh"
 
@@ -33,6 +34,7 @@ constexpr int kGrid = 19;       // default_nu_grid (fit.cpp:180-184)
 constexpr int kLocalK = 64;     // rows up to this length are sorted in thread-local memory
 
 enum { F_MU, F_SIGMA, F_NU, F_RATE, F_LL, F_ITERS, F_CONV, F_DEGEN, F_KSD, F_KSP };
+constexpr unsigned kGiven = 0x10000u;  // families flag: the fits are inputs (tie_ks_test_fit)
 
 struct FitTmp {
   double* mu;
@@ -81,10 +83,11 @@ template <class Row>
 __device__ void stats_one(const StatsArgs& a, uint64_t p, const double* x, Row s) {
   const int K = a.K;
   const uint64_t P = a.P;
+  const bool given = a.families & kGiven;  // ks_test(x, fit_cdf(fit, .)) of caller fits only
   // ks_test / tail_stats sort a copy of the row (insertion sort: K is small)
   for (int i = 0; i < K; ++i) {
     s[i] = x[i];
-    if (!(x[i] > 0.0) || !isfinite(x[i])) report(a.err, p, kSampleBad);  // check_samples
+    if (!given && (!(x[i] > 0.0) || !isfinite(x[i]))) report(a.err, p, kSampleBad);  // check_samples
   }
   for (int i = 1; i < K; ++i) {
     const double v = s[i];
@@ -100,7 +103,11 @@ __device__ void stats_one(const StatsArgs& a, uint64_t p, const double* x, Row s
     if (!(a.families >> f & 1)) continue;
     double* o = a.fits + (uint64_t)f * kFields * P;
     double mu = 0.0, sigma = 0.0, rate = 0.0;
-    if (f == 2) {  // fit_lognormal (fit.cpp:202-230)
+    if (given) {
+      mu = o[F_MU * P + p];
+      sigma = o[F_SIGMA * P + p];
+      rate = o[F_RATE * P + p];
+    } else if (f == 2) {  // fit_lognormal (fit.cpp:202-230)
       double mean = 0.0;
       for (int i = 0; i < K; ++i) mean += log(x[i]);
       mean /= n;
@@ -149,7 +156,7 @@ __device__ void stats_one(const StatsArgs& a, uint64_t p, const double* x, Row s
     }
     // constants of the fit's nu for the log-t CDF
     const TdistConst* td = a.td;
-    if (f == 1) {
+    if (f == 1 && !given) {
       const int g = (int)llrint((o[F_NU * P + p] - a.grid0) / a.grid_step);
       td = a.td + 1 + min(max(g, 0), kGrid - 1);
     }
@@ -271,13 +278,13 @@ cudaError_t launch_fit_report(tie_ctx* ctx, const double* x, uint64_t P, uint64_
   TdistConst* d_td = (TdistConst*)((char*)rows + rows_bytes);
   cudaMemcpyAsync(d_td, tds.data(), sizeof(TdistConst) * tds.size(), cudaMemcpyHostToDevice, s);
   const unsigned g = (unsigned)((P + 255) / 256);
-  if (families & 1u) {
+  if ((families & 1u) && !(families & kGiven)) {
     if ((e = launch_fit(ctx, x, P, K, nu, t.mu, t.sigma, t.ll, t.iters, t.conv, t.degen, s)))
       return e;
     keep_fit_kernel<<<g, 256, 0, s>>>(t, P, nu, 1, fits);
     capi::count_launch();
   }
-  if (families & 2u) {
+  if ((families & 2u) && !(families & kGiven)) {
     double* fam = fits + (uint64_t)1 * kFields * P;
     for (size_t i = 0; i < grid.size(); ++i) {
       if ((e = launch_fit(ctx, x, P, K, grid[i], t.mu, t.sigma, t.ll, t.iters, t.conv, t.degen,
@@ -313,3 +320,46 @@ cudaError_t launch_fit_report(tie_ctx* ctx, const double* x, uint64_t P, uint64_
 
 }  // namespace dev
 }  // namespace tie
+
+using tie::capi::set_error;
+
+// ks_test(x, fit_cdf(fit, .)) (fit.cpp:245-284) for one caller-given fit: the report kernel's
+// KS pass with the fit as input.  family: 0 LogTFixedNu, 1 LogTFreeNu, 2 LogNormal,
+// 3 Exponential (fit.hpp:11).
+extern "C" int tie_ks_test_fit_host(tie_ctx* ctx, const double* x, uint64_t K, int family,
+                                    double mu, double sigma, double nu, double rate,
+                                    double* statistic, double* p_value) {
+  if (!ctx || !x || !statistic || !p_value)
+    return set_error(TIE_EINVALID, "tie_ks_test_fit_host: null argument");
+  if (K < 5) return set_error(TIE_EINVALID, "ks_test: need at least 5 samples");
+  if (family < 0 || family > 3) return set_error(TIE_EINVALID, "ks_test_fit: bad family");
+  const bool logt = family <= 1;
+  if (logt && (!(nu > 0.0) || !std::isfinite(nu)))
+    return set_error(TIE_EDOMAIN, "t_cdf: nu must be finite and > 0");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const uint64_t nf = 4 * tie::dev::kFields;
+  std::vector<double> fits(nf, 0.0);
+  double* o = fits.data() + (uint64_t)family * tie::dev::kFields;
+  o[tie::dev::F_MU] = mu;
+  o[tie::dev::F_SIGMA] = sigma;
+  o[tie::dev::F_NU] = nu;
+  o[tie::dev::F_RATE] = rate;
+  double* d = nullptr;
+  if (cudaMalloc(&d, 8 * (K + nf)) != cudaSuccess)
+    return set_error(TIE_ECUDA, "tie_ks_test_fit_host: device allocation failed");
+  cudaMemcpyAsync(d, x, 8 * K, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d + K, fits.data(), 8 * nf, cudaMemcpyHostToDevice, s);
+  ctx->err_op = "ks_test";
+  cudaError_t e = tie::dev::launch_fit_report(ctx, d, 1, K, logt ? nu : 3.5,
+                                              (1u << family) | tie::dev::kGiven, d + K, nullptr, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(fits.data(), d + K, 8 * nf, cudaMemcpyDeviceToHost, s);
+  int rc = e == cudaSuccess ? tie_sync(ctx, s) : tie::capi::cuda_error(e, "ks_test_fit");
+  cudaStreamSynchronize(s);
+  cudaFree(d);
+  if (rc) return rc;
+  *statistic = o[tie::dev::F_KSD];
+  *p_value = o[tie::dev::F_KSP];
+  return TIE_OK;
+}

@@ -48,9 +48,9 @@ CensoredLogT::CensoredLogT(LogTParams d, double x_max_) : dist(d), x_max(x_max_)
 
 McContext::McContext(double nu_, int n_samples, uint64_t seed_, int device)
     : nu(nu_), seed(seed_) {
-  samples_ = host::mc_samples(nu, n_samples, seed);  // throws std::domain_error
+  samples = host::mc_samples(nu, n_samples, seed);  // throws std::domain_error
   tie_ctx* raw = nullptr;
-  throw_code(tie_ctx_create(device, samples_.data(), n_samples, nu, 0.0, &raw));
+  throw_code(tie_ctx_create(device, samples.data(), n_samples, nu, 0.0, &raw));
   ctx_.reset(raw, tie_ctx_destroy);
 }
 
@@ -59,7 +59,7 @@ McContext::McContext(const double* sorted_samples, int n_samples, double nu_, in
   tie_ctx* raw = nullptr;
   throw_code(tie_ctx_create(device, sorted_samples, n_samples, nu, 0.0, &raw));
   ctx_.reset(raw, tie_ctx_destroy);
-  samples_.assign(sorted_samples, sorted_samples + n_samples);
+  samples.assign(sorted_samples, sorted_samples + n_samples);
 }
 
 double t_pdf(double y, double nu) { return host::t_pdf(y, nu); }
@@ -68,6 +68,72 @@ double t_quantile(double p, double nu) { return host::t_quantile(p, nu); }
 
 std::vector<double> sample_logt(const LogTParams& p, size_t n, uint64_t seed) {
   return host::sample_logt(p.mu, p.sigma, p.nu, n, seed);
+}
+
+std::vector<double> eval_batch(int op, const double* a, const double* b, const double* c,
+                               size_t n, double param, const McContext* mc) {
+  std::vector<double> out(n);
+  tie_ctx* ctx = mc ? mc->handle() : default_context();
+  throw_code(tie_eval_host(ctx, op, a, b, c, n, param, out.data()));
+  return out;
+}
+
+namespace {
+
+double eval1(int op, double a, double b, double c, double param, const McContext* mc = nullptr) {
+  return eval_batch(op, &a, &b, &c, 1, param, mc)[0];
+}
+
+}  // namespace
+
+double regularized_incomplete_beta(double a, double b, double x) {
+  return eval1(TIE_EVAL_INCBETA, a, b, x, 0.0);
+}
+double logt_pdf(double x, const LogTParams& p) {
+  return eval1(TIE_EVAL_LOGT_PDF, x, p.mu, p.sigma, p.nu);
+}
+double logt_cdf(double x, const LogTParams& p) {
+  return eval1(TIE_EVAL_LOGT_CDF, x, p.mu, p.sigma, p.nu);
+}
+double psi(double y, const LogTParams& p, const McContext& mc) {
+  return eval1(TIE_EVAL_PSI, y, p.mu, p.sigma, p.nu, &mc);
+}
+double normal_cdf(double z) { return eval1(TIE_EVAL_NORMAL_CDF, z, 0.0, 0.0, 0.0); }
+double normal_quantile(double p) { return eval1(TIE_EVAL_NORMAL_QUANTILE, p, 0.0, 0.0, 0.0); }
+double lognormal_censored_expectation(double mu, double sigma, double x_max) {
+  return eval1(TIE_EVAL_LOGNORMAL_E, mu, sigma, x_max, 0.0);
+}
+double lognormal_censored_cvar(double mu, double sigma, double x_max, double alpha) {
+  return eval1(TIE_EVAL_LOGNORMAL_CVAR, mu, sigma, x_max, alpha);
+}
+
+std::vector<double> poisson_arrivals(double rps, size_t n, uint64_t seed) {
+  if (!(rps > 0.0) || !std::isfinite(rps))
+    throw std::domain_error("poisson_arrivals: rps must be finite and > 0");
+  host::Sampler r(seed);
+  std::vector<double> out(n);
+  double t = 0.0;
+  for (double& a : out) a = (t += r.exponential(rps));
+  return out;
+}
+
+std::vector<Request> gen_logt_workload(const WorkloadSpec& spec, uint64_t seed) {
+  const host::Workload w = host::gen_logt_workload(
+      spec.n_requests, seed, spec.mu_range.first, spec.mu_range.second, spec.sigma_range.first,
+      spec.sigma_range.second, spec.nu, spec.prompt_range.first, spec.prompt_range.second,
+      spec.max_tokens, spec.rps);
+  std::vector<Request> out(spec.n_requests);
+  for (size_t i = 0; i < out.size(); ++i) {
+    Request& r = out[i];
+    r.id = i;
+    r.arrival_s = w.arrival[i];
+    r.prompt_tokens = w.prompt_tokens[i];
+    r.true_output_tokens = w.true_len[i];
+    r.max_tokens = w.max_tokens[i];
+    r.true_mu = w.mu[i];
+    r.true_sigma = w.sigma[i];
+  }
+  return out;
 }
 
 namespace {

@@ -351,3 +351,62 @@ def fnv1a64_np(arr) -> str:
         for byte in b:
             h = (h ^ np.uint64(byte)) * prime
     return f"{int(h):016x}"
+
+
+# ---- the reference's per-item API, run_sim and ks_test_fit (oracle/ref_harness.cpp)
+EVAL_OPS = {"psi": 1, "regularized_incomplete_beta": 2, "t_pdf": 3, "t_cdf": 4, "logt_pdf": 5,
+            "logt_cdf": 6, "normal_cdf": 7, "normal_quantile": 8,
+            "lognormal_censored_expectation": 9, "lognormal_censored_cvar": 10}
+
+
+def ref_eval(R, fn, a, b=None, c=None, param=0.0):
+    f = R._fn("eval", [_i32, _p, _p, _p, _u64, _d, _p])
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.zeros_like(a) if b is None else np.ascontiguousarray(b, np.float64)
+    c = np.zeros_like(a) if c is None else np.ascontiguousarray(c, np.float64)
+    out = np.empty_like(a)
+    R._check(f(EVAL_OPS[fn], _ptr(a), _ptr(b), _ptr(c), len(a), param, _ptr(out)), "eval")
+    return out
+
+
+def ref_ks_test_fit(R, x, family, mu=0.0, sigma=0.0, nu=0.0, rate=0.0):
+    f = R._fn("ks_test_fit", [_p, _u64, _i32, _d, _d, _d, _d, _p, _p])
+    x = np.ascontiguousarray(x, np.float64)
+    st, p = ctypes.c_double(), ctypes.c_double()
+    R._check(f(_ptr(x), len(x), family, mu, sigma, nu, rate, ctypes.byref(st), ctypes.byref(p)),
+             "ks_test_fit")
+    return st.value, p.value
+
+
+# canonical.json (proj/configs/canonical.json:1-29) as run_sim arguments
+CANONICAL = dict(n=8000, rps=100.0, mu_range=(0.1, 2.7), sigma_range=(0.4, 1.2),
+                 prompt_range=(16, 128), max_tokens=512, alpha=0.9, adaptive=True,
+                 beta_fixed=0.1, beta_max=0.5, q_sat=128.0, threshold=0.1, slots=8, c0=0.02,
+                 c1=0.002, c2=1e-4, kind=1, family=0, mu_sd=0.0, ls_sd=0.0, batched=True)
+
+
+def ref_run_sim(R, wseed, policy, seed, **kw):
+    """run_sim of the reference on gen_logt_workload(spec, wseed): per-event arrays (id order),
+    metrics (ttft_avg, ttft_p90, ptla_avg, ptla_p90) and run_sim's own wall seconds."""
+    a = dict(CANONICAL)
+    a.update(kw)
+    f = R._fn("run_sim", [_u64, _d, _d, _d, _d, _d, ctypes.c_uint32, ctypes.c_uint32,
+                          ctypes.c_uint32, _u64, _i32, _d, _i32, _d, _d, _d, _d, _i32, _d, _d,
+                          _d, _i32, _i32, _d, _d, _i32, _u64] + [_p] * 8)
+    n = a["n"]
+    ev = {k: np.empty(n) for k in ("arrival_s", "predict_ready_s", "admit_s", "first_token_s",
+                                   "completion_s")}
+    emitted = np.empty(n, np.uint32)
+    metrics = np.empty(4)
+    secs = ctypes.c_double()
+    rc = f(n, a["rps"], a["mu_range"][0], a["mu_range"][1], a["sigma_range"][0],
+           a["sigma_range"][1], a["prompt_range"][0], a["prompt_range"][1], a["max_tokens"],
+           wseed, policy, a["alpha"], int(a["adaptive"]), a["beta_fixed"], a["beta_max"],
+           a["q_sat"], a["threshold"], a["slots"], a["c0"], a["c1"], a["c2"], a["kind"],
+           a["family"], a["mu_sd"], a["ls_sd"], int(a["batched"]), seed,
+           _ptr(ev["arrival_s"]), _ptr(ev["predict_ready_s"]), _ptr(ev["admit_s"]),
+           _ptr(ev["first_token_s"]), _ptr(ev["completion_s"]), _ptr(emitted), _ptr(metrics),
+           ctypes.byref(secs))
+    R._check(rc, "run_sim")
+    ev["emitted_tokens"] = emitted
+    return ev, metrics, secs.value

@@ -250,12 +250,21 @@ def test_fit_input_errors(lib, tmp_path, name, text, msg):
 def test_python_api_trace_and_fit_input(tie, tmp_path):
     t = synth_trace(500, 2)
     p = tmp_path / "t.jsonl"
-    tie.save_trace(str(p), t["ids"], t["arrival"], t["prompt_tokens"], t["output_tokens"],
-                   t["max_tokens"], t["mu"], t["sigma"])
-    d = tie.load_trace(str(p))
+    tie.save_trace_soa(str(p), t["ids"], t["arrival"], t["prompt_tokens"], t["output_tokens"],
+                       t["max_tokens"], t["mu"], t["sigma"])
+    d = tie.load_trace_soa(str(p))
     order = np.argsort(t["arrival"], kind="stable")
     np.testing.assert_array_equal(d["id"], t["ids"][order])
     np.testing.assert_array_equal(d["mu"], t["mu"][order])
+    # the reference's list-of-Request form (module.cpp:154-156): round trip through both
+    reqs = tie.load_trace(str(p))
+    assert [r.id for r in reqs] == d["id"].tolist()
+    assert [r.true_mu for r in reqs] == [None if np.isnan(v) else v for v in d["mu"]]
+    p2 = tmp_path / "t2.jsonl"
+    tie.save_trace(reqs, str(p2))
+    d2 = tie.load_trace_soa(str(p2))
+    for k in ("id", "arrival_s", "prompt_tokens", "output_tokens", "max_tokens"):
+        np.testing.assert_array_equal(d2[k], d[k])
     c = tmp_path / "f.csv"
     c.write_text("prompt_id,length\na,3\nb,4\na,5\n")
     ids, off, lens = tie.load_fit_input(str(c))
