@@ -121,7 +121,7 @@ class ClockSampler:
                 "window": "warm-up + soak + timed region"}
 
 
-def cpu_baseline(n_target_s=10.0, per_step_s=None):
+def cpu_baseline(n_target_s=10.0, per_step_s=None, full=False):
     """The reference's CPU path on this host: oracle/_ref (untouched reference sources) if it
     was built, else the oracle port.  Scores with all host threads, ranks with the reference
     WaitingQueue (single-threaded, as the reference does)."""
@@ -147,7 +147,7 @@ def cpu_baseline(n_target_s=10.0, per_step_s=None):
     score(mu[:m0], sg[:m0], xm[:m0])
     rate = m0 / max(time.perf_counter() - t0, 1e-6)
     budget = per_step_s if per_step_s else n_target_s
-    m = int(min(N_CONFIG2, max(m0, rate * budget)))
+    m = N_CONFIG2 if full else int(min(N_CONFIG2, max(m0, rate * budget)))
 
     def one():
         t1 = time.perf_counter()
@@ -163,18 +163,21 @@ def cpu_baseline(n_target_s=10.0, per_step_s=None):
 def run_reference_arm(args, world, rank):
     if rank != 0:
         return
-    step, m, threads, kind = cpu_baseline(per_step_s=1.0)
-    for _ in range(args.warmup):
+    # the FULL config-2 queue every step (same config as our arm): ~9-10 s per step on 16
+    # cores.  One warm-up step (a CPU has no JIT / allocation warm-up beyond the first pass),
+    # so --steps 20 ends within ~3.5 minutes.
+    step, m, threads, kind = cpu_baseline(full=True)
+    for _ in range(min(args.warmup, 1)):
         step()
     ts = [sum(step()) for _ in range(args.steps)]
     value = m / float(np.mean(ts))
-    sample = (f"first {m} requests of the config-2 queue (gen_logt_workload n=1M seed 1), "
-              f"scored with {threads} threads + ranked by the reference WaitingQueue, per step")
+    sample = (f"the full config-2 queue ({m} requests, gen_logt_workload seed 1) per step: "
+              f"scored with {threads} threads + ranked by the reference WaitingQueue")
     line = {"metric": "requests scored+ranked/sec", "value": value, "unit": "requests/s",
             "impl": "reference", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * float(np.mean(ts)), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config2: 1M-request queue score+rank (sampled on CPU)",
+            "config": {"workload": "config2: 1M-request queue score+rank per GPU",
                        "n_requests": N_CONFIG2, "sample_requests": m, "nu": 3.5,
                        "alpha": ALPHA, "beta": 0.5, "mc_samples": 10000},
             "cpu_baseline": {"value": value, "unit": "requests/s", "cores": threads,
@@ -206,8 +209,15 @@ def main():
     n_global = n_local * world
     cfg = tie.ScoreConfig()  # alpha 0.9, adaptive beta_max 0.5, q_sat 128
     beta = tie.compute_beta(cfg, n_global)  # GLOBAL queue length (sched.cpp:9-17)
+    torch.cuda.synchronize()
+    t_ctx = time.perf_counter()
     mc = tie.McContext(3.5, 10000, 12, local)
+    t_ctx = time.perf_counter() - t_ctx
     ctx = mc.handle
+    ctx_cost = {"create_ms": t_ctx * 1e3, "device_bytes": int(mc.device_bytes),
+                "note": "McContext(3.5, 10000, 12): host sample set + upload + request-invariant "
+                        "tables (moment / bin / tail); built once per process like the "
+                        "reference's McContext, excluded from the per-step numbers"}
 
     # ---------------- inputs: config-2 queue (this rank's contiguous shard)
     w = tie.gen_logt_workload_soa(n_global, 1)
@@ -317,6 +327,18 @@ def main():
         e2e_s = float(t.item())
     e2e_value = n_global / e2e_s
     e2e_order_ok = bool(np.array_equal(ord_p.numpy(), order_h))
+    # the same call on PAGEABLE host buffers (NumPy arrays, as reference callers hold their
+    # std::vector / NumPy inputs): the driver stages every copy through its own bounce buffer
+    ord_np = np.empty(n_local, np.uint64)
+    pg_ts = []
+    for i in range(3 + 10):
+        t0 = time.perf_counter()
+        tie.score_rank_host_ptr(ctx, mu_h.ctypes.data, sg_h.ctypes.data, mt_h.ctypes.data,
+                                n_local, ALPHA, beta, 0, ord_np.ctypes.data, 0)
+        if i >= 3:
+            pg_ts.append(time.perf_counter() - t0)
+    e2e_pageable_s = float(np.median(pg_ts))
+    pageable_ok = bool(np.array_equal(ord_np.view(np.int64), order_h))
 
     # ---------------- kernel-level profile of one step (separate from the timed loop)
     tie.profile(ctx, True)
@@ -428,8 +450,14 @@ def main():
                     "ms_per_step": e2e_s * 1e3, "ms_per_step_mean": e2e_mean_s * 1e3,
                     "statistic": f"median of {len(e2e_ts)} wall-clocked calls",
                     "api": "tie_score_rank_host (C-ABI), pinned",
-                    "order_matches_device_path": e2e_order_ok},
-            "gpu_launches": launches, "roofline": roof, "roofline_other_kernels": others,
+                    "order_matches_device_path": e2e_order_ok,
+                    "pageable": {"value": n_global / e2e_pageable_s, "unit": "requests/s",
+                                 "ms_per_step": e2e_pageable_s * 1e3,
+                                 "statistic": f"median of {len(pg_ts)} calls",
+                                 "api": "tie_score_rank_host on pageable NumPy buffers",
+                                 "order_matches_device_path": pageable_ok}},
+            "gpu_launches": launches, "context": ctx_cost,
+            "roofline": roof, "roofline_other_kernels": others,
             "clocks": clk,
             "kernels_ms_per_step": {k: round(v["ms_per_step"], 5) for k, v in kern.items()},
             "sorted_check": sorted_ok}
@@ -597,11 +625,91 @@ def run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream, 
         del rep, tl
     except Exception as exc:
         out["fit_report"] = {"error": repr(exc)}
+    # north-star fit target: 10M prompts x 16 lengths on one GPU (1.28 GB resident input)
+    try:
+        del xd
+        torch.cuda.empty_cache()
+        P10 = 10_000_000
+        x10, _, _ = tie.gen_fit_data(P10, K, 1)
+        x10d = torch.from_numpy(x10).to(dev)
+        del x10
+        o10 = [torch.empty(P10, dtype=t, device=dev) for t in
+               (torch.float64, torch.float64, torch.float64, torch.int32, torch.uint8,
+                torch.uint8)]
+        a10 = (ctx, x10d.data_ptr(), P10, K, 3.5) + tuple(t.data_ptr() for t in o10) + (sh,)
+        tie.fit_device(*a10)
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(stream)
+        for _ in range(2):
+            tie.fit_device(*a10)
+        b.record(stream)
+        torch.cuda.synchronize()
+        tie.sync(ctx, sh)
+        ms10 = a.elapsed_time(b) / 2
+        it10 = o10[3].cpu().numpy()
+        out["fit_10M"] = {"metric": "log-t fits/sec (north star: 10M prompts x 16 lengths, "
+                                    "one B200, input resident)",
+                          "value": P10 / (ms10 * 1e-3), "unit": "fits/s", "ms": ms10,
+                          "iterations_mean": float(it10.mean()),
+                          "converged_frac": float(o10[4].float().mean().item())}
+        del x10d, o10
+        torch.cuda.empty_cache()
+    except Exception as exc:  # never blocks the headline line
+        out["fit_10M"] = {"error": repr(exc)}
+    # BASELINE config 5: the trace simulation (canonical.json, TIE, rebuild_threshold 0) through
+    # the drop-in run_sim, wall-clocked, next to the reference's run_sim on this host
+    try:
+        out["config5_sim"] = run_config5(tie)
+    except Exception as exc:
+        out["config5_sim"] = {"error": repr(exc)}
     out["fit"] = {"metric": "log-t fits/sec (config 3: 1M prompts x 16 lengths)",
                   "value": P / (fms * 1e-3), "unit": "fits/s", "ms": fms,
                   "e2e": {"value": P / fe2e, "unit": "fits/s", "h2d_bytes": 8 * P * K,
                           "d2h_bytes": P * (8 * 3 + 4 + 2)},
                   "iterations_mean": float(iters.mean()), "iterations_max": int(iters.max())}
+    return out
+
+
+def run_config5(tie, seeds=(1, 2, 3)):
+    """run_sim on canonical.json (8000 requests, 100 RPS, TIE, batched oracle predictor) with
+    rebuild_threshold 0, seeds 1..3: our wall time per simulation vs the reference's run_sim
+    (oracle/_ref, single-threaded as the reference is) on the same host, and whether the
+    per-request event times are identical."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import CANONICAL, RefLib, ref_available, ref_run_sim
+
+    c = CANONICAL
+    ws = tie.WorkloadSpec()
+    ws.n_requests, ws.rps = c["n"], c["rps"]
+    ws.mu_range, ws.sigma_range = c["mu_range"], c["sigma_range"]
+    ws.prompt_range, ws.max_tokens = c["prompt_range"], c["max_tokens"]
+    sc = tie.ScoreConfig()
+    sc.rebuild_threshold = 0.0
+    ec, pc = tie.EngineConfig(), tie.PredictorConfig()
+    R = RefLib() if ref_available() else None
+    ours, ref, same = [], [], []
+    for seed in seeds:
+        w = tie.gen_logt_workload(ws, seed)
+        tie.run_sim(w, tie.Policy.TIE, sc, ec, pc, seed)  # warm (context, allocations)
+        t0 = time.perf_counter()
+        r = tie.run_sim(w, tie.Policy.TIE, sc, ec, pc, seed)
+        ours.append(time.perf_counter() - t0)
+        if R is not None:
+            ev, _, secs = ref_run_sim(R, seed, 2, seed, threshold=0.0)
+            ref.append(secs)
+            same.append(bool(np.array_equal(
+                np.array([e.completion_s for e in r.events]), ev["completion_s"]) and
+                np.array_equal(np.array([e.admit_s for e in r.events]), ev["admit_s"])))
+    out = {"metric": "trace simulations/sec (config 5: canonical.json, 8000 requests, TIE, "
+                     "rebuild_threshold 0; run_sim wall time)",
+           "value": 1.0 / float(np.median(ours)), "unit": "simulations/s",
+           "ms_per_sim": 1e3 * float(np.median(ours)), "seeds": list(seeds)}
+    if ref:
+        out["reference"] = {"ms_per_sim": 1e3 * float(np.median(ref)),
+                            "kind": "oracle/_ref run_sim (the reference, 1 thread)"}
+        out["speedup_vs_reference"] = float(np.median(ref) / np.median(ours))
+        out["events_identical_to_reference"] = all(same)
     return out
 
 

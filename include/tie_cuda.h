@@ -59,6 +59,9 @@ int tie_ctx_create_mc(int device, double nu, int n_samples, uint64_t seed, tie_c
 void tie_ctx_destroy(tie_ctx* ctx);
 int tie_ctx_samples(const tie_ctx* ctx, double* host_out, int n); /* copy of the set */
 int tie_ctx_info(const tie_ctx* ctx, double* nu, int* n_samples, int* device);
+/* device bytes of the context's request-invariant tables (samples, bucket index, sample bins,
+ * tail table, sigma-grid moment tables); built once at creation, like McContext itself */
+uint64_t tie_ctx_device_bytes(const tie_ctx* ctx);
 
 /* Wait for `stream` and report the first device-side validation failure since the last
  * check (reference exception type + message), then clear it. */

@@ -216,6 +216,8 @@ int tie_ctx_create(int device, const double* samples, int n_samples, double nu,
   return TIE_OK;
 }
 
+uint64_t tie_ctx_device_bytes(const tie_ctx* ctx) { return ctx ? ctx->table_bytes : 0; }
+
 int tie_ctx_create_mc(int device, double nu, int n_samples, uint64_t seed, tie_ctx** out) {
   std::vector<double> y;
   try {

@@ -83,7 +83,9 @@ PYBIND11_MODULE(_core, m) {
                                                      mc.samples.data());
                              })
       .def_property_readonly("handle",
-                             [](const McContext& mc) { return (uintptr_t)mc.handle(); });
+                             [](const McContext& mc) { return (uintptr_t)mc.handle(); })
+      .def_property_readonly("device_bytes",
+                             [](const McContext& mc) { return tie_ctx_device_bytes(mc.handle()); });
 
   m.def("t_pdf", &t_pdf, py::arg("y"), py::arg("nu"));
   m.def("t_cdf", &t_cdf, py::arg("y"), py::arg("nu"));

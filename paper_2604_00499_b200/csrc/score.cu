@@ -702,6 +702,7 @@ cudaError_t build_context_tables(tie_ctx* ctx) {
   const std::vector<double>& Y = ctx->host_samples;
   cudaError_t e;
   if ((e = cudaMalloc(&ctx->d_Y, sizeof(double) * std::max(N, 1))) != cudaSuccess) return e;
+  ctx->table_bytes = sizeof(double) * std::max(N, 1);
   if ((e = cudaMemcpy(ctx->d_Y, Y.data(), sizeof(double) * N, cudaMemcpyHostToDevice)) !=
       cudaSuccess)
     return e;
@@ -716,6 +717,7 @@ cudaError_t build_context_tables(tie_ctx* ctx) {
       yb[b] = (uint32_t)(std::upper_bound(Y.begin(), Y.end(), edge) - Y.begin());
     }
   if ((e = cudaMalloc(&ctx->d_ybucket, sizeof(uint32_t) * yb.size())) != cudaSuccess) return e;
+  ctx->table_bytes += sizeof(uint32_t) * yb.size();
   if ((e = cudaMemcpy(ctx->d_ybucket, yb.data(), sizeof(uint32_t) * yb.size(),
                       cudaMemcpyHostToDevice)) != cudaSuccess)
     return e;
@@ -791,6 +793,7 @@ cudaError_t build_context_tables(tie_ctx* ctx) {
       tail_coefs(c, kBinCoef, row + kBinTail);
     }
     if ((e = cudaMalloc(&ctx->d_bins, sizeof(double) * ent.size())) != cudaSuccess) return e;
+    ctx->table_bytes += sizeof(double) * ent.size();
     if ((e = cudaMemcpy(ctx->d_bins, ent.data(), sizeof(double) * ent.size(),
                         cudaMemcpyHostToDevice)) != cudaSuccess)
       return e;
@@ -805,6 +808,7 @@ cudaError_t build_context_tables(tie_ctx* ctx) {
     for (int b = 0; b < kTailBuckets && ctx->t_w > 0.0; ++b)
       tail_coefs(((double)b + 0.5) * ctx->t_w, kTailCoef, tt.data() + (size_t)b * kTailCoef);
     if ((e = cudaMalloc(&ctx->d_tail, sizeof(double) * tt.size())) != cudaSuccess) return e;
+    ctx->table_bytes += sizeof(double) * tt.size();
     if ((e = cudaMemcpy(ctx->d_tail, tt.data(), sizeof(double) * tt.size(),
                         cudaMemcpyHostToDevice)) != cudaSuccess)
       return e;
@@ -813,6 +817,7 @@ cudaError_t build_context_tables(tie_ctx* ctx) {
   ctx->G = (int)std::lrint(ctx->sigma_table_max * kGridInvH) + 1;
   const size_t bytes = (size_t)ctx->G * (size_t)(N + 1) * kMoments * sizeof(double);
   if ((e = cudaMalloc(&ctx->d_table, bytes)) != cudaSuccess) return e;
+  ctx->table_bytes += bytes;
   build_moment_table_kernel<<<ctx->G, 512>>>(ctx->d_Y, N, ctx->d_table);
   capi::count_launch();
   if ((e = cudaGetLastError()) != cudaSuccess) return e;

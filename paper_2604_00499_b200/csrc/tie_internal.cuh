@@ -190,6 +190,7 @@ struct tie_ctx {
   double ka_alpha = -1.0;
   uint32_t ka_k = 0;
   double* d_ka_table = nullptr;          // [G][kMoments] rows at k = ka_table_k
+  size_t table_bytes = 0;                 // device bytes of the request-invariant tables
   uint32_t ka_table_k = 0xffffffffu;
   // pinned host staging for the *_host entry points
   void* pinned = nullptr;
