@@ -756,6 +756,7 @@ constexpr uint64_t kPartMaxN = 1ull << 21;
 constexpr uint32_t kPartMaxP = 2048;
 constexpr uint32_t kPartMaxFineLog2 = 10;
 constexpr int kPartThreads = 256;
+constexpr int kFusedThreadsFwd = 512;  // = kFusedThreads (the group sorts split it)
 
 struct Part {
   const uint64_t* keys;
@@ -1048,6 +1049,162 @@ __device__ __forceinline__ void sort_partition(const Part& q, uint32_t s0, uint3
   }
 }
 
+// Group-parallel partition sorts (level 2 of the two-level path).  A sub-partition holds
+// ~0.5-1.5k keys, and sorting one with the whole 512-thread CTA is a chain of barriers over
+// loops of 1-3 iterations.  Instead the CTA splits into kGroups groups, each sorting its OWN
+// sub-partition with its own named barrier (bar.sync id, n) in its own shared-memory slice
+// -- kGroups sub-partitions in flight per CTA; those above kGrpCap keys are sorted CTA-wide
+// afterwards.  The fine buckets are the top kGrpFineLog2 fine bits (~2-4 keys per bucket).
+// Same-box A/B on B200 (64M keys, level 2): 1.77 ms vs 1.87 ms CTA-wide; in the one-level
+// fused kernel (1M keys) the groups were slower (91-94 vs 85 us per step), so it keeps the
+// CTA-wide sorts.
+#ifndef TIE_GRP_GROUPS
+#define TIE_GRP_GROUPS 4
+#endif
+#ifndef TIE_GRP_CAP
+#define TIE_GRP_CAP 1408
+#endif
+#ifndef TIE_GRP_FINE_LOG2
+#define TIE_GRP_FINE_LOG2 8
+#endif
+constexpr int kGroups = TIE_GRP_GROUPS;
+constexpr uint32_t kGrpCap = TIE_GRP_CAP;
+constexpr uint32_t kGrpFineLog2 = TIE_GRP_FINE_LOG2;
+constexpr uint32_t kGrpFine = 1u << kGrpFineLog2;
+constexpr size_t kGrpBytes =
+    ((size_t)kGrpCap * (8 + 4 + 2 + 2) + 4 * (2 * kGrpFine + 1) + 15) & ~(size_t)15;
+
+template <int kN>
+__device__ __forceinline__ void grp_bar(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kN) : "memory");
+}
+
+// exclusive scan over the group's kN threads (kN / 32 <= 32 warps)
+template <int kN>
+__device__ __forceinline__ uint32_t grp_excl_scan(uint32_t v, uint32_t* sh, int bar, int gtid) {
+  const int lane = gtid & 31, warp = gtid >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[warp] = x;
+  grp_bar<kN>(bar);
+  uint32_t pre = 0;
+  for (int w = 0; w < warp; ++w) pre += sh[w];
+  grp_bar<kN>(bar);  // sh is reused by the next scan
+  return x - v + pre;
+}
+
+template <int kN>
+__device__ __forceinline__ void sort_partition_grp(const Part& q, uint32_t s0, uint32_t m,
+                                                   const uint64_t* __restrict__ ids,
+                                                   uint64_t* __restrict__ order,
+                                                   unsigned char* gmem, uint32_t* sh, int bar,
+                                                   int gtid) {
+  uint64_t* sk = reinterpret_cast<uint64_t*>(gmem);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + kGrpCap);
+  uint16_t* sf = reinterpret_cast<uint16_t*>(sv + kGrpCap);
+  uint16_t* perm = sf + kGrpCap;
+  uint32_t* fb = reinterpret_cast<uint32_t*>(perm + kGrpCap);  // [nf + 1]
+  uint32_t* fc = fb + kGrpFine + 1;                             // [nf]
+  const uint32_t flog = min(q.fine_log2, kGrpFineLog2);
+  const uint32_t fshift = q.fine_log2 - flog, nf = 1u << flog;
+  const uint32_t fmask = (1u << q.fine_log2) - 1u;
+  for (uint32_t j = gtid; j < nf; j += kN) fc[j] = 0;
+  grp_bar<kN>(bar);
+  const KeyRange r = key_range(q.mm, q.total_bits);
+  for (uint32_t j = gtid; j < m; j += kN) {
+    const uint64_t k = q.tk[s0 + j];
+    sk[j] = k;
+    sv[j] = q.tv[s0 + j];
+    const uint32_t fine = (part_bucket(q, r, k) & fmask) >> fshift;
+    sf[j] = (uint16_t)fine;
+    atomicAdd(&fc[fine], 1u);
+  }
+  grp_bar<kN>(bar);
+  {
+    constexpr int kPer = kGrpFine / kN > 0 ? kGrpFine / kN : 1;
+    uint32_t c[kPer], t = 0;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t j = gtid * kPer + u;
+      c[u] = j < nf ? fc[j] : 0u;
+      t += c[u];
+    }
+    uint32_t v = grp_excl_scan<kN>(t, sh, bar, gtid);
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint32_t j = gtid * kPer + u;
+      if (j < nf) {
+        fb[j] = v;
+        fc[j] = v;
+      }
+      v += c[u];
+    }
+    if (gtid == 0) fb[nf] = m;
+  }
+  grp_bar<kN>(bar);
+  for (uint32_t j = gtid; j < m; j += kN) perm[atomicAdd(&fc[sf[j]], 1u)] = (uint16_t)j;
+  grp_bar<kN>(bar);
+  uint16_t* spos = sf;
+  for (uint32_t j = gtid; j < m; j += kN) {
+    const uint64_t k = sk[j];
+    const uint32_t v = sv[j], fine = sf[j];
+    const uint32_t lo = fb[fine], hi = fb[fine + 1];
+    uint32_t below = 0;
+    for (uint32_t s = lo; s < hi; ++s) {
+      const uint32_t o = perm[s];
+      const uint64_t kq = sk[o];
+      below += (kq < k || (kq == k && sv[o] < v)) ? 1u : 0u;
+    }
+    spos[j] = (uint16_t)(lo + below);
+  }
+  grp_bar<kN>(bar);
+  uint32_t* outv = reinterpret_cast<uint32_t*>(sk);
+  for (uint32_t j = gtid; j < m; j += kN) outv[spos[j]] = sv[j];
+  grp_bar<kN>(bar);
+  for (uint32_t t = gtid; t < m; t += kN) {
+    const uint32_t v = outv[t];
+    order[s0 + t] = ids ? ids[v] : (uint64_t)v;
+  }
+  grp_bar<kN>(bar);  // the slice is reused by the group's next partition
+}
+
+// Sort partitions [0, np) of (bases[p], bases[p+1]) with the CTA's groups (slot = the CTA's
+// group g takes p = first + g * stride0 + j * stride), then the oversized ones CTA-wide.
+template <int kT>
+__device__ __forceinline__ void sort_partitions_grouped(const Part& q, const uint32_t* bases,
+                                                        uint32_t p_begin, uint32_t p_step,
+                                                        uint32_t np, uint32_t s_off,
+                                                        const uint64_t* __restrict__ ids,
+                                                        uint64_t* __restrict__ order,
+                                                        unsigned char* smem_raw,
+                                                        uint32_t (*gsh)[32]) {
+#ifdef TIE_NO_GROUPS
+  for (uint32_t p = p_begin; p < np; p += p_step) {
+    const uint32_t s0 = bases[p], m = bases[p + 1] - s0;
+    if (m) sort_partition<kT>(q, s_off + s0, m, ids, order, smem_raw);
+    __syncthreads();
+  }
+  return;
+#endif
+  const int grp = threadIdx.x / (kT / kGroups), gtid = threadIdx.x % (kT / kGroups);
+  for (uint32_t p = p_begin + grp * p_step; p < np; p += kGroups * p_step) {
+    const uint32_t s0 = bases[p], m = bases[p + 1] - s0;
+    if (m && m <= kGrpCap)
+      sort_partition_grp<kT / kGroups>(q, s_off + s0, m, ids, order, smem_raw + grp * kGrpBytes,
+                                       gsh[grp], 1 + grp, gtid);
+  }
+  __syncthreads();
+  for (uint32_t p = p_begin; p < np; p += p_step) {
+    const uint32_t s0 = bases[p], m = bases[p + 1] - s0;
+    if (m > kGrpCap) sort_partition<kT>(q, s_off + s0, m, ids, order, smem_raw);
+    __syncthreads();
+  }
+}
+
 template <int kT>
 __global__ void __launch_bounds__(kT, 1536 / kT) part_sort_kernel(Part q, uint64_t n,
                                                                    const uint64_t* __restrict__ ids,
@@ -1192,6 +1349,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
     }
   }
   grid.sync();
+  // CTA-wide sorts here: the group-parallel sorts measured slower on this path (1M keys:
+  // 91-94 vs 85 us per score+rank step), they pay off only in level 2 below
   for (uint32_t p = blockIdx.x; p < P; p += gridDim.x) {
     const uint32_t s0 = pb[p], m = pb[p + 1] - s0;
     if (m) sort_partition<kFusedThreads>(q, s0, m, ids, order, smem_raw);
@@ -1277,11 +1436,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_l2_kernel(
   Part q2 = q;
   q2.tk = q.tk2;
   q2.tv = q.tv2;
-  for (uint32_t b = 0; b < P2; ++b) {
-    const uint32_t m = sb[b + 1] - sb[b];
-    if (m) sort_partition<kFusedThreads>(q2, s0 + sb[b], m, ids, order, smem_raw);
-    __syncthreads();
-  }
+  __shared__ uint32_t gsh[kGroups][32];
+  sort_partitions_grouped<kFusedThreads>(q2, sb, 0, 1, P2, s0, ids, order, smem_raw, gsh);
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -1343,10 +1499,17 @@ Layout layout(uint64_t n, bool with_ids) {
   L.part = n <= kPartMaxN;
   // two levels pay off from ~6M keys (B200: 8M 0.32 vs 0.37 ms bucket path; 4M 0.18 vs 0.15)
   L.part2 = !L.part && two_level && n >= (6ull << 20) && n < (1ull << 32);
-  L.p_log2 = std::min<uint32_t>(std::max<uint32_t>(ceil_log2((n + 1023) / 1024), 6u), 11u);
-  // two-level: 2048 level-1 partitions of P2 ~1k-key sub-partitions each
+  // ~kSubLog2-key (sub-)partitions: the group sorts' size (kGrpCap ~2.7x the mean)
+#ifndef TIE_SUB_LOG2
+#define TIE_SUB_LOG2 10
+#endif
+  constexpr uint32_t kSubLog2 = TIE_SUB_LOG2;
+  L.p_log2 = std::min<uint32_t>(
+      std::max<uint32_t>(ceil_log2((n + (1ull << kSubLog2) - 1) >> kSubLog2), 6u), 11u);
+  // two-level: 2048 level-1 partitions of P2 sub-partitions each
   L.p2_log2 = L.part2 ? std::min<uint32_t>(std::max<uint32_t>(
-                            ceil_log2((n + (1024ull << L.p_log2) - 1) >> (L.p_log2 + 10)), 1u),
+                            ceil_log2((n + (1ull << (L.p_log2 + kSubLog2)) - 1) >>
+                                      (L.p_log2 + kSubLog2)), 1u),
                         10u)
                       : 0u;
   L.fine_log2 = std::min<uint32_t>(
@@ -1469,8 +1632,9 @@ cudaError_t part_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_t*
                       uint64_t n, const uint64_t* ids, uint64_t* order, const Fallback& f,
                       int sms, cudaStream_t s) {
   static bool attr = false;
-  const size_t smem = (size_t)kPartCap * (8 + 4 + 2 + 2) +
-                      4 * (2 * (1u << kPartMaxFineLog2) + 1);
+  const size_t smem = std::max((size_t)kPartCap * (8 + 4 + 2 + 2) +
+                                   4 * (2 * (1u << kPartMaxFineLog2) + 1),
+                               kGroups * kGrpBytes);
   if (!attr) {
     cudaFuncSetAttribute(part_sort_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);

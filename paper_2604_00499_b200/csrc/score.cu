@@ -423,6 +423,25 @@ __device__ __noinline__ void exact_sums_slow(const double* __restrict__ Y, doubl
   exact_sums(Y, mu, sg, k_a, k_max, *s_a, *s_all);
 }
 
+// the exact-sum fallback of the pipelined kernel (rare: outside the sigma grid or |mu| > 700)
+struct OutW {
+  double E, C, S;
+  uint32_t why;
+};
+__device__ __noinline__ OutW exact_epilogue_slow(const ScoreParams& p, double m, double sg,
+                                                 uint32_t k_a, uint32_t k_max, double xm,
+                                                 double T, bool saturated) {
+  double s_a = 0.0, s_all = 0.0;
+  exact_sums(p.Y, m, sg, k_a, k_max, s_a, s_all);
+  Out o;
+  OutW w;
+  w.why = epilogue<false>(p, xm, T, saturated, s_a, s_all, o);
+  w.E = o.E;
+  w.C = o.C;
+  w.S = o.S;
+  return w;
+}
+
 template <int R>
 __device__ __forceinline__ void stage_rows(const double* myrow, double* slab,
                                            const double** ptrs) {
@@ -674,6 +693,255 @@ __global__ void __launch_bounds__(256, kMinBlocks) score_coop_kernel(const __gri
   if (minmax) key_range_flush(minmax, kmin, kmax);
 }
 
+// ------------------------------------------------------------------ pipelined path (A/B)
+// The moment-table path as a three-stage software pipeline per warp:
+//   S1(j): block j's inputs -> y_max -> its 96-byte sample-bin rows in flight (into bslab)
+//   S2(j): T(y_max), k_max, grid point from bslab -> the moment rows in flight (mslab[j & 1])
+//   S3(j): the two Horner sums from mslab[j & 1], E / CVaR / score, stores
+// issued as S2(j), S1(j+1), S3(j-1) in one loop body behind ONE wait for the copies issued by
+// the previous body, so both gathers of a body overlap the previous block's S3 (ncu on the
+// two-wait cooperative kernel: 18 % of the stall samples on the LDGSTS wait).  Rows are
+// gathered cooperatively (consecutive lanes copy consecutive 16-byte chunks of one row with
+// LDGSTS, ~6 lines per warp instruction instead of 32); the row pointers are exchanged with
+// shuffles.  (Per-lane TMA bulk copies of the same rows measured 2.3x slower: ~14 SM cycles
+// per 96-byte bulk copy.)  One 512-thread CTA per SM: 16 warps x 3 slabs + the k_alpha rows.
+constexpr int kPipeThreads = 512;
+constexpr int kPipeWarps = kPipeThreads / 32;
+constexpr int kSlabDoubles = 32 * kSlabStride;
+static_assert(kBinEntry == kMoments, "bin and moment rows share the slab layout");
+
+// every lane's row (nullptr: none) into its slot of `slab`: LDGSTS, committed as one group
+__device__ __forceinline__ void coop_issue(const double* row, double* slab) {
+  const int lane = threadIdx.x & 31;
+  constexpr int C = kMoments / 2;  // 16-byte chunks per row
+  const unsigned long long mine = (unsigned long long)row;
+#pragma unroll
+  for (int it = 0; it < C; ++it) {
+    const int c = it * 32 + lane;
+    const int r = c / C, sub = c - r * C;
+    const double* rp = (const double*)__shfl_sync(0xffffffffu, mine, r);
+    if (rp) {
+      const unsigned dst =
+          (unsigned)__cvta_generic_to_shared(slab + r * kSlabStride + 2 * sub);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                   "l"(reinterpret_cast<const double2*>(rp) + sub)
+                   : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void coop_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+}
+
+struct PipeA {  // after S1
+  uint64_t i;
+  double m, sg, xm, y_max;
+  uint32_t why;
+  bool active, ok, binned;
+};
+
+struct PipeB {  // after S2
+  uint64_t i;
+  double m, xm, T, delta, sg;
+  uint32_t why, k_max, k_a;
+  int g;
+  bool active, ok, use_table, saturated;
+};
+
+// S1: inputs of the lane's request in block `base` -> y_max -> bin rows in flight
+__device__ __forceinline__ PipeA pipe_s1(const ScoreParams& p, uint64_t n, uint64_t base,
+                                         double m, double sig, double xm, LogMemo& lnx,
+                                         double* bslab) {
+  PipeA a;
+  a.i = base + (threadIdx.x & 31);
+  a.active = a.i < n;
+  a.why = kOk;
+  if (!isfinite(m)) a.why = kMuNotFinite;  // LogTParams / CensoredLogT (dist.cpp:108-120)
+  else if (!(sig > 0.0) || !isfinite(sig)) a.why = kSigmaBad;
+  else if (!(xm > 0.0) || !isfinite(xm)) a.why = kXmaxBad;
+  a.ok = a.active && a.why == kOk;
+  a.m = m;
+  a.xm = xm;
+  a.sg = a.ok ? (sig < 1e-9 ? 1e-9 : sig) : 1.0;
+  a.y_max = a.ok ? __dsub_rn(lnx(xm), m) / a.sg : 0.0;
+  a.binned = a.ok && fabs(a.y_max) < p.bin_ylim;
+  const uint64_t ybits = (uint64_t)__double_as_longlong(a.y_max);
+  coop_issue(a.binned ? p.bins + (size_t)sample_bin(ybits, p.bin_e0, p.bin_m, p.bin_mid) *
+                                     kBinEntry
+                      : nullptr,
+             bslab);
+  return a;
+}
+
+// S2: T, k_max and the grid point from the (landed) bin rows -> moment rows in flight
+__device__ __forceinline__ PipeB pipe_s2(const ScoreParams& p, const PipeA& a,
+                                         const double* bslab, double* mslab) {
+  PipeB b;
+  b.i = a.i;
+  b.active = a.active;
+  b.ok = a.ok;
+  b.why = a.why;
+  b.m = a.m;
+  b.xm = a.xm;
+  b.sg = a.sg;
+  const double* my = bslab + (threadIdx.x & 31) * kSlabStride;
+  b.T = 0.5;
+  b.k_max = 0;
+  const double y_max = a.y_max;
+  if (a.binned) {
+    const uint64_t ybits = (uint64_t)__double_as_longlong(y_max);
+    const double c =
+        __longlong_as_double((long long)sample_bin_centre_bits(ybits, p.bin_e0, p.bin_m));
+    const double v = smem_horner<kBinCoef>(my + kBinTail, __dsub_rn(fabs(y_max), c));
+    b.T = y_max >= 0.0 ? __dsub_rn(1.0, v) : v;  // dist.cpp:80
+    b.k_max = bin_cut(p, my, y_max);
+  } else if (a.ok) {  // |y_max| beyond the bins: continued fraction, cut at the sample ends
+    b.T = t_cdf_slow(p.td, y_max);
+    b.k_max = y_max >= p.yN ? (uint32_t)p.N
+                            : (y_max < p.y0 ? 0u : bin_search_slow(p.Y, 0, p.N, y_max));
+  }
+  __syncwarp();  // every lane is done with bslab before S1 refills it
+  b.g = a.ok ? __double2int_rn(a.sg * kGridInvH) : 0;
+  b.delta = a.sg - b.g * kGridH;  // exact: h is a power of two
+  const double reach = fmax(p.taylor_y0, fmin(fmax(y_max, 0.0), p.yN));
+  b.use_table =
+      a.ok && b.g < p.G && fabs(a.m) <= 700.0 && fabs(b.delta) * reach <= kTaylorReach;
+  b.saturated = p.alpha >= b.T;  // censored_cvar case 1 (dist.cpp:187)
+  b.k_a = b.saturated ? 0u : p.k_alpha;
+  const double* gbase =
+      p.table + (size_t)(b.use_table ? b.g : 0) * (size_t)(p.N + 1) * kMoments;
+  coop_issue(b.use_table && b.k_max ? gbase + (size_t)b.k_max * kMoments : nullptr, mslab);
+  return b;
+}
+
+// S3: Horner sums from the (landed) moment rows, epilogue, stores
+__device__ __forceinline__ void pipe_s3(const ScoreParams& p, const PipeB& b,
+                                        const double* mslab, const double* ka_rows,
+                                        bool ka_smem, double* __restrict__ E,
+                                        double* __restrict__ C, double* __restrict__ S,
+                                        uint64_t* __restrict__ keys, uint64_t& kmin,
+                                        uint64_t& kmax) {
+  const double F_all = slab_horner<kMoments>(mslab, b.delta);
+  double F_a = 0.0;
+  if (b.use_table && b.k_a) {
+    if (ka_smem) {
+      F_a = smem_horner<kMoments>(ka_rows + b.g * kSlabStride, b.delta);
+    } else {
+      Row row_a;
+      load_row(p.table + ((size_t)b.g * (size_t)(p.N + 1) + b.k_a) * kMoments, row_a);
+      F_a = horner(row_a, b.delta);
+    }
+  }
+  __syncwarp();  // every lane is done with this mslab before S2 refills it
+  Out o;
+  uint32_t why = b.why;
+  if (b.ok) {
+    if (b.use_table) {
+      const double em = exp(b.m);
+      const double s_all = b.k_max ? em * F_all : 0.0;
+      const double s_a = b.k_a ? em * F_a : 0.0;
+      why = epilogue<true>(p, b.xm, b.T, b.saturated, s_a, s_all, o);
+    } else {
+      const OutW w = exact_epilogue_slow(p, b.m, b.sg, b.k_a, b.k_max, b.xm, b.T, b.saturated);
+      why = w.why;
+      o.E = w.E;
+      o.C = w.C;
+      o.S = w.S;
+    }
+  }
+  if (!b.active) return;
+  if (why != kOk) {
+    report(p.err, p.index_base + b.i, why);
+    o.E = o.C = o.S = __longlong_as_double(0x7ff8000000000000LL);
+  }
+  if (E) E[b.i] = o.E;
+  if (C) C[b.i] = o.C;
+  if (S) S[b.i] = o.S;
+  if (keys) {
+    const uint64_t k = why == kOk ? ((uint64_t)__double_as_longlong(o.S) | (1ull << 63)) : ~0ull;
+    keys[b.i] = k;
+    kmin = k < kmin ? k : kmin;
+    kmax = k > kmax ? k : kmax;
+  }
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(kPipeThreads, 1) score_pipe_kernel(
+    const __grid_constant__ ScoreParams p, const double* __restrict__ mu,
+    const double* __restrict__ sigma, const XT* __restrict__ xmax, uint64_t n,
+    double* __restrict__ E, double* __restrict__ C, double* __restrict__ S,
+    uint64_t* __restrict__ keys, unsigned long long* __restrict__ minmax) {
+  extern __shared__ __align__(128) double pipe_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* bslab = pipe_smem + (size_t)wib * 3 * kSlabDoubles;
+  double* mslab0 = bslab + kSlabDoubles;
+  double* mslab1 = mslab0 + kSlabDoubles;
+  double* ka_rows = pipe_smem + (size_t)kPipeWarps * 3 * kSlabDoubles;
+  const bool ka_smem = p.ka_smem && p.G <= kKaMaxG && p.k_alpha > 0;
+  if (ka_smem) {
+    const int nc = p.G * (kMoments / 2);
+    for (int c = threadIdx.x; c < nc; c += kPipeThreads) {
+      const int g = c / (kMoments / 2), sub = c % (kMoments / 2);
+      *reinterpret_cast<double2*>(ka_rows + g * kSlabStride + 2 * sub) =
+          __ldg(reinterpret_cast<const double2*>(p.ka_table) + c);
+    }
+  }
+  __syncthreads();
+  LogMemo lnx;
+  uint64_t kmin = ~0ull, kmax = 0;
+  const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t step = ((uint64_t)gridDim.x * blockDim.x >> 5) * 32;
+  uint64_t base = warp0 * 32;
+  if (base < n) {
+    // raw inputs one block ahead (converted when used)
+    double m0 = 0.0, s0 = 1.0, nm = 0.0, nsig = 1.0;
+    XT x0 = (XT)1, nxm = (XT)1;
+    if (base + lane < n) {
+      m0 = mu[base + lane];
+      s0 = sigma[base + lane];
+      x0 = xmax[base + lane];
+    }
+    if (base + step + lane < n) {
+      nm = mu[base + step + lane];
+      nsig = sigma[base + step + lane];
+      nxm = xmax[base + step + lane];
+    }
+    PipeA a = pipe_s1(p, n, base, m0, s0, (double)x0, lnx, bslab);
+    PipeB b;
+    bool have_b = false;
+    bool odd = false;  // block parity j & 1
+    // body j: S3(j-1) [its moment rows: the older of the two groups in flight], S2(j) [the
+    // bin rows: the newer group], S1(j+1) -- at most two blocks' state live at a time
+    for (; base < n; base += step, odd = !odd) {
+      if (have_b) {  // S3(j-1)
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();
+        pipe_s3(p, b, odd ? mslab0 : mslab1, ka_rows, ka_smem, E, C, S, keys, kmin, kmax);
+      }
+      coop_wait_all();
+      b = pipe_s2(p, a, bslab, odd ? mslab1 : mslab0);  // S2(j)
+      have_b = true;
+      const uint64_t nbase = base + step;
+      if (nbase < n) {  // S1(j+1)
+        const double cm = nm, cs = nsig, cx = (double)nxm;
+        const uint64_t i2 = nbase + step + lane;
+        if (i2 < n) {
+          nm = mu[i2];
+          nsig = sigma[i2];
+          nxm = xmax[i2];
+        }
+        a = pipe_s1(p, n, nbase, cm, cs, cx, lnx, bslab);
+      }
+    }
+    coop_wait_all();  // S3 of the last block (parity !odd)
+    pipe_s3(p, b, odd ? mslab0 : mslab1, ka_rows, ka_smem, E, C, S, keys, kmin, kmax);
+  }
+  if (minmax) key_range_flush(minmax, kmin, kmax);
+}
+
 // k_alpha rows of every grid point into one contiguous [G][kMoments] table (once per alpha)
 __global__ void gather_ka_rows_kernel(const double* __restrict__ table, int G, int N,
                                       uint32_t k_alpha, double* __restrict__ out) {
@@ -905,6 +1173,31 @@ cudaError_t launch_score(tie_ctx* ctx, const double* mu, const double* sigma, co
           p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out, minmax);
     else
       score_kernel<double, false><<<(unsigned)grid, 256, 0, s>>>(
+          p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, minmax);
+  } else if ((flags & 16u) && n >= 4096) {
+    // pipelined variant (A/B only): one 512-thread CTA per SM.  Measured on B200 at 1M
+    // requests: 44-46 us vs 42 us for the two-round cooperative kernel below (ncu: +32 %
+    // instructions and 128-register spills from two blocks' state live across the stages;
+    // the per-lane TMA bulk-copy version of it: 97 us)
+    p.ka_smem = ctx->G <= kKaMaxG ? 1 : 0;
+    const size_t smem = sizeof(double) * ((size_t)kPipeWarps * 3 * kSlabDoubles +
+                                          (p.ka_smem ? (size_t)kSlabStride * ctx->G : 0));
+    static bool pattr = false;
+    if (!pattr) {
+      const int mx = (int)(sizeof(double) * ((size_t)kPipeWarps * 3 * kSlabDoubles +
+                                             (size_t)kSlabStride * kKaMaxG));
+      cudaFuncSetAttribute(score_pipe_kernel<uint32_t>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(score_pipe_kernel<double>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      pattr = true;
+    }
+    const uint64_t grid = std::min<uint64_t>((n + kPipeThreads - 1) / kPipeThreads, (uint64_t)sms);
+    if (x_is_u32)
+      score_pipe_kernel<uint32_t><<<(unsigned)grid, kPipeThreads, smem, s>>>(
+          p, mu, sigma, (const uint32_t*)x_max, n, E, C, S, keys_out, minmax);
+    else
+      score_pipe_kernel<double><<<(unsigned)grid, kPipeThreads, smem, s>>>(
           p, mu, sigma, (const double*)x_max, n, E, C, S, keys_out, minmax);
   } else {
     const int minb = (flags & 8u) ? 3 : 2;  // 2 CTAs/SM, 128 regs, no spills (A/B: 3, spills)
