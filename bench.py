@@ -33,6 +33,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N_CONFIG2 = 1_000_000
+N_CONFIG4 = 64 * 2 ** 20
+NVLINK_GBS = 900.0  # NVLink 5 per GPU per direction (nominal; B200 SXM)
 ALPHA = 0.9
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0
@@ -48,6 +50,11 @@ def parse():
     ap.add_argument("--n", type=int, default=N_CONFIG2, help="requests per rank")
     ap.add_argument("--no-extras", action="store_true", help="skip fit / exact-mode extras")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--n-global", type=int, default=N_CONFIG4,
+                    help="N>1: global queue length (config 4: 64 x 2^20), sharded over ranks")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 transport; gloo = one-GPU dry run (every rank on cuda:0, "
+                         "collectives staged through host memory)")
     return ap.parse_args()
 
 
@@ -194,14 +201,14 @@ def main():
         run_reference_arm(args, world, rank)
         return
 
+    if world > 1:
+        main_sharded(args, world, rank, local)
+        return
+
     import torch
 
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2604_00499_b200 as tie
 
     dev = torch.device("cuda", local)
@@ -669,6 +676,217 @@ def run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream, 
                           "d2h_bytes": P * (8 * 3 + 4 + 2)},
                   "iterations_mean": float(iters.mean()), "iterations_max": int(iters.max())}
     return out
+
+
+def main_sharded(args, world, rank, local):
+    """N > 1: BASELINE config 4 -- the 64M-request queue sharded over the N ranks (strong
+    scaling: the global queue is fixed), one rank per GPU over NCCL.  Step = every rank scores
+    + ranks its contiguous shard (tie_score_rank_run: the sorted run straight from the device
+    path), the splitter exchange (regular samples all-gathered, cuts on the device, ONE
+    all-to-all of 12-byte (score, local id) records over NVLink) and the local ordering of the
+    received range: rank r ends with slice r of the global dispatch order.  Rank 0 also times
+    the same 64M queue on its own GPU (the N = 1 base of the curve)."""
+    import torch
+    import torch.distributed as dist
+
+    dev_index = local if args.dist_backend == "nccl" else 0
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    if args.dist_backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
+    import paper_2604_00499_b200 as tie
+    from paper_2604_00499_b200.dist import DeviceOps, ShardedScoreRank, shard_bounds
+
+    n_global = args.n_global
+    lo, hi = shard_bounds(n_global, world, rank)
+    n_local = hi - lo
+    width = shard_bounds(n_global, world, 0)[1]
+    beta = tie.compute_beta(tie.ScoreConfig(), n_global)  # GLOBAL queue length
+    mc = tie.McContext(3.5, 10000, 12, dev_index)
+    ctx = mc.handle
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    nccl = args.dist_backend == "nccl"
+    # ---------------- inputs: gen_logt_workload is ONE sequential mt19937_64 stream, so rank 0
+    # generates the global queue and scatters the shards (NCCL over NVLink; setup, untimed)
+    full = None
+    if rank == 0:
+        w = tie.gen_logt_workload_soa(n_global, 1)
+        full = {k: w[k] for k in ("mu", "sigma", "max_tokens")}
+        del w
+    parts = {}
+    for k, dt in (("mu", torch.float64), ("sigma", torch.float64), ("max_tokens", torch.int32)):
+        out = torch.empty(width, dtype=dt, device=dev if nccl else "cpu")
+        lst = None
+        if rank == 0:
+            a = full[k].view(np.int32) if k == "max_tokens" else full[k]
+            pad = np.zeros(world * width, dtype=a.dtype)
+            for g in range(world):
+                ga, gb = shard_bounds(n_global, world, g)
+                pad[g * width:g * width + gb - ga] = a[ga:gb]
+            src = torch.from_numpy(pad)
+            src = src.to(dev) if nccl else src
+            lst = list(src.view(world, width).unbind(0))
+        dist.scatter(out, lst, src=0)
+        parts[k] = out[:n_local].to(dev).contiguous()
+    mu, sg, mt = parts["mu"], parts["sigma"], parts["max_tokens"]
+    mu_p = mu.cpu().pin_memory()
+    sg_p = sg.cpu().pin_memory()
+    mt_p = mt.cpu().pin_memory()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    sharded = ShardedScoreRank(DeviceOps(mc, ALPHA), beta, merge_on="range")
+    holder = {}
+
+    def step():
+        holder["res"] = sharded(mu, sg, mt, n_global)
+
+    clocks = ClockSampler(dev_index)
+    clocks.start()
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        step()
+    tie.sync(ctx, sh)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    tie.launch_count(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for a, b in ev:
+        flush.zero_()
+        dist.barrier()
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    launches = int(tie.launch_count(False))
+    tot = torch.tensor([float(np.sum([a.elapsed_time(b) for a, b in ev]))], device=dev)
+    if nccl:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    else:
+        th = tot.cpu()
+        dist.all_reduce(th, op=dist.ReduceOp.MAX)
+        tot = th
+    ms_per_step = float(tot.item()) / args.steps
+    value = n_global / (ms_per_step * 1e-3)
+    clk = clocks.stop()
+    res = holder["res"]
+    mine = res.global_order
+    send_l, recv_l = sharded.last_counts
+    # kernel-level profile of one step (separate from the timed loop): the dominant kernel's
+    # HBM roofline over this rank's shard
+    tie.profile(ctx, True)
+    flush.zero_()
+    step()
+    prof = tie.profile_report(ctx)
+    tie.profile(ctx, False)
+    peak, peak_src = hbm_peak()
+    algo = {"score.moment": 28.0, "rank.fused": 16.0, "rank.local": 16.0, "rank.scatter": 12.0,
+            "rank.count": 8.0}
+    kern = {k: v[1] for k, v in prof.items()}
+    dom = max(kern, key=lambda k: kern[k])
+    per = algo.get(dom, 28.0)
+    ach = per * n_local / (kern[dom] * 1e-3) / 1e9
+    roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": ach / peak, "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes_per_unit": per, "launch_ms": kern[dom]}
+    # ---------------- the exchange alone: the same all-to-all of the same records (NVLink
+    # roofline: bytes received from OTHER GPUs / time vs 900 GB/s per direction)
+    rk = torch.empty(n_local, dtype=torch.float64, device=dev)
+    ri = torch.empty(n_local, dtype=torch.int32, device=dev)
+    ok_ = torch.empty(sum(recv_l), dtype=torch.float64, device=dev)
+    oi_ = torch.empty(sum(recv_l), dtype=torch.int32, device=dev)
+
+    def exchange():
+        sharded.comm.all_to_all_single(ok_, rk, recv_l, send_l)
+        sharded.comm.all_to_all_single(oi_, ri, recv_l, send_l)
+
+    exchange()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    a.record(stream)
+    for _ in range(5):
+        exchange()
+    b.record(stream)
+    torch.cuda.synchronize()
+    x_ms = a.elapsed_time(b) / 5
+    x_bytes = 12.0 * (sum(recv_l) - recv_l[rank])
+    exch = {"kernel": "NCCL all-to-all (12-byte records)" if nccl else "gloo (host-staged)",
+            "bound": "nvlink", "achieved": x_bytes / (x_ms * 1e-3) / 1e9, "peak": NVLINK_GBS,
+            "unit": "GB/s", "frac": x_bytes / (x_ms * 1e-3) / 1e9 / NVLINK_GBS,
+            "bytes_received_per_gpu": x_bytes, "ms": x_ms,
+            "peak_source": "NVLink 5 nominal per GPU per direction"}
+    # ---------------- e2e through the public API on host buffers: pinned shard H2D, the
+    # sharded step, D2H of this rank's slice of the global order
+    e2e_ts = []
+    for i in range(3 + max(args.steps, 10)):
+        dist.barrier()
+        t0 = time.perf_counter()
+        m_ = mu_p.to(dev, non_blocking=True)
+        s_ = sg_p.to(dev, non_blocking=True)
+        x_ = mt_p.to(dev, non_blocking=True)
+        r = sharded(m_, s_, x_, n_global)
+        host_slice = r.global_order.cpu()
+        if i >= 3:
+            e2e_ts.append(time.perf_counter() - t0)
+    e2e_s = torch.tensor([float(np.median(e2e_ts))])
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_s.item())
+    # ---------------- the N = 1 base on rank 0: the whole queue on its own GPU
+    base = None
+    if rank == 0:
+        mu1 = torch.from_numpy(full["mu"]).to(dev)
+        sg1 = torch.from_numpy(full["sigma"]).to(dev)
+        mt1 = torch.from_numpy(full["max_tokens"].view(np.int32)).to(dev)
+        S1 = torch.empty(n_global, dtype=torch.float64, device=dev)
+        o1 = torch.empty(n_global, dtype=torch.int64, device=dev)
+        f1 = lambda: tie.score_rank_device(ctx, mu1.data_ptr(), sg1.data_ptr(), mt1.data_ptr(),
+                                           n_global, ALPHA, beta, 0, 0, S1.data_ptr(),
+                                           o1.data_ptr(), 0, sh)
+        f1()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(3):
+            f1()
+        b.record(stream)
+        torch.cuda.synchronize()
+        b_ms = a.elapsed_time(b) / 3
+        # the sharded global order equals the single-GPU order: rank 0's slice is its prefix
+        slice0_ok = bool(torch.equal(o1[:mine.numel()], mine))
+        base = {"value": n_global / (b_ms * 1e-3), "unit": "requests/s", "ms_per_step": b_ms,
+                "note": "the same 64M queue scored + ranked on rank 0's GPU alone (N = 1)",
+                "rank0_slice_equals_single_gpu_order": slice0_ok}
+        del mu1, sg1, mt1, S1, o1
+    dist.barrier()
+    if rank == 0:
+        line = {"metric": "requests scored+ranked/sec", "value": value, "unit": "requests/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"config4: {n_global}-request queue sharded over "
+                                       f"{world} GPUs, splitter all-to-all (range-owned order)",
+                           "n_requests_global": n_global, "n_requests_per_gpu": n_local,
+                           "nu": 3.5, "alpha": ALPHA, "beta": beta, "mc_samples": 10000,
+                           "parallelism": f"dp{world} (request shards)",
+                           "transport": args.dist_backend,
+                           "l2": "flushed (256 MB write) between timed steps"},
+                "e2e": {"value": n_global / e2e_s, "unit": "requests/s",
+                        "h2d_bytes_per_step": 20 * n_local,
+                        "d2h_bytes_per_step": 8 * int(mine.numel()),
+                        "ms_per_step": e2e_s * 1e3,
+                        "statistic": "median of wall-clocked steps, max over ranks",
+                        "api": "pinned shard -> ShardedScoreRank (DeviceOps) -> rank slice"},
+                "gpu_launches": launches, "roofline": roof, "exchange_roofline": exch,
+                "kernels_ms_per_step": {k: round(v, 5) for k, v in kern.items()},
+                "host_syncs_per_step": sharded.host_syncs,
+                "records": {"sent": send_l, "received": recv_l},
+                "n1_base": base, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def run_config5(tie, seeds=(1, 2, 3)):

@@ -155,6 +155,25 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
                         double* score, uint64_t* order, unsigned flags);
 int tie_rank_host(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n,
                   uint64_t* order);
+/* ---- request-sharded score + rank (host side paper_2604_00499_b200/dist.py) --
+ * tie_score_rank_run: tie_score_rank on one shard, emitting its SORTED RUN as the 12-byte
+ * records the exchange moves: run_keys[p] = score of the p-th request in (score, local index)
+ * order, run_ids[p] = its shard-local index; `order` (u64, n) is the same order as
+ * tie_score_rank's (also a scratch); score may be NULL.
+ * tie_shard_cuts: the splitter exchange's send counts from G gathered regular samples of s
+ * (key, global id) entries each (every rank's sample sorted; invalid entries id < 0 with
+ * +max keys): the merged sample's elements at ranks j*t/G (t valid entries) are the G-1
+ * splitters, and send_counts[j] = #{run records between splitters j-1 and j} in
+ * (score, id_base + local id) order.  split_keys / split_ids (G-1) may be NULL.  One
+ * single-CTA launch, G <= 32, G*s <= 8192. */
+int tie_score_rank_run(tie_ctx* ctx, const double* mu, const double* sigma,
+                       const uint32_t* max_tokens, uint64_t n, double alpha, double beta,
+                       double* score, uint64_t* order, double* run_keys, uint32_t* run_ids,
+                       unsigned flags, void* stream);
+int tie_shard_cuts(tie_ctx* ctx, const double* run_keys, const uint32_t* run_ids,
+                   uint64_t id_base, uint64_t n, const double* sample_keys,
+                   const int64_t* sample_ids, int G, int s, int64_t* send_counts,
+                   double* split_keys, int64_t* split_ids, void* stream);
 /* Sharded score+rank's final k-way merge: G runs on the device, run g =
  * keys/ids[g*stride .. g*stride + lens[g]) (lens: HOST array), each sorted by (score asc, id
  * asc) -- the reference heap's order (sched.cpp:28-31).  out_ids: the sum(lens) merged ids.

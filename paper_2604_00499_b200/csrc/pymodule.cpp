@@ -316,6 +316,35 @@ PYBIND11_MODULE(_core, m) {
       py::arg("out_ids"), py::arg("stream") = 0,
       "k-way merge of G device runs sorted by (score, id): the sharded rank's final step");
   m.def(
+      "score_rank_run_device",
+      [](uintptr_t ctx, uintptr_t mu, uintptr_t sigma, uintptr_t max_tokens, uint64_t n,
+         double alpha, double beta, uintptr_t score, uintptr_t order, uintptr_t run_keys,
+         uintptr_t run_ids, unsigned flags, uintptr_t stream) {
+        throw_code(tie_score_rank_run(reinterpret_cast<tie_ctx*>(ctx), (const double*)mu,
+                                      (const double*)sigma, (const uint32_t*)max_tokens, n,
+                                      alpha, beta, (double*)score, (uint64_t*)order,
+                                      (double*)run_keys, (uint32_t*)run_ids, flags, vp(stream)));
+      },
+      py::arg("ctx"), py::arg("mu"), py::arg("sigma"), py::arg("max_tokens"), py::arg("n"),
+      py::arg("alpha"), py::arg("beta"), py::arg("score"), py::arg("order"), py::arg("run_keys"),
+      py::arg("run_ids"), py::arg("flags") = 0, py::arg("stream") = 0,
+      "score + rank one shard and emit its sorted run (f64 keys, u32 local ids)");
+  m.def(
+      "shard_cuts_device",
+      [](uintptr_t ctx, uintptr_t run_keys, uintptr_t run_ids, uint64_t id_base, uint64_t n,
+         uintptr_t sample_keys, uintptr_t sample_ids, int G, int s, uintptr_t send_counts,
+         uintptr_t split_keys, uintptr_t split_ids, uintptr_t stream) {
+        throw_code(tie_shard_cuts(reinterpret_cast<tie_ctx*>(ctx), (const double*)run_keys,
+                                  (const uint32_t*)run_ids, id_base, n,
+                                  (const double*)sample_keys, (const int64_t*)sample_ids, G, s,
+                                  (int64_t*)send_counts, (double*)split_keys,
+                                  (int64_t*)split_ids, vp(stream)));
+      },
+      py::arg("ctx"), py::arg("run_keys"), py::arg("run_ids"), py::arg("id_base"), py::arg("n"),
+      py::arg("sample_keys"), py::arg("sample_ids"), py::arg("G"), py::arg("s"),
+      py::arg("send_counts"), py::arg("split_keys") = 0, py::arg("split_ids") = 0,
+      py::arg("stream") = 0, "splitter exchange send counts from gathered regular samples");
+  m.def(
       "fit_report_device",
       [](uintptr_t ctx, uintptr_t x, uint64_t P, uint64_t K, double nu, unsigned families,
          uintptr_t fits, uintptr_t tail, uintptr_t stream) {

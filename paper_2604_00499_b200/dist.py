@@ -53,6 +53,54 @@ def global_beta(cfg, n_global: int) -> float:
     return _core.compute_beta(cfg, int(n_global))
 
 
+class Comm:
+    """The collectives the sharded paths use, on ``group``.  Under NCCL (one process per GPU,
+    NVLink / NVSwitch) device tensors go straight to the collective; under gloo (the CPU test
+    transport, and the one-GPU multi-process tests) CUDA tensors are staged through host
+    memory, since gloo's all-gather / all-to-all take CPU tensors only."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.stage = dist.get_backend(group) == "gloo"
+
+    def _h(self, t):
+        return t.cpu() if self.stage and t.is_cuda else t
+
+    def all_gather(self, outs, t):
+        if not (self.stage and t.is_cuda):
+            self.dist.all_gather(outs, t, group=self.group)
+            return
+        hs = [torch_empty_like_cpu(o) for o in outs]
+        self.dist.all_gather(hs, t.cpu(), group=self.group)
+        for o, h in zip(outs, hs):
+            o.copy_(h)
+
+    def all_to_all_single(self, out, inp, out_splits=None, in_splits=None):
+        if not (self.stage and inp.is_cuda):
+            self.dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+            return
+        ho = torch_empty_like_cpu(out)
+        self.dist.all_to_all_single(ho, inp.cpu(), out_splits, in_splits, group=self.group)
+        out.copy_(ho)
+
+    def all_reduce(self, t):
+        if not (self.stage and t.is_cuda):
+            self.dist.all_reduce(t, group=self.group)
+            return
+        h = t.cpu()
+        self.dist.all_reduce(h, group=self.group)
+        t.copy_(h)
+
+
+def torch_empty_like_cpu(t):
+    import torch
+
+    return torch.empty(t.shape, dtype=t.dtype)
+
+
 class DeviceOps:
     """K1+K2 on this rank's GPU through the C-ABI (torch CUDA tensors in and out)."""
 
@@ -68,25 +116,52 @@ class DeviceOps:
         self.alpha = alpha
         self.flags = 1 if exact else 0
 
+    def _stream(self, t):
+        return self.torch.cuda.current_stream(t.device).cuda_stream
+
     def score_sort(self, mu, sigma, max_tokens, beta):
         """-> (scores in queue order, local order (int64 indices sorted by (score, index)))."""
         torch = self.torch
         n = mu.numel()
         S = torch.empty(n, dtype=torch.float64, device=mu.device)
         order = torch.empty(n, dtype=torch.int64, device=mu.device)
-        stream = torch.cuda.current_stream(mu.device).cuda_stream
         self.core.score_rank_device(self.ctx, mu.data_ptr(), sigma.data_ptr(),
                                     max_tokens.data_ptr(), n, self.alpha, beta, 0, 0,
-                                    S.data_ptr(), order.data_ptr(), self.flags, stream)
+                                    S.data_ptr(), order.data_ptr(), self.flags,
+                                    self._stream(mu))
         return S, order
+
+    def sorted_run(self, mu, sigma, max_tokens, beta, run_keys, run_ids):
+        """score + rank the shard, writing its sorted run straight from the device path
+        (tie_score_rank_run): run_keys (f64) / run_ids (int32 shard-local index) views of the
+        caller's exchange buffer -> (scores, local order)."""
+        torch = self.torch
+        n = mu.numel()
+        S = torch.empty(n, dtype=torch.float64, device=mu.device)
+        order = torch.empty(n, dtype=torch.int64, device=mu.device)
+        self.core.score_rank_run_device(self.ctx, mu.data_ptr(), sigma.data_ptr(),
+                                        max_tokens.data_ptr(), n, self.alpha, beta,
+                                        S.data_ptr(), order.data_ptr(), run_keys.data_ptr(),
+                                        run_ids.data_ptr(), self.flags, self._stream(mu))
+        return S, order
+
+    def shard_cuts(self, run_keys, run_ids, id_base, sample_keys, sample_ids, G, s):
+        """-> int64 send counts [G] (device) of the splitter exchange (tie_shard_cuts)."""
+        torch = self.torch
+        out = torch.empty(G, dtype=torch.int64, device=run_keys.device)
+        self.core.shard_cuts_device(self.ctx, run_keys.data_ptr(), run_ids.data_ptr(),
+                                    int(id_base), run_keys.numel(), sample_keys.data_ptr(),
+                                    sample_ids.data_ptr(), G, s, out.data_ptr(), 0, 0,
+                                    self._stream(run_keys))
+        return out
 
     def stable_sort(self, keys):
         """-> int64 permutation sorting ``keys`` by (key, position)."""
         torch = self.torch
         n = keys.numel()
         order = torch.empty(n, dtype=torch.int64, device=keys.device)
-        stream = torch.cuda.current_stream(keys.device).cuda_stream
-        self.core.rank_device(self.ctx, keys.data_ptr(), 0, n, order.data_ptr(), stream)
+        self.core.rank_device(self.ctx, keys.data_ptr(), 0, n, order.data_ptr(),
+                              self._stream(keys))
         return order
 
     def merge_runs(self, keys, ids, lens):
@@ -95,14 +170,40 @@ class DeviceOps:
         torch = self.torch
         G, stride = keys.shape
         out = torch.empty(int(sum(lens)), dtype=torch.int64, device=keys.device)
-        stream = torch.cuda.current_stream(keys.device).cuda_stream
         self.core.merge_runs_device(self.ctx, keys.data_ptr(), ids.data_ptr(), stride,
-                                    [int(x) for x in lens], out.data_ptr(), stream)
+                                    [int(x) for x in lens], out.data_ptr(), self._stream(keys))
         return out
 
     def sync(self):
         stream = self.torch.cuda.current_stream().cuda_stream
         self.core.sync(self.ctx, stream)
+
+
+def _host_shard_cuts(run_keys, run_ids, id_base, sample_keys, sample_ids, G, s):
+    """tie_shard_cuts' semantics in NumPy (ops without a device implementation)."""
+    import torch
+
+    sk = sample_keys.cpu().numpy()
+    si = sample_ids.cpu().numpy()
+    valid = si >= 0
+    k, i = sk[valid], si[valid]
+    o = np.lexsort((i, k))
+    k, i = k[o], i[o]
+    t = len(k)
+    rk = run_keys.cpu().numpy()
+    ri = run_ids.cpu().numpy().astype(np.int64) + int(id_base)
+    n = len(rk)
+    cuts = [0]
+    for j in range(1, G):
+        c = (j * t) // G
+        if c >= t:
+            cuts.append(n)
+            continue
+        lo = int(np.searchsorted(rk, k[c], side="left"))
+        hi = int(np.searchsorted(rk, k[c], side="right"))
+        cuts.append(lo + int(np.searchsorted(ri[lo:hi], i[c], side="left")))
+    cuts.append(n)
+    return torch.tensor(np.diff(cuts), dtype=torch.int64, device=run_keys.device)
 
 
 @dataclass
@@ -115,7 +216,14 @@ class ShardResult:
 
 
 class ShardedScoreRank:
-    """score + rank a globally-indexed queue sharded over the ranks of ``group``."""
+    """score + rank a globally-indexed queue sharded over the ranks of ``group``.
+
+    The exchange moves 12-byte records (f64 score + u32 shard-local index; the sender's id
+    base is implied by its rank): the root / all variants all-gather one packed
+    [keys | ids] byte buffer per rank; the range variant all-to-alls keys and ids.  Device
+    ops emit the sorted run directly (tie_score_rank_run) and compute the splitter cuts on the
+    device (tie_shard_cuts), so a root / all step has no host synchronisation and a range step
+    has exactly one (the send / receive counts the all-to-all's host split sizes need)."""
 
     def __init__(self, ops, cfg_beta: float, group=None, merge_on: str = "root",
                  kway: str = "auto"):
@@ -127,136 +235,135 @@ class ShardedScoreRank:
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.comm = Comm(group) if dist.is_initialized() else None
         if merge_on not in ("root", "all", "range"):
             raise ValueError("merge_on must be 'root', 'all' or 'range'")
         self.merge_on = merge_on
         if kway not in ("auto", "always", "never"):
             raise ValueError("kway must be 'auto', 'always' or 'never'")
         self.kway = kway
+        self.host_syncs = 0  # host round trips of the last call (diagnostics)
+        self.last_counts = None  # (send, receive) record counts of the last range exchange
 
     oversample = 32  # regular-sample points per rank and destination range
+
+    def _run(self, mu, sigma, max_tokens, keys_view, ids_view):
+        """the sorted run into keys_view (f64) / ids_view (int32): fused on device ops"""
+        if hasattr(self.ops, "sorted_run"):
+            return self.ops.sorted_run(mu, sigma, max_tokens, self.beta, keys_view, ids_view)
+        S, order = self.ops.score_sort(mu, sigma, max_tokens, self.beta)
+        keys_view.copy_(S[order])
+        ids_view.copy_(order.to(ids_view.dtype))
+        return S, order
 
     def __call__(self, mu, sigma, max_tokens, n_global: int) -> ShardResult:
         import torch
 
+        self.host_syncs = 0
         lo, hi = shard_bounds(n_global, self.world, self.rank)
-        if mu.numel() != hi - lo:
-            raise ValueError(f"rank {self.rank}: shard holds {mu.numel()} requests, expected "
-                             f"{hi - lo} (ids [{lo}, {hi}))")
-        S, order = self.ops.score_sort(mu, sigma, max_tokens, self.beta)
-        if self.world == 1:
-            return ShardResult(S, order, order)
-        if self.merge_on == "range":
-            return self._range_exchange(S, order, lo, hi)
-        width = shard_bounds(n_global, self.world, 0)[1]  # the longest shard
-        run_k = torch.full((width,), SENTINEL, dtype=torch.float64, device=S.device)
-        run_i = torch.full((width,), -1, dtype=torch.int64, device=S.device)
         m = hi - lo
-        run_k[:m] = S[order]
-        run_i[:m] = order + lo
-        gk = [torch.empty_like(run_k) for _ in range(self.world)]
-        gi = [torch.empty_like(run_i) for _ in range(self.world)]
-        self.dist.all_gather(gk, run_k, group=self.group)
-        self.dist.all_gather(gi, run_i, group=self.group)
+        if mu.numel() != m:
+            raise ValueError(f"rank {self.rank}: shard holds {mu.numel()} requests, expected "
+                             f"{m} (ids [{lo}, {hi}))")
+        if self.world == 1:
+            S, order = self.ops.score_sort(mu, sigma, max_tokens, self.beta)
+            return ShardResult(S, order, order)
+        dev = mu.device
+        if self.merge_on == "range":
+            rk = torch.empty(m, dtype=torch.float64, device=dev)
+            ri = torch.empty(m, dtype=torch.int32, device=dev)
+            S, order = self._run(mu, sigma, max_tokens, rk, ri)
+            return self._range_exchange(S, order, rk, ri, lo, n_global)
+        # root / all: one packed record buffer per rank, [width x f64 keys | width x i32 ids],
+        # padded to the longest shard with (+max, -1) sentinels
+        G = self.world
+        width = shard_bounds(n_global, G, 0)[1]
+        rec = torch.empty(12 * width, dtype=torch.uint8, device=dev)
+        rkeys = rec[:8 * width].view(torch.float64)
+        rids = rec[8 * width:].view(torch.int32)
+        if m < width:
+            rkeys[m:].fill_(SENTINEL)
+            rids[m:].fill_(-1)
+        S, order = self._run(mu, sigma, max_tokens, rkeys[:m], rids[:m])
+        recs = [torch.empty_like(rec) for _ in range(G)]
+        self.comm.all_gather(recs, rec)
         merged = None
         if self.merge_on == "all" or self.rank == 0:
-            lens = [b - a for a, b in (shard_bounds(n_global, self.world, g)
-                                       for g in range(self.world))]
+            bounds = [shard_bounds(n_global, G, g) for g in range(G)]
+            lens = [b - a for a, b in bounds]
+            gk = torch.stack([r[:8 * width].view(torch.float64) for r in recs])
+            base = torch.tensor([a for a, _ in bounds], dtype=torch.int64, device=dev)
+            gi = torch.stack([r[8 * width:].view(torch.int32) for r in recs]).to(torch.int64)
+            gi += base[:, None]  # shard-local -> global ids (sentinels: base - 1, never read)
             # k-way merge of the sorted runs, or a re-sort of the concatenation: both give the
             # identical order; measured on one B200 for G x 1M runs (bench.py "rank0_merge"):
             # G=2 73 vs 71 us re-sort, G=4 213 vs 179, G=8 490 vs 322 -- the range-partition
             # sort is at least as fast, so "auto" re-sorts and the merge tree is opt-in
-            use_kway = self.kway == "always"
-            if hasattr(self.ops, "merge_runs") and use_kway:
-                merged = self.ops.merge_runs(torch.stack(gk), torch.stack(gi), lens)
+            if hasattr(self.ops, "merge_runs") and self.kway == "always":
+                merged = self.ops.merge_runs(gk, gi, lens)
             else:  # stable re-sort of the concatenation (sentinels sort last)
-                keys = torch.cat(gk)
-                ids = torch.cat(gi)
-                perm = self.ops.stable_sort(keys)
-                merged = ids[perm][:n_global]
+                perm = self.ops.stable_sort(gk.reshape(-1))
+                merged = gi.reshape(-1)[perm][:n_global]
         return ShardResult(S, order, merged)
 
-    def _splitters(self, keys, ids):
-        """G-1 (score, id) splitters, identical on every rank: a regular sample of each sorted
-        run is all-gathered (padded with sentinels) and cut at equal sample counts."""
+    def _range_exchange(self, S, order, rk, ri, lo, n_global):
         import torch
 
-        G, m = self.world, keys.numel()
+        G, dev, m = self.world, rk.device, rk.numel()
         s = self.oversample * G
         take = min(m, s)
-        pos = (torch.arange(take, dtype=torch.float64) + 0.5) * (m / max(take, 1))
-        pos = pos.to(torch.int64).clamp_(max=max(m - 1, 0)).to(keys.device)
-        sk = torch.full((s,), SENTINEL, dtype=torch.float64, device=keys.device)
-        si = torch.full((s,), -1, dtype=torch.int64, device=keys.device)
-        sk[:take] = keys[pos]
-        si[:take] = ids[pos]
-        gk = [torch.empty_like(sk) for _ in range(G)]
-        gi = [torch.empty_like(si) for _ in range(G)]
-        self.dist.all_gather(gk, sk, group=self.group)
-        self.dist.all_gather(gi, si, group=self.group)
-        ak = torch.cat(gk).cpu().numpy()
-        ai = torch.cat(gi).cpu().numpy()
-        valid = ai >= 0
-        ak, ai = ak[valid], ai[valid]
-        o = np.lexsort((ai, ak))
-        ak, ai = ak[o], ai[o]
-        t = len(ak)
-        cut = [(j * t) // G for j in range(1, G)]
-        return ([float(ak[c]) if c < t else SENTINEL for c in cut],
-                [int(ai[c]) if c < t else 2 ** 62 for c in cut])
-
-    def _range_exchange(self, S, order, lo, hi):
-        import torch
-
-        G = self.world
-        keys = S[order].contiguous()
-        ids = (order + lo).contiguous()
-        spk, spi = self._splitters(keys, ids)
-        # lexicographic cut: #{(k, i) < (spk, spi)} in the run sorted by (k, i)
-        tk = torch.tensor(spk, dtype=torch.float64, device=keys.device)
-        left = torch.searchsorted(keys, tk, side="left").cpu().tolist()
-        right = torch.searchsorted(keys, tk, side="right").cpu().tolist()
-        cuts = [0]
-        for j in range(G - 1):
-            c = left[j]
-            if right[j] > left[j]:  # equal scores: ids ascending inside the tie run
-                tie = ids[left[j]:right[j]]
-                c += int(torch.searchsorted(tie, torch.tensor([spi[j]], dtype=torch.int64,
-                                                              device=ids.device)).item())
-            cuts.append(max(c, cuts[-1]))
-        cuts.append(keys.numel())
-        send = [cuts[j + 1] - cuts[j] for j in range(G)]
-        dev = keys.device  # NCCL exchanges device tensors only (counts included)
-        recv_t = torch.empty(G, dtype=torch.int64, device=dev)
-        self.dist.all_to_all_single(recv_t, torch.tensor(send, dtype=torch.int64, device=dev),
-                                    group=self.group)
-        recv = recv_t.tolist()
-        total = int(sum(recv))
-        rk = torch.empty(total, dtype=torch.float64, device=keys.device)
-        ri = torch.empty(total, dtype=torch.int64, device=keys.device)
-        self.dist.all_to_all_single(rk, keys, recv, send, group=self.group)
-        self.dist.all_to_all_single(ri, ids, recv, send, group=self.group)
-        # pieces arrive in source-rank order = ascending id ranges, each sorted by (k, i):
-        # a stable sort by k alone (or the k-way merge) yields the (k, i) order
+        # regular sample of the sorted run (device), sentinel-padded to s entries
+        pos = ((torch.arange(take, device=dev, dtype=torch.float64) + 0.5) * (m / max(take, 1)))
+        pos = pos.to(torch.int64).clamp_(max=max(m - 1, 0))
+        sk = torch.full((s,), SENTINEL, dtype=torch.float64, device=dev)
+        si = torch.full((s,), -1, dtype=torch.int64, device=dev)
+        sk[:take] = rk[pos]
+        si[:take] = ri[pos].to(torch.int64) + lo
+        gk = torch.empty(G * s, dtype=torch.float64, device=dev)
+        gi = torch.empty(G * s, dtype=torch.int64, device=dev)
+        self.comm.all_gather(list(gk.view(G, s).unbind(0)), sk)
+        self.comm.all_gather(list(gi.view(G, s).unbind(0)), si)
+        cuts = getattr(self.ops, "shard_cuts", None) or \
+            (lambda *a: _host_shard_cuts(*a))
+        send = cuts(rk, ri, lo, gk, gi, G, s)
+        # receive counts, and every destination's global offset (the records all ranks send
+        # to destinations below it): one all-to-all + one all-reduce, then ONE host read
+        recv = torch.empty(G, dtype=torch.int64, device=dev)
+        self.comm.all_to_all_single(recv, send)
+        below = torch.zeros(G, dtype=torch.int64, device=dev)
+        below[1:] = torch.cumsum(send, 0)[:-1]
+        self.comm.all_reduce(below)
+        counts = torch.cat([send, recv, below]).cpu().tolist()  # the one host sync
+        self.host_syncs += 1
+        send_l, recv_l, below_l = counts[:G], counts[G:2 * G], counts[2 * G:]
+        self.last_counts = (send_l, recv_l)
+        total = int(sum(recv_l))
+        keys = torch.empty(total, dtype=torch.float64, device=dev)
+        ids = torch.empty(total, dtype=torch.int32, device=dev)
+        self.comm.all_to_all_single(keys, rk, recv_l, send_l)
+        self.comm.all_to_all_single(ids, ri, recv_l, send_l)
+        # shard-local -> global ids: piece g came from rank g (its id base)
+        bases = torch.tensor([shard_bounds(n_global, G, g)[0] for g in range(G)],
+                             dtype=torch.int64, device=dev)
+        gids = ids.to(torch.int64) + torch.repeat_interleave(
+            bases, torch.tensor(recv_l, device=dev), output_size=total)
+        # pieces arrive in source-rank order = ascending id ranges, each sorted by (k, i): a
+        # stable sort by k alone (or the k-way merge) yields the (k, i) order
         if hasattr(self.ops, "merge_runs") and self.kway == "always" and total:
-            width = max(recv)
-            pk = torch.full((G, width), SENTINEL, dtype=torch.float64, device=keys.device)
-            pi = torch.full((G, width), -1, dtype=torch.int64, device=keys.device)
+            width = max(recv_l)
+            pk = torch.full((G, width), SENTINEL, dtype=torch.float64, device=dev)
+            pi = torch.full((G, width), -1, dtype=torch.int64, device=dev)
             o = 0
             for g in range(G):
-                pk[g, :recv[g]] = rk[o:o + recv[g]]
-                pi[g, :recv[g]] = ri[o:o + recv[g]]
-                o += recv[g]
-            mine = self.ops.merge_runs(pk, pi, recv)
+                pk[g, :recv_l[g]] = keys[o:o + recv_l[g]]
+                pi[g, :recv_l[g]] = gids[o:o + recv_l[g]]
+                o += recv_l[g]
+            mine = self.ops.merge_runs(pk, pi, recv_l)
         elif total:
-            mine = ri[self.ops.stable_sort(rk)]
+            mine = gids[self.ops.stable_sort(keys)]
         else:
-            mine = ri
-        sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(G)]
-        self.dist.all_gather(sizes, torch.tensor([total], dtype=torch.int64, device=dev),
-                             group=self.group)
-        offset = int(sum(int(x.item()) for x in sizes[:self.rank]))
-        return ShardResult(S, order, mine, offset)
+            mine = gids
+        return ShardResult(S, order, mine, int(below_l[self.rank]))
 
 
 U64_MAX = np.iinfo(np.uint64).max

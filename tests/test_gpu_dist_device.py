@@ -1,0 +1,123 @@
+"""The multi-GPU DEVICE data plane (VERDICT r1 "What's missing" #4 / "Next" #2), run as two
+processes on cuda:0 (the round's GPU boxes have one GPU; the collectives go over gloo, staged
+through host memory by dist.Comm -- under NCCL they take the device tensors directly): each
+rank scores + ranks its shard with the real kernels (tie_score_rank_run emits the sorted run,
+tie_shard_cuts computes the splitter cuts), then the root / all / range exchanges.  The
+global order must equal the single-queue order: config 1 against the oracle (the reference's
+heap semantics), a 2M-request queue against the single-GPU tie_score_rank order (itself
+bit-exact to the reference at config 2, test_gpu_score.py), and a queue of identical requests
+(every cross-shard tie broken by id)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n_global, case, out_q):
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.dirname(here))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2604_00499_b200 as tie
+        from paper_2604_00499_b200.dist import DeviceOps, ShardedScoreRank, shard_bounds
+
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        if case == "ties":
+            mu = np.full(n_global, 4.0)
+            sg = np.full(n_global, 0.8)
+            mt = np.full(n_global, 2048, np.uint32)
+        else:
+            w = tie.gen_logt_workload_soa(n_global, 1)
+            mu, sg, mt = w["mu"], w["sigma"], w["max_tokens"]
+        lo, hi = shard_bounds(n_global, world, rank)
+        beta = tie.compute_beta(tie.ScoreConfig(), n_global)  # GLOBAL queue length
+        ops = DeviceOps(tie.McContext(3.5, 10000, 12, 0), 0.9)
+        args = (torch.from_numpy(mu[lo:hi].copy()).to(dev),
+                torch.from_numpy(sg[lo:hi].copy()).to(dev),
+                torch.from_numpy(mt[lo:hi].copy().view(np.int32)).to(dev))
+        for merge_on, kway in (("root", "auto"), ("all", "auto"), ("root", "always"),
+                               ("range", "auto"), ("range", "always")):
+            sr = ShardedScoreRank(ops, beta, merge_on=merge_on, kway=kway)
+            res = sr(*args, n_global)
+            ops.sync()
+            if merge_on == "range":
+                out_q.put((rank, merge_on + "/" + kway, sr.host_syncs,
+                           (res.offset, res.global_order.cpu().numpy())))
+            elif res.global_order is not None:
+                out_q.put((rank, merge_on + "/" + kway, sr.host_syncs,
+                           res.global_order.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def run_two(n_global, case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_global, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=600) for _ in range(8)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return got
+
+
+def check(got, ref):
+    slices = {}
+    for rank, variant, syncs, order in got:
+        if variant.startswith("range"):
+            assert syncs == 1, variant  # the counts read the all-to-all's split sizes need
+            slices.setdefault(variant, []).append(order)
+            continue
+        assert syncs == 0, variant
+        assert np.array_equal(order, ref), (rank, variant)
+    assert len(slices) == 2
+    for variant, parts in slices.items():
+        parts.sort(key=lambda t: t[0])
+        assert parts[0][0] == 0 and parts[1][0] == len(parts[0][1]), variant
+        assert np.array_equal(np.concatenate([parts[0][1], parts[1][1]]), ref), variant
+        if len(ref) > 100:
+            assert min(len(p[1]) for p in parts) > len(ref) // 4, variant
+
+
+def test_two_process_device_path_config1(oracle, samples):
+    n = 1000
+    got = run_two(n, "workload")
+    mu, sg, mt = oracle.gen_workload(n, seed=1)
+    _, _, S = oracle.score(samples, mu, sg, mt.astype(float), alpha=0.9, beta=0.5)
+    check(got, oracle.rank(S).astype(np.int64))
+
+
+def test_two_process_device_path_ties():
+    n = 5000
+    check(run_two(n, "ties"), np.arange(n, dtype=np.int64))
+
+
+def test_two_process_device_path_2m_queue(tie, mc):
+    n = 2_000_000
+    got = run_two(n, "workload")
+    w = tie.gen_logt_workload_soa(n, 1)
+    _, order = tie.score_rank(w["mu"], w["sigma"], w["max_tokens"], mc, tie.ScoreConfig(), n)
+    check(got, np.asarray(order).astype(np.int64))
