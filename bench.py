@@ -858,7 +858,7 @@ def main_sharded(args, world, rank, local):
         # the sharded global order equals the single-GPU order: rank 0's slice is its prefix
         slice0_ok = bool(torch.equal(o1[:mine.numel()], mine))
         base = {"value": n_global / (b_ms * 1e-3), "unit": "requests/s", "ms_per_step": b_ms,
-                "note": "the same 64M queue scored + ranked on rank 0's GPU alone (N = 1)",
+                "note": f"the same {n_global}-request queue scored + ranked on rank 0's GPU alone (N = 1)",
                 "rank0_slice_equals_single_gpu_order": slice0_ok}
         del mu1, sg1, mt1, S1, o1
     dist.barrier()
