@@ -10,7 +10,8 @@ own WaitingQueue (push x n, pop_min until empty).  The 512 MB score vector and o
 cached under _cache/config4/ (git- and gpurun-ignored); only digests are committed:
 
 * sha256 of the complete reference dispatch order (u64 ids);
-* the tie runs of the reference order at the survey's tolerance (SURVEY.md 8d "parity
+* the tie runs of the reference order at the survey's tolerance (and the reference's ids
+  inside each run, to count the runs another implementation orders differently) (SURVEY.md 8d "parity
   checks": adjacent reference scores within 1e-12 relative) as (start, length) -- a GPU order
   that differs from the reference only by permutations inside these runs is within the bar,
   and its run-canonicalised sha256 (ids sorted inside each run) must equal the reference's;
@@ -97,6 +98,7 @@ def main():
         "sha256_order": hashlib.sha256(order.tobytes()).hexdigest(),
         "sha256_order_canonical": hashlib.sha256(canon.tobytes()).hexdigest(),
         "tie_runs": runs.tolist(),
+        "tie_run_ids_ref": [order[s:s + n].astype(np.int64).tolist() for s, n in runs],
         "chunk": CHUNK,
         "chunk_sha256_order": [hashlib.sha256(order[i:i + CHUNK].tobytes()).hexdigest()[:16]
                                for i in range(0, N4, CHUNK)],
@@ -112,7 +114,8 @@ def main():
     with open(os.path.join(HERE, "config4.json"), "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps({k: v for k, v in out.items() if k not in
-                      ("tie_runs", "chunk_sha256_order", "chunk_fsum_S")}, indent=1))
+                      ("tie_runs", "tie_run_ids_ref", "chunk_sha256_order", "chunk_fsum_S")},
+                     indent=1))
 
 
 if __name__ == "__main__":

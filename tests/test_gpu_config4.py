@@ -1,23 +1,35 @@
-"""GPU parity at BASELINE config 4's full size on one GPU: a 64M-request queue (64 * 2^20,
-gen_logt_workload seed 1) scored and ranked through the C-ABI host call.  The CPU oracle
-cannot score 64M requests in test time (~45 min on 8 cores), so the full-size checks are the
-size-independent properties (SURVEY.md 8c / task 3): the order is a permutation, it is sorted
-by (score, id) with ties broken by id, and a random sample of the scores equals the oracle's
-within the 1e-12 bar (1e-6 is the north star's).  This exercises the large-queue bucket sort
-path (n > 2^21) end to end."""
-import os
+"""GPU parity at BASELINE config 4's full size on one GPU: the 64M-request queue (64 * 2^20,
+gen_logt_workload seed 1) scored and ranked through the C-ABI host call, pinned to the REAL
+reference (tests/golden/config4.json, made by tests/golden/make_golden_config4.py from
+oracle/_ref: the untouched reference's censored_expectation / censored_cvar / compute_score
+chain and its WaitingQueue push + pop_min over all 64M requests, ~50 min on 8 cores):
+
+* the dispatch order equals the reference's up to permutations inside the reference's
+  near-tie runs -- maximal runs of adjacent reference scores within tol = 1e-12 relative
+  (SURVEY.md 8d parity row; 2,246 such pairs at this size, no exact ties): the order with ids
+  sorted inside every run must hash to the reference's run-canonical sha256, and the number
+  of runs the GPU orders differently from the reference (the "exempt" pairs) is reported;
+* the per-2^20-chunk sums of the scores (in id order) equal the reference's within 1e-12
+  relative (a checksum of checksums over all 64M scores);
+* size-independent properties: a permutation, sorted by (score, id).
+The two-level partition sort path (n > 6M) is what runs here."""
+import hashlib
+import math
 
 import numpy as np
 import pytest
 
-from cabi import CAbi, rel_err
+from cabi import CAbi
+from conftest import golden
 
 pytestmark = pytest.mark.gpu
 
 N4 = 64 * 2 ** 20
 
 
-def test_config4_64m_queue_single_gpu(tie, oracle, samples):
+def test_config4_64m_queue_single_gpu_vs_reference(tie):
+    g = golden("config4.json")
+    assert g["n"] == N4 and g["beta"] == 0.5
     w = tie.gen_logt_workload_soa(N4, 1)
     mu, sg, mt = w["mu"], w["sigma"], w["max_tokens"]
     abi = CAbi()
@@ -26,18 +38,31 @@ def test_config4_64m_queue_single_gpu(tie, oracle, samples):
         S, order = abi.score_rank(h, mu, sg, mt, 0.9, 0.5)
     finally:
         abi.destroy(h)
-    # 1. a permutation of 0..n-1
+    order = order.astype(np.uint64)
+    # a permutation, sorted by (score, id): the heap's pop order under the GPU's own scores
     seen = np.zeros(N4, bool)
     seen[order.astype(np.int64)] = True
     assert seen.all()
-    # 2. sorted by (score, id): the heap's pop order
     s = S[order.astype(np.int64)]
     d = np.diff(s)
     assert (d >= 0).all()
     ties = np.flatnonzero(d == 0)
     assert (order[ties] < order[ties + 1]).all()
-    # 3. scores: a random sample against the oracle
-    idx = np.random.default_rng(4).choice(N4, 20000, replace=False)
-    _, _, So = oracle.score(samples, mu[idx], sg[idx], mt[idx].astype(float), alpha=0.9,
-                            beta=0.5, threads=os.cpu_count())
-    assert rel_err(S[idx], So).max() <= 1e-12
+    # the scores: per-chunk checksums vs the reference's
+    C = g["chunk"]
+    for c, ref in enumerate(g["chunk_fsum_S"]):
+        got = math.fsum(S[c * C:(c + 1) * C].tolist())
+        assert abs(got - ref) <= 1e-12 * abs(ref), (c, got, ref)
+    # the order: equal to the reference's up to permutations inside its near-tie runs
+    runs = np.asarray(g["tie_runs"], np.int64).reshape(-1, 2)
+    canon = order.copy()
+    exempt = 0
+    for (st, ln), ref_ids in zip(runs, g["tie_run_ids_ref"]):
+        seg = canon[st:st + ln]
+        exempt += int(not np.array_equal(seg, np.asarray(ref_ids, np.uint64)))
+        canon[st:st + ln] = np.sort(seg)
+    assert hashlib.sha256(canon.tobytes()).hexdigest() == g["sha256_order_canonical"]
+    exact = hashlib.sha256(order.tobytes()).hexdigest() == g["sha256_order"]
+    print(f"config 4: {len(runs)} reference near-tie runs (tol 1e-12), {exempt} ordered "
+          f"differently by the GPU; raw order sha256 {'equal' if exact else 'differs'}")
+    assert exact == (exempt == 0)
