@@ -511,32 +511,59 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
     ncand = 0;
     overflow = 0;
   }
-  // 1. the B smallest block minima (B rounds of a CTA argmin; a thread's local best is
-  //    rescanned only when it wins)
-  auto local_best = [&](uint64_t& k, uint64_t& i, uint32_t& b, const uint32_t* excl, int nex) {
-    k = kDead;
-    i = kDead;
-    b = 0xffffffffu;
-    for (uint32_t x = threadIdx.x; x < nblocks; x += blockDim.x) {
-      bool ex = false;
-      for (int e = 0; e < nex; ++e) ex |= excl[e] == x;
-      if (ex) continue;
-      const uint64_t kk = q.bkey[x], ii = q.bid[x];
-      if (less_kv(kk, ii, k, i)) {
-        k = kk;
-        i = ii;
-        b = x;
+  // 1. the B smallest block minima: every thread keeps the two smallest minima of its
+  //    strided share in registers (one pass, 4 loads in flight per thread: at 64M slots a
+  //    thread owns 64 blocks), then B rounds of a CTA argmin over the threads' heads; the
+  //    winner shifts its pair, and only a thread that wins a third time rescans (excluding
+  //    the chosen blocks).  A one-best-per-thread rescan after every win made each round
+  //    a dependent walk over the winner's share (the 64M step's ~170 us over 10M's).
+  uint64_t k0, i0, k1, i1;
+  uint32_t b0, b1;
+  bool more;  // the thread's share held more than two live blocks when last scanned
+  auto scan_top2 = [&](int nex) {
+    k0 = i0 = k1 = i1 = kDead;
+    b0 = b1 = 0xffffffffu;
+    uint32_t live = 0;
+    constexpr int kU = 4;
+    for (uint32_t x0 = threadIdx.x; x0 < nblocks; x0 += kU * blockDim.x) {
+      uint64_t kk[kU], ii[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {  // all loads in flight before the first use
+        const uint32_t x = x0 + u * blockDim.x;
+        kk[u] = x < nblocks ? q.bkey[x] : kDead;
+        ii[u] = x < nblocks ? q.bid[x] : kDead;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (kk[u] == kDead) continue;
+        const uint32_t x = x0 + u * blockDim.x;
+        bool ex = false;
+        for (int e = 0; e < nex; ++e) ex |= chosen[e] == x;
+        if (ex) continue;
+        ++live;
+        if (!less_kv(kk[u], ii[u], k1, i1)) continue;
+        if (less_kv(kk[u], ii[u], k0, i0)) {
+          k1 = k0;
+          i1 = i0;
+          b1 = b0;
+          k0 = kk[u];
+          i0 = ii[u];
+          b0 = x;
+        } else {
+          k1 = kk[u];
+          i1 = ii[u];
+          b1 = x;
+        }
       }
     }
+    more = live > 2;
   };
-  uint64_t lk, li;
-  uint32_t lb;
-  local_best(lk, li, lb, chosen, 0);
+  scan_top2(0);
   uint32_t nchosen = 0;
   uint64_t vB_k = kDead, vB_i = kDead;
   for (uint32_t r = 0; r < pops; ++r) {
-    uint64_t k = lk, i = li;
-    uint32_t b = lb;
+    uint64_t k = k0, i = i0;
+    uint32_t b = b0;
     block_argmin(k, i, b, sk, si, ss);
     if (k == kDead) break;  // fewer live blocks than pops
     if (threadIdx.x == 0) chosen[r] = b;
@@ -544,7 +571,14 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
     nchosen = r + 1;
     vB_k = k;
     vB_i = i;
-    if (lb == b) local_best(lk, li, lb, chosen, (int)nchosen);
+    if (k0 != kDead && b0 == b) {  // this thread won: its head advances
+      k0 = k1;
+      i0 = i1;
+      b0 = b1;
+      k1 = i1 = kDead;
+      b1 = 0xffffffffu;
+      if (k0 == kDead && more) scan_top2((int)nchosen);
+    }
   }
   if (nchosen == 0) {
     if (threadIdx.x == 0) *out_n = 0;

@@ -989,13 +989,27 @@ __device__ __forceinline__ void sort_partition(const Part& q, uint32_t s0, uint3
   for (uint32_t j = threadIdx.x; j < nf; j += kT) fc[j] = 0;
   __syncthreads();
   const KeyRange r = key_range(q.mm, q.total_bits);
-  for (uint32_t j = threadIdx.x; j < m; j += kT) {
-    const uint64_t k = q.tk[s0 + j];
-    sk[j] = k;
-    sv[j] = q.tv[s0 + j];
-    const uint32_t fine = part_bucket(q, r, k) & fmask;
-    sf[j] = (uint16_t)fine;
-    atomicAdd(&fc[fine], 1u);
+  constexpr int kLd = 4;  // (key, index) loads in flight per thread before the first use
+  for (uint32_t j0 = threadIdx.x; j0 < m; j0 += kLd * kT) {
+    uint64_t kk[kLd];
+    uint32_t vv[kLd];
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const uint32_t j = j0 + u * kT;
+      kk[u] = j < m ? q.tk[s0 + j] : 0ull;
+      vv[u] = j < m ? q.tv[s0 + j] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const uint32_t j = j0 + u * kT;
+      if (j < m) {
+        sk[j] = kk[u];
+        sv[j] = vv[u];
+        const uint32_t fine = part_bucket(q, r, kk[u]) & fmask;
+        sf[j] = (uint16_t)fine;
+        atomicAdd(&fc[fine], 1u);
+      }
+    }
   }
   __syncthreads();
   {  // exclusive scan of the nf (<= 1024) fine counts, 4 per thread
@@ -1115,13 +1129,27 @@ __device__ __forceinline__ void sort_partition_grp(const Part& q, uint32_t s0, u
   for (uint32_t j = gtid; j < nf; j += kN) fc[j] = 0;
   grp_bar<kN>(bar);
   const KeyRange r = key_range(q.mm, q.total_bits);
-  for (uint32_t j = gtid; j < m; j += kN) {
-    const uint64_t k = q.tk[s0 + j];
-    sk[j] = k;
-    sv[j] = q.tv[s0 + j];
-    const uint32_t fine = (part_bucket(q, r, k) & fmask) >> fshift;
-    sf[j] = (uint16_t)fine;
-    atomicAdd(&fc[fine], 1u);
+  constexpr int kLd = 4;  // (key, index) loads in flight per thread before the first use
+  for (uint32_t j0 = gtid; j0 < m; j0 += kLd * kN) {
+    uint64_t kk[kLd];
+    uint32_t vv[kLd];
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const uint32_t j = j0 + u * kN;
+      kk[u] = j < m ? q.tk[s0 + j] : 0ull;
+      vv[u] = j < m ? q.tv[s0 + j] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const uint32_t j = j0 + u * kN;
+      if (j < m) {
+        sk[j] = kk[u];
+        sv[j] = vv[u];
+        const uint32_t fine = (part_bucket(q, r, kk[u]) & fmask) >> fshift;
+        sf[j] = (uint16_t)fine;
+        atomicAdd(&fc[fine], 1u);
+      }
+    }
   }
   grp_bar<kN>(bar);
   {
@@ -1396,8 +1424,19 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_l2_kernel(
   for (uint32_t j = threadIdx.x; j < P2; j += kFusedThreads) cur[j] = 0;
   if (threadIdx.x == 0) big = 0;
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < m1; j += kFusedThreads)
-    atomicAdd(&cur[(part_bucket(q, r, q.tk[s0 + j]) >> q.fine_log2) & mask2], 1u);
+  constexpr int kLd = 8;  // loads in flight per thread before the first use
+  for (uint32_t j0 = threadIdx.x; j0 < m1; j0 += kLd * kFusedThreads) {
+    uint64_t kk[kLd];
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const uint32_t j = j0 + u * kFusedThreads;
+      kk[u] = j < m1 ? q.tk[s0 + j] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kLd; ++u)
+      if (j0 + u * kFusedThreads < m1)
+        atomicAdd(&cur[(part_bucket(q, r, kk[u]) >> q.fine_log2) & mask2], 1u);
+  }
   __syncthreads();
   {
     constexpr int kPer = kL2MaxP / kFusedThreads;
@@ -1426,18 +1465,32 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_l2_kernel(
     if (threadIdx.x == 0) atomicExch(q.overflow, 1);
     return;
   }
-  for (uint32_t j = threadIdx.x; j < m1; j += kFusedThreads) {
-    const uint64_t k = q.tk[s0 + j];
-    const uint32_t pos = atomicAdd(&cur[(part_bucket(q, r, k) >> q.fine_log2) & mask2], 1u);
-    q.tk2[s0 + pos] = k;
-    q.tv2[s0 + pos] = q.tv[s0 + j];
+  for (uint32_t j0 = threadIdx.x; j0 < m1; j0 += kLd * kFusedThreads) {
+    uint64_t kk[kLd];
+    uint32_t vv[kLd];
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const uint32_t j = j0 + u * kFusedThreads;
+      kk[u] = j < m1 ? q.tk[s0 + j] : 0ull;
+      vv[u] = j < m1 ? q.tv[s0 + j] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kLd; ++u)
+      if (j0 + u * kFusedThreads < m1) {
+        const uint32_t pos =
+            atomicAdd(&cur[(part_bucket(q, r, kk[u]) >> q.fine_log2) & mask2], 1u);
+        q.tk2[s0 + pos] = kk[u];
+        q.tv2[s0 + pos] = vv[u];
+      }
   }
   __syncthreads();  // this CTA's global writes are visible to it after the barrier
   Part q2 = q;
   q2.tk = q.tk2;
   q2.tv = q.tv2;
   __shared__ uint32_t gsh[kGroups][32];
+#ifndef TIE_L2_NOSORT
   sort_partitions_grouped<kFusedThreads>(q2, sb, 0, 1, P2, s0, ids, order, smem_raw, gsh);
+#endif
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
