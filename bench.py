@@ -38,7 +38,7 @@ NVLINK_GBS = 900.0  # NVLink 5 per GPU per direction (nominal; B200 SXM)
 ALPHA = 0.9
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0
-TRAFFIC_FILE = "ncu_traffic_r01p.json"
+TRAFFIC_FILE = "ncu_traffic_r02.json"
 
 
 def parse():
@@ -382,42 +382,62 @@ def main():
     roof = roofline(dom)
     others = {k: roofline(k) for k in kern if k != dom and k in algo}
 
-    # the score kernel against the FP64 roofline SURVEY.md 8d defines for it: one sample-term
-    # exp(mu + sigma Y_i) = 32 FP64 flops, k_max(r) = #{Y_i <= y_max(r)} terms per request;
-    # the moment tables evaluate O(1) work per request instead, so the per-term rate is an
-    # EFFECTIVE figure (the reference's arithmetic it replaces), the executed FP64-pipe share
-    # comes from ncu
+    # DRAM traffic per launch from the committed ncu --set full capture of this same
+    # configuration (profiles/TRAFFIC_FILE), scaled to this n, and what bounds the kernel
+    # according to that capture
+    try:
+        with open(os.path.join(ROOT, "profiles", TRAFFIC_FILE)) as f:
+            tr = json.load(f)
+    except (OSError, ValueError):
+        tr = {}
+    for r in [roof] + list(others.values()):
+        k = r["kernel"]
+        if k in tr:
+            t = tr[k]
+            r["traffic"] = (t["dram_read_bytes"] + t["dram_write_bytes"]) * (n_local / t["n"])
+            r["traffic_source"] = f"profiles/{TRAFFIC_FILE}: " + t["capture"]
+            r["limiter"] = {"l1_throughput_pct": t.get("l1_throughput_pct"),
+                            "issue_active_pct": t.get("issue_active_pct"),
+                            "fp64_pipe_pct": t.get("fp64_pipe_pct"),
+                            "achieved_occupancy_pct": t.get("achieved_occupancy_pct"),
+                            "top_stalls": t.get("top_stalls"),
+                            "source": "ncu --set full, same capture"}
+
+    # K1 against the roofline SURVEY.md 8d names for it, the FP64 pipe: the moment tables
+    # evaluate O(1) work per request, so the roofline is the ncu-EXECUTED FP64-pipe share
+    # (with the issue share, which is what bounds the kernel), and the reference's per-sample
+    # arithmetic it replaces is reported separately as an effective rate (score_effective)
     score_roof = roof if dom == "score.moment" else others.get("score.moment")
+    score_effective = None
+    if score_roof is not None and "score.moment" in tr:
+        t = tr["score.moment"]
+        score_roof["fp64_pipe"] = {
+            "bound": "fp64", "frac": t["fp64_pipe_pct"] / 100.0,
+            "issue_frac": t["issue_active_pct"] / 100.0,
+            "inst_executed_per_request": t["inst_executed"] / t["n"] if t.get("inst_executed")
+            else None,
+            "source": f"profiles/{TRAFFIC_FILE}: " + t["capture"]}
     if score_roof is not None and n_local == N_CONFIG2:
         Ys = np.asarray(mc.samples)
         y_max = (np.log(mt_h.astype(np.float64)) - mu_h) / sg_h
         terms = float(np.searchsorted(Ys, y_max, side="right").sum())
         t_k = kern["score.moment"]["ms_per_step"] * 1e-3 / max(kern["score.moment"]["launches"], 1)
-        score_roof["fp64_effective"] = {
+        score_effective = {
             "sample_terms_per_launch": terms, "flops_per_term": 32,
             "effective_tflops": 32.0 * terms / t_k / 1e12,
             "fp64_peak_tflops_nominal": 148 * 64 * 2 * 1.965e9 / 1e12,
-            "note": "reference arithmetic replaced per second; not executed flops"}
-
-    # DRAM traffic per launch from the committed ncu --set full capture of this same
-    # configuration (profiles/ncu_traffic_r01h.json), scaled to this n, and what bounds the
-    # kernel according to that capture
-    try:
-        with open(os.path.join(ROOT, "profiles", TRAFFIC_FILE)) as f:
-            tr = json.load(f)
-        for r in [roof] + list(others.values()):
-            k = r["kernel"]
-            if k in tr:
-                r["traffic"] = (tr[k]["dram_read_bytes"] + tr[k]["dram_write_bytes"]) * (
-                    n_local / tr["n"])
-                r["traffic_source"] = f"profiles/{TRAFFIC_FILE}: " + tr[k]["capture"]
-                r["limiter"] = {"l1_throughput_pct": tr[k].get("l1_throughput_pct"),
-                                "issue_active_pct": tr[k].get("issue_active_pct"),
-                                "fp64_pipe_pct": tr[k].get("fp64_pipe_pct"),
-                                "top_stalls": tr[k].get("top_stalls"),
-                                "source": "ncu --set full, same capture"}
-    except (OSError, KeyError, ValueError):
-        pass
+            "note": "the reference's per-sample-term arithmetic (SURVEY.md 8d: 32 FP64 flops "
+                    "per exp(mu + sigma Y_i) term) replaced per second by the moment tables; "
+                    "not executed flops -- the executed share is roofline.fp64_pipe"}
+    fit_roof = None
+    if "fit.lanes" in tr:
+        t = tr["fit.lanes"]
+        fit_roof = {"kernel": "fit.lanes", "bound": "fp64", "frac": t["fp64_pipe_pct"] / 100.0,
+                    "issue_frac": t["issue_active_pct"] / 100.0,
+                    "top_stalls": t.get("top_stalls"),
+                    "note": "ncu-executed FP64-pipe share of the lane-per-sample BFGS fit "
+                            "(config 3, 1M x 16), SURVEY.md 8d K3",
+                    "source": f"profiles/{TRAFFIC_FILE}: " + t["capture"]}
 
     extras = {}
     if rank == 0 and not args.no_extras:
@@ -465,10 +485,13 @@ def main():
                                  "order_matches_device_path": pageable_ok}},
             "gpu_launches": launches, "context": ctx_cost,
             "roofline": roof, "roofline_other_kernels": others,
+            "score_effective": score_effective,
             "clocks": clk,
             "kernels_ms_per_step": {k: round(v["ms_per_step"], 5) for k, v in kern.items()},
             "sorted_check": sorted_ok}
     line.update(extras)
+    if fit_roof is not None and isinstance(line.get("fit"), dict):
+        line["fit"]["roofline"] = fit_roof
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             one, m, threads, kind = cpu_baseline()

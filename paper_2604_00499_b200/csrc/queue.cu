@@ -739,6 +739,9 @@ __global__ void __launch_bounds__(1024) unpop_kernel(QDev q, const uint32_t* slo
 // predictions (run_sim's max(C, E), compute_score, plus the score kernel's own validation
 // in the error word) and -- only if all pass -- key and write them; refresh the touched
 // blocks; then the fixed-key pops.  Any error: no prediction written, nothing popped.
+// kSmall: the instantiation for queues with fewer live blocks than pops can reach (the
+// register pop path included; the large-queue instantiation keeps the smaller footprint)
+template <bool kSmall>
 __global__ void __launch_bounds__(1024) step_apply_kernel(
     QDev q, uint64_t first, uint64_t n_arr, const uint64_t* arr_ids, const double* arr_keys,
     const uint32_t* slots, uint64_t np, const double* E, double* C, double beta,
@@ -796,7 +799,7 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
   if (skip || pops == 0) {
     if (threadIdx.x == 0) *out_n = 0;
   } else {
-    pop_topb<false>(q, nblocks, n_slots, pops, out_id, out_slot, out_n);
+    pop_topb<kSmall>(q, nblocks, n_slots, pops, out_id, out_slot, out_n);
   }
   if (status_seq) {  // the step's last kernel: publish the completion record (step_finish)
     __syncthreads();
@@ -1332,7 +1335,7 @@ uint64_t launch_plan(tie_queue* Q, const std::vector<Seg>& plan, size_t first_se
                                                    Q->d_out_id + off, Q->d_out_slot + off,
                                                    Q->d_out_n + g, nullptr, err);
     else
-      tie::dev::step_apply_kernel<<<1, 1024, 0, s>>>(
+      tie::dev::step_apply_kernel<false><<<1, 1024, 0, s>>>(
           Q->q, 0, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0.0, nullptr, 0, 0, nb,
           Q->n_slots, plan[g].pops, Q->d_out_id + off, Q->d_out_slot + off, Q->d_out_n + g,
           err);
@@ -1636,7 +1639,8 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
   uint64_t planned = 0;
   for (const Seg& g : plan) planned += g.pops;
   // segment 0's pops ride in the apply kernel unless a rebuild must precede them
-  const bool seg0_fused = !plan.empty() && !plan[0].rebuild && !small_queue(Q);
+  const bool seg0_fused = !plan.empty() && !plan[0].rebuild;
+  const bool sq = small_queue(Q);  // its pops need the register path (step_apply<true>)
   const uint32_t fused_pops = seg0_fused ? plan[0].pops : 0;
   // ---- pack: [arr ids | arr keys | mu | sigma | E | C | key | pred slots | pred max_tokens |
   //            blocks]  (E, C, key: device-only scratch)
@@ -1698,7 +1702,7 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
   // the apply kernel is the step's last kernel when no further plan segments follow it
   const bool apply_last = small && plan.size() <= (seg0_fused ? 1u : 0u);
   if (small) {  // everything after the scoring in one single-CTA kernel
-    tie::dev::step_apply_kernel<<<1, 1024, 0, s>>>(
+    (sq ? tie::dev::step_apply_kernel<true> : tie::dev::step_apply_kernel<false>)<<<1, 1024, 0, s>>>(
         Q->q, first, n_arr, (const uint64_t*)(in + o_aid), (const double*)(in + o_akey),
         (const uint32_t*)(in + o_slot), np, (const double*)(d + o_E), (double*)(d + o_C), beta,
         (const uint32_t*)(in + o_blk), (uint32_t)blocks.size(), n_uncond, nb, Q->n_slots,
@@ -1724,9 +1728,10 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
           Q->q, (const uint32_t*)(d + o_blk), (uint32_t)blocks.size(), Q->n_slots, ctx->d_err,
           n_uncond);
     if (fused_pops)
-      tie::dev::step_apply_kernel<<<1, 1024, 0, s>>>(  // the pops alone (nothing to apply)
+      (sq ? tie::dev::step_apply_kernel<true> : tie::dev::step_apply_kernel<false>)<<<1, 1024, 0, s>>>(
           Q->q, 0, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, beta, nullptr, 0, 0, nb,
-          Q->n_slots, fused_pops, Q->d_out_id, Q->d_out_slot, seg0_n, ctx->d_err);
+          Q->n_slots, fused_pops, Q->d_out_id, Q->d_out_slot, seg0_n, ctx->d_err, nullptr,
+          nullptr, 0u);
     tie::capi::count_launch((n_arr ? 1 : 0) + (np ? 2 : 0) + (blocks.empty() ? 0 : 1) +
                             (fused_pops ? 1 : 0));
   }
