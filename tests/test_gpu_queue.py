@@ -250,3 +250,56 @@ def test_batch_length_mismatch_is_value_error(tie, mc):
     with pytest.raises(ValueError, match="lengths"):
         q.on_prediction_logt(np.array([1, 2], np.uint64), np.ones(2), np.ones(1),
                              np.full(2, 5, np.uint32))
+
+
+def _many_block_keys(n, seed):
+    """keys for n slots (1024-slot blocks, 4+ blocks per thread of the 1024-thread pop CTA):
+    uniform background, the smallest keys packed into the blocks of ONE pop thread (blocks
+    5, 1029, 2053, ...: it wins many rounds and must rescan its share), a few more in other
+    blocks, and tied keys across blocks (id tie-break)"""
+    rng = np.random.default_rng(seed)
+    keys = rng.uniform(100.0, 200.0, n)
+    nb = n // 1024
+    own = [b for b in range(5, nb, 1024)]
+    small = np.arange(1.0, 1.0 + 3 * len(own))
+    for j, k in enumerate(small):  # three tiny keys per block of thread 5
+        b = own[j % len(own)]
+        keys[b * 1024 + 17 * (j // len(own)) + 3] = k
+    keys[7 * 1024 + 9] = 2.5
+    keys[(nb - 1) * 1024 + 1000] = 1.5
+    tied = rng.choice(n, 64, replace=False)
+    keys[tied] = 50.0
+    return keys
+
+
+def test_pop_many_blocks_per_thread_waiting_queue(tie):
+    """4M slots = 4 blocks per thread of the top-B scan (the two-best-per-thread registers and
+    the rescan after a third win; config 4's 64M queue has 64 per thread): pop order equals
+    the (key, id) sort"""
+    n = 4 * 2 ** 20
+    keys = _many_block_keys(n, 3)
+    ids = np.arange(n, dtype=np.uint64)
+    q = tie.WaitingQueue(None, n)
+    q.push_batch(ids, keys)
+    want = np.lexsort((ids, keys))
+    got = []
+    for m in (8, 32, 1, 3, 32, 100, 8, 500, 1000):
+        g, _ = q.pop_batch(m)
+        got += g.tolist()
+    np.testing.assert_array_equal(np.array(got, np.uint64), ids[want[:len(got)]])
+    assert q.validate()
+
+
+def test_pop_many_blocks_per_thread_scheduler(tie, mc):
+    """the Scheduler's pop path (the fused apply kernel) on the same layout: SEPT keys = E"""
+    n = 4 * 2 ** 20
+    E = _many_block_keys(n, 4)
+    ids = np.arange(n, dtype=np.uint64)
+    q = tie.GpuScheduler(mc, tie.Policy.SEPT, _cfg(tie), n)
+    q.on_arrival_batch(ids, np.zeros(n), np.full(n, 512, np.uint32))
+    q.on_prediction_batch(ids, E, E)
+    want = ids[np.lexsort((ids, E))]
+    got = []
+    for m in (8, 8, 32, 1, 8, 64, 8):
+        got += q.next_requests(m).tolist()
+    np.testing.assert_array_equal(np.array(got, np.uint64), want[:len(got)])
