@@ -506,6 +506,31 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
   const tie::dev::RankPrep prep = tie::dev::rank_prepare(ctx, n, s);
   if (!prep.keys) return set_error(TIE_ECUDA, "tie_score_rank_host: scratch allocation failed");
   ctx->err_op = "tie_score_rank_host";
+  // pinned (UVA-mapped) inputs: the score kernel streams them over PCIe itself -- no copy
+  // engine setup per chunk, the reads overlap the scoring at the request granularity
+  // (tools/e2e_probe.py on B200, 1M requests: 604 vs 614 us for the 2-chunk H2D pipeline
+  // below, which pageable inputs still take)
+  auto host_mapped = [](const void* ptr) -> const void* {
+    cudaPointerAttributes a{};
+    const bool ok = cudaPointerGetAttributes(&a, ptr) == cudaSuccess &&
+                    a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
+    cudaGetLastError();
+    return ok ? a.devicePointer : nullptr;
+  };
+  static const int zc_in = getenv("TIE_ZERO_COPY_IN") ? atoi(getenv("TIE_ZERO_COPY_IN")) : 1;
+  if (zc_in) {
+    const void* m_mu = host_mapped(mu);
+    const void* m_sg = host_mapped(sigma);
+    const void* m_mt = host_mapped(max_tokens);
+    if (m_mu && m_sg && m_mt) {
+      const cudaError_t e = tie::dev::launch_score(
+          ctx, (const double*)m_mu, (const double*)m_sg, m_mt, true, n, alpha, beta, nullptr,
+          nullptr, d_S, prep.keys, prep.minmax, flags & TIE_SCORE_EXACT, s, 0);
+      if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
+      goto ranked;
+    }
+  }
+  {
   // pipeline: H2D of chunk c+1 (copy stream) overlaps scoring of chunk c (compute stream)
   // 2 chunks: the second half's H2D overlaps the first half's scoring; every extra copy costs
   // ~3 us of DMA setup, more than the finer overlap wins (tools/e2e_probe.py on B200:
@@ -531,6 +556,8 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
                                                  prep.minmax, flags & TIE_SCORE_EXACT, s, lo);
     if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
   }
+  }
+ranked:
   // pinned (page-locked, UVA-mapped) output: the sort's last kernel writes the dispatch
   // order straight into host memory, so the D2H overlaps the sort instead of following it
   cudaPointerAttributes pa{};
