@@ -13,7 +13,7 @@ def main(bench, ref, tests):
     d = json.load(open(bench))
     r = json.load(open(ref)) if ref else None
     c = d["clocks"]
-    L = [f"# Results (round 1)", "",
+    L = [f"# Results (round 2)", "",
          f"1x B200 via gpurun, `python bench.py` ({bench}); reference arm `python bench.py "
          f"--impl reference` ({ref}).",
          "Config 2 = 1M-request queue (gen_logt_workload seed 1), McContext(3.5, 10000, 12), "
@@ -26,6 +26,13 @@ def main(bench, ref, tests):
          f"| score+rank end to end, C-ABI host call, pinned (`e2e`) | {fmt(d['e2e']['value'])} "
          f"req/s ({1e3 * d['e2e']['ms_per_step']:.0f} us, {d['e2e']['statistic']}; 20 MB H2D + "
          f"8 MB D2H per call) |"]
+    pg = d["e2e"].get("pageable")
+    if pg:
+        L.append(f"| e2e on pageable NumPy buffers | {fmt(pg['value'])} req/s "
+                 f"({1e3 * pg['ms_per_step']:.0f} us) |")
+    if d.get("context"):
+        L.append(f"| McContext creation (once per process, excluded from steps) | "
+                 f"{d['context']['create_ms']:.0f} ms, {d['context']['device_bytes'] / 1e6:.0f} MB |")
     if r and "value" in r:
         L += [f"| reference arm (`--impl reference`: oracle/_ref, {r['cpu_baseline']['cores']} "
               f"cores, sampled) | {fmt(r['value'])} req/s |",
@@ -37,6 +44,13 @@ def main(bench, ref, tests):
           f"| config 3 fits (1M x 16), device | {fmt(d['fit']['value'])} fits/s "
           f"({d['fit']['ms']:.1f} ms) |",
           f"| config 3 fits, e2e (host buffers) | {fmt(d['fit']['e2e']['value'])} fits/s |",
+          f"| north-star fits, 10M x 16, one GPU | {fmt(d['fit_10M']['value'])} fits/s "
+          f"({d['fit_10M']['ms']:.0f} ms) |",
+          f"| config 5 trace simulation (run_sim, canonical.json, rebuild_threshold 0) | "
+          f"{d['config5_sim']['ms_per_sim']:.0f} ms/sim vs reference "
+          f"{d['config5_sim']['reference']['ms_per_sim']:.0f} ms "
+          f"({d['config5_sim']['speedup_vs_reference']:.1f}x), events identical: "
+          f"{d['config5_sim']['events_identical_to_reference']} |",
           f"| `tie fit` analysis (4 families + KS + tail), 1M x 16 | "
           f"{fmt(d['fit_report']['value'])} prompts/s ({d['fit_report']['ms']:.0f} ms) |",
           f"| config 4 size (64M requests) on one GPU | "
@@ -72,13 +86,22 @@ def main(bench, ref, tests):
                  f"{(ro['traffic'] or 0) / 1e6:.1f} MB/launch (ncu); limiter: L1 "
                  f"{lim.get('l1_throughput_pct')}%, issue {lim.get('issue_active_pct')}%, FP64 "
                  f"pipe {lim.get('fp64_pipe_pct')}%, top stalls {lim.get('top_stalls')}.")
-        if "fp64_effective" in ro:
-            fe = ro["fp64_effective"]
-            L.append(f"  Effective rate vs the reference arithmetic: "
-                     f"{fe['sample_terms_per_launch']:.3e} sample-terms x {fe['flops_per_term']} "
-                     f"flops per launch = {fe['effective_tflops']:.0f} TFLOP/s equivalent -- the "
-                     f"moment tables replace ~9,900 exp per request with two table rows.")
+        if "fp64_pipe" in ro:
+            fp = ro["fp64_pipe"]
+            L.append(f"  FP64-pipe roofline (SURVEY 8d K1, ncu-executed): {100 * fp['frac']:.1f}% "
+                     f"of the FP64 pipe, issue {100 * fp['issue_frac']:.1f}%, "
+                     f"{fp['inst_executed_per_request']:.1f} warp-instructions per request.")
         L.append("")
+    fe = d.get("score_effective")
+    if fe:
+        L += [f"Effective rate vs the reference arithmetic: {fe['sample_terms_per_launch']:.3e} "
+              f"sample-terms x {fe['flops_per_term']} flops per launch = "
+              f"{fe['effective_tflops']:.0f} TFLOP/s equivalent -- the moment tables replace "
+              f"~9,900 exp per request with two table rows (not executed flops).", ""]
+    fr = d.get("fit", {}).get("roofline")
+    if fr:
+        L += [f"Roofline fit.lanes (SURVEY 8d K3, FP64 pipe, ncu): {100 * fr['frac']:.1f}% of the "
+              f"FP64 pipe, issue {100 * fr['issue_frac']:.1f}%, top stalls {fr['top_stalls']}.", ""]
     if tests:
         last = open(tests).read().strip().splitlines()[-1]
         L.append(f"Parity on the same box: {tests} (`pytest tests -m gpu`: {last.strip()}).")
