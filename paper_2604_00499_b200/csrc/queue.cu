@@ -305,16 +305,11 @@ struct SegBetas {
 };
 constexpr int kRekeyThreads = 256;
 
-__global__ void __launch_bounds__(kRekeyThreads) rekey_pop_seq_kernel(
-    QDev q, uint32_t nb, uint64_t n_slots, SegBetas betas, uint32_t nseg, uint64_t* out_id,
-    uint32_t* out_slot, uint32_t* out_n, uint64_t* cmin, const unsigned long long* err) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ uint64_t sk[32], si[32];
-  __shared__ uint32_t ss[32];
-  __shared__ int skip;
-  if (threadIdx.x == 0) skip = err && *(const volatile unsigned long long*)err != ~0ull;
-  __syncthreads();
-  if (skip) return;  // the same decision in every CTA: err is final before this launch
+__device__ void rekey_seq_body(const QDev& q, uint32_t nb, uint64_t n_slots,
+                               const SegBetas& betas, uint32_t nseg, uint64_t* out_id,
+                               uint32_t* out_slot, uint32_t* out_n, uint64_t* cmin,
+                               uint64_t* sk, uint64_t* si, uint32_t* ss,
+                               cg::grid_group& grid) {
   const uint32_t G = gridDim.x;
   uint64_t killed = ~0ull;
   for (uint32_t g = 0; g < nseg; ++g) {
@@ -408,6 +403,393 @@ __global__ void __launch_bounds__(kRekeyThreads) rekey_pop_seq_kernel(
     if (threadIdx.x == 0) q.key[killed] = kDead;
     __syncthreads();
     refresh_block(q, (uint32_t)(killed / kBlockSlots), n_slots, sk, si, ss);
+  }
+}
+
+__global__ void __launch_bounds__(kRekeyThreads) rekey_pop_seq_kernel(
+    QDev q, uint32_t nb, uint64_t n_slots, SegBetas betas, uint32_t nseg, uint64_t* out_id,
+    uint32_t* out_slot, uint32_t* out_n, uint64_t* cmin, const unsigned long long* err) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint64_t sk[32], si[32];
+  __shared__ uint32_t ss[32];
+  __shared__ int skip;
+  if (threadIdx.x == 0) skip = err && *(const volatile unsigned long long*)err != ~0ull;
+  __syncthreads();
+  if (skip) return;  // the same decision in every CTA: err is final before this launch
+  rekey_seq_body(q, nb, n_slots, betas, nseg, out_id, out_slot, out_n, cmin, sk, si, ss, grid);
+}
+
+// The same run of (drift rebuild, pop) segments with ONE pass over the queue instead of one
+// per segment.  Keys are monotone in beta (fl(E + fl(beta C)) with C >= 0; unpredicted keys
+// are constants), so every key of the run lies in [k_lo, k_hi] = its keys at the smallest /
+// largest beta of the run.  Let T = the nseg-th smallest (k_hi, id) over the block minima: at
+// any segment at least one not-yet-popped entry has (key, id) <= T, so every entry the run
+// pops has (k_lo, id) <= T -- the candidates, a handful.  The pass keys every entry at the
+// run's LAST beta (the reference's final state, sched.cpp:159-164), stores keys and block
+// minima, and records each block's minimum (k_lo, id) and (k_hi, id); CTA 0 selects T; the
+// candidates are gathered; CTA 0 replays the segments over them exactly (re-key at beta_g,
+// (key, id) argmin, kill); the popped blocks are refreshed.  A candidate list above
+// kSeqCandCap falls back to the per-segment passes (rekey_seq_body) in the same launch.
+constexpr uint32_t kSeqCandCap = 1024;
+struct CandScratch {
+  uint64_t* blo;   // [nb][2] block minimum (k_lo, id)
+  uint64_t* bhi;   // [nb][2] block minimum (k_hi, id)
+  uint32_t* cand;  // [kSeqCandCap] candidate slots
+  uint32_t* hdr;   // [0] count, [1] overflow
+  uint64_t* thr;   // [2] T = (key, id)
+  uint64_t* clist; // [kCminCtas][32][2] each CTA's smallest block minima (k_hi, id)
+};
+
+__device__ __forceinline__ void warp_min3(uint64_t& k, uint64_t& i, uint32_t& s) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t k2 = __shfl_down_sync(0xffffffffu, k, o);
+    const uint64_t i2 = __shfl_down_sync(0xffffffffu, i, o);
+    const uint32_t s2 = __shfl_down_sync(0xffffffffu, s, o);
+    if (less_kv(k2, i2, k, i)) {
+      k = k2;
+      i = i2;
+      s = s2;
+    }
+  }
+}
+
+// the r-th smallest (key, id) pair of pairs[0..n) (r < rmax), by one CTA: every thread keeps
+// the two smallest of its strided share, then r + 1 rounds of a CTA argmin over the heads
+// (a thread that wins a third time rescans, excluding the pairs already taken)
+__device__ void cta_rth_smallest(const uint64_t* __restrict__ pairs, uint32_t n, uint32_t r,
+                                 uint64_t& ok, uint64_t& oi, uint64_t* sk, uint64_t* si,
+                                 uint32_t* ss, uint32_t* taken) {
+  uint64_t k0, i0, k1, i1;
+  uint32_t b0, b1;
+  bool more;
+  auto scan = [&](uint32_t ntaken) {
+    k0 = i0 = k1 = i1 = kDead;
+    b0 = b1 = 0xffffffffu;
+    uint32_t live = 0;
+    constexpr int kU = 4;  // loads in flight per thread
+    for (uint32_t x0 = threadIdx.x; x0 < n; x0 += kU * blockDim.x) {
+      uint64_t kk[kU], ii[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t x = x0 + u * blockDim.x;
+        kk[u] = x < n ? __ldcg(pairs + 2 * x) : kDead;
+        ii[u] = x < n ? __ldcg(pairs + 2 * x + 1) : kDead;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (kk[u] == kDead) continue;
+        const uint32_t x = x0 + u * blockDim.x;
+        bool ex = false;
+        for (uint32_t e = 0; e < ntaken; ++e) ex |= taken[e] == x;
+        if (ex) continue;
+        ++live;
+        if (!less_kv(kk[u], ii[u], k1, i1)) continue;
+        if (less_kv(kk[u], ii[u], k0, i0)) {
+          k1 = k0;
+          i1 = i0;
+          b1 = b0;
+          k0 = kk[u];
+          i0 = ii[u];
+          b0 = x;
+        } else {
+          k1 = kk[u];
+          i1 = ii[u];
+          b1 = x;
+        }
+      }
+    }
+    more = live > 2;
+  };
+  scan(0);
+  ok = oi = kDead;
+  for (uint32_t t = 0; t <= r; ++t) {
+    uint64_t k = k0, i = i0;
+    uint32_t b = b0;
+    block_argmin(k, i, b, sk, si, ss);
+    if (k == kDead) {  // fewer than r + 1 pairs: no bound
+      ok = oi = kDead;
+      return;
+    }
+    ok = k;
+    oi = i;
+    if (threadIdx.x == 0) taken[t] = b;
+    __syncthreads();
+    if (k0 != kDead && b0 == b) {
+      k0 = k1;
+      i0 = i1;
+      b0 = b1;
+      k1 = i1 = kDead;
+      b1 = 0xffffffffu;
+      if (k0 == kDead && more) scan(t + 1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRekeyThreads) rekey_pop_cand_kernel(
+    QDev q, uint32_t nb, uint64_t n_slots, SegBetas betas, uint32_t nseg, uint64_t* out_id,
+    uint32_t* out_slot, uint32_t* out_n, uint64_t* cmin, CandScratch cs,
+    const unsigned long long* err) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint64_t sk[32], si[32];
+  __shared__ uint32_t ss[32];
+  __shared__ uint32_t taken[32];
+  __shared__ int skip;
+  __shared__ double cE[kSeqCandCap], cC[kSeqCandCap];
+  __shared__ uint64_t cK[kSeqCandCap], cI[kSeqCandCap];
+  if (threadIdx.x == 0) skip = err && *(const volatile unsigned long long*)err != ~0ull;
+  __syncthreads();
+  if (skip) return;  // the same decision in every CTA: err is final before this launch
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // the gather's header, visible after sync 1
+    cs.hdr[0] = 0;
+    cs.hdr[1] = 0;
+  }
+  double b_lo = betas.b[0], b_hi = betas.b[0];
+  for (uint32_t g = 1; g < nseg; ++g) {
+    b_lo = fmin(b_lo, betas.b[g]);
+    b_hi = fmax(b_hi, betas.b[g]);
+  }
+  const double b_last = betas.b[nseg - 1];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t W = (gridDim.x * blockDim.x) >> 5;
+  // every warp's nseg smallest block minima (k_hi, id), sorted (lane 0 inserts)
+  __shared__ uint64_t wl[kRekeyThreads / 32][32][2];
+  __shared__ uint32_t wn[kRekeyThreads / 32];
+  if (lane == 0) wn[wib] = 0;
+  // ---- A: one pass, a warp per block: keys at b_last stored; minima at b_last, b_lo, b_hi
+  for (uint32_t b = warp; b < nb; b += W) {
+    uint64_t mk = kDead, mi = kDead, lk = kDead, li = kDead, hk = kDead, hi = kDead;
+    uint32_t ms = 0, dummy = 0;
+    constexpr int kU = 8;
+#pragma unroll
+    for (int base = 0; base < kBlockSlots; base += 32 * kU) {
+      uint64_t kk[kU], ii[kU];
+      double ee[kU], cc[kU];
+      uint8_t pr[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {  // all loads in flight first
+        const uint64_t slot = (uint64_t)b * kBlockSlots + base + u * 32 + lane;
+        const bool in = slot < n_slots;
+        kk[u] = in ? q.key[slot] : kDead;
+        ii[u] = in ? q.id[slot] : kDead;
+        pr[u] = in ? q.predicted[slot] : 0;
+        ee[u] = in ? q.E[slot] : 0.0;
+        cc[u] = in ? q.C[slot] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (kk[u] == kDead) continue;
+        const uint64_t slot = (uint64_t)b * kBlockSlots + base + u * 32 + lane;
+        uint64_t kx = kk[u], kl = kk[u], kh = kk[u];
+        if (pr[u]) {
+          kx = order_bits(__dadd_rn(ee[u], __dmul_rn(b_last, cc[u])));
+          kl = order_bits(__dadd_rn(ee[u], __dmul_rn(b_lo, cc[u])));
+          kh = order_bits(__dadd_rn(ee[u], __dmul_rn(b_hi, cc[u])));
+          q.key[slot] = kx;
+        }
+        if (less_kv(kx, ii[u], mk, mi)) {
+          mk = kx;
+          mi = ii[u];
+          ms = (uint32_t)slot;
+        }
+        if (less_kv(kl, ii[u], lk, li)) {
+          lk = kl;
+          li = ii[u];
+        }
+        if (less_kv(kh, ii[u], hk, hi)) {
+          hk = kh;
+          hi = ii[u];
+        }
+      }
+    }
+    warp_min3(mk, mi, ms);
+    warp_min3(lk, li, dummy);
+    warp_min3(hk, hi, dummy);
+    if (lane == 0) {
+      q.bkey[b] = mk;
+      q.bid[b] = mi;
+      q.bslot[b] = ms;
+      cs.blo[2 * b] = lk;
+      cs.blo[2 * b + 1] = li;
+      if (hk != kDead) {  // insert into the warp's sorted list of nseg
+        uint32_t c = wn[wib];
+        if (c < nseg || less_kv(hk, hi, wl[wib][c - 1][0], wl[wib][c - 1][1])) {
+          uint32_t at = c < nseg ? c : nseg - 1;
+          while (at > 0 && less_kv(hk, hi, wl[wib][at - 1][0], wl[wib][at - 1][1])) {
+            wl[wib][at][0] = wl[wib][at - 1][0];
+            wl[wib][at][1] = wl[wib][at - 1][1];
+            --at;
+          }
+          wl[wib][at][0] = hk;
+          wl[wib][at][1] = hi;
+          if (c < nseg) wn[wib] = c + 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  {  // the CTA's nseg smallest of its warps' lists (rank by counting), into its clist row
+    const uint32_t w = threadIdx.x >> 5, pos = threadIdx.x & 31;
+    const bool have = pos < wn[w];
+    const uint64_t k = have ? wl[w][pos][0] : kDead, i = have ? wl[w][pos][1] : kDead;
+    uint32_t rank = 0;
+    if (have)
+      for (uint32_t w2 = 0; w2 < kRekeyThreads / 32; ++w2)
+        for (uint32_t p2 = 0; p2 < wn[w2]; ++p2)
+          rank += less_kv(wl[w2][p2][0], wl[w2][p2][1], k, i) ? 1u : 0u;
+    uint64_t* row = cs.clist + (size_t)blockIdx.x * 64;
+    if (threadIdx.x < 32) {  // clear the row first (kDead pairs), then place the ranked
+      row[2 * threadIdx.x] = kDead;
+      row[2 * threadIdx.x + 1] = kDead;
+    }
+    __syncthreads();
+    if (have && rank < nseg) {
+      row[2 * rank] = k;
+      row[2 * rank + 1] = i;
+    }
+  }
+  grid.sync();
+  // ---- T: the nseg-th smallest block minimum (k_hi, id) over the CTAs' sorted lists, by
+  // EVERY CTA (no serial phase, no extra grid sync): each thread owns the lists t, t + 256,
+  // ...; nseg rounds of a CTA argmin over the owned lists' heads, the winner's head advances
+  uint64_t tk = kDead, ti = kDead;
+  {
+    constexpr int kMaxOwned = 4096 / kRekeyThreads;  // kCminCtas lists at most
+    uint8_t head[kMaxOwned];
+#pragma unroll
+    for (int j = 0; j < kMaxOwned; ++j) head[j] = 0;
+    for (uint32_t r = 0; r < nseg; ++r) {
+      uint64_t k = kDead, i = kDead;
+      uint32_t s = 0xffffffffu;
+#pragma unroll
+      for (int j = 0; j < kMaxOwned; ++j) {
+        const uint32_t L = threadIdx.x + j * kRekeyThreads;
+        if (L >= gridDim.x || head[j] >= 32) continue;
+        const uint64_t* e = cs.clist + (size_t)L * 64 + 2 * head[j];
+        const uint64_t kk = __ldcg(e), ii = __ldcg(e + 1);
+        if (less_kv(kk, ii, k, i)) {
+          k = kk;
+          i = ii;
+          s = (uint32_t)j;
+        }
+      }
+      const uint32_t mine = s == 0xffffffffu ? 0xffffffffu : threadIdx.x * kMaxOwned + s;
+      uint32_t win = mine;
+      block_argmin(k, i, win, sk, si, ss);
+      if (k == kDead) {  // fewer than nseg block minima: no bound
+        tk = ti = kDead;
+        break;
+      }
+      tk = k;
+      ti = i;
+      if (win == mine && mine != 0xffffffffu) {
+#pragma unroll
+        for (int j = 0; j < kMaxOwned; ++j) head[j] += (uint32_t)j == s ? 1 : 0;
+      }
+    }
+  }
+  // ---- B: candidates (k_lo, id) <= T, from the blocks whose minimum (k_lo, id) is <= T
+  for (uint32_t b = warp; b < nb; b += W) {
+    if (less_kv(tk, ti, __ldcg(cs.blo + 2 * b), __ldcg(cs.blo + 2 * b + 1))) continue;
+    constexpr int kU = 8;
+#pragma unroll
+    for (int base = 0; base < kBlockSlots; base += 32 * kU) {
+      uint64_t kk[kU], ii[kU];
+      double ee[kU], cc[kU];
+      uint8_t pr[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {  // all loads in flight first
+        const uint64_t slot = (uint64_t)b * kBlockSlots + base + u * 32 + lane;
+        const bool in = slot < n_slots;
+        kk[u] = in ? q.key[slot] : kDead;  // stored at b_last by this warp in A
+        ii[u] = in ? q.id[slot] : kDead;
+        pr[u] = in ? q.predicted[slot] : 0;
+        ee[u] = in ? q.E[slot] : 0.0;
+        cc[u] = in ? q.C[slot] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint64_t slot = (uint64_t)b * kBlockSlots + base + u * 32 + lane;
+        bool take = false;
+        if (kk[u] != kDead) {
+          const uint64_t kl =
+              pr[u] ? order_bits(__dadd_rn(ee[u], __dmul_rn(b_lo, cc[u]))) : kk[u];
+          take = !less_kv(tk, ti, kl, ii[u]);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, take);
+        if (!m) continue;
+        uint32_t at = 0;
+        if (lane == 0) at = atomicAdd(cs.hdr, (uint32_t)__popc(m));
+        at = __shfl_sync(0xffffffffu, at, 0) + __popc(m & ((1u << lane) - 1u));
+        if (take) {
+          if (at < kSeqCandCap) cs.cand[at] = (uint32_t)slot;
+          else cs.hdr[1] = 1;
+        }
+      }
+    }
+  }
+  grid.sync();
+  const uint32_t nc = __ldcg(cs.hdr), over = __ldcg(cs.hdr + 1);
+  if (over || nc > kSeqCandCap) {  // identical decision in every CTA
+    rekey_seq_body(q, nb, n_slots, betas, nseg, out_id, out_slot, out_n, cmin, sk, si, ss, grid);
+    return;
+  }
+  // ---- C: CTA 0 replays the segments over the candidates (keys re-made at every beta_g)
+  if (blockIdx.x == 0) {
+    for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
+      const uint32_t slot = cs.cand[c];
+      cE[c] = q.E[slot];
+      cC[c] = q.C[slot];
+      cK[c] = q.key[slot];
+      cI[c] = q.id[slot];
+      if (!q.predicted[slot]) cC[c] = -1.0;  // unpredicted: key constant
+    }
+    __syncthreads();
+    uint32_t g = 0;
+    for (; g < nseg; ++g) {
+      const double beta = betas.b[g];
+      uint64_t k = kDead, i = kDead;
+      uint32_t s = 0xffffffffu;
+      for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
+        if (cK[c] == kDead) continue;  // popped earlier in the run
+        const uint64_t kc = cC[c] >= 0.0 ? order_bits(__dadd_rn(cE[c], __dmul_rn(beta, cC[c])))
+                                         : cK[c];
+        if (less_kv(kc, cI[c], k, i)) {
+          k = kc;
+          i = cI[c];
+          s = c;
+        }
+      }
+      block_argmin(k, i, s, sk, si, ss);
+      if (k == kDead) break;  // the queue ran dry
+      if (threadIdx.x == 0) {
+        const uint32_t slot = cs.cand[s];
+        out_id[g] = i;
+        out_slot[g] = slot;
+        out_n[g] = 1;
+        q.key[slot] = kDead;
+        cK[s] = kDead;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0)
+      for (uint32_t r = g; r < nseg; ++r) out_n[r] = 0;
+  }
+  grid.sync();
+  // ---- D: refresh the popped blocks (a warp per pop; a block popped twice is refreshed
+  // twice, identically -- every kill happened before the grid sync)
+  for (uint32_t j = warp; j < nseg; j += W) {
+    if (__ldcg(out_n + j) == 0) continue;
+    const uint32_t blk = __ldcg(out_slot + j) / kBlockSlots;
+    uint64_t k, i;
+    uint32_t s;
+    warp_block_min(q, blk, n_slots, lane, k, i, s);
+    if (lane == 0) {
+      q.bkey[blk] = k;
+      q.bid[blk] = i;
+      q.bslot[blk] = s;
+    }
   }
 }
 
@@ -909,6 +1291,7 @@ using tie::capi::cuda_error;
 using tie::capi::set_error;
 
 constexpr uint32_t kCminCtas = 4096;  // grid cap of the cooperative re-key + pop kernel
+static_assert(kCminCtas <= 4096, "rekey_pop_cand_kernel: lists per thread");
 
 struct tie_queue {
   tie_ctx* ctx = nullptr;
@@ -953,6 +1336,8 @@ struct tie_queue {
   uint64_t pack_cap = 0;
   uint64_t peers = 0;             // waiting requests held by other shards (beta's queue length)
   uint64_t* d_cmin = nullptr;     // [2][3][kCminCtas] CTA minima of the re-key + pop kernel
+  void* d_cand = nullptr;         // CandScratch of the one-pass re-key + pop kernel
+  uint64_t cand_nb = 0;           // blocks it is sized for
   uint64_t* h_peek_key = nullptr; // mapped pinned: keys of a peek's (undone) pops
   uint64_t peek_cap = 0;
   uint64_t* h_out_id = nullptr;   // pinned
@@ -1291,10 +1676,54 @@ struct QDevArgs {
   const unsigned long long* err;
 };
 
+#ifndef TIE_CAND_MIN_BLOCKS
+#define TIE_CAND_MIN_BLOCKS 512
+#endif
+constexpr uint32_t kCandMinBlocks = TIE_CAND_MIN_BLOCKS;
+
+// the one-pass re-key + pop kernel's scratch: per-block (k_lo, id) / (k_hi, id) minima, the
+// candidate slots, a count / overflow header and the threshold pair (grow-only)
+int ensure_cand(tie_queue* Q, uint64_t nb) {
+  if (nb <= Q->cand_nb && Q->d_cand) return TIE_OK;
+  const uint64_t want = std::max<uint64_t>(nb, 1024);
+  cudaFree(Q->d_cand);
+  Q->d_cand = nullptr;
+  Q->cand_nb = 0;
+  const size_t bytes = 32 * want + 16 + 16 + 4 * tie::dev::kSeqCandCap + 512 * kCminCtas;
+  if (cudaMalloc(&Q->d_cand, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return TIE_ECUDA;
+  }
+  Q->cand_nb = want;
+  return TIE_OK;
+}
+
+tie::dev::CandScratch cand_scratch(tie_queue* Q) {
+  char* b = (char*)Q->d_cand;
+  tie::dev::CandScratch cs;
+  cs.blo = (uint64_t*)b;
+  cs.bhi = (uint64_t*)(b + 16 * Q->cand_nb);
+  cs.thr = (uint64_t*)(b + 32 * Q->cand_nb);
+  cs.hdr = (uint32_t*)(b + 32 * Q->cand_nb + 16);
+  cs.cand = (uint32_t*)(b + 32 * Q->cand_nb + 32);
+  cs.clist = (uint64_t*)(b + 32 * Q->cand_nb + 32 + 4 * tie::dev::kSeqCandCap);
+  return cs;
+}
+
 uint64_t launch_plan(tie_queue* Q, const std::vector<Seg>& plan, size_t first_seg,
                      uint32_t off, cudaStream_t s, unsigned long long* err) {
   const uint32_t nb = (uint32_t)((Q->n_slots + tie::dev::kBlockSlots - 1) / tie::dev::kBlockSlots);
   static int rekey_ctas = -1;  // co-resident CTAs of the cooperative re-key + pop kernel
+  static int cand_ctas = -1;   // ... of the one-pass (candidate) variant
+  if (cand_ctas < 0) {
+    int bpsm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, tie::dev::rekey_pop_cand_kernel,
+                                                  tie::dev::kRekeyThreads, 0);
+    cand_ctas = std::min(bpsm * sms, (int)kCminCtas);
+    if (getenv("TIE_NO_REKEY_CAND")) cand_ctas = 0;  // A/B switch
+  }
   if (rekey_ctas < 0) {
     int bpsm = 0, dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -1310,6 +1739,30 @@ uint64_t launch_plan(tie_queue* Q, const std::vector<Seg>& plan, size_t first_se
   while (g < plan.size()) {
     size_t e = g;  // [g, e): a run of (rebuild, 1 pop) segments for one cooperative launch
     while (e < plan.size() && e - g < 32 && single_rebuild_pop(e)) ++e;
+    // small queues: the per-segment passes are short and the one-pass kernel's fixed phases
+    // (three grid syncs, the replay) dominate (B200 step p50: 300k slots 109 vs 86 us,
+    // 1M 109 vs 122, 10M 197 vs 546, 64M 570 vs 2991)
+    if (e - g >= 2 && cand_ctas > 0 && nb >= kCandMinBlocks && ensure_cand(Q, nb) == TIE_OK) {
+      tie::dev::SegBetas sb{};
+      for (size_t j = g; j < e; ++j) sb.b[j - g] = plan[j].beta;
+      tie::dev::CandScratch cs = cand_scratch(Q);
+      uint32_t nseg = (uint32_t)(e - g);
+      uint64_t* out_id = Q->d_out_id + off;
+      uint32_t* out_slot = Q->d_out_slot + off;
+      uint32_t* out_n = Q->d_out_n + g;
+      uint64_t n_slots = Q->n_slots;
+      const uint32_t grid = std::min<uint32_t>(nb, (uint32_t)cand_ctas);
+      void* args[] = {&Q->q, (void*)&nb, &n_slots, &sb, &nseg, &out_id, &out_slot, &out_n,
+                      &Q->d_cmin, &cs, &err};
+      if (cudaLaunchCooperativeKernel((const void*)tie::dev::rekey_pop_cand_kernel, grid,
+                                      tie::dev::kRekeyThreads, args, 0, s) == cudaSuccess) {
+        tie::capi::count_launch(1);
+        off += nseg;
+        g = e;
+        continue;
+      }
+      cudaGetLastError();  // not launchable here: the per-segment variant below
+    }
     if (e - g >= 2 && rekey_ctas > 0 && nb > 0) {
       tie::dev::SegBetas sb{};
       for (size_t j = g; j < e; ++j) sb.b[j - g] = plan[j].beta;
@@ -1435,7 +1888,8 @@ void tie_queue_destroy(tie_queue* Q) {
   for (void* p : {(void*)Q->q.key, (void*)Q->q.id, (void*)Q->q.E, (void*)Q->q.C,
                   (void*)Q->q.predicted, (void*)Q->q.bkey, (void*)Q->q.bid,
                   (void*)Q->q.bslot, (void*)Q->d_ids, (void*)Q->d_a, (void*)Q->d_b,
-                  (void*)Q->d_c, (void*)Q->d_slots, (void*)Q->d_blocks, (void*)Q->d_cmin})
+                  (void*)Q->d_c, (void*)Q->d_slots, (void*)Q->d_blocks, (void*)Q->d_cmin,
+                  Q->d_cand})
     cudaFree(p);
   cudaFreeHost(Q->h_out);
   cudaFreeHost(Q->h_peek_key);
