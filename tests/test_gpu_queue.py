@@ -303,3 +303,50 @@ def test_pop_many_blocks_per_thread_scheduler(tie, mc):
     for m in (8, 8, 32, 1, 8, 64, 8):
         got += q.next_requests(m).tolist()
     np.testing.assert_array_equal(np.array(got, np.uint64), want[:len(got)])
+
+
+def _rekey_expected(tie, sc, pred, E, C, mkey, ids, pops):
+    """the reference's pop sequence at rebuild_threshold 0 with beta moving at every pop
+    (sched.cpp:152-175): before pop j every predicted key is re-made at beta(Q_j) =
+    compute_beta(Q_j) (E + beta * C, the same IEEE operations), then the (key, id) minimum"""
+    alive = np.ones(len(ids), bool)
+    out = []
+    q = len(ids)
+    for _ in range(pops):
+        b = tie.compute_beta(sc, q)
+        keys = np.where(pred, E + b * C, mkey)
+        keys = np.where(alive, keys, np.inf)
+        j = np.lexsort((ids, keys))[0]
+        out.append(int(ids[j]))
+        alive[j] = False
+        q -= 1
+    return out
+
+
+@pytest.mark.parametrize("ties", [False, True])
+def test_rekey_every_pop_one_pass_matches_reference(tie, mc, ties):
+    """the one-pass re-key + pop kernel (>= 512 blocks; a run of (rebuild, pop) segments): pops
+    at rebuild_threshold 0 with beta moving every pop equal the reference's re-key-then-pop
+    sequence; mixed unpredicted entries (constant keys) pop among the predicted ones; with
+    `ties`, 3,000 identical (E, C) pairs at the front make the candidate list overflow (the
+    in-launch per-segment fallback) and pop in id order"""
+    n = 600_000
+    rng = np.random.default_rng(11 + ties)
+    ids = rng.permutation(np.arange(10, 10 + n, dtype=np.uint64))
+    E = rng.uniform(50.0, 500.0, n)
+    C = E * rng.uniform(1.0, 3.0, n)
+    pred = rng.random(n) > 0.05
+    mt = rng.integers(60, 4000, n).astype(np.uint32)
+    if ties:
+        E[:3000], C[:3000] = 20.0, 30.0
+        pred[:3000] = True
+    sc = _cfg(tie, q_sat=1e9, thr=0.0)
+    q = tie.GpuScheduler(mc, tie.Policy.TIE, sc, n)
+    q.on_arrival_batch(ids, np.zeros(n), mt)
+    q.on_prediction_batch(ids[pred], E[pred], C[pred])
+    mkey = mt.astype(np.float64)  # unpredicted TIE entries are keyed at max_tokens
+    got = []
+    for m in (8, 8, 32, 5, 32, 32, 3):
+        got += q.next_requests(m).tolist()
+    want = _rekey_expected(tie, sc, pred, E, C, mkey, ids, len(got))
+    assert got == want
