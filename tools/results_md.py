@@ -35,7 +35,7 @@ def main(bench, ref, tests):
                  f"{d['context']['create_ms']:.0f} ms, {d['context']['device_bytes'] / 1e6:.0f} MB |")
     if r and "value" in r:
         L += [f"| reference arm (`--impl reference`: oracle/_ref, {r['cpu_baseline']['cores']} "
-              f"cores, sampled) | {fmt(r['value'])} req/s |",
+              f"cores, the full 1M queue per step) | {fmt(r['value'])} req/s |",
               f"| e2e / reference arm | {d['e2e']['value'] / r['value']:.0f}x |"]
     cb = d["cpu_baseline"]
     L += [f"| `cpu_baseline` in the bench line ({cb['kind']}, {cb['cores']} cores) | "
