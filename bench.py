@@ -853,6 +853,52 @@ def main_sharded(args, world, rank, local):
             "unit": "GB/s", "frac": x_bytes / (x_ms * 1e-3) / 1e9 / NVLINK_GBS,
             "bytes_received_per_gpu": x_bytes, "ms": x_ms,
             "peak_source": "NVLink 5 nominal per GPU per direction"}
+    # the same exchange over peer memory (dist.PeerExchange: CUDA-IPC-mapped receive buffers,
+    # ONE launch of peer stores for keys and ids), and the whole step with that transport
+    try:
+        from paper_2604_00499_b200.dist import PeerExchange
+
+        pe = PeerExchange(sharded.ops)
+        G = world
+        M = np.zeros((G, G), np.int64)
+        M[rank] = send_l
+        Mt = torch.from_numpy(M).to(dev if nccl else "cpu")
+        dist.all_reduce(Mt)
+        M = Mt.cpu().numpy()
+        dst_l = [int(M[:rank, g].sum()) for g in range(G)]
+        pe.ensure(int(sum(recv_l)))
+        pe.put(rk, ri, send_l, dst_l)  # warm-up (maps the peers)
+        ts = []
+        for _ in range(5):
+            dist.barrier()
+            t0 = time.perf_counter()
+            pe.put(rk, ri, send_l, dst_l)  # includes its stream sync + barrier
+            ts.append(time.perf_counter() - t0)
+        p_ms = float(np.median(ts)) * 1e3
+        exch["p2p"] = {"kernel": "tie_peer_put_runs (CUDA IPC peer stores, keys + ids)",
+                       "ms_wall_incl_barrier": p_ms,
+                       "achieved": x_bytes / (p_ms * 1e-3) / 1e9, "unit": "GB/s",
+                       "frac": x_bytes / (p_ms * 1e-3) / 1e9 / NVLINK_GBS}
+        pe.close()
+        sp = ShardedScoreRank(DeviceOps(mc, ALPHA), beta, merge_on="range", transport="p2p")
+        sp(mu, sg, mt, n_global)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(max(args.steps, 5)):
+            flush.zero_()
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rp = sp(mu, sg, mt, n_global)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        tt = torch.tensor([float(np.median(ts))], device=dev if nccl else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        exch["p2p"]["step_ms_wall_max_over_ranks"] = float(tt.item()) * 1e3
+        exch["p2p"]["step_order_equals_collective"] = bool(torch.equal(rp.global_order, mine))
+        sp.peer.close()
+    except Exception as exc:  # the peer path never blocks the headline line
+        exch["p2p"] = {"error": repr(exc)}
     # ---------------- e2e through the public API on host buffers: pinned shard H2D, the
     # sharded step, D2H of this rank's slice of the global order
     e2e_ts = []

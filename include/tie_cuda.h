@@ -174,6 +174,22 @@ int tie_shard_cuts(tie_ctx* ctx, const double* run_keys, const uint32_t* run_ids
                    uint64_t id_base, uint64_t n, const double* sample_keys,
                    const int64_t* sample_ids, int G, int s, int64_t* send_counts,
                    double* split_keys, int64_t* split_ids, void* stream);
+/* The range exchange over peer memory: receive buffers allocated with
+ * tie_ipc_alloc (cudaMalloc + a 64-byte cudaIpcMemHandle) are mapped into every other rank's
+ * address space with tie_ipc_open (NVLink / NVSwitch peers), and tie_peer_put_runs writes this
+ * rank's sorted run straight into them: piece g (send_counts[g] records, consecutive in the
+ * run) lands at peer_keys[g] / peer_ids[g] + dst_offsets[g] -- one launch of peer stores in
+ * place of the NCCL all-to-all of keys and ids (sched.cpp:28-31 order is kept: every piece
+ * stays sorted).  The caller orders completion (stream sync + a barrier) before the
+ * receivers read.  G <= 64; send_counts / dst_offsets / peer_* are HOST arrays. */
+int tie_ipc_alloc(tie_ctx* ctx, uint64_t bytes, void** ptr, void* handle);
+int tie_ipc_free(tie_ctx* ctx, void* ptr);
+int tie_ipc_open(tie_ctx* ctx, const void* handle, void** ptr);
+int tie_ipc_close(tie_ctx* ctx, void* ptr);
+int tie_peer_put_runs(tie_ctx* ctx, const double* run_keys, const uint32_t* run_ids,
+                      uint64_t n, int G, const uint64_t* send_counts,
+                      const uint64_t* dst_offsets, void* const* peer_keys,
+                      void* const* peer_ids, void* stream);
 /* Sharded score+rank's final k-way merge: G runs on the device, run g =
  * keys/ids[g*stride .. g*stride + lens[g]) (lens: HOST array), each sorted by (score asc, id
  * asc) -- the reference heap's order (sched.cpp:28-31).  out_ids: the sum(lens) merged ids.

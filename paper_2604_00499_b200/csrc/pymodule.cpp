@@ -344,6 +344,58 @@ PYBIND11_MODULE(_core, m) {
       py::arg("sample_keys"), py::arg("sample_ids"), py::arg("G"), py::arg("s"),
       py::arg("send_counts"), py::arg("split_keys") = 0, py::arg("split_ids") = 0,
       py::arg("stream") = 0, "splitter exchange send counts from gathered regular samples");
+  // CUDA IPC + the range exchange over peer memory (tie_ipc_*, tie_peer_put_runs)
+  m.def(
+      "ipc_alloc",
+      [](uintptr_t ctx, uint64_t bytes) {
+        void* ptr = nullptr;
+        char h[64];
+        throw_code(tie_ipc_alloc(reinterpret_cast<tie_ctx*>(ctx), bytes, &ptr, h));
+        return py::make_tuple((uintptr_t)ptr, py::bytes(h, 64));
+      },
+      py::arg("ctx"), py::arg("bytes"), "cudaMalloc + its IPC handle -> (device pointer, handle)");
+  m.def(
+      "ipc_free",
+      [](uintptr_t ctx, uintptr_t ptr) {
+        throw_code(tie_ipc_free(reinterpret_cast<tie_ctx*>(ctx), (void*)ptr));
+      },
+      py::arg("ctx"), py::arg("ptr"));
+  m.def(
+      "ipc_open",
+      [](uintptr_t ctx, py::bytes handle) {
+        const std::string h = handle;
+        if (h.size() != 64) throw py::value_error("ipc_open: a handle is 64 bytes");
+        void* ptr = nullptr;
+        throw_code(tie_ipc_open(reinterpret_cast<tie_ctx*>(ctx), h.data(), &ptr));
+        return (uintptr_t)ptr;
+      },
+      py::arg("ctx"), py::arg("handle"), "map another process's buffer -> device pointer");
+  m.def(
+      "ipc_close",
+      [](uintptr_t ctx, uintptr_t ptr) {
+        throw_code(tie_ipc_close(reinterpret_cast<tie_ctx*>(ctx), (void*)ptr));
+      },
+      py::arg("ctx"), py::arg("ptr"));
+  m.def(
+      "peer_put_runs_device",
+      [](uintptr_t ctx, uintptr_t run_keys, uintptr_t run_ids, uint64_t n,
+         std::vector<uint64_t> send_counts, std::vector<uint64_t> dst_offsets,
+         std::vector<uintptr_t> peer_keys, std::vector<uintptr_t> peer_ids, uintptr_t stream) {
+        const size_t G = send_counts.size();
+        if (dst_offsets.size() != G || peer_keys.size() != G || peer_ids.size() != G)
+          throw py::value_error("peer_put_runs_device: per-peer lists differ in length");
+        std::vector<void*> pk(G), pi(G);
+        for (size_t g = 0; g < G; ++g) {
+          pk[g] = (void*)peer_keys[g];
+          pi[g] = (void*)peer_ids[g];
+        }
+        throw_code(tie_peer_put_runs(reinterpret_cast<tie_ctx*>(ctx), (const double*)run_keys,
+                                     (const uint32_t*)run_ids, n, (int)G, send_counts.data(),
+                                     dst_offsets.data(), pk.data(), pi.data(), vp(stream)));
+      },
+      py::arg("ctx"), py::arg("run_keys"), py::arg("run_ids"), py::arg("n"),
+      py::arg("send_counts"), py::arg("dst_offsets"), py::arg("peer_keys"), py::arg("peer_ids"),
+      py::arg("stream") = 0, "write this rank's sorted run pieces into the peers' buffers");
   m.def(
       "fit_report_device",
       [](uintptr_t ctx, uintptr_t x, uint64_t P, uint64_t K, double nu, unsigned families,

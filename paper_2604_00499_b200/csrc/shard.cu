@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "../../include/tie_cuda.h"
 #include "tie_internal.cuh"
@@ -111,6 +112,36 @@ __global__ void __launch_bounds__(kCutThreads) shard_cuts_kernel(
   }
 }
 
+// The range exchange over peer memory: the sorted run's piece g (run positions
+// [start[g], start[g+1])) goes to rank g's receive buffer at dst[g] + (p - start[g]) -- keys and
+// ids in ONE launch of SM-driven stores into the CUDA-IPC-mapped buffers (NVLink / NVSwitch
+// between GPUs), in place of the two NCCL all-to-alls.  Consecutive records of a piece go to
+// consecutive addresses of one peer (coalesced peer stores).
+constexpr int kMaxPeers = 64;
+struct PeerTab {
+  uint64_t start[kMaxPeers + 1];
+  uint64_t dst[kMaxPeers];
+  double* k[kMaxPeers];
+  uint32_t* i[kMaxPeers];
+  int G;
+};
+
+__global__ void __launch_bounds__(256) peer_put_kernel(const double* __restrict__ rk,
+                                                       const uint32_t* __restrict__ ri,
+                                                       uint64_t n, const __grid_constant__ PeerTab t) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+    int lo = 0, hi = t.G;  // piece g with start[g] <= p < start[g + 1] (non-empty)
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (t.start[mid] <= p) lo = mid; else hi = mid;
+    }
+    const uint64_t q = t.dst[lo] + (p - t.start[lo]);
+    t.k[lo][q] = rk[p];
+    t.i[lo][q] = ri[p];
+  }
+}
+
 }  // namespace
 }  // namespace dev
 }  // namespace tie
@@ -162,4 +193,78 @@ extern "C" int tie_shard_cuts(tie_ctx* ctx, const double* run_keys, const uint32
   tie::capi::count_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TIE_OK : cuda_error(e, "tie_shard_cuts");
+}
+
+// ---- CUDA IPC + peer put (SURVEY.md 8e range exchange over peer memory) -----------------
+extern "C" int tie_ipc_alloc(tie_ctx* ctx, uint64_t bytes, void** ptr, void* handle) {
+  if (!ctx || !ptr || !handle) return set_error(TIE_EINVALID, "tie_ipc_alloc: null argument");
+  cudaSetDevice(ctx->device);
+  *ptr = nullptr;
+  cudaError_t e = cudaMalloc(ptr, bytes ? bytes : 1);
+  if (e == cudaSuccess)
+    e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle), *ptr);
+  if (e != cudaSuccess) {
+    if (*ptr) cudaFree(*ptr);
+    *ptr = nullptr;
+    return cuda_error(e, "tie_ipc_alloc");
+  }
+  return TIE_OK;
+}
+
+extern "C" int tie_ipc_free(tie_ctx* ctx, void* ptr) {
+  if (!ctx) return set_error(TIE_EINVALID, "tie_ipc_free: null context");
+  cudaSetDevice(ctx->device);
+  const cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? TIE_OK : cuda_error(e, "tie_ipc_free");
+}
+
+extern "C" int tie_ipc_open(tie_ctx* ctx, const void* handle, void** ptr) {
+  if (!ctx || !handle || !ptr) return set_error(TIE_EINVALID, "tie_ipc_open: null argument");
+  cudaSetDevice(ctx->device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? TIE_OK : cuda_error(e, "tie_ipc_open");
+}
+
+extern "C" int tie_ipc_close(tie_ctx* ctx, void* ptr) {
+  if (!ctx) return set_error(TIE_EINVALID, "tie_ipc_close: null context");
+  cudaSetDevice(ctx->device);
+  const cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? TIE_OK : cuda_error(e, "tie_ipc_close");
+}
+
+extern "C" int tie_peer_put_runs(tie_ctx* ctx, const double* run_keys, const uint32_t* run_ids,
+                                 uint64_t n, int G, const uint64_t* send_counts,
+                                 const uint64_t* dst_offsets, void* const* peer_keys,
+                                 void* const* peer_ids, void* stream) {
+  if (!ctx) return set_error(TIE_EINVALID, "tie_peer_put_runs: null context");
+  if (G < 1 || G > tie::dev::kMaxPeers)
+    return set_error(TIE_EINVALID, "tie_peer_put_runs: need 1 <= G <= 64");
+  if (!send_counts || !dst_offsets || !peer_keys || !peer_ids)
+    return set_error(TIE_EINVALID, "tie_peer_put_runs: null argument");
+  tie::dev::PeerTab t{};
+  t.G = G;
+  uint64_t acc = 0;
+  for (int g = 0; g < G; ++g) {
+    t.start[g] = acc;
+    acc += send_counts[g];
+    t.dst[g] = dst_offsets[g];
+    t.k[g] = static_cast<double*>(peer_keys[g]);
+    t.i[g] = static_cast<uint32_t*>(peer_ids[g]);
+    if (send_counts[g] && (!t.k[g] || !t.i[g]))
+      return set_error(TIE_EINVALID, "tie_peer_put_runs: null peer buffer");
+  }
+  t.start[G] = acc;
+  if (acc != n) return set_error(TIE_EINVALID, "tie_peer_put_runs: send counts != run length");
+  if (n == 0) return TIE_OK;
+  // empty pieces must never be chosen by the search: start[g] == start[g+1] is skipped
+  // because the search picks the LAST g with start[g] <= p
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8);
+  tie::dev::peer_put_kernel<<<grid, 256, 0, st>>>(run_keys, run_ids, n, t);
+  tie::capi::count_launch();
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TIE_OK : cuda_error(e, "tie_peer_put_runs");
 }

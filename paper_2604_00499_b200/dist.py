@@ -206,6 +206,96 @@ def _host_shard_cuts(run_keys, run_ids, id_base, sample_keys, sample_ids, G, s):
     return torch.tensor(np.diff(cuts), dtype=torch.int64, device=run_keys.device)
 
 
+class _DevArray:
+    """a raw device allocation as a torch tensor (__cuda_array_interface__, no copy)"""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 2,
+                                         "strides": None}
+
+
+class PeerExchange:
+    """The range exchange's records over peer memory (NVLink / NVSwitch between
+    the GPUs of a node): every rank owns one receive buffer [cap x f64 keys | cap x u32 ids]
+    allocated by ``tie_ipc_alloc`` and mapped into every other rank with ``tie_ipc_open``
+    (CUDA IPC handles exchanged once with ``all_gather_object``), and ONE launch of
+    ``tie_peer_put_runs`` writes this rank's sorted run pieces straight into the destinations
+    at their final offsets -- no staging buffer, no NCCL all-to-all of keys and ids.  Completion
+    is ordered by a stream synchronisation and a barrier before any rank reads its buffer.
+    Capacity grows collectively (every rank re-allocates and re-exchanges handles together)."""
+
+    def __init__(self, ops, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.ops = ops
+        self.core = ops.core
+        self.ctx = ops.ctx
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.cap = 0
+        self.mine = 0          # this rank's buffer (device pointer)
+        self.peers = []        # every rank's buffer base in THIS address space
+        self.opened = []
+
+    def _release(self):
+        for ptr in self.opened:
+            self.core.ipc_close(self.ctx, ptr)
+        if self.mine:
+            self.core.ipc_free(self.ctx, self.mine)
+        self.opened, self.peers, self.mine, self.cap = [], [], 0, 0
+
+    def ensure(self, need: int):
+        """collective: every rank's buffer holds >= max over ranks of ``need`` records"""
+        import torch
+
+        t = torch.tensor([int(need)], dtype=torch.int64)
+        if self.dist.get_backend(self.group) == "nccl":
+            t = t.cuda()
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        want = int(t.item())
+        if want <= self.cap:
+            return
+        self.ops.torch.cuda.synchronize()
+        self.dist.barrier(group=self.group)  # nobody still writes into the old buffers
+        self._release()
+        cap = max(want + want // 8, 1 << 16)
+        ptr, handle = self.core.ipc_alloc(self.ctx, 12 * cap)
+        handles = [None] * self.world
+        self.dist.all_gather_object(handles, handle, group=self.group)
+        peers = []
+        for g, h in enumerate(handles):
+            if g == self.rank:
+                peers.append(ptr)
+            else:
+                q = self.core.ipc_open(self.ctx, h)
+                self.opened.append(q)
+                peers.append(q)
+        self.mine, self.peers, self.cap = ptr, peers, cap
+
+    def views(self, total: int):
+        """this rank's received (keys f64, ids int32) records as torch tensors"""
+        torch = self.ops.torch
+        k = torch.as_tensor(_DevArray(self.mine, total, "<f8"), device="cuda")
+        i = torch.as_tensor(_DevArray(self.mine + 8 * self.cap, total, "<i4"), device="cuda")
+        return k, i
+
+    def put(self, rk, ri, send_l, dst_l):
+        """write the sorted run's pieces (send_l records each) into the peers at dst_l"""
+        stream = self.ops.torch.cuda.current_stream(rk.device).cuda_stream
+        self.core.peer_put_runs_device(
+            self.ctx, rk.data_ptr(), ri.data_ptr(), rk.numel(), [int(x) for x in send_l],
+            [int(x) for x in dst_l], [int(p) for p in self.peers],
+            [int(p) + 8 * self.cap for p in self.peers], stream)
+        self.ops.torch.cuda.current_stream(rk.device).synchronize()
+        self.dist.barrier(group=self.group)  # every piece has landed in every buffer
+
+    def close(self):
+        self._release()
+
+
 @dataclass
 class ShardResult:
     scores: object            # this rank's scores, queue order (device tensor)
@@ -226,13 +316,20 @@ class ShardedScoreRank:
     has exactly one (the send / receive counts the all-to-all's host split sizes need)."""
 
     def __init__(self, ops, cfg_beta: float, group=None, merge_on: str = "root",
-                 kway: str = "auto"):
+                 kway: str = "auto", transport: str = "collective"):
         import torch.distributed as dist
 
         self.dist = dist
         self.ops = ops
         self.beta = cfg_beta
         self.group = group
+        if transport not in ("collective", "p2p"):
+            raise ValueError("transport must be 'collective' or 'p2p'")
+        # "p2p": the range exchange writes the records into the destinations' buffers over
+        # peer memory (PeerExchange); needs device ops and merge_on="range"
+        if transport == "p2p" and merge_on != "range":
+            raise ValueError("transport='p2p' moves the range exchange (merge_on='range')")
+        self.peer = PeerExchange(ops, group) if transport == "p2p" else None
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.comm = Comm(group) if dist.is_initialized() else None
@@ -326,22 +423,41 @@ class ShardedScoreRank:
         cuts = getattr(self.ops, "shard_cuts", None) or \
             (lambda *a: _host_shard_cuts(*a))
         send = cuts(rk, ri, lo, gk, gi, G, s)
-        # receive counts, and every destination's global offset (the records all ranks send
-        # to destinations below it): one all-to-all + one all-reduce, then ONE host read
-        recv = torch.empty(G, dtype=torch.int64, device=dev)
-        self.comm.all_to_all_single(recv, send)
-        below = torch.zeros(G, dtype=torch.int64, device=dev)
-        below[1:] = torch.cumsum(send, 0)[:-1]
-        self.comm.all_reduce(below)
-        counts = torch.cat([send, recv, below]).cpu().tolist()  # the one host sync
-        self.host_syncs += 1
-        send_l, recv_l, below_l = counts[:G], counts[G:2 * G], counts[2 * G:]
-        self.last_counts = (send_l, recv_l)
-        total = int(sum(recv_l))
-        keys = torch.empty(total, dtype=torch.float64, device=dev)
-        ids = torch.empty(total, dtype=torch.int32, device=dev)
-        self.comm.all_to_all_single(keys, rk, recv_l, send_l)
-        self.comm.all_to_all_single(ids, ri, recv_l, send_l)
+        if self.peer is not None:
+            # the G x G send matrix (one all-gather, ONE host read): the receive counts are
+            # its column, a piece's landing offset in its destination the column sum above
+            # this rank, the destinations' global offsets its prefix sums; then one launch of
+            # peer stores moves every piece (PeerExchange)
+            mat = torch.empty((G, G), dtype=torch.int64, device=dev)
+            self.comm.all_gather(list(mat.unbind(0)), send)
+            M = mat.cpu().numpy()
+            self.host_syncs += 1
+            send_l = [int(x) for x in M[self.rank]]
+            recv_l = [int(x) for x in M[:, self.rank]]
+            below_l = [int(M[:, :g].sum()) for g in range(G)]
+            dst_l = [int(M[:self.rank, g].sum()) for g in range(G)]
+            self.last_counts = (send_l, recv_l)
+            total = int(sum(recv_l))
+            self.peer.ensure(total)
+            self.peer.put(rk, ri, send_l, dst_l)
+            keys, ids = self.peer.views(total)
+        else:
+            # receive counts, and every destination's global offset (the records all ranks
+            # send to destinations below it): one all-to-all + one all-reduce, ONE host read
+            recv = torch.empty(G, dtype=torch.int64, device=dev)
+            self.comm.all_to_all_single(recv, send)
+            below = torch.zeros(G, dtype=torch.int64, device=dev)
+            below[1:] = torch.cumsum(send, 0)[:-1]
+            self.comm.all_reduce(below)
+            counts = torch.cat([send, recv, below]).cpu().tolist()  # the one host sync
+            self.host_syncs += 1
+            send_l, recv_l, below_l = counts[:G], counts[G:2 * G], counts[2 * G:]
+            self.last_counts = (send_l, recv_l)
+            total = int(sum(recv_l))
+            keys = torch.empty(total, dtype=torch.float64, device=dev)
+            ids = torch.empty(total, dtype=torch.int32, device=dev)
+            self.comm.all_to_all_single(keys, rk, recv_l, send_l)
+            self.comm.all_to_all_single(ids, ri, recv_l, send_l)
         # shard-local -> global ids: piece g came from rank g (its id base)
         bases = torch.tensor([shard_bounds(n_global, G, g)[0] for g in range(G)],
                              dtype=torch.int64, device=dev)

@@ -6,7 +6,10 @@ tie_shard_cuts computes the splitter cuts), then the root / all / range exchange
 global order must equal the single-queue order: config 1 against the oracle (the reference's
 heap semantics), a 2M-request queue against the single-GPU tie_score_rank order (itself
 bit-exact to the reference at config 2, test_gpu_score.py), and a queue of identical requests
-(every cross-shard tie broken by id)."""
+(every cross-shard tie broken by id).  The range exchange runs over the collectives AND over
+peer memory (transport="p2p": CUDA-IPC-mapped receive buffers written by one peer-store launch,
+dist.PeerExchange) -- two processes on one GPU exercise the same IPC mapping that NVLink peers
+use."""
 import os
 import socket
 
@@ -55,14 +58,19 @@ def _worker(rank, world, port, n_global, case, out_q):
         args = (torch.from_numpy(mu[lo:hi].copy()).to(dev),
                 torch.from_numpy(sg[lo:hi].copy()).to(dev),
                 torch.from_numpy(mt[lo:hi].copy().view(np.int32)).to(dev))
-        for merge_on, kway in (("root", "auto"), ("all", "auto"), ("root", "always"),
-                               ("range", "auto"), ("range", "always")):
-            sr = ShardedScoreRank(ops, beta, merge_on=merge_on, kway=kway)
+        for merge_on, kway, tr in (("root", "auto", "collective"), ("all", "auto", "collective"),
+                                   ("root", "always", "collective"),
+                                   ("range", "auto", "collective"),
+                                   ("range", "always", "collective"),
+                                   ("range", "auto", "p2p"), ("range", "always", "p2p")):
+            sr = ShardedScoreRank(ops, beta, merge_on=merge_on, kway=kway, transport=tr)
             res = sr(*args, n_global)
             ops.sync()
             if merge_on == "range":
-                out_q.put((rank, merge_on + "/" + kway, sr.host_syncs,
+                out_q.put((rank, merge_on + "/" + kway + "/" + tr, sr.host_syncs,
                            (res.offset, res.global_order.cpu().numpy())))
+                if sr.peer is not None:
+                    sr.peer.close()
             elif res.global_order is not None:
                 out_q.put((rank, merge_on + "/" + kway, sr.host_syncs,
                            res.global_order.cpu().numpy()))
@@ -77,7 +85,7 @@ def run_two(n_global, case):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, n_global, case, q)) for r in range(2)]
     for p in procs:
         p.start()
-    got = [q.get(timeout=600) for _ in range(8)]
+    got = [q.get(timeout=600) for _ in range(12)]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
@@ -93,7 +101,7 @@ def check(got, ref):
             continue
         assert syncs == 0, variant
         assert np.array_equal(order, ref), (rank, variant)
-    assert len(slices) == 2
+    assert len(slices) == 4  # range x {auto, always} x {collective, p2p (CUDA IPC)}
     for variant, parts in slices.items():
         parts.sort(key=lambda t: t[0])
         assert parts[0][0] == 0 and parts[1][0] == len(parts[0][1]), variant
