@@ -15,6 +15,8 @@
 """
 import math
 
+import zlib
+
 import numpy as np
 import pytest
 
@@ -53,15 +55,8 @@ def test_psi_matches_reference(tie, mc, R):
     assert abs(tie.psi(ym, p, mc) + 512.0 * (1 - tie.t_cdf(ym, 3.5)) - e) <= 1e-12 * e
 
 
-@needs_ref
-@pytest.mark.parametrize("fn,nargs,param", [
-    ("regularized_incomplete_beta", 3, 0.0), ("t_pdf", 1, 3.5), ("t_cdf", 1, 2.5),
-    ("logt_pdf", 3, 3.5), ("logt_cdf", 3, 1.5), ("normal_cdf", 1, 0.0),
-    ("normal_quantile", 1, 0.0), ("lognormal_censored_expectation", 3, 0.0),
-    ("lognormal_censored_cvar", 3, 0.9), ("lognormal_censored_cvar", 3, 0.0)])
-def test_dist_functions_match_reference(tie, R, fn, nargs, param):
-    rng = np.random.default_rng(hash(fn) % 1000)
-    n = 2000
+def _dist_inputs(fn, rng, n=2000):
+    """the inputs of one dist-function parity case (the reference's valid domains)"""
     if fn == "regularized_incomplete_beta":
         a, b, c = rng.uniform(0.05, 30, n), rng.uniform(0.05, 30, n), rng.uniform(0, 1, n)
         c[:3] = [0.0, 1.0, 0.5]
@@ -75,12 +70,35 @@ def test_dist_functions_match_reference(tie, R, fn, nargs, param):
         a, b, c = np.concatenate([rng.uniform(0, 1, n - 4), [1e-300, 0.01, 0.99, 1 - 1e-16]]), None, None
     else:
         a, b, c = rng.uniform(-1, 8, n), rng.uniform(0.05, 3, n), rng.uniform(1, 4096, n)
+    return a, b, c
+
+
+def _dist_err(fn, got, ref):
+    """relative error; absolute where the reference underflows.  normal_quantile is measured
+    against max(|x|, 1): near p = 1/2 the quantile is ~0 and its last-ulp difference (device
+    vs glibc erfc in the Newton step, dist.cpp:193-225) is an absolute ~1e-16"""
+    scale = np.maximum(np.abs(ref), 1.0) if fn == "normal_quantile" else np.abs(ref)
+    return np.where(np.abs(ref) < 1e-280, np.abs(got - ref),
+                    np.abs(got - ref) / np.maximum(scale, 1e-300))
+
+
+@needs_ref
+@pytest.mark.parametrize("fn,nargs,param", [
+    ("regularized_incomplete_beta", 3, 0.0), ("t_pdf", 1, 3.5), ("t_cdf", 1, 2.5),
+    ("logt_pdf", 3, 3.5), ("logt_cdf", 3, 1.5), ("normal_cdf", 1, 0.0),
+    ("normal_quantile", 1, 0.0), ("lognormal_censored_expectation", 3, 0.0),
+    ("lognormal_censored_cvar", 3, 0.9), ("lognormal_censored_cvar", 3, 0.0)])
+def test_dist_functions_match_reference(tie, R, fn, nargs, param):
+    # a fixed seed per function (hash(str) is salted per process: inputs must not vary run
+    # to run)
+    a, b, c = _dist_inputs(fn, np.random.default_rng(zlib.crc32(fn.encode()) % 1000))
     got = tie.dist_eval(fn, a, b, c, param)
     ref = ref_eval(R, fn, a, b, c, param)
     # device vs glibc libm (lgamma / exp / log / erfc): a few ulp, amplified by cancellation in
-    # 1 - F near F -> 1; the north star's bar is 1e-6
+    # 1 - F near F -> 1; the north star's bar is 1e-6 (worst over 100 input seeds:
+    # tools/dist_eval_probe.py)
     tol = 1e-9 if fn in ("regularized_incomplete_beta", "t_cdf", "logt_cdf", "normal_cdf") else 1e-12
-    err = np.where(np.abs(ref) < 1e-280, np.abs(got - ref), rel(got, ref))
+    err = _dist_err(fn, got, ref)
     assert err.max() <= tol, (fn, float(err.max()), int(err.argmax()))
 
 
