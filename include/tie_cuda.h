@@ -263,6 +263,13 @@ int tie_queue_step(tie_queue* q, const uint64_t* arr_ids, const double* arr_time
                    const uint32_t* arr_max_tokens, uint64_t n_arr, const uint64_t* pred_ids,
                    const double* mu, const double* sigma, const uint32_t* pred_max_tokens,
                    uint64_t n_pred, uint64_t max_pops, uint64_t* out_ids, uint64_t* n_out);
+/* The same iteration with the predictions as on_prediction's (E, C) pairs (sched.cpp:136-150;
+ * run_sim's precomputed scores): tie_queue_arrive + tie_queue_predict + tie_queue_next with
+ * one device round trip. */
+int tie_queue_step_ec(tie_queue* q, const uint64_t* arr_ids, const double* arr_time,
+                      const uint32_t* arr_max_tokens, uint64_t n_arr, const uint64_t* pred_ids,
+                      const double* E, const double* C, uint64_t n_pred, uint64_t max_pops,
+                      uint64_t* out_ids, uint64_t* n_out);
 /* Scheduler::rebuild_if_drifted() (sched.cpp:152-167) */
 int tie_queue_rebuild_if_drifted(tie_queue* q, int* rebuilt);
 /* Shard-level primitives for a scheduler sharded by request (coordinated by

@@ -208,6 +208,11 @@ class Scheduler {
   void on_prediction_batch(const uint64_t* ids, const double* expectation, const double* cvar,
                            size_t m);
   std::vector<uint64_t> next_requests(size_t k);
+  // on_arrival x n_arr, on_prediction x n_pred, next_request() up to max_pops times, in that
+  // order, with one device round trip (tie_queue_step_ec)
+  std::vector<uint64_t> step(const Request* arrivals, size_t n_arr, const uint64_t* pred_ids,
+                             const double* expectation, const double* cvar, size_t n_pred,
+                             size_t max_pops);
   tie_queue* handle() const { return q_; }
 
  private:

@@ -2013,11 +2013,16 @@ int tie_queue_next(tie_queue* Q, uint64_t max_pops, uint64_t* out_ids, uint64_t*
 // host validation first, then one packed H2D, the kernels (the score / compute_score checks
 // run on the device and make the writes and pops skip), one packed D2H and one sync.  Pops
 // that a drift rebuild could precede continue through tie_queue_next.
-int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time,
-                   const uint32_t* arr_max_tokens, uint64_t n_arr, const uint64_t* pred_ids,
-                   const double* mu, const double* sigma, const uint32_t* pred_max_tokens,
-                   uint64_t n_pred, uint64_t max_pops, uint64_t* out_ids, uint64_t* n_out) {
+namespace {
+// one scheduler iteration; predictions as log-t (mu, sigma, max_tokens), scored on the device
+// (E_in == nullptr), or as the caller's (E, C) pairs (on_prediction's arguments)
+int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time,
+                    const uint32_t* arr_max_tokens, uint64_t n_arr, const uint64_t* pred_ids,
+                    const double* mu, const double* sigma, const uint32_t* pred_max_tokens,
+                    const double* E_in, const double* C_in, uint64_t n_pred, uint64_t max_pops,
+                    uint64_t* out_ids, uint64_t* n_out) {
   if (!Q || !n_out) return set_error(TIE_EINVALID, "tie_queue: null argument");
+  const bool ec = E_in != nullptr;
   *n_out = 0;
   if (Q->policy == kPolicyRaw)
     return set_error(TIE_EINVALID, "tie_queue: a WaitingQueue has no Scheduler operations");
@@ -2037,7 +2042,8 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
     // predictions see the queue length after this step's arrivals (compute_beta at
     // on_prediction time, sched.cpp:139)
     Q->size += n_arr;
-    const int rc = check_predictions(Q, pred_ids, n_pred, arr_ids, n_arr, first, slots, &beta);
+    const int rc = check_predictions(Q, pred_ids, n_pred, arr_ids, n_arr, first, slots, &beta,
+                                     E_in, C_in);  // (E, C) given: checked here, as predict's
     Q->size -= n_arr;
     if (rc) {
       const std::string msg = tie_last_error();
@@ -2126,11 +2132,11 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
   char* h = Q->h_pack;
   std::memcpy(h + o_aid, arr_ids, 8 * n_arr);
   std::memcpy(h + o_akey, akeys.data(), 8 * n_arr);
-  if (np) {
-    std::memcpy(h + o_mu, mu, 8 * np);
-    std::memcpy(h + o_sg, sigma, 8 * np);
+  if (np) {  // (E, C) steps carry E / C in the mu / sigma fields and no max_tokens
+    std::memcpy(h + o_mu, ec ? E_in : mu, 8 * np);
+    std::memcpy(h + o_sg, ec ? C_in : sigma, 8 * np);
     std::memcpy(h + o_slot, slots.data(), 4 * np);
-    std::memcpy(h + o_mt, pred_max_tokens, 4 * np);
+    if (!ec) std::memcpy(h + o_mt, pred_max_tokens, 4 * np);
   }
   std::memcpy(h + o_blk, blocks.data(), 4 * blocks.size());
   char* d = Q->d_pack;
@@ -2141,7 +2147,10 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
   if (!small) cudaMemcpyAsync(d, h, o_h2d_end, cudaMemcpyHostToDevice, s);  // ONE H2D
   ctx->err_op = "tie_queue_step";
   const uint32_t nb = (uint32_t)((Q->n_slots + tie::dev::kBlockSlots - 1) / tie::dev::kBlockSlots);
-  if (np) {
+  // the predictions' (E, C): scored here, or the caller's (in the pack)
+  const double* pE = ec ? (const double*)(in + o_mu) : (const double*)(d + o_E);
+  double* pC = ec ? (double*)(in + o_sg) : (double*)(d + o_C);
+  if (np && !ec) {
     const cudaError_t e = tie::dev::launch_score(
         ctx, (const double*)(in + o_mu), (const double*)(in + o_sg), in + o_mt, true, np, Q->alpha,
         0.0, (double*)(d + o_E), (double*)(d + o_C), nullptr, nullptr, nullptr, TIE_SCORE_RAW,
@@ -2158,7 +2167,7 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
   if (small) {  // everything after the scoring in one single-CTA kernel
     (sq ? tie::dev::step_apply_kernel<true> : tie::dev::step_apply_kernel<false>)<<<1, 1024, 0, s>>>(
         Q->q, first, n_arr, (const uint64_t*)(in + o_aid), (const double*)(in + o_akey),
-        (const uint32_t*)(in + o_slot), np, (const double*)(d + o_E), (double*)(d + o_C), beta,
+        (const uint32_t*)(in + o_slot), np, pE, pC, beta,
         (const uint32_t*)(in + o_blk), (uint32_t)blocks.size(), n_uncond, nb, Q->n_slots,
         fused_pops, Q->d_out_id, Q->d_out_slot, seg0_n, ctx->d_err,
         apply_last ? &Q->status->err : nullptr, apply_last ? &Q->status->seq : nullptr, seq);
@@ -2169,12 +2178,11 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
           Q->q, first, n_arr, (const uint64_t*)(d + o_aid), (const double*)(d + o_akey));
     if (np) {
       const unsigned g = (unsigned)((np + 255) / 256);
-      tie::dev::predict_keys_kernel<<<g, 256, 0, s>>>((const double*)(d + o_E),
-                                                      (double*)(d + o_C), np, beta,
-                                                      (double*)(d + o_key), ctx->d_err);
+      tie::dev::predict_keys_kernel<<<g, 256, 0, s>>>(pE, pC, np, beta, (double*)(d + o_key),
+                                                      ctx->d_err);
       tie::dev::write_predictions_checked_kernel<<<g, 256, 0, s>>>(
-          Q->q, (const uint32_t*)(d + o_slot), np, (const double*)(d + o_E),
-          (const double*)(d + o_C), (const double*)(d + o_key), beta, ctx->d_err);
+          Q->q, (const uint32_t*)(d + o_slot), np, pE, pC, (const double*)(d + o_key), beta,
+          ctx->d_err);
     }
     if (!blocks.empty())
       tie::dev::refresh_blocks_checked_kernel<<<
@@ -2234,6 +2242,27 @@ int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time
   }
   *n_out = k;
   return TIE_OK;
+}
+
+}  // namespace
+
+int tie_queue_step(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time,
+                   const uint32_t* arr_max_tokens, uint64_t n_arr, const uint64_t* pred_ids,
+                   const double* mu, const double* sigma, const uint32_t* pred_max_tokens,
+                   uint64_t n_pred, uint64_t max_pops, uint64_t* out_ids, uint64_t* n_out) {
+  return queue_step_impl(Q, arr_ids, arr_time, arr_max_tokens, n_arr, pred_ids, mu, sigma,
+                         pred_max_tokens, nullptr, nullptr, n_pred, max_pops, out_ids, n_out);
+}
+
+int tie_queue_step_ec(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time,
+                      const uint32_t* arr_max_tokens, uint64_t n_arr, const uint64_t* pred_ids,
+                      const double* E, const double* C, uint64_t n_pred, uint64_t max_pops,
+                      uint64_t* out_ids, uint64_t* n_out) {
+  if (n_pred && (!E || !C)) return set_error(TIE_EINVALID, "tie_queue_step_ec: null E / C");
+  static const double kNone = 0.0;  // E_in != nullptr selects the (E, C) mode
+  return queue_step_impl(Q, arr_ids, arr_time, arr_max_tokens, n_arr, pred_ids, nullptr,
+                         nullptr, nullptr, n_pred ? E : &kNone, n_pred ? C : &kNone, n_pred,
+                         max_pops, out_ids, n_out);
 }
 
 // ---- shard-level primitives (the scheduler sharded by request) ------------

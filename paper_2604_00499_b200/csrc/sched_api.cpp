@@ -282,6 +282,26 @@ std::vector<uint64_t> Scheduler::next_requests(size_t k) {
   return out;
 }
 
+std::vector<uint64_t> Scheduler::step(const Request* arrivals, size_t n_arr,
+                                      const uint64_t* pred_ids, const double* expectation,
+                                      const double* cvar, size_t n_pred, size_t max_pops) {
+  view_.flush();
+  std::vector<uint64_t> ids(n_arr);
+  std::vector<double> arr(n_arr);
+  std::vector<uint32_t> mt(n_arr);
+  for (size_t j = 0; j < n_arr; ++j) {
+    ids[j] = arrivals[j].id;
+    arr[j] = arrivals[j].arrival_s;
+    mt[j] = arrivals[j].max_tokens;
+  }
+  std::vector<uint64_t> out(max_pops);
+  uint64_t n = 0;
+  throw_code(tie_queue_step_ec(q_, ids.data(), arr.data(), mt.data(), n_arr, pred_ids,
+                               expectation, cvar, n_pred, max_pops, out.data(), &n));
+  out.resize(n);
+  return out;
+}
+
 bool Scheduler::waiting_on(uint64_t req_id) const { return tie_queue_contains(q_, req_id) != 0; }
 
 size_t Scheduler::waiting() const { return tie_queue_size(q_); }
