@@ -668,6 +668,25 @@ PYBIND11_MODULE(_core, m) {
            py::arg("k"),
            "one scheduler iteration (on_arrival x, on_prediction x, next_request x k) with one "
            "device round trip")
+      .def("step_ec",
+           [](GpuQueue& g, carray<uint64_t> arr_ids, carray<double> arrival_s,
+              carray<uint32_t> arr_max_tokens, carray<uint64_t> pred_ids, carray<double> E,
+              carray<double> C, uint64_t k) {
+             if (arrival_s.size() != arr_ids.size() || arr_max_tokens.size() != arr_ids.size() ||
+                 E.size() != pred_ids.size() || C.size() != pred_ids.size())
+               throw py::value_error("step_ec: array lengths differ");
+             std::vector<uint64_t> out(k);
+             uint64_t n = 0;
+             throw_code(tie_queue_step_ec(g.q, arr_ids.data(), arrival_s.data(),
+                                          arr_max_tokens.data(), (uint64_t)arr_ids.size(),
+                                          pred_ids.data(), E.data(), C.data(),
+                                          (uint64_t)pred_ids.size(), k, out.data(), &n));
+             out.resize(n);
+             return carray<uint64_t>((py::ssize_t)n, out.data());
+           },
+           py::arg("arr_ids"), py::arg("arrival_s"), py::arg("arr_max_tokens"),
+           py::arg("pred_ids"), py::arg("E"), py::arg("C"), py::arg("k"),
+           "on_arrival x n, on_prediction(E, C) x m, next_request() x k: one device round trip")
       .def("next_request",
            [](GpuQueue& g) -> py::object {
              uint64_t id = 0, n = 0;

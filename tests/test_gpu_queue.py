@@ -350,3 +350,44 @@ def test_rekey_every_pop_one_pass_matches_reference(tie, mc, ties):
         got += q.next_requests(m).tolist()
     want = _rekey_expected(tie, sc, pred, E, C, mkey, ids, len(got))
     assert got == want
+
+
+@pytest.mark.parametrize("policy,q_sat,thr", [(2, 128.0, 0.1), (2, 1e9, 0.0), (1, 128.0, 0.1),
+                                              (0, 128.0, 0.1)])
+def test_step_ec_equals_separate_calls(tie, mc, oracle, policy, q_sat, thr):
+    """tie_queue_step_ec (Scheduler::step: on_prediction's (E, C) pairs) == on_arrival_batch +
+    on_prediction_batch + next_requests; a C < E prediction raises the reference's error
+    (compute_score, sched.cpp:19-26) with the step's arrivals applied"""
+    pol = [tie.Policy.FCFS, tie.Policy.SEPT, tie.Policy.TIE][policy]
+    n0, steps, per, pops = 3000, 30, 32, 8
+    tot = n0 + steps * per
+    rng = np.random.default_rng(9)
+    ids = rng.permutation(tot * 3)[:tot].astype(np.uint64)
+    arr = np.arange(tot, dtype=np.float64) * 0.01
+    mt = rng.integers(64, 4096, tot).astype(np.uint32)
+    E = rng.uniform(10.0, 800.0, tot)
+    C = E * rng.uniform(1.0, 2.5, tot)
+    qa = tie.GpuScheduler(mc, pol, _cfg(tie, q_sat, thr), tot)
+    qb = tie.GpuScheduler(mc, pol, _cfg(tie, q_sat, thr), tot)
+    for q in (qa, qb):
+        q.on_arrival_batch(ids[:n0], arr[:n0], mt[:n0])
+        q.on_prediction_batch(ids[:n0 // 2], E[:n0 // 2], C[:n0 // 2])
+    pending = list(range(n0 // 2, n0))
+    for s in range(steps):
+        lo, hi = n0 + s * per, n0 + (s + 1) * per
+        pa = np.array(pending[:per] + list(range(lo, lo + 4)), np.int64)  # + same-step arrivals
+        got_a = qa.step_ec(ids[lo:hi], arr[lo:hi], mt[lo:hi], ids[pa], E[pa], C[pa], pops)
+        qb.on_arrival_batch(ids[lo:hi], arr[lo:hi], mt[lo:hi])
+        qb.on_prediction_batch(ids[pa], E[pa], C[pa])
+        got_b = qb.next_requests(pops)
+        assert np.array_equal(got_a, got_b), (s, got_a, got_b)
+        popped = set(got_a.tolist())
+        pending = [p for p in pending[per:] if ids[p] not in popped] + \
+                  [p for p in range(lo + 4, hi) if ids[p] not in popped]
+    assert np.array_equal(qa.next_requests(500), qb.next_requests(500))
+    if policy != 0:  # FCFS validates too, but a bad prediction never reaches a key there
+        nid = np.array([10 ** 9], np.uint64)
+        with pytest.raises(ValueError):
+            qa.step_ec(nid, np.zeros(1), np.array([64], np.uint32), nid, np.array([5.0]),
+                       np.array([4.0]), 1)
+        assert nid[0] in qa.next_requests(qa.waiting()).tolist()  # the arrival stayed
