@@ -671,6 +671,59 @@ int tie_fit_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double n
   uint8_t* d_cv = (uint8_t*)(b + off); off += al(P);
   uint8_t* d_dg = (uint8_t*)(b + off);
   cudaStream_t s = ctx->stream, cs = ctx->copy_stream;
+  // pinned (UVA-mapped) samples: the fit kernel reads them over PCIe itself (each prompt's K
+  // samples once, then ~260 likelihood evaluations on them: the reads hide under the compute)
+  // and, with pinned outputs, writes each prompt's results straight back (B200, 1M x 16:
+  // 8.0 ms end to end vs 8.95 for the 4-chunk copy pipeline below, 7.9 ms device-only)
+  static const int zc_in = getenv("TIE_FIT_ZERO_COPY") ? atoi(getenv("TIE_FIT_ZERO_COPY")) : 2;
+  if (zc_in) {
+    cudaPointerAttributes pa{};
+    const bool mapped = cudaPointerGetAttributes(&pa, x) == cudaSuccess &&
+                        pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr;
+    cudaGetLastError();
+    // pinned outputs too: the kernel writes each prompt's results straight to the host
+    auto dev_of = [](void* p) -> void* {
+      if (!p) return nullptr;
+      cudaPointerAttributes a{};
+      const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess &&
+                      a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
+      cudaGetLastError();
+      return ok ? a.devicePointer : nullptr;
+    };
+    void* o_mu = dev_of(mu);
+    void* o_sg = dev_of(sigma);
+    void* o_ll = dev_of(log_likelihood);
+    void* o_it = dev_of(iterations);
+    void* o_cv = dev_of(converged);
+    void* o_dg = dev_of(degenerate);
+    const bool out_mapped = zc_in >= 2 && o_mu && o_sg && (o_ll || !log_likelihood) &&
+                            (o_it || !iterations) && (o_cv || !converged) &&
+                            (o_dg || !degenerate);
+    if (mapped && out_mapped) {
+      const cudaError_t e = tie::dev::launch_fit(
+          ctx, (const double*)pa.devicePointer, P, K, nu, (double*)o_mu, (double*)o_sg,
+          (double*)o_ll, (int32_t*)o_it, (uint8_t*)o_cv, (uint8_t*)o_dg, s, 0);
+      if (e != cudaSuccess) return cuda_error(e, "tie_fit_host");
+      return tie_sync(ctx, s);
+    }
+    if (mapped) {
+      const cudaError_t e = tie::dev::launch_fit(ctx, (const double*)pa.devicePointer, P, K, nu,
+                                                 d_mu, d_sg, d_ll, d_it, d_cv, d_dg, s, 0);
+      if (e != cudaSuccess) return cuda_error(e, "tie_fit_host");
+      TIE_CUDA_TRY(cudaMemcpyAsync(mu, d_mu, 8 * P, cudaMemcpyDeviceToHost, s), "d2h");
+      TIE_CUDA_TRY(cudaMemcpyAsync(sigma, d_sg, 8 * P, cudaMemcpyDeviceToHost, s), "d2h");
+      if (log_likelihood)
+        TIE_CUDA_TRY(cudaMemcpyAsync(log_likelihood, d_ll, 8 * P, cudaMemcpyDeviceToHost, s),
+                     "d2h");
+      if (iterations)
+        TIE_CUDA_TRY(cudaMemcpyAsync(iterations, d_it, 4 * P, cudaMemcpyDeviceToHost, s), "d2h");
+      if (converged)
+        TIE_CUDA_TRY(cudaMemcpyAsync(converged, d_cv, P, cudaMemcpyDeviceToHost, s), "d2h");
+      if (degenerate)
+        TIE_CUDA_TRY(cudaMemcpyAsync(degenerate, d_dg, P, cudaMemcpyDeviceToHost, s), "d2h");
+      return tie_sync(ctx, s);
+    }
+  }
   // pipeline over prompt chunks (fits are independent per prompt): all H2D copies queued on
   // the copy stream, chunk c's fit waits for its copy, its results go back on the copy
   // stream behind the H2Ds -- copies in both directions overlap the fits

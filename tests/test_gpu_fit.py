@@ -238,3 +238,23 @@ def test_north_star_10m_fits_vs_oracle(abi, h, oracle):
     got = abi.fit(h, x)
     mism = _compare(got, oracle.fit(x), "north-star-10M")
     assert mism <= P // 10
+
+
+def test_fit_host_pinned_zero_copy_equals_device(tie, mc):
+    """tie_fit_host on pinned buffers (the kernel reads the samples and writes the results
+    through UVA-mapped host memory) == the device-buffer fit, bitwise"""
+    import torch
+
+    P, K = 50_000, 16
+    x, _, _ = tie.gen_fit_data(P, K, 3)
+    xp = torch.from_numpy(x).pin_memory()
+    hb = [torch.zeros(P, dtype=t).pin_memory() for t in
+          (torch.float64, torch.float64, torch.float64, torch.int32, torch.uint8, torch.uint8)]
+    tie.fit_host_ptr(mc.handle, xp.data_ptr(), P, K, 3.5, *[t.data_ptr() for t in hb])
+    xd = xp.cuda()
+    db = [torch.empty(P, dtype=t.dtype, device="cuda") for t in hb]
+    sh = torch.cuda.current_stream().cuda_stream
+    tie.fit_device(mc.handle, xd.data_ptr(), P, K, 3.5, *[t.data_ptr() for t in db], sh)
+    tie.sync(mc.handle, sh)
+    for h, d in zip(hb, db):
+        assert torch.equal(h, d.cpu())
