@@ -247,6 +247,18 @@ class PeerExchange:
             self.core.ipc_free(self.ctx, self.mine)
         self.opened, self.peers, self.mine, self.cap = [], [], 0, 0
 
+    def _agree(self, ok: bool, what: str):
+        """collective: every rank learns whether ALL ranks succeeded (a failure on one rank
+        must not leave the others waiting in the next collective); raises on every rank"""
+        import torch
+
+        t = torch.tensor([1 if ok else 0], dtype=torch.int64)
+        if self.dist.get_backend(self.group) == "nccl":
+            t = t.cuda()
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        if int(t.item()) == 0:
+            raise RuntimeError(f"PeerExchange: {what} failed on some rank")
+
     def ensure(self, need: int):
         """collective: every rank's buffer holds >= max over ranks of ``need`` records"""
         import torch
@@ -262,18 +274,32 @@ class PeerExchange:
         self.dist.barrier(group=self.group)  # nobody still writes into the old buffers
         self._release()
         cap = max(want + want // 8, 1 << 16)
-        ptr, handle = self.core.ipc_alloc(self.ctx, 12 * cap)
+        ptr, handle, ok = 0, b"", True
+        try:
+            ptr, handle = self.core.ipc_alloc(self.ctx, 12 * cap)
+        except Exception:  # noqa: BLE001 -- reported collectively below
+            ok = False
         handles = [None] * self.world
-        self.dist.all_gather_object(handles, handle, group=self.group)
+        self.dist.all_gather_object(handles, handle if ok else None, group=self.group)
         peers = []
-        for g, h in enumerate(handles):
-            if g == self.rank:
-                peers.append(ptr)
-            else:
-                q = self.core.ipc_open(self.ctx, h)
-                self.opened.append(q)
-                peers.append(q)
+        ok = ok and all(h is not None for h in handles)
+        if ok:
+            try:
+                for g, h in enumerate(handles):
+                    if g == self.rank:
+                        peers.append(ptr)
+                    else:
+                        q = self.core.ipc_open(self.ctx, h)
+                        self.opened.append(q)
+                        peers.append(q)
+            except Exception:  # noqa: BLE001
+                ok = False
         self.mine, self.peers, self.cap = ptr, peers, cap
+        try:
+            self._agree(ok, "CUDA IPC buffer mapping")
+        except RuntimeError:
+            self._release()
+            raise
 
     def views(self, total: int):
         """this rank's received (keys f64, ids int32) records as torch tensors"""
@@ -284,13 +310,18 @@ class PeerExchange:
 
     def put(self, rk, ri, send_l, dst_l):
         """write the sorted run's pieces (send_l records each) into the peers at dst_l"""
-        stream = self.ops.torch.cuda.current_stream(rk.device).cuda_stream
-        self.core.peer_put_runs_device(
-            self.ctx, rk.data_ptr(), ri.data_ptr(), rk.numel(), [int(x) for x in send_l],
-            [int(x) for x in dst_l], [int(p) for p in self.peers],
-            [int(p) + 8 * self.cap for p in self.peers], stream)
-        self.ops.torch.cuda.current_stream(rk.device).synchronize()
-        self.dist.barrier(group=self.group)  # every piece has landed in every buffer
+        ok = True
+        try:
+            stream = self.ops.torch.cuda.current_stream(rk.device).cuda_stream
+            self.core.peer_put_runs_device(
+                self.ctx, rk.data_ptr(), ri.data_ptr(), rk.numel(), [int(x) for x in send_l],
+                [int(x) for x in dst_l], [int(p) for p in self.peers],
+                [int(p) + 8 * self.cap for p in self.peers], stream)
+            self.ops.torch.cuda.current_stream(rk.device).synchronize()
+        except Exception:  # noqa: BLE001 -- reported collectively
+            ok = False
+        # the all-reduce is also the barrier: every piece has landed in every buffer
+        self._agree(ok, "peer put")
 
     def close(self):
         self._release()
