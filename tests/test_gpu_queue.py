@@ -323,8 +323,8 @@ def _rekey_expected(tie, sc, pred, E, C, mkey, ids, pops):
     return out
 
 
-@pytest.mark.parametrize("ties", [False, True])
-def test_rekey_every_pop_one_pass_matches_reference(tie, mc, ties):
+@pytest.mark.parametrize("ties,q_sat_gap", [(False, None), (True, None), (False, 40)])
+def test_rekey_every_pop_one_pass_matches_reference(tie, mc, ties, q_sat_gap):
     """the one-pass re-key + pop kernel (>= 512 blocks; a run of (rebuild, pop) segments): pops
     at rebuild_threshold 0 with beta moving every pop equal the reference's re-key-then-pop
     sequence; mixed unpredicted entries (constant keys) pop among the predicted ones; with
@@ -340,7 +340,9 @@ def test_rekey_every_pop_one_pass_matches_reference(tie, mc, ties):
     if ties:
         E[:3000], C[:3000] = 20.0, 30.0
         pred[:3000] = True
-    sc = _cfg(tie, q_sat=1e9, thr=0.0)
+    # q_sat_gap: beta saturated (constant, no rebuilds) for the first pops, then moving with
+    # every pop -- the plan switches from fixed-key pops to (rebuild, pop) runs
+    sc = _cfg(tie, q_sat=1e9 if q_sat_gap is None else float(n - q_sat_gap), thr=0.0)
     q = tie.GpuScheduler(mc, tie.Policy.TIE, sc, n)
     q.on_arrival_batch(ids, np.zeros(n), mt)
     q.on_prediction_batch(ids[pred], E[pred], C[pred])
