@@ -173,3 +173,31 @@ def test_sigma_table_boundary(abi, oracle, samples):
         assert rel_err(S, So).max() <= TOL
     finally:
         abi.destroy(h2)
+
+
+@pytest.mark.parametrize("n", [1000, 300_001])
+def test_host_call_pinned_zero_copy_equals_pageable(tie, mc, n):
+    """tie_score_rank_host on pinned buffers (the score kernel reads the inputs and the sort
+    writes the order through UVA-mapped host memory) == the same call on pageable NumPy
+    buffers (staged copies), scores and order bitwise; plus the error path (a bad request is
+    reported with its index from the zero-copy kernel)"""
+    import torch
+
+    w = tie.gen_logt_workload_soa(n, 5)
+    mu, sg, mt = w["mu"].copy(), w["sigma"].copy(), w["max_tokens"].copy()
+    pin = lambda a: torch.from_numpy(a).pin_memory()
+    mu_p, sg_p, mt_p = pin(mu), pin(sg), pin(mt.view(np.int32))
+    s_p = torch.empty(n, dtype=torch.float64).pin_memory()
+    o_p = torch.empty(n, dtype=torch.int64).pin_memory()
+    tie.score_rank_host_ptr(mc.handle, mu_p.data_ptr(), sg_p.data_ptr(), mt_p.data_ptr(), n,
+                            0.9, 0.5, s_p.data_ptr(), o_p.data_ptr(), 0)
+    s_h = np.empty(n)
+    o_h = np.empty(n, np.uint64)
+    tie.score_rank_host_ptr(mc.handle, mu.ctypes.data, sg.ctypes.data, mt.ctypes.data, n, 0.9,
+                            0.5, s_h.ctypes.data, o_h.ctypes.data, 0)
+    assert np.array_equal(s_p.numpy().view(np.uint64), s_h.view(np.uint64))
+    assert np.array_equal(o_p.numpy().view(np.uint64), o_h)
+    sg_p[n // 2] = -1.0  # LogTParams: sigma must be finite and > 0
+    with pytest.raises(ValueError, match=f"item {n // 2}"):
+        tie.score_rank_host_ptr(mc.handle, mu_p.data_ptr(), sg_p.data_ptr(), mt_p.data_ptr(),
+                                n, 0.9, 0.5, s_p.data_ptr(), o_p.data_ptr(), 0)
