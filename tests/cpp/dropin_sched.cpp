@@ -294,6 +294,48 @@ static void scheduler_drift_rebuild() {  // test_sched.cpp:246-292
   CHECK(stale.next_request() == 2u);
 }
 
+static void scheduler_step_batching() {  // Scheduler::step == the per-event call sequence
+  ScoreConfig cfg;
+  cfg.q_sat = 1e9;  // beta moves with every queue-length change
+  cfg.rebuild_threshold = 0.0;
+  Scheduler a(Policy::TIE, cfg), b(Policy::TIE, cfg);
+  std::mt19937_64 rng(17);
+  std::uniform_real_distribution<double> u(10.0, 900.0);
+  uint64_t next_id = 1;
+  for (int step = 0; step < 40; ++step) {
+    std::vector<Request> arr;
+    for (int j = 0; j < 6; ++j) arr.push_back(arrival(next_id++, 0.1 * step, 64 + 7 * j));
+    std::vector<uint64_t> pid;
+    std::vector<double> pe, pc;
+    for (const Request& r : arr)
+      if (r.id % 3) {  // predictions for two thirds of this step's arrivals
+        pid.push_back(r.id);
+        const double e = u(rng);
+        pe.push_back(e);
+        pc.push_back(e * 1.5);
+      }
+    const std::vector<uint64_t> got =
+        a.step(arr.data(), arr.size(), pid.data(), pe.data(), pc.data(), pid.size(), 4);
+    for (const Request& r : arr) b.on_arrival(r);
+    for (size_t j = 0; j < pid.size(); ++j) b.on_prediction(pid[j], pe[j], pc[j]);
+    std::vector<uint64_t> want;
+    for (int j = 0; j < 4; ++j) {
+      const auto id = b.next_request();
+      if (!id) break;
+      want.push_back(*id);
+    }
+    CHECK(got == want);
+  }
+  CHECK(a.waiting() == b.waiting());
+  // a prediction the reference rejects (cvar < expectation): the step throws like
+  // on_prediction, the step's arrivals stay applied
+  Request r = arrival(next_id++, 9.0, 64);
+  const uint64_t id = r.id;
+  const double e = 100.0, c = 50.0;
+  CHECK_THROWS_AS(a.step(&r, 1, &id, &e, &c, 1, 1), std::invalid_argument);
+  CHECK(a.waiting_on(id));
+}
+
 static void distribution_api() {  // test_smoke.py:8-26, dist.hpp per-item functions
   McContext mc(3.5);
   CHECK(mc.samples.size() == 10000 && std::is_sorted(mc.samples.begin(), mc.samples.end()));
@@ -350,6 +392,7 @@ int main() {
   waiting_queue_entry_edits();
   scheduler_policies();
   scheduler_drift_rebuild();
+  scheduler_step_batching();
   distribution_api();
   simulator_api();
   std::printf("dropin_sched: %d passed, %d failed\n", g_pass, g_fail);
