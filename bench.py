@@ -164,6 +164,18 @@ def cpu_baseline(n_target_s=10.0, per_step_s=None, full=False):
         t3 = time.perf_counter()
         return t2 - t1, t3 - t2
 
+    def single_thread_rate(m1=2000):
+        # report the 1-thread rate beside the all-core one (scoring only: the
+        # reference's ranking is single-threaded in both)
+        if kind == "reference":
+            f1 = lambda a, b, c: lib.score(a, b, c, alpha=ALPHA, beta=0.5, threads=1)
+        else:
+            f1 = lambda a, b, c: lib.score(Y, a, b, c, alpha=ALPHA, beta=0.5, threads=1)
+        t1 = time.perf_counter()
+        f1(mu[:m1], sg[:m1], xm[:m1])
+        return m1 / (time.perf_counter() - t1)
+
+    one.single_thread_rate = single_thread_rate
     return one, m, threads, kind
 
 
@@ -511,7 +523,9 @@ def main():
             line["cpu_baseline"] = {
                 "value": cb, "unit": "requests/s", "cores": threads, "kind": kind,
                 "sample": f"first {m} requests of the config-2 queue: score on {threads} threads "
-                          f"({ts[0]:.2f} s) + reference WaitingQueue rank ({ts[1]:.2f} s)"}
+                          f"({ts[0]:.2f} s) + reference WaitingQueue rank ({ts[1]:.2f} s)",
+                "score_rate_1_thread": one.single_thread_rate(),
+                "score_rate_all_threads": m / ts[0]}
         except Exception as exc:  # the baseline never blocks the GPU line
             line["cpu_baseline"] = {"value": None, "error": repr(exc)}
     if rank == 0:
