@@ -461,6 +461,17 @@ static char* io_buffer(tie_ctx* ctx, size_t bytes) {
 
 static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// the device address of a pinned (page-locked, UVA-mapped) host buffer; nullptr for pageable
+// or null pointers (the caller then stages copies)
+static void* mapped_device_ptr(const void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes a{};
+  const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess &&
+                  a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
+  cudaGetLastError();  // a pageable pointer is not an error here
+  return ok ? a.devicePointer : nullptr;
+}
+
 int tie_score_host(tie_ctx* ctx, const double* mu, const double* sigma, const double* x_max,
                    uint64_t n, double alpha, double beta, double* E, double* cvar, double* score,
                    unsigned flags) {
@@ -510,27 +521,16 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
   // engine setup per chunk, the reads overlap the scoring at the request granularity
   // (tools/e2e_probe.py on B200, 1M requests: 604 vs 614 us for the 2-chunk H2D pipeline
   // below, which pageable inputs still take)
-  auto host_mapped = [](const void* ptr) -> const void* {
-    cudaPointerAttributes a{};
-    const bool ok = cudaPointerGetAttributes(&a, ptr) == cudaSuccess &&
-                    a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
-    cudaGetLastError();
-    return ok ? a.devicePointer : nullptr;
-  };
   static const int zc_in = getenv("TIE_ZERO_COPY_IN") ? atoi(getenv("TIE_ZERO_COPY_IN")) : 1;
-  if (zc_in) {
-    const void* m_mu = host_mapped(mu);
-    const void* m_sg = host_mapped(sigma);
-    const void* m_mt = host_mapped(max_tokens);
-    if (m_mu && m_sg && m_mt) {
-      const cudaError_t e = tie::dev::launch_score(
-          ctx, (const double*)m_mu, (const double*)m_sg, m_mt, true, n, alpha, beta, nullptr,
-          nullptr, d_S, prep.keys, prep.minmax, flags & TIE_SCORE_EXACT, s, 0);
-      if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
-      goto ranked;
-    }
-  }
-  {
+  const void* m_mu = zc_in ? mapped_device_ptr(mu) : nullptr;
+  const void* m_sg = zc_in ? mapped_device_ptr(sigma) : nullptr;
+  const void* m_mt = zc_in ? mapped_device_ptr(max_tokens) : nullptr;
+  if (m_mu && m_sg && m_mt) {
+    const cudaError_t e = tie::dev::launch_score(
+        ctx, (const double*)m_mu, (const double*)m_sg, m_mt, true, n, alpha, beta, nullptr,
+        nullptr, d_S, prep.keys, prep.minmax, flags & TIE_SCORE_EXACT, s, 0);
+    if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
+  } else {
   // pipeline: H2D of chunk c+1 (copy stream) overlaps scoring of chunk c (compute stream)
   // 2 chunks: the second half's H2D overlaps the first half's scoring; every extra copy costs
   // ~3 us of DMA setup, more than the finer overlap wins (tools/e2e_probe.py on B200:
@@ -556,18 +556,15 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
                                                  prep.minmax, flags & TIE_SCORE_EXACT, s, lo);
     if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
   }
-  }
-ranked:
+  }  // (zero-copy inputs | staged pipeline)
   // pinned (page-locked, UVA-mapped) output: the sort's last kernel writes the dispatch
   // order straight into host memory, so the D2H overlaps the sort instead of following it
-  cudaPointerAttributes pa{};
   static const int zero_copy = getenv("TIE_NO_ZERO_COPY") ? 0 : 1;  // A/B switch
-  const bool mapped = zero_copy && tie::dev::rank_output_coalesced(n) &&
-                      cudaPointerGetAttributes(&pa, order) == cudaSuccess &&
-                      pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr;
-  cudaGetLastError();  // a pageable pointer is not an error here
-  cudaError_t e = tie::dev::rank_prepared(ctx, n, mapped ? (uint64_t*)pa.devicePointer : d_order,
-                                          s);
+  uint64_t* m_order = zero_copy && tie::dev::rank_output_coalesced(n)
+                          ? (uint64_t*)mapped_device_ptr(order)
+                          : nullptr;
+  const bool mapped = m_order != nullptr;
+  cudaError_t e = tie::dev::rank_prepared(ctx, n, mapped ? m_order : d_order, s);
   if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
   if (!mapped)
     TIE_CUDA_TRY(cudaMemcpyAsync(order, d_order, 8 * n, cudaMemcpyDeviceToHost, s), "d2h");
@@ -676,39 +673,28 @@ int tie_fit_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double n
   // and, with pinned outputs, writes each prompt's results straight back (B200, 1M x 16:
   // 8.0 ms end to end vs 8.95 for the 4-chunk copy pipeline below, 7.9 ms device-only)
   static const int zc_in = getenv("TIE_FIT_ZERO_COPY") ? atoi(getenv("TIE_FIT_ZERO_COPY")) : 2;
-  if (zc_in) {
-    cudaPointerAttributes pa{};
-    const bool mapped = cudaPointerGetAttributes(&pa, x) == cudaSuccess &&
-                        pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr;
-    cudaGetLastError();
+  const void* x_dev = zc_in ? mapped_device_ptr(x) : nullptr;
+  if (x_dev) {
     // pinned outputs too: the kernel writes each prompt's results straight to the host
-    auto dev_of = [](void* p) -> void* {
-      if (!p) return nullptr;
-      cudaPointerAttributes a{};
-      const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess &&
-                      a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
-      cudaGetLastError();
-      return ok ? a.devicePointer : nullptr;
-    };
-    void* o_mu = dev_of(mu);
-    void* o_sg = dev_of(sigma);
-    void* o_ll = dev_of(log_likelihood);
-    void* o_it = dev_of(iterations);
-    void* o_cv = dev_of(converged);
-    void* o_dg = dev_of(degenerate);
+    void* o_mu = mapped_device_ptr(mu);
+    void* o_sg = mapped_device_ptr(sigma);
+    void* o_ll = mapped_device_ptr(log_likelihood);
+    void* o_it = mapped_device_ptr(iterations);
+    void* o_cv = mapped_device_ptr(converged);
+    void* o_dg = mapped_device_ptr(degenerate);
     const bool out_mapped = zc_in >= 2 && o_mu && o_sg && (o_ll || !log_likelihood) &&
                             (o_it || !iterations) && (o_cv || !converged) &&
                             (o_dg || !degenerate);
-    if (mapped && out_mapped) {
+    if (out_mapped) {
       const cudaError_t e = tie::dev::launch_fit(
-          ctx, (const double*)pa.devicePointer, P, K, nu, (double*)o_mu, (double*)o_sg,
+          ctx, (const double*)x_dev, P, K, nu, (double*)o_mu, (double*)o_sg,
           (double*)o_ll, (int32_t*)o_it, (uint8_t*)o_cv, (uint8_t*)o_dg, s, 0);
       if (e != cudaSuccess) return cuda_error(e, "tie_fit_host");
       return tie_sync(ctx, s);
     }
-    if (mapped) {
-      const cudaError_t e = tie::dev::launch_fit(ctx, (const double*)pa.devicePointer, P, K, nu,
-                                                 d_mu, d_sg, d_ll, d_it, d_cv, d_dg, s, 0);
+    {
+      const cudaError_t e = tie::dev::launch_fit(ctx, (const double*)x_dev, P, K, nu, d_mu,
+                                                 d_sg, d_ll, d_it, d_cv, d_dg, s, 0);
       if (e != cudaSuccess) return cuda_error(e, "tie_fit_host");
       TIE_CUDA_TRY(cudaMemcpyAsync(mu, d_mu, 8 * P, cudaMemcpyDeviceToHost, s), "d2h");
       TIE_CUDA_TRY(cudaMemcpyAsync(sigma, d_sg, 8 * P, cudaMemcpyDeviceToHost, s), "d2h");
