@@ -1405,8 +1405,8 @@ int check_predictions(const tie_queue* Q, const uint64_t* ids, uint64_t m,
                       std::vector<uint32_t>& slots, double* beta, const double* E = nullptr,
                       const double* C = nullptr) {
   slots.resize(m);
-  std::unordered_map<uint64_t, uint32_t> pend;
-  for (uint64_t t = 0; t < n_pending; ++t) pend.emplace(pending[t], (uint32_t)(first_pending + t));
+  std::unordered_map<uint64_t, uint32_t> pend;  // this step's arrivals, built on first need
+  bool pend_built = false;
   const uint64_t dup = Q->policy == 0 ? m : first_batch_duplicate(ids, m);
   *beta = 0.0;
   bool have_beta = false;
@@ -1414,11 +1414,17 @@ int check_predictions(const tie_queue* Q, const uint64_t* ids, uint64_t m,
     auto it = Q->slot_of.find(ids[t]);
     if (it != Q->slot_of.end()) {
       slots[t] = it->second;
-    } else if (auto p = pend.find(ids[t]); p != pend.end()) {
-      slots[t] = p->second;
     } else {
-      return set_error(TIE_EINVALID, "Scheduler::on_prediction: id " + std::to_string(ids[t]) +
-                                         " not waiting");
+      if (!pend_built) {
+        for (uint64_t u = 0; u < n_pending; ++u)
+          pend.emplace(pending[u], (uint32_t)(first_pending + u));
+        pend_built = true;
+      }
+      const auto p = pend.find(ids[t]);
+      if (p == pend.end())
+        return set_error(TIE_EINVALID, "Scheduler::on_prediction: id " +
+                                           std::to_string(ids[t]) + " not waiting");
+      slots[t] = p->second;
     }
     if (Q->policy == 0) continue;  // FCFS: arrival order is the schedule (sched.cpp:138)
     if (!have_beta) {  // the first waiting prediction evaluates compute_beta
