@@ -1140,6 +1140,10 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
     q.id[s] = arr_ids[t];
     q.predicted[s] = 0;
   }
+  // launched as a programmatic dependent of the score kernel (tie_queue_step): the arrivals
+  // above overlap its tail; its E / C (and error word) are read only after this wait (a no-op
+  // without a dependency)
+  cudaGridDependencySynchronize();
   for (uint64_t t = threadIdx.x; t < np; t += blockDim.x) {
     const double e = E[t];
     double c = C[t];
@@ -2171,12 +2175,28 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
   // the apply kernel is the step's last kernel when no further plan segments follow it
   const bool apply_last = small && plan.size() <= (seg0_fused ? 1u : 0u);
   if (small) {  // everything after the scoring in one single-CTA kernel
-    (sq ? tie::dev::step_apply_kernel<true> : tie::dev::step_apply_kernel<false>)<<<1, 1024, 0, s>>>(
-        Q->q, first, n_arr, (const uint64_t*)(in + o_aid), (const double*)(in + o_akey),
-        (const uint32_t*)(in + o_slot), np, pE, pC, beta,
-        (const uint32_t*)(in + o_blk), (uint32_t)blocks.size(), n_uncond, nb, Q->n_slots,
-        fused_pops, Q->d_out_id, Q->d_out_slot, seg0_n, ctx->d_err,
-        apply_last ? &Q->status->err : nullptr, apply_last ? &Q->status->seq : nullptr, seq);
+    // after a score launch: a programmatic dependent launch, so its launch and the arrivals'
+    // writes overlap the score kernel (the kernel waits before reading E / C)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(1024);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (np && !ec) ? 1 : 0;
+    const cudaError_t le0 = cudaLaunchKernelEx(
+        &cfg, sq ? tie::dev::step_apply_kernel<true> : tie::dev::step_apply_kernel<false>, Q->q,
+        first, n_arr, (const uint64_t*)(in + o_aid), (const double*)(in + o_akey),
+        (const uint32_t*)(in + o_slot), np, pE, pC, beta, (const uint32_t*)(in + o_blk),
+        (uint32_t)blocks.size(), n_uncond, nb, Q->n_slots, fused_pops, Q->d_out_id,
+        Q->d_out_slot, seg0_n, ctx->d_err, apply_last ? &Q->status->err : nullptr,
+        apply_last ? &Q->status->seq : nullptr, seq);
+    if (le0 != cudaSuccess) {
+      if (use_pred) pred_mirror(false);
+      return cuda_error(le0, "tie_queue_step");
+    }
     tie::capi::count_launch(1);
   } else {
     if (n_arr)

@@ -582,6 +582,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) score_coop_kernel(const __gri
     }
   }
   __syncthreads();
+  // a programmatic dependent (the scheduler step's apply kernel) may launch now: it waits
+  // for this grid's completion before reading E / C
+  cudaTriggerProgrammaticLaunchCompletion();
   LogMemo lnx;
   uint64_t kmin = ~0ull, kmax = 0;
   const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
