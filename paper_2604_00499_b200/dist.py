@@ -360,6 +360,9 @@ class ShardedScoreRank:
         # peer memory (PeerExchange); needs device ops and merge_on="range"
         if transport == "p2p" and merge_on != "range":
             raise ValueError("transport='p2p' moves the range exchange (merge_on='range')")
+        if transport == "p2p" and not hasattr(ops, "core"):
+            raise ValueError("transport='p2p' needs device ops (DeviceOps): the records move "
+                             "between GPU buffers")
         self.peer = PeerExchange(ops, group) if transport == "p2p" else None
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0

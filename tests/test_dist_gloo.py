@@ -72,6 +72,13 @@ def _worker(rank, world, port, n_global, case, out_q):
         lo, hi = shard_bounds(n_global, world, rank)
         beta = o.compute_beta(True, 0.1, 0.5, 128.0, n_global)  # GLOBAL queue length
         ops = OracleOps()
+        for bad in ({"transport": "p2p"}, {"transport": "p2p", "merge_on": "range"},
+                    {"transport": "nvlink"}):  # p2p needs device ops and the range exchange
+            try:
+                ShardedScoreRank(ops, beta, **bad)
+                out_q.put((rank, "bad-config-accepted", bad))
+            except ValueError:
+                pass
         for merge_on, kway in (("root", "auto"), ("all", "auto"), ("root", "always"),
                                ("range", "auto"), ("range", "always")):
             res = ShardedScoreRank(ops, beta, merge_on=merge_on, kway=kway)(
