@@ -6,7 +6,7 @@ ARRIVE, PREDICT, POP = 0, 1, 2
 
 
 def make_script(seed, oracle, policy=2, n_req=600, max_tokens_choices=(256, 512, 2048),
-                runs=80, **cfg):
+                runs=80, arr_max=24, **cfg):
     """`oracle` replays the prefix after every pop run so predictions only name requests
     that are still waiting (the simulator drops stale predictions the same way)."""
     rng = np.random.default_rng(seed)
@@ -17,7 +17,7 @@ def make_script(seed, oracle, policy=2, n_req=600, max_tokens_choices=(256, 512,
     for _ in range(runs):
         kind = rng.choice(3, p=[0.4, 0.35, 0.25])
         if kind == 0 and nxt < n_req:
-            for _ in range(int(rng.integers(1, 24))):
+            for _ in range(int(rng.integers(1, arr_max))):
                 if nxt >= n_req:
                     break
                 t += float(rng.exponential(0.01))

@@ -393,3 +393,16 @@ def test_step_ec_equals_separate_calls(tie, mc, oracle, policy, q_sat, thr):
             qa.step_ec(nid, np.zeros(1), np.array([64], np.uint32), nid, np.array([5.0]),
                        np.array([4.0]), 1)
         assert nid[0] in qa.next_requests(qa.waiting()).tolist()  # the arrival stayed
+
+
+@pytest.mark.parametrize("policy,thr,q_sat", [(2, 0.0, 1e9), (2, 0.05, 4096.0), (1, 0.1, 64.0)])
+def test_pop_sequence_matches_reference_multi_block(tie, mc, oracle, policy, thr, q_sat):
+    """random event scripts whose queue grows to ~10 blocks (arrival runs of up to 400): the
+    multi-CTA re-key + pop runs, multi-block top-B pops and drift rebuilds against the
+    reference Scheduler (oracle restatement)"""
+    cfg = dict(adaptive=True, beta_max=0.5, q_sat=q_sat, rebuild_threshold=thr)
+    ops, ids, a, b = make_script(7, oracle, policy=policy, n_req=12_000, runs=160,
+                                 arr_max=400, **cfg)
+    ref = oracle.scheduler_script(policy, ops, ids, a, b, **cfg)
+    got = run_gpu(tie, mc, policy, ops, ids, a, b, cfg)
+    assert np.array_equal(got, ref), (policy, thr, q_sat)
