@@ -406,3 +406,33 @@ def test_pop_sequence_matches_reference_multi_block(tie, mc, oracle, policy, thr
     ref = oracle.scheduler_script(policy, ops, ids, a, b, **cfg)
     got = run_gpu(tie, mc, policy, ops, ids, a, b, cfg)
     assert np.array_equal(got, ref), (policy, thr, q_sat)
+
+
+@pytest.mark.parametrize("q_sat,thr", [(1e9, 0.0), (128.0, 0.1)])
+def test_large_step_equals_separate_calls(tie, mc, oracle, q_sat, thr):
+    """a step above the small-step limits (> 16,384 arrivals / predictions: one packed H2D and
+    the multi-kernel apply path) == on_arrival_batch + on_prediction_logt + next_requests"""
+    n0, big, pops = 5000, 20_000, 24
+    tot = n0 + 2 * big
+    mu, sg, mt = oracle.gen_workload(tot, seed=12)
+    ids = np.random.default_rng(8).permutation(tot * 2)[:tot].astype(np.uint64)
+    arr = np.arange(tot, dtype=np.float64) * 0.001
+    cfg = _cfg(tie, q_sat=q_sat, thr=thr)  # q_sat 1e9: beta moves, the pops are rebuild segments
+    qa = tie.GpuScheduler(mc, tie.Policy.TIE, cfg, tot)
+    qb = tie.GpuScheduler(mc, tie.Policy.TIE, cfg, tot)
+    for q in (qa, qb):
+        q.on_arrival_batch(ids[:n0], arr[:n0], mt[:n0])
+    popped, done = set(), 0
+    for s in range(2):
+        lo, hi = n0 + s * big, n0 + (s + 1) * big
+        pr = np.array([p for p in range(done, hi - 1000) if int(ids[p]) not in popped], np.int64)
+        done = hi - 1000  # old ids + ids arriving in this same step
+        got_a = qa.step(ids[lo:hi], arr[lo:hi], mt[lo:hi], ids[pr], mu[pr], sg[pr], mt[pr],
+                        pops)
+        qb.on_arrival_batch(ids[lo:hi], arr[lo:hi], mt[lo:hi])
+        qb.on_prediction_logt(ids[pr], mu[pr], sg[pr], mt[pr])
+        got_b = qb.next_requests(pops)
+        assert len(pr) > 16_384 and np.array_equal(got_a, got_b), s
+        popped |= set(got_a.tolist())
+    assert qa.waiting() == qb.waiting()
+    assert np.array_equal(qa.next_requests(300), qb.next_requests(300))
