@@ -270,6 +270,18 @@ int tie_queue_step_ec(tie_queue* q, const uint64_t* arr_ids, const double* arr_t
                       const uint32_t* arr_max_tokens, uint64_t n_arr, const uint64_t* pred_ids,
                       const double* E, const double* C, uint64_t n_pred, uint64_t max_pops,
                       uint64_t* out_ids, uint64_t* n_out);
+/* A run of interleaved events, then pops: for r = 0..n_runs-1, on_arrival for the arrivals
+ * [arr_end[r-1], arr_end[r]), then on_prediction for [pred_end[r-1], pred_end[r]) (arr_end[-1]
+ * = pred_end[-1] = 0); then next_request() up to max_pops times -- each prediction run sees
+ * the queue length after the arrivals before it (compute_beta, sched.cpp:139), exactly as the
+ * reference's call sequence (sim.cpp:123-147 between two admissions).  One device round trip
+ * when the sequence validates; otherwise the runs are applied as consecutive
+ * tie_queue_step_ec calls, raising the first error where the call sequence raises it. */
+int tie_queue_step_ec_runs(tie_queue* q, const uint64_t* arr_ids, const double* arr_time,
+                           const uint32_t* arr_max_tokens, const uint64_t* arr_end,
+                           const uint64_t* pred_ids, const double* E, const double* C,
+                           const uint64_t* pred_end, uint64_t n_runs, uint64_t max_pops,
+                           uint64_t* out_ids, uint64_t* n_out);
 /* Scheduler::rebuild_if_drifted() (sched.cpp:152-167) */
 int tie_queue_rebuild_if_drifted(tie_queue* q, int* rebuilt);
 /* Shard-level primitives for a scheduler sharded by request (coordinated by

@@ -213,6 +213,12 @@ class Scheduler {
   std::vector<uint64_t> step(const Request* arrivals, size_t n_arr, const uint64_t* pred_ids,
                              const double* expectation, const double* cvar, size_t n_pred,
                              size_t max_pops);
+  // runs r of (arrivals [arr_end[r-1], arr_end[r]), predictions [pred_end[r-1], pred_end[r]))
+  // in order, then next_request() up to max_pops times: one round trip (tie_queue_step_ec_runs)
+  std::vector<uint64_t> step_runs(const Request* arrivals, const uint64_t* arr_end,
+                                  const uint64_t* pred_ids, const double* expectation,
+                                  const double* cvar, const uint64_t* pred_end, size_t n_runs,
+                                  size_t max_pops);
   tie_queue* handle() const { return q_; }
 
  private:

@@ -687,6 +687,31 @@ PYBIND11_MODULE(_core, m) {
            py::arg("arr_ids"), py::arg("arrival_s"), py::arg("arr_max_tokens"),
            py::arg("pred_ids"), py::arg("E"), py::arg("C"), py::arg("k"),
            "on_arrival x n, on_prediction(E, C) x m, next_request() x k: one device round trip")
+      .def("step_ec_runs",
+           [](GpuQueue& g, carray<uint64_t> arr_ids, carray<double> arrival_s,
+              carray<uint32_t> arr_max_tokens, carray<uint64_t> arr_end,
+              carray<uint64_t> pred_ids, carray<double> E, carray<double> C,
+              carray<uint64_t> pred_end, uint64_t k) {
+             const uint64_t nr = (uint64_t)arr_end.size();
+             if (arrival_s.size() != arr_ids.size() || arr_max_tokens.size() != arr_ids.size() ||
+                 E.size() != pred_ids.size() || C.size() != pred_ids.size() ||
+                 pred_end.size() != arr_end.size() ||
+                 (nr && (arr_end.data()[nr - 1] != (uint64_t)arr_ids.size() ||
+                         pred_end.data()[nr - 1] != (uint64_t)pred_ids.size())))
+               throw py::value_error("step_ec_runs: array lengths / run ends differ");
+             std::vector<uint64_t> out(k);
+             uint64_t n = 0;
+             throw_code(tie_queue_step_ec_runs(g.q, arr_ids.data(), arrival_s.data(),
+                                               arr_max_tokens.data(), arr_end.data(),
+                                               pred_ids.data(), E.data(), C.data(),
+                                               pred_end.data(), nr, k, out.data(), &n));
+             out.resize(n);
+             return carray<uint64_t>((py::ssize_t)n, out.data());
+           },
+           py::arg("arr_ids"), py::arg("arrival_s"), py::arg("arr_max_tokens"),
+           py::arg("arr_end"), py::arg("pred_ids"), py::arg("E"), py::arg("C"),
+           py::arg("pred_end"), py::arg("k"),
+           "runs of (arrivals, predictions(E, C)) then next_request() x k: one device round trip")
       .def("next_request",
            [](GpuQueue& g) -> py::object {
              uint64_t id = 0, n = 0;

@@ -20,6 +20,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cassert>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -1129,8 +1132,8 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
     const uint32_t* slots, uint64_t np, const double* E, double* C, double beta,
     const uint32_t* blocks, uint32_t nblk, uint32_t n_uncond, uint32_t nblocks, uint64_t n_slots,
     uint32_t pops, uint64_t* out_id, uint32_t* out_slot, uint32_t* out_n,
-    unsigned long long* err, unsigned long long* status_err = nullptr,
-    volatile uint32_t* status_seq = nullptr, uint32_t seq = 0) {
+    unsigned long long* err, unsigned long long* status_err, volatile uint32_t* status_seq,
+    uint32_t seq, const double* betas) {  // betas: per-prediction beta (a multi-run step) or null
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
@@ -1150,7 +1153,7 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
     c = c < e ? e : c;  // sim.cpp:94
     C[t] = c;
     uint32_t why = kOk;
-    if (!isfinite(e) || !isfinite(c) || !isfinite(beta)) why = kScoreNotFinite;
+    if (!isfinite(e) || !isfinite(c) || !isfinite(betas ? betas[t] : beta)) why = kScoreNotFinite;
     else if (!(e > 0.0)) why = kExpectationNonPos;
     else if (c < e) why = kCvarBelowE;
     if (why != kOk) {
@@ -1163,7 +1166,7 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
   if (!skip)
     for (uint64_t t = threadIdx.x; t < np; t += blockDim.x) {
       const uint32_t s = slots[t];
-      q.key[s] = order_bits(__dadd_rn(E[t], __dmul_rn(beta, C[t])));
+      q.key[s] = order_bits(__dadd_rn(E[t], __dmul_rn(betas ? betas[t] : beta, C[t])));
       q.E[s] = E[t];
       q.C[s] = C[t];
           q.predicted[s] = 1;
@@ -1801,7 +1804,7 @@ uint64_t launch_plan(tie_queue* Q, const std::vector<Seg>& plan, size_t first_se
       tie::dev::step_apply_kernel<false><<<1, 1024, 0, s>>>(
           Q->q, 0, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0.0, nullptr, 0, 0, nb,
           Q->n_slots, plan[g].pops, Q->d_out_id + off, Q->d_out_slot + off, Q->d_out_n + g,
-          err);
+          err, nullptr, nullptr, 0u, nullptr);
     off += plan[g].pops;
     tie::capi::count_launch(1);
     ++g;
@@ -2030,7 +2033,8 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
                     const uint32_t* arr_max_tokens, uint64_t n_arr, const uint64_t* pred_ids,
                     const double* mu, const double* sigma, const uint32_t* pred_max_tokens,
                     const double* E_in, const double* C_in, uint64_t n_pred, uint64_t max_pops,
-                    uint64_t* out_ids, uint64_t* n_out) {
+                    uint64_t* out_ids, uint64_t* n_out, const uint64_t* arr_end = nullptr,
+                    const uint64_t* pred_end = nullptr, uint64_t n_runs = 0) {
   if (!Q || !n_out) return set_error(TIE_EINVALID, "tie_queue: null argument");
   const bool ec = E_in != nullptr;
   *n_out = 0;
@@ -2038,6 +2042,46 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
     return set_error(TIE_EINVALID, "tie_queue: a WaitingQueue has no Scheduler operations");
   tie_ctx* ctx = Q->ctx;
   cudaStream_t s = ctx->stream;
+  // ---- a multi-run step (tie_queue_step_ec_runs): runs r = 0..n_runs-1 of (arrivals, then
+  // predictions), each prediction run scored with the beta of the queue length after the
+  // arrivals up to its run.  One round trip when the whole sequence validates and fits the
+  // small-step kernel; otherwise the runs go as consecutive single-run steps (the last one
+  // popping), which is the definition -- and which raises the first error exactly where the
+  // reference's call sequence does.
+  std::vector<double> run_beta;  // per prediction, multi-run steps only
+  if (n_runs > 1) {
+    // (small enough for the single-CTA kernel: <= 4096 blocks touched, whatever the slots)
+    static const bool no_runs = std::getenv("TIE_NO_STEP_RUNS") != nullptr;  // A/B switch
+    bool one = !no_runs && ec && Q->policy != 0 && n_arr <= 16384 &&
+               n_arr / tie::dev::kBlockSlots + 2 + n_pred <= 4096 &&
+               ensure_capacity(Q, n_arr) == TIE_OK;
+    std::vector<double> ak;
+    if (one) one = check_arrivals(Q, arr_ids, arr_time, arr_max_tokens, n_arr, ak) == TIE_OK;
+    if (one) one = first_batch_duplicate(pred_ids, n_pred) == n_pred;
+    const uint64_t first_slot = Q->n_slots;
+    run_beta.resize(one ? n_pred : 0);
+    for (uint64_t r = 0, p0 = 0; one && r < n_runs; p0 = pred_end[r++]) {
+      std::vector<uint32_t> sl;
+      double b = 0.0;
+      Q->size += arr_end[r];
+      one = check_predictions(Q, pred_ids + p0, pred_end[r] - p0, arr_ids, arr_end[r],
+                              first_slot, sl, &b, E_in + p0, C_in + p0) == TIE_OK;
+      Q->size -= arr_end[r];
+      for (uint64_t t = p0; one && t < pred_end[r]; ++t) run_beta[t] = b;
+    }
+    if (!one) {
+      for (uint64_t r = 0, a0 = 0, p0 = 0; r < n_runs; a0 = arr_end[r], p0 = pred_end[r++]) {
+        uint64_t k = 0;
+        if (int rc = queue_step_impl(Q, arr_ids + a0, arr_time + a0, arr_max_tokens + a0,
+                                     arr_end[r] - a0, pred_ids + p0, nullptr, nullptr, nullptr,
+                                     E_in + p0, C_in + p0, pred_end[r] - p0,
+                                     r + 1 == n_runs ? max_pops : 0, out_ids, &k))
+          return rc;
+        *n_out = k;
+      }
+      return TIE_OK;
+    }
+  }
   // ---- host validation of the whole step before any host state changes: the arrivals
   // (tie_queue_arrive), then the predictions with this step's arrivals counted as waiting
   // (tie_queue_predict).  A prediction error leaves the arrivals applied, as the reference's
@@ -2054,7 +2098,8 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
     Q->size += n_arr;
     const int rc = check_predictions(Q, pred_ids, n_pred, arr_ids, n_arr, first, slots, &beta,
                                      E_in, C_in);  // (E, C) given: checked here, as predict's
-    Q->size -= n_arr;
+    Q->size -= n_arr;  // (a multi-run step passed this per run above: rc 0, run_beta holds
+                       // the betas; `beta` here is the last run's and unused)
     if (rc) {
       const std::string msg = tie_last_error();
       if (int rc2 = tie_queue_arrive(Q, arr_ids, arr_time, arr_max_tokens, n_arr)) return rc2;
@@ -2088,18 +2133,30 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
   }
   // ---- predictions' host mirror, tentatively (rolled back if the device rejects them), so
   // the pop plan sees betas_in_use_ as the reference's next_request() will
+  const bool multi = !run_beta.empty();
   auto pred_mirror = [&](bool apply) {
-    for (uint32_t sl : slots) {
+    for (uint64_t t = 0; t < slots.size(); ++t) {
+      const uint32_t sl = slots[t];
+      const double b = multi ? run_beta[t] : beta;
       Q->predicted[sl] = apply ? 1 : 0;
-      Q->pred_beta[sl] = beta;
+      Q->pred_beta[sl] = b;
       Q->pred_epoch[sl] = Q->epoch;
+      if (!multi) continue;
+      if (apply) {
+        ++Q->betas[b];
+      } else {
+        auto it = Q->betas.find(b);
+        if (it != Q->betas.end() && --it->second == 0) Q->betas.erase(it);
+      }
     }
     if (apply) {
-      Q->betas[beta] += n_pred;
+      if (!multi) Q->betas[beta] += n_pred;
       Q->n_predicted += n_pred;
     } else {
-      auto it = Q->betas.find(beta);
-      if (it != Q->betas.end() && (it->second -= n_pred) == 0) Q->betas.erase(it);
+      if (!multi) {
+        auto it = Q->betas.find(beta);
+        if (it != Q->betas.end() && (it->second -= n_pred) == 0) Q->betas.erase(it);
+      }
       Q->n_predicted -= n_pred;
     }
   };
@@ -2119,7 +2176,8 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
   const uint64_t o_aid = 0, o_akey = o_aid + al(8 * n_arr), o_mu = o_akey + al(8 * n_arr),
                  o_sg = o_mu + al(8 * np), o_slot = o_sg + al(8 * np),
                  o_mt = o_slot + al(4 * np), o_blk = o_mt + al(4 * np),
-                 o_h2d_end = o_blk + al(4 * blocks.size()),  // host-provided up to here
+                 o_bet = o_blk + al(4 * blocks.size()),
+                 o_h2d_end = o_bet + al(multi ? 8 * np : 0),  // host-provided up to here
                  o_E = o_h2d_end, o_C = o_E + al(8 * np), o_key = o_C + al(8 * np),
                  total = o_key + al(8 * np);
   if (total > Q->pack_cap) {
@@ -2149,8 +2207,10 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
     if (!ec) std::memcpy(h + o_mt, pred_max_tokens, 4 * np);
   }
   std::memcpy(h + o_blk, blocks.data(), 4 * blocks.size());
+  if (multi && np) std::memcpy(h + o_bet, run_beta.data(), 8 * np);
   char* d = Q->d_pack;
   const bool small = n_arr <= 16384 && np <= 16384 && blocks.size() <= 4096;
+  assert(!multi || small);  // the multi-run fast path's size condition above
   // small steps: the kernels read the pack straight from pinned host memory (no H2D copy);
   // the device pack keeps the scratch (E, C, key)
   const char* in = small ? h : d;
@@ -2192,7 +2252,8 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
         (const uint32_t*)(in + o_slot), np, pE, pC, beta, (const uint32_t*)(in + o_blk),
         (uint32_t)blocks.size(), n_uncond, nb, Q->n_slots, fused_pops, Q->d_out_id,
         Q->d_out_slot, seg0_n, ctx->d_err, apply_last ? &Q->status->err : nullptr,
-        apply_last ? &Q->status->seq : nullptr, seq);
+        apply_last ? &Q->status->seq : nullptr, seq,
+        multi && np ? (const double*)(in + o_bet) : nullptr);
     if (le0 != cudaSuccess) {
       if (use_pred) pred_mirror(false);
       return cuda_error(le0, "tie_queue_step");
@@ -2219,7 +2280,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
       (sq ? tie::dev::step_apply_kernel<true> : tie::dev::step_apply_kernel<false>)<<<1, 1024, 0, s>>>(
           Q->q, 0, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, beta, nullptr, 0, 0, nb,
           Q->n_slots, fused_pops, Q->d_out_id, Q->d_out_slot, seg0_n, ctx->d_err, nullptr,
-          nullptr, 0u);
+          nullptr, 0u, nullptr);
     tie::capi::count_launch((n_arr ? 1 : 0) + (np ? 2 : 0) + (blocks.empty() ? 0 : 1) +
                             (fused_pops ? 1 : 0));
   }
@@ -2241,6 +2302,11 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
     const auto t0 = std::chrono::steady_clock::now();
     while (Q->status->seq != seq) {
       if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(20)) {
+        if (std::getenv("TIE_STEP_DEBUG"))
+          std::fprintf(stderr, "tie_queue_step: 20 ms poll timeout (seq %u, n_arr %llu, n_pred %llu, "
+                       "pops %llu, plan %zu, small %d, apply_last %d)\n", seq,
+                       (unsigned long long)n_arr, (unsigned long long)n_pred,
+                       (unsigned long long)pops, plan.size(), (int)small, (int)apply_last);
         const cudaError_t se = cudaStreamSynchronize(s);
         if (se != cudaSuccess) {
           if (use_pred) pred_mirror(false);
@@ -2289,6 +2355,30 @@ int tie_queue_step_ec(tie_queue* Q, const uint64_t* arr_ids, const double* arr_t
   return queue_step_impl(Q, arr_ids, arr_time, arr_max_tokens, n_arr, pred_ids, nullptr,
                          nullptr, nullptr, n_pred ? E : &kNone, n_pred ? C : &kNone, n_pred,
                          max_pops, out_ids, n_out);
+}
+
+int tie_queue_step_ec_runs(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time,
+                           const uint32_t* arr_max_tokens, const uint64_t* arr_end,
+                           const uint64_t* pred_ids, const double* E, const double* C,
+                           const uint64_t* pred_end, uint64_t n_runs, uint64_t max_pops,
+                           uint64_t* out_ids, uint64_t* n_out) {
+  if (!n_out || (n_runs && (!arr_end || !pred_end)))
+    return set_error(TIE_EINVALID, "tie_queue_step_ec_runs: null argument");
+  if (n_runs == 0)
+    return tie_queue_step_ec(Q, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0,
+                             max_pops, out_ids, n_out);
+  for (uint64_t r = 1; r < n_runs; ++r)
+    if (arr_end[r] < arr_end[r - 1] || pred_end[r] < pred_end[r - 1])
+      return set_error(TIE_EINVALID, "tie_queue_step_ec_runs: run ends must not decrease");
+  const uint64_t n_arr = arr_end[n_runs - 1], n_pred = pred_end[n_runs - 1];
+  if (n_pred && (!E || !C)) return set_error(TIE_EINVALID, "tie_queue_step_ec_runs: null E / C");
+  if (n_runs == 1)
+    return tie_queue_step_ec(Q, arr_ids, arr_time, arr_max_tokens, n_arr, pred_ids, E, C, n_pred,
+                             max_pops, out_ids, n_out);
+  static const double kNone = 0.0;
+  return queue_step_impl(Q, arr_ids, arr_time, arr_max_tokens, n_arr, pred_ids, nullptr,
+                         nullptr, nullptr, n_pred ? E : &kNone, n_pred ? C : &kNone, n_pred,
+                         max_pops, out_ids, n_out, arr_end, pred_end, n_runs);
 }
 
 // ---- shard-level primitives (the scheduler sharded by request) ------------

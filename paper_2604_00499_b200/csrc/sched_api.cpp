@@ -302,6 +302,29 @@ std::vector<uint64_t> Scheduler::step(const Request* arrivals, size_t n_arr,
   return out;
 }
 
+std::vector<uint64_t> Scheduler::step_runs(const Request* arrivals, const uint64_t* arr_end,
+                                           const uint64_t* pred_ids, const double* expectation,
+                                           const double* cvar, const uint64_t* pred_end,
+                                           size_t n_runs, size_t max_pops) {
+  view_.flush();
+  const size_t n_arr = n_runs ? arr_end[n_runs - 1] : 0;
+  std::vector<uint64_t> ids(n_arr);
+  std::vector<double> arr(n_arr);
+  std::vector<uint32_t> mt(n_arr);
+  for (size_t j = 0; j < n_arr; ++j) {
+    ids[j] = arrivals[j].id;
+    arr[j] = arrivals[j].arrival_s;
+    mt[j] = arrivals[j].max_tokens;
+  }
+  std::vector<uint64_t> out(max_pops);
+  uint64_t n = 0;
+  throw_code(tie_queue_step_ec_runs(q_, ids.data(), arr.data(), mt.data(), arr_end, pred_ids,
+                                    expectation, cvar, pred_end, n_runs, max_pops, out.data(),
+                                    &n));
+  out.resize(n);
+  return out;
+}
+
 bool Scheduler::waiting_on(uint64_t req_id) const { return tie_queue_contains(q_, req_id) != 0; }
 
 size_t Scheduler::waiting() const { return tie_queue_size(q_); }

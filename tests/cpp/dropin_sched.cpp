@@ -336,6 +336,49 @@ static void scheduler_step_batching() {  // Scheduler::step == the per-event cal
   CHECK(a.waiting_on(id));
 }
 
+static void scheduler_step_runs() {  // Scheduler::step_runs == the per-event call sequence
+  ScoreConfig cfg;
+  cfg.q_sat = 1e9;  // every prediction run sees its own beta
+  cfg.rebuild_threshold = 0.0;
+  Scheduler a(Policy::TIE, cfg), b(Policy::TIE, cfg);
+  std::mt19937_64 rng(23);
+  std::uniform_real_distribution<double> u(10.0, 900.0);
+  uint64_t next_id = 1;
+  for (int step = 0; step < 30; ++step) {
+    // runs: [arrivals 3][predictions of them][arrivals 2][predictions of all 5]...
+    std::vector<Request> arr;
+    std::vector<uint64_t> pid, arr_end, pred_end;
+    std::vector<double> pe, pc;
+    for (int r = 0; r < 3; ++r) {
+      for (int j = 0; j <= r; ++j) arr.push_back(arrival(next_id++, 0.1 * step, 64 + 9 * j));
+      arr_end.push_back(arr.size());
+      for (size_t j = pid.size(); j + 1 < arr.size(); ++j) {  // all but the newest arrival
+        pid.push_back(arr[j].id);
+        pe.push_back(u(rng));
+        pc.push_back(pe.back() * 1.25);
+      }
+      pred_end.push_back(pid.size());
+    }
+    const std::vector<uint64_t> got = a.step_runs(arr.data(), arr_end.data(), pid.data(),
+                                                  pe.data(), pc.data(), pred_end.data(), 3, 2);
+    size_t a0 = 0, p0 = 0;
+    for (int r = 0; r < 3; ++r) {
+      for (size_t j = a0; j < arr_end[r]; ++j) b.on_arrival(arr[j]);
+      for (size_t j = p0; j < pred_end[r]; ++j) b.on_prediction(pid[j], pe[j], pc[j]);
+      a0 = arr_end[r];
+      p0 = pred_end[r];
+    }
+    std::vector<uint64_t> want;
+    for (int j = 0; j < 2; ++j) {
+      const auto id = b.next_request();
+      if (!id) break;
+      want.push_back(*id);
+    }
+    CHECK(got == want);
+  }
+  CHECK(a.waiting() == b.waiting());
+}
+
 static void distribution_api() {  // test_smoke.py:8-26, dist.hpp per-item functions
   McContext mc(3.5);
   CHECK(mc.samples.size() == 10000 && std::is_sorted(mc.samples.begin(), mc.samples.end()));
@@ -393,6 +436,7 @@ int main() {
   scheduler_policies();
   scheduler_drift_rebuild();
   scheduler_step_batching();
+  scheduler_step_runs();
   distribution_api();
   simulator_api();
   std::printf("dropin_sched: %d passed, %d failed\n", g_pass, g_fail);

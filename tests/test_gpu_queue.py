@@ -436,3 +436,96 @@ def test_large_step_equals_separate_calls(tie, mc, oracle, q_sat, thr):
         popped |= set(got_a.tolist())
     assert qa.waiting() == qb.waiting()
     assert np.array_equal(qa.next_requests(300), qb.next_requests(300))
+
+
+# ---- tie_queue_step_ec_runs: a run of interleaved (arrivals, predictions) then pops ----------
+def _ec(rng, m):
+    e = rng.uniform(10.0, 500.0, m)
+    return e, e * rng.uniform(1.0, 3.0, m)
+
+
+def _seq_runs(q, ids, arr, mt, ae, pids, E, C, pe, k):
+    """the definition: consecutive step_ec calls, the last one popping"""
+    got, a0, p0 = np.zeros(0, np.uint64), 0, 0
+    for r in range(len(ae)):
+        got = q.step_ec(ids[a0:ae[r]], arr[a0:ae[r]], mt[a0:ae[r]], pids[p0:pe[r]], E[p0:pe[r]],
+                        C[p0:pe[r]], k if r + 1 == len(ae) else 0)
+        a0, p0 = ae[r], pe[r]
+    return got
+
+
+@pytest.mark.parametrize("policy,q_sat,thr", [(2, 128.0, 0.1), (2, 1e9, 0.0), (2, 40.0, 0.05),
+                                              (1, 128.0, 0.1), (0, 128.0, 0.1)])
+def test_step_ec_runs_equals_step_sequence(tie, mc, policy, q_sat, thr):
+    pol = [tie.Policy.FCFS, tie.Policy.SEPT, tie.Policy.TIE][policy]
+    rng = np.random.default_rng(31 + policy)
+    tot = 6000
+    ids = rng.permutation(tot * 4)[:tot].astype(np.uint64)
+    arr = np.arange(tot, dtype=np.float64) * 0.01
+    mt = rng.integers(16, 4096, tot).astype(np.uint32)
+    Eall, Call = _ec(rng, tot)
+    qa = tie.GpuScheduler(mc, pol, _cfg(tie, q_sat, thr), tot)
+    qb = tie.GpuScheduler(mc, pol, _cfg(tie, q_sat, thr), tot)
+    nxt, unpred, popped = 0, [], set()
+    for f in range(80):
+        a_ids, p_idx, ae, pe = [], [], [], []
+        for _ in range(int(rng.integers(1, 7))):
+            na = int(rng.integers(0, 9)) if nxt < tot - 10 else 0
+            a_ids += range(nxt, nxt + na)
+            unpred += range(nxt, nxt + na)
+            nxt += na
+            ae.append(len(a_ids))
+            npd = min(len(unpred), int(rng.integers(0, 9)))
+            pick = sorted(rng.choice(len(unpred), npd, replace=False).tolist(), reverse=True)
+            p_idx += [unpred.pop(j) for j in pick]
+            pe.append(len(p_idx))
+        a = np.array(a_ids, np.int64)
+        p = np.array(p_idx, np.int64)
+        k = int(rng.integers(0, 9))
+        args = (ids[a], arr[a], mt[a], np.array(ae, np.uint64), ids[p], Eall[p], Call[p],
+                np.array(pe, np.uint64), k)
+        got_a = qa.step_ec_runs(*args)
+        got_b = _seq_runs(qb, ids[a], arr[a], mt[a], ae, ids[p], Eall[p], Call[p], pe, k)
+        assert np.array_equal(got_a, got_b), (f, got_a, got_b)
+        popped |= set(got_a.tolist())
+        unpred = [u for u in unpred if int(ids[u]) not in popped]
+    assert qa.waiting() == qb.waiting()
+    assert np.array_equal(qa.next_requests(tot), qb.next_requests(tot))
+
+
+@pytest.mark.parametrize("case", ["pred_before_arrival", "pred_twice", "arrival_twice",
+                                  "bad_cvar"])
+def test_step_ec_runs_errors_match_step_sequence(tie, mc, case):
+    """an invalid sequence raises the error of the first failing call, with the calls before it
+    applied -- exactly as consecutive step_ec calls"""
+    rng = np.random.default_rng(5)
+    ids = np.arange(100, 160, dtype=np.uint64)
+    arr = np.arange(60, dtype=np.float64)
+    mt = np.full(60, 512, np.uint32)
+    E, C = _ec(rng, 60)
+    a = np.arange(10, 30)  # arrivals of the step, 4 runs of 5
+    ae = [5, 10, 15, 20]
+    p = {"pred_before_arrival": [0, 1, 5, 12, 16],   # 16 arrives in run 3, predicted in run 2
+         "pred_twice": [0, 1, 5, 1, 14],
+         "arrival_twice": [0, 1, 5, 12, 14],           # arrival 17 repeats 3: run 3 fails
+         "bad_cvar": [0, 1, 5, 12, 14]}[case]
+    pe = [2, 3, 5, 5]
+    aid = ids[a].copy()
+    if case == "arrival_twice":
+        aid[17] = aid[3]
+    pid = aid[p]
+    Ec, Cc = E[:5].copy(), C[:5].copy()
+    if case == "bad_cvar":
+        Cc[3] = Ec[3] * 0.5
+    qa = tie.GpuScheduler(mc, tie.Policy.TIE, _cfg(tie), 64)
+    qb = tie.GpuScheduler(mc, tie.Policy.TIE, _cfg(tie), 64)
+    for q in (qa, qb):
+        q.on_arrival_batch(ids[:10], arr[:10], mt[:10])
+    with pytest.raises(Exception) as ea:
+        qa.step_ec_runs(aid, arr[a], mt[a], np.array(ae, np.uint64), pid, Ec, Cc,
+                        np.array(pe, np.uint64), 4)
+    with pytest.raises(Exception) as eb:
+        _seq_runs(qb, aid, arr[a], mt[a], ae, pid, Ec, Cc, pe, 4)
+    assert type(ea.value) is type(eb.value) and str(ea.value) == str(eb.value), (ea, eb)
+    assert qa.waiting() == qb.waiting()
+    assert np.array_equal(qa.next_requests(64), qb.next_requests(64))
