@@ -33,6 +33,7 @@
 
 #include "../../include/tie_cuda.h"
 #include "tie_internal.cuh"
+#include "flat_idmap.hpp"
 
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
@@ -1306,7 +1307,7 @@ struct tie_queue {
   int adaptive = 1;
   double beta_fixed = 0.1, beta_max = 0.5, q_sat = 128.0, threshold = 0.1, alpha = 0.9;
   uint64_t capacity = 0, n_slots = 0, size = 0, n_predicted = 0;
-  std::unordered_map<uint64_t, uint32_t> slot_of;  // the heap's pos_ index (sched.hpp:67)
+  tie::host::FlatIdMap slot_of;  // the heap's pos_ index (sched.hpp:67)
   std::vector<uint8_t> alive, predicted;
   // beta_at_update per slot (host mirror): the beta of its prediction, or of the last drift
   // rebuild if that came later (tracked by epoch so a rebuild is O(1) on the host)
