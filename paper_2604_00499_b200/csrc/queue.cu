@@ -2030,6 +2030,33 @@ int tie_queue_next(tie_queue* Q, uint64_t max_pops, uint64_t* out_ids, uint64_t*
 namespace {
 // one scheduler iteration; predictions as log-t (mu, sigma, max_tokens), scored on the device
 // (E_in == nullptr), or as the caller's (E, C) pairs (on_prediction's arguments)
+// TIE_STEP_PROFILE (development): host time per stage of tie_queue_step, summed over the
+// process and printed at exit -- validation, mirror + plan, pack, launches, completion wait,
+// replay
+struct StepProfile {
+  double ns[6] = {};
+  uint64_t calls = 0;
+  bool on = std::getenv("TIE_STEP_PROFILE") != nullptr;
+  ~StepProfile() {
+    if (!on || !calls) return;
+    static const char* names[6] = {"validate", "mirror+plan", "pack", "launch", "wait", "replay"};
+    std::fprintf(stderr, "tie_queue_step profile over %llu calls (us per call):",
+                 (unsigned long long)calls);
+    for (int i = 0; i < 6; ++i) std::fprintf(stderr, " %s %.2f", names[i], ns[i] / calls * 1e-3);
+    std::fprintf(stderr, "\n");
+  }
+};
+StepProfile g_step_prof;
+struct StageClock {
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(int i) {
+    if (!g_step_prof.on) return;
+    const auto n = std::chrono::steady_clock::now();
+    g_step_prof.ns[i] += std::chrono::duration<double, std::nano>(n - t).count();
+    t = n;
+  }
+};
+
 int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_time,
                     const uint32_t* arr_max_tokens, uint64_t n_arr, const uint64_t* pred_ids,
                     const double* mu, const double* sigma, const uint32_t* pred_max_tokens,
@@ -2087,6 +2114,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
   // (tie_queue_arrive), then the predictions with this step's arrivals counted as waiting
   // (tie_queue_predict).  A prediction error leaves the arrivals applied, as the reference's
   // on_arrival calls stay applied when a later on_prediction throws.
+  StageClock clk;
   if (int rc = ensure_capacity(Q, n_arr)) return rc;
   std::vector<double> akeys;
   if (int rc = check_arrivals(Q, arr_ids, arr_time, arr_max_tokens, n_arr, akeys)) return rc;
@@ -2163,6 +2191,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
   };
   if (use_pred) pred_mirror(true);
   const uint64_t pops = std::min<uint64_t>(max_pops, Q->size);
+  clk.mark(0);
   const std::vector<Seg> plan = plan_pops(Q, pops);
   uint64_t planned = 0;
   for (const Seg& g : plan) planned += g.pops;
@@ -2198,6 +2227,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
     if (use_pred) pred_mirror(false);
     return rc;
   }
+  clk.mark(1);
   char* h = Q->h_pack;
   std::memcpy(h + o_aid, arr_ids, 8 * n_arr);
   std::memcpy(h + o_akey, akeys.data(), 8 * n_arr);
@@ -2214,6 +2244,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
   assert(!multi || small);  // the multi-run fast path's size condition above
   // small steps: the kernels read the pack straight from pinned host memory (no H2D copy);
   // the device pack keeps the scratch (E, C, key)
+  clk.mark(2);
   const char* in = small ? h : d;
   if (!small) cudaMemcpyAsync(d, h, o_h2d_end, cudaMemcpyHostToDevice, s);  // ONE H2D
   ctx->err_op = "tie_queue_step";
@@ -2294,6 +2325,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
                                                  seq);
     tie::capi::count_launch();
   }
+  clk.mark(3);
   cudaError_t le = cudaGetLastError();
   if (le != cudaSuccess) {
     if (use_pred) pred_mirror(false);
@@ -2324,6 +2356,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
       return rc;
     }
   }
+  clk.mark(4);
   std::vector<uint64_t> got;
   const bool dry = !replay_plan(Q, plan, got);
   uint64_t k = got.size();
@@ -2334,6 +2367,8 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
     k += more;
   }
   *n_out = k;
+  clk.mark(5);
+  ++g_step_prof.calls;
   return TIE_OK;
 }
 

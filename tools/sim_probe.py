@@ -29,12 +29,14 @@ tie.run_sim(w, tie.Policy.TIE, sc, ec, pc, seed)
 if os.environ.get("WITH_REF"):
     from oracle_lib import RefLib, ref_run_sim
     ref_run_sim(RefLib(), 1, 2, 1, threshold=0.0)
+tie.launch_count(True)
 ts = []
 for _ in range(5):
     t0 = time.perf_counter()
     r = tie.run_sim(w, tie.Policy.TIE, sc, ec, pc, seed)
     ts.append(time.perf_counter() - t0)
 print(json.dumps({"tag": os.environ.get("TAG", ""), "seed": seed,
+                  "launches_per_sim": tie.launch_count(False) / 5,
                   "ms_per_sim": round(1e3 * float(np.median(ts)), 1),
                   "all_ms": [round(1e3 * t, 1) for t in ts],
                   "admit_sum": float(sum(e.admit_s for e in r.events))}))
