@@ -1134,9 +1134,34 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
     const uint32_t* blocks, uint32_t nblk, uint32_t n_uncond, uint32_t nblocks, uint64_t n_slots,
     uint32_t pops, uint64_t* out_id, uint32_t* out_slot, uint32_t* out_n,
     unsigned long long* err, unsigned long long* status_err, volatile uint32_t* status_seq,
-    uint32_t seq, const double* betas) {  // betas: per-prediction beta (a multi-run step) or null
+    uint32_t seq, const double* betas,  // betas: per-prediction beta (a multi-run step) or null
+    const char* pack = nullptr, uint32_t pack_bytes = 0) {
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
+  // a small step's pack in pinned host memory (zero-copy): staged into shared memory in one
+  // parallel burst -- one PCIe round trip instead of one per dependent phase below (arrivals,
+  // predictions, slots, blocks); the pointers into it are redirected to the copy
+  if (pack_bytes) {
+    extern __shared__ uint4 stage[];
+    const uint4* src = reinterpret_cast<const uint4*>(pack);
+    for (uint32_t x = threadIdx.x; x < pack_bytes / 16; x += blockDim.x) stage[x] = src[x];
+    const char* sb = reinterpret_cast<const char*>(stage);
+    auto in_pack = [&](const void* ptr) {
+      const char* c = static_cast<const char*>(ptr);
+      return c >= pack && c < pack + pack_bytes;
+    };
+    auto tr = [&](auto* ptr) {
+      using T = decltype(ptr);
+      return in_pack(ptr) ? (T)(sb + (static_cast<const char*>((const void*)ptr) - pack)) : ptr;
+    };
+    arr_ids = tr(arr_ids);
+    arr_keys = tr(arr_keys);
+    slots = tr(slots);
+    blocks = tr(blocks);
+    if (betas) betas = tr(betas);
+    E = tr(E);
+    C = tr(C);
+  }
   __syncthreads();
   for (uint64_t t = threadIdx.x; t < n_arr; t += blockDim.x) {
     const uint64_t s = first + t;
@@ -2273,6 +2298,10 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
     cfg.gridDim = dim3(1);
     cfg.blockDim = dim3(1024);
     cfg.stream = s;
+    // packs up to 32 KB are staged into the kernel's shared memory (one PCIe round trip)
+    static const bool no_stage = std::getenv("TIE_NO_PACK_STAGE") != nullptr;  // A/B switch
+    const uint32_t stage = !no_stage && o_h2d_end <= 32768 ? (uint32_t)o_h2d_end : 0u;
+    cfg.dynamicSmemBytes = stage;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
@@ -2285,7 +2314,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
         (uint32_t)blocks.size(), n_uncond, nb, Q->n_slots, fused_pops, Q->d_out_id,
         Q->d_out_slot, seg0_n, ctx->d_err, apply_last ? &Q->status->err : nullptr,
         apply_last ? &Q->status->seq : nullptr, seq,
-        multi && np ? (const double*)(in + o_bet) : nullptr);
+        multi && np ? (const double*)(in + o_bet) : nullptr, (const char*)h, stage);
     if (le0 != cudaSuccess) {
       if (use_pred) pred_mirror(false);
       return cuda_error(le0, "tie_queue_step");
@@ -2312,7 +2341,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
       (sq ? tie::dev::step_apply_kernel<true> : tie::dev::step_apply_kernel<false>)<<<1, 1024, 0, s>>>(
           Q->q, 0, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, beta, nullptr, 0, 0, nb,
           Q->n_slots, fused_pops, Q->d_out_id, Q->d_out_slot, seg0_n, ctx->d_err, nullptr,
-          nullptr, 0u, nullptr);
+          nullptr, 0u, nullptr, nullptr, 0u);
     tie::capi::count_launch((n_arr ? 1 : 0) + (np ? 2 : 0) + (blocks.empty() ? 0 : 1) +
                             (fused_pops ? 1 : 0));
   }
