@@ -1077,14 +1077,15 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
   }
 }
 
-// the fused step's completion record: the error word, then (after a system fence) the
-// step's sequence number, which the host polls instead of synchronising the stream
-__global__ void step_finish_kernel(const unsigned long long* err,
-                                   unsigned long long* status_err,
-                                   volatile uint32_t* status_seq, uint32_t seq) {
-  *status_err = *(const volatile unsigned long long*)err;
+// the fused step's completion record: the step's sequence number, with kStatusErrBit set when
+// the error word holds an error (the host then decodes it with tie_sync), after a system fence
+// -- one fence, the host polls this word instead of synchronising the stream
+constexpr uint32_t kStatusErrBit = 0x80000000u;
+__global__ void step_finish_kernel(const unsigned long long* err, volatile uint32_t* status_seq,
+                                   uint32_t seq) {
+  const bool failed = *(const volatile unsigned long long*)err != ~0ull;
   __threadfence_system();
-  *status_seq = seq;
+  *status_seq = seq | (failed ? kStatusErrBit : 0u);
 }
 
 __global__ void __launch_bounds__(1024) pop_topb_kernel(QDev q, uint32_t nblocks,
@@ -1133,7 +1134,7 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
     const uint32_t* slots, uint64_t np, const double* E, double* C, double beta,
     const uint32_t* blocks, uint32_t nblk, uint32_t n_uncond, uint32_t nblocks, uint64_t n_slots,
     uint32_t pops, uint64_t* out_id, uint32_t* out_slot, uint32_t* out_n,
-    unsigned long long* err, unsigned long long* status_err, volatile uint32_t* status_seq,
+    unsigned long long* err, volatile uint32_t* status_seq,
     uint32_t seq, const double* betas,  // betas: per-prediction beta (a multi-run step) or null
     const char* pack = nullptr, uint32_t pack_bytes = 0) {
   __shared__ int bad;
@@ -1219,10 +1220,9 @@ __global__ void __launch_bounds__(1024) step_apply_kernel(
   if (status_seq) {  // the step's last kernel: publish the completion record (step_finish)
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence_system();
-      *status_err = *(const volatile unsigned long long*)err;
-      __threadfence_system();
-      *status_seq = seq;
+      const bool failed = *(const volatile unsigned long long*)err != ~0ull;
+      __threadfence_system();  // the CTA's output writes (seen through the barrier) first
+      *status_seq = seq | (failed ? kStatusErrBit : 0u);
     }
   }
 }
@@ -1830,7 +1830,7 @@ uint64_t launch_plan(tie_queue* Q, const std::vector<Seg>& plan, size_t first_se
       tie::dev::step_apply_kernel<false><<<1, 1024, 0, s>>>(
           Q->q, 0, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0.0, nullptr, 0, 0, nb,
           Q->n_slots, plan[g].pops, Q->d_out_id + off, Q->d_out_slot + off, Q->d_out_n + g,
-          err, nullptr, nullptr, 0u, nullptr);
+          err, nullptr, 0u, nullptr);
     off += plan[g].pops;
     tie::capi::count_launch(1);
     ++g;
@@ -2288,7 +2288,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
     }
   }
   uint32_t* seg0_n = Q->d_out_n + (seg0_fused ? 0 : plan.size());  // unused slot if not fused
-  const uint32_t seq = ++Q->seq;
+  const uint32_t seq = ++Q->seq & ~tie::dev::kStatusErrBit;  // 31 bits: the top is the error bit
   // the apply kernel is the step's last kernel when no further plan segments follow it
   const bool apply_last = small && plan.size() <= (seg0_fused ? 1u : 0u);
   if (small) {  // everything after the scoring in one single-CTA kernel
@@ -2312,8 +2312,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
         first, n_arr, (const uint64_t*)(in + o_aid), (const double*)(in + o_akey),
         (const uint32_t*)(in + o_slot), np, pE, pC, beta, (const uint32_t*)(in + o_blk),
         (uint32_t)blocks.size(), n_uncond, nb, Q->n_slots, fused_pops, Q->d_out_id,
-        Q->d_out_slot, seg0_n, ctx->d_err, apply_last ? &Q->status->err : nullptr,
-        apply_last ? &Q->status->seq : nullptr, seq,
+        Q->d_out_slot, seg0_n, ctx->d_err, apply_last ? &Q->status->seq : nullptr, seq,
         multi && np ? (const double*)(in + o_bet) : nullptr, (const char*)h, stage);
     if (le0 != cudaSuccess) {
       if (use_pred) pred_mirror(false);
@@ -2341,7 +2340,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
       (sq ? tie::dev::step_apply_kernel<true> : tie::dev::step_apply_kernel<false>)<<<1, 1024, 0, s>>>(
           Q->q, 0, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, beta, nullptr, 0, 0, nb,
           Q->n_slots, fused_pops, Q->d_out_id, Q->d_out_slot, seg0_n, ctx->d_err, nullptr,
-          nullptr, 0u, nullptr, nullptr, 0u);
+          0u, nullptr, nullptr, 0u);
     tie::capi::count_launch((n_arr ? 1 : 0) + (np ? 2 : 0) + (blocks.empty() ? 0 : 1) +
                             (fused_pops ? 1 : 0));
   }
@@ -2350,7 +2349,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
   // mapped host memory; the host polls it (a stream synchronisation costs more than the
   // whole small step) and falls back to synchronising after 20 ms
   if (!apply_last) {
-    tie::dev::step_finish_kernel<<<1, 1, 0, s>>>(ctx->d_err, &Q->status->err, &Q->status->seq,
+    tie::dev::step_finish_kernel<<<1, 1, 0, s>>>(ctx->d_err, &Q->status->seq,
                                                  seq);
     tie::capi::count_launch();
   }
@@ -2362,7 +2361,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
   }
   {
     const auto t0 = std::chrono::steady_clock::now();
-    while (Q->status->seq != seq) {
+    while ((Q->status->seq & ~tie::dev::kStatusErrBit) != seq) {
       if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(20)) {
         if (std::getenv("TIE_STEP_DEBUG"))
           std::fprintf(stderr, "tie_queue_step: 20 ms poll timeout (seq %u, n_arr %llu, n_pred %llu, "
@@ -2379,7 +2378,7 @@ int queue_step_impl(tie_queue* Q, const uint64_t* arr_ids, const double* arr_tim
     }
   }
   // the error word (tie_sync decodes + resets it); arrivals stay applied like the reference's
-  if (Q->status->err != ~0ull) {
+  if (Q->status->seq & tie::dev::kStatusErrBit) {
     if (int rc = tie_sync(ctx, s)) {
       if (use_pred) pred_mirror(false);
       return rc;
