@@ -66,21 +66,32 @@ __device__ __forceinline__ bool less_kv(uint64_t ka, uint64_t ia, uint64_t kb, u
   return ka < kb || (ka == kb && ia < ib);
 }
 
+// (key, id, slot) argmin across a warp, in every lane: the lexicographic minimum of the 128-bit
+// (key, id) as four 32-bit redux.sync minima over the lanes still tied, then the slot of the
+// lowest tied lane (what the shuffle tree below picked: ties keep the lower lane) -- 4 REDUX
+// + a ballot + a shuffle instead of 25 shuffles and 5 dependent 128-bit compares
+__device__ __forceinline__ void warp_argmin_redux(uint64_t& k, uint64_t& i, uint32_t& s) {
+  const uint32_t kh = (uint32_t)(k >> 32), kl = (uint32_t)k;
+  const uint32_t ih = (uint32_t)(i >> 32), il = (uint32_t)i;
+  const uint32_t m1 = __reduce_min_sync(0xffffffffu, kh);
+  bool t = kh == m1;
+  const uint32_t m2 = __reduce_min_sync(0xffffffffu, t ? kl : 0xffffffffu);
+  t = t && kl == m2;
+  const uint32_t m3 = __reduce_min_sync(0xffffffffu, t ? ih : 0xffffffffu);
+  t = t && ih == m3;
+  const uint32_t m4 = __reduce_min_sync(0xffffffffu, t ? il : 0xffffffffu);
+  t = t && il == m4;
+  const int w = __ffs(__ballot_sync(0xffffffffu, t)) - 1;
+  k = ((uint64_t)m1 << 32) | m2;
+  i = ((uint64_t)m3 << 32) | m4;
+  s = __shfl_sync(0xffffffffu, s, w);
+}
+
 // (key, id, slot) argmin across a CTA (blockDim multiple of 32, <= 1024)
 __device__ __forceinline__ void block_argmin(uint64_t& k, uint64_t& i, uint32_t& s,
                                              uint64_t* sk, uint64_t* si, uint32_t* ss) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t k2 = __shfl_down_sync(0xffffffffu, k, o);
-    const uint64_t i2 = __shfl_down_sync(0xffffffffu, i, o);
-    const uint32_t s2 = __shfl_down_sync(0xffffffffu, s, o);
-    if (less_kv(k2, i2, k, i)) {
-      k = k2;
-      i = i2;
-      s = s2;
-    }
-  }
+  warp_argmin_redux(k, i, s);
   if (lane == 0) {
     sk[warp] = k;
     si[warp] = i;
@@ -92,17 +103,7 @@ __device__ __forceinline__ void block_argmin(uint64_t& k, uint64_t& i, uint32_t&
     k = lane < nw ? sk[lane] : kDead;
     i = lane < nw ? si[lane] : kDead;
     s = lane < nw ? ss[lane] : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t k2 = __shfl_down_sync(0xffffffffu, k, o);
-      const uint64_t i2 = __shfl_down_sync(0xffffffffu, i, o);
-      const uint32_t s2 = __shfl_down_sync(0xffffffffu, s, o);
-      if (less_kv(k2, i2, k, i)) {
-        k = k2;
-        i = i2;
-        s = s2;
-      }
-    }
+    warp_argmin_redux(k, i, s);
     if (lane == 0) {
       sk[0] = k;
       si[0] = i;
@@ -165,17 +166,7 @@ __device__ __forceinline__ void warp_block_min(const QDev& q, uint32_t blk, uint
         s = (uint32_t)((uint64_t)blk * kBlockSlots + base + u * 32 + lane);
       }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t k2 = __shfl_down_sync(0xffffffffu, k, o);
-    const uint64_t i2 = __shfl_down_sync(0xffffffffu, i, o);
-    const uint32_t s2 = __shfl_down_sync(0xffffffffu, s, o);
-    if (less_kv(k2, i2, k, i)) {
-      k = k2;
-      i = i2;
-      s = s2;
-    }
-  }
+  warp_argmin_redux(k, i, s);
 }
 
 // one CTA per listed block (or per block b < nb when list == nullptr)
@@ -445,17 +436,7 @@ struct CandScratch {
 };
 
 __device__ __forceinline__ void warp_min3(uint64_t& k, uint64_t& i, uint32_t& s) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t k2 = __shfl_down_sync(0xffffffffu, k, o);
-    const uint64_t i2 = __shfl_down_sync(0xffffffffu, i, o);
-    const uint32_t s2 = __shfl_down_sync(0xffffffffu, s, o);
-    if (less_kv(k2, i2, k, i)) {
-      k = k2;
-      i = i2;
-      s = s2;
-    }
-  }
+  warp_argmin_redux(k, i, s);
 }
 
 // the r-th smallest (key, id) pair of pairs[0..n) (r < rmax), by one CTA: every thread keeps
