@@ -117,6 +117,28 @@ __device__ __forceinline__ void block_argmin(uint64_t& k, uint64_t& i, uint32_t&
   __syncthreads();
 }
 
+// block_argmin for a loop of rounds with ONE CTA barrier per round: every warp reduces the 32
+// warp minima itself (redux.sync is cheap), reading a double buffer indexed by the round's
+// parity -- a warp can run one round ahead of the slowest, never two (the barrier)
+__device__ __forceinline__ void block_argmin_round(uint64_t& k, uint64_t& i, uint32_t& s,
+                                                   uint64_t* dk, uint64_t* di, uint32_t* ds,
+                                                   uint32_t round) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  warp_argmin_redux(k, i, s);
+  const uint32_t o = (round & 1u) * 32u;
+  if (lane == 0) {
+    dk[o + warp] = k;
+    di[o + warp] = i;
+    ds[o + warp] = s;
+  }
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  k = lane < nw ? dk[o + lane] : kDead;
+  i = lane < nw ? di[o + lane] : kDead;
+  s = lane < nw ? ds[o + lane] : 0;
+  warp_argmin_redux(k, i, s);
+}
+
 __device__ __forceinline__ void refresh_block(const QDev& q, uint32_t b, uint64_t n_slots,
                                               uint64_t* sk, uint64_t* si, uint32_t* ss) {
   uint64_t k = kDead, i = kDead;
@@ -795,8 +817,8 @@ __device__ __forceinline__ void pop_from_blocks_regs(const QDev& q, const uint32
                                                   uint32_t nchosen, uint64_t n_slots,
                                                   uint32_t pops, uint64_t* out_id,
                                                   uint32_t* out_slot, uint32_t* out_n,
-                                                  uint64_t* out_key, uint64_t* sk,
-                                                  uint64_t* si, uint32_t* ss) {
+                                                  uint64_t* out_key, uint64_t* dk,
+                                                  uint64_t* di, uint32_t* ds) {
   constexpr int kF = 8;
   uint64_t fk[kF], fi[kF];
   uint32_t fs[kF];
@@ -826,7 +848,7 @@ __device__ __forceinline__ void pop_from_blocks_regs(const QDev& q, const uint32
   for (; done < pops; ++done) {
     uint64_t k = fk[0], i = fi[0];
     uint32_t s = fs[0];
-    block_argmin(k, i, s, sk, si, ss);
+    block_argmin_round(k, i, s, dk, di, ds, done);
     if (k == kDead) break;
     if (threadIdx.x == 0) {
       out_id[done] = i;
@@ -870,6 +892,8 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
                                          uint32_t* out_n, uint64_t* out_key = nullptr) {
   __shared__ uint64_t sk[32], si[32];
   __shared__ uint32_t ss[32];
+  __shared__ uint64_t dk[64], di[64];  // block_argmin_round's double buffer
+  __shared__ uint32_t ds[64];
   __shared__ uint32_t chosen[kTopB];
   __shared__ uint64_t ck[kCandCap], ci[kCandCap];
   __shared__ uint32_t cs[kCandCap];
@@ -887,7 +911,7 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
   uint64_t k0, i0, k1, i1;
   uint32_t b0, b1;
   bool more;  // the thread's share held more than two live blocks when last scanned
-  auto scan_top2 = [&](int nex) {
+  auto scan_top2 = [&](int nex, uint32_t also) {  // excluding chosen[0..nex) and `also`
     k0 = i0 = k1 = i1 = kDead;
     b0 = b1 = 0xffffffffu;
     uint32_t live = 0;
@@ -904,7 +928,7 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
       for (int u = 0; u < kU; ++u) {
         if (kk[u] == kDead) continue;
         const uint32_t x = x0 + u * blockDim.x;
-        bool ex = false;
+        bool ex = x == also;
         for (int e = 0; e < nex; ++e) ex |= chosen[e] == x;
         if (ex) continue;
         ++live;
@@ -925,16 +949,15 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
     }
     more = live > 2;
   };
-  scan_top2(0);
+  scan_top2(0, 0xffffffffu);
   uint32_t nchosen = 0;
   uint64_t vB_k = kDead, vB_i = kDead;
   for (uint32_t r = 0; r < pops; ++r) {
     uint64_t k = k0, i = i0;
     uint32_t b = b0;
-    block_argmin(k, i, b, sk, si, ss);
+    block_argmin_round(k, i, b, dk, di, ds, r);
     if (k == kDead) break;  // fewer live blocks than pops
-    if (threadIdx.x == 0) chosen[r] = b;
-    __syncthreads();
+    if (threadIdx.x == 0) chosen[r] = b;  // visible after the next round's barrier
     nchosen = r + 1;
     vB_k = k;
     vB_i = i;
@@ -944,9 +967,11 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
       b0 = b1;
       k1 = i1 = kDead;
       b1 = 0xffffffffu;
-      if (k0 == kDead && more) scan_top2((int)nchosen);
+      // chosen[r] may not be visible yet: excluded as `also`
+      if (k0 == kDead && more) scan_top2((int)r, b);
     }
   }
+  __syncthreads();  // chosen[] complete for the steps below
   if (nchosen == 0) {
     if (threadIdx.x == 0) *out_n = 0;
     return;
@@ -954,7 +979,7 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
   if (kSmallPath && nchosen < pops && nchosen <= 8 && blockDim.x == 1024) {
     // every live block is chosen (a small queue): select among all their entries directly
     pop_from_blocks_regs(q, chosen, nchosen, n_slots, pops, out_id, out_slot, out_n, out_key,
-                         sk, si, ss);
+                         dk, di, ds);
     return;
   }
   if (nchosen < pops) {  // every live block is chosen: all their live entries are candidates

@@ -9,4 +9,5 @@ import bench_sched  # noqa: E402
 import paper_2604_00499_b200 as tie  # noqa: E402
 
 mc = tie.McContext(3.5)
-bench_sched.run(tie, mc, sizes=(1000,), steps=60, variants=("steady",), cpu=False)
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
+bench_sched.run(tie, mc, sizes=(n,), steps=60, variants=("steady",), cpu=False)
