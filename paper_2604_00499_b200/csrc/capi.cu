@@ -3,7 +3,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -241,6 +248,7 @@ void tie_ctx_destroy(tie_ctx* ctx) {
   cudaFree(ctx->d_err);
   cudaFree(ctx->scratch);
   cudaFree(ctx->io);
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
@@ -461,6 +469,137 @@ static char* io_buffer(tie_ctx* ctx, size_t bytes) {
 
 static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// A small persistent pool of host threads for the pageable-buffer copies of the *_host entry
+// points: one thread copies pageable memory at ~10 GB/s, 4-8 at ~60 GB/s (B200 box host,
+// tools/memcpy_probe.cpp), and a persistent pool avoids a thread spawn per copy.  run()
+// splits [0, bytes) into 1 MB tasks over the workers and the calling thread.
+namespace {
+class CopyPool {
+ public:
+  struct Seg {
+    void* dst;
+    const void* src;
+    size_t bytes;
+  };
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  void copy(void* dst, const void* src, size_t bytes) { copy({Seg{dst, src, bytes}}); }
+  // the segments' copies, split into 1 MB tasks over the workers and the calling thread
+  void copy(std::initializer_list<Seg> segs) {
+    Job job;
+    size_t total = 0;
+    for (const Seg& g : segs) {
+      if (job.nseg == kMaxSeg) break;
+      job.seg[job.nseg] = g;
+      job.first[job.nseg++] = total;
+      total += (g.bytes + kTask - 1) / kTask;
+    }
+    job.ntask = total;
+    if (workers_.empty() || total <= 2) {
+      for (int g = 0; g < job.nseg; ++g) std::memcpy(job.seg[g].dst, job.seg[g].src, job.seg[g].bytes);
+      return;
+    }
+    std::lock_guard<std::mutex> one(call_);  // one parallel copy at a time
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      job_ = &job;
+      gen_.fetch_add(1, std::memory_order_release);
+    }
+    cv_.notify_all();
+    work(job);
+    while (job.done.load(std::memory_order_acquire) < job.ntask) std::this_thread::yield();
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      job_ = nullptr;  // a worker arriving from now on finds no job
+    }
+    // workers that took the job hold a reference until they leave it
+    while (job.refs.load(std::memory_order_acquire) != 0) std::this_thread::yield();
+  }
+
+ private:
+  static constexpr size_t kTask = 1u << 20;
+  static constexpr int kMaxSeg = 4;
+  struct Job {
+    Seg seg[kMaxSeg];
+    size_t first[kMaxSeg];
+    int nseg = 0;
+    size_t ntask = 0;
+    std::atomic<size_t> next{0}, done{0};
+    std::atomic<int> refs{0};
+  };
+  CopyPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const unsigned nw = std::min(7u, hw > 1 ? hw - 1 : 0u);
+    for (unsigned t = 0; t < nw; ++t)
+      workers_.emplace_back([this] {
+        uint64_t seen = 0;
+        for (;;) {
+          // spin ~0.5 ms for the next job (a call issues several back to back), then sleep
+          const auto t0 = std::chrono::steady_clock::now();
+          while (gen_.load(std::memory_order_acquire) == seen && !stop_.load() &&
+                 std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(500))
+            std::this_thread::yield();
+          Job* j = nullptr;
+          {
+            std::unique_lock<std::mutex> lk(m_);
+            cv_.wait(lk, [&] { return stop_.load() || gen_.load() != seen; });
+            if (stop_.load()) return;
+            seen = gen_.load();
+            j = job_;
+            if (j) j->refs.fetch_add(1);
+          }
+          if (j) {
+            work(*j);
+            j->refs.fetch_sub(1, std::memory_order_release);
+          }
+        }
+      });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_.store(true);
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  static void work(Job& j) {
+    for (size_t t; (t = j.next.fetch_add(1)) < j.ntask;) {
+      int g = 0;
+      while (g + 1 < j.nseg && t >= j.first[g + 1]) ++g;
+      const size_t lo = (t - j.first[g]) * kTask;
+      const size_t len = std::min(kTask, j.seg[g].bytes - lo);
+      std::memcpy(static_cast<char*>(j.seg[g].dst) + lo,
+                  static_cast<const char*>(j.seg[g].src) + lo, len);
+      j.done.fetch_add(1, std::memory_order_release);
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_, call_;
+  std::condition_variable cv_;
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<bool> stop_{false};
+  Job* job_ = nullptr;
+};
+}  // namespace
+
+static char* host_stage(tie_ctx* ctx, size_t bytes) {  // grow-only, mapped pinned
+  if (bytes <= ctx->h_stage_bytes) return (char*)ctx->h_stage;
+  cudaDeviceSynchronize();
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+  ctx->h_stage = nullptr;
+  ctx->h_stage_bytes = 0;
+  const size_t want = bytes + bytes / 8 + (1 << 20);
+  if (cudaHostAlloc(&ctx->h_stage, want, cudaHostAllocMapped) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  ctx->h_stage_bytes = want;
+  return (char*)ctx->h_stage;
+}
+
 // the device address of a pinned (page-locked, UVA-mapped) host buffer; nullptr for pageable
 // or null pointers (the caller then stages copies)
 static void* mapped_device_ptr(const void* p) {
@@ -525,7 +664,38 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
   const void* m_mu = zc_in ? mapped_device_ptr(mu) : nullptr;
   const void* m_sg = zc_in ? mapped_device_ptr(sigma) : nullptr;
   const void* m_mt = zc_in ? mapped_device_ptr(max_tokens) : nullptr;
-  if (m_mu && m_sg && m_mt) {
+  // pageable caller buffers (a std::vector / NumPy array): copied by the host pool into the
+  // context's pinned staging in chunks, each chunk scored zero-copy while the next is copied
+  // -- the driver's own pageable copies run at ~10 GB/s on one thread
+  static const bool no_stage = getenv("TIE_NO_HOST_STAGE") != nullptr;  // A/B switch
+  const bool big = n >= (1u << 18) && !no_stage;
+  const bool stage_in = big && zc_in && !(m_mu && m_sg && m_mt);
+  const bool stage_out = big && !mapped_device_ptr(order) && tie::dev::rank_output_coalesced(n);
+  char* hs = (stage_in || stage_out)
+                 ? host_stage(ctx, 2 * al(8 * n) + al(4 * n) + al(8 * n))
+                 : nullptr;
+  uint64_t* h_order = hs && stage_out ? (uint64_t*)(hs + 2 * al(8 * n) + al(4 * n)) : nullptr;
+  if (hs && stage_in) {
+    double* h_mu = (double*)hs;
+    double* h_sg = (double*)(hs + al(8 * n));
+    uint32_t* h_mt = (uint32_t*)(hs + 2 * al(8 * n));
+    static const int chunks =
+        getenv("TIE_STAGE_CHUNKS") ? std::max(1, atoi(getenv("TIE_STAGE_CHUNKS"))) : 2;
+    const uint64_t step = ((n + chunks - 1) / chunks + 1023) & ~(uint64_t)1023;
+    CopyPool& pool = CopyPool::get();
+    for (uint64_t lo = 0; lo < n; lo += step) {
+      const uint64_t m = std::min<uint64_t>(step, n - lo);
+      pool.copy({{h_mu + lo, mu + lo, 8 * m}, {h_sg + lo, sigma + lo, 8 * m},
+                 {h_mt + lo, max_tokens + lo, 4 * m}});
+      const cudaError_t e = tie::dev::launch_score(
+          ctx, (const double*)mapped_device_ptr(h_mu) + lo,
+          (const double*)mapped_device_ptr(h_sg) + lo,
+          (const uint32_t*)mapped_device_ptr(h_mt) + lo, true, m, alpha, beta, nullptr,
+          nullptr, d_S ? d_S + lo : nullptr, prep.keys + lo, prep.minmax,
+          flags & TIE_SCORE_EXACT, s, lo);
+      if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
+    }
+  } else if (m_mu && m_sg && m_mt) {
     const cudaError_t e = tie::dev::launch_score(
         ctx, (const double*)m_mu, (const double*)m_sg, m_mt, true, n, alpha, beta, nullptr,
         nullptr, d_S, prep.keys, prep.minmax, flags & TIE_SCORE_EXACT, s, 0);
@@ -560,16 +730,18 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
   // pinned (page-locked, UVA-mapped) output: the sort's last kernel writes the dispatch
   // order straight into host memory, so the D2H overlaps the sort instead of following it
   static const int zero_copy = getenv("TIE_NO_ZERO_COPY") ? 0 : 1;  // A/B switch
-  uint64_t* m_order = zero_copy && tie::dev::rank_output_coalesced(n)
-                          ? (uint64_t*)mapped_device_ptr(order)
-                          : nullptr;
+  uint64_t* m_order = !zero_copy || !tie::dev::rank_output_coalesced(n) ? nullptr
+                     : h_order ? (uint64_t*)mapped_device_ptr(h_order)
+                               : (uint64_t*)mapped_device_ptr(order);
   const bool mapped = m_order != nullptr;
   cudaError_t e = tie::dev::rank_prepared(ctx, n, mapped ? m_order : d_order, s);
   if (e != cudaSuccess) return cuda_error(e, "tie_score_rank_host");
   if (!mapped)
     TIE_CUDA_TRY(cudaMemcpyAsync(order, d_order, 8 * n, cudaMemcpyDeviceToHost, s), "d2h");
   if (score) TIE_CUDA_TRY(cudaMemcpyAsync(score, d_S, 8 * n, cudaMemcpyDeviceToHost, s), "d2h");
-  return tie_sync(ctx, s);
+  if (int rc = tie_sync(ctx, s)) return rc;
+  if (mapped && h_order) CopyPool::get().copy(order, h_order, 8 * n);  // staged order out
+  return TIE_OK;
 }
 
 int tie_rank_host(tie_ctx* ctx, const double* key, const uint64_t* ids, uint64_t n,

@@ -186,6 +186,10 @@ struct tie_ctx {
   // device I/O arena of the *_host entry points
   void* io = nullptr;
   size_t io_bytes = 0;
+  // pinned, UVA-mapped host staging of the *_host entry points for pageable caller buffers
+  // (filled / drained by the host copy pool, read / written by the kernels zero-copy)
+  void* h_stage = nullptr;
+  size_t h_stage_bytes = 0;
   // cached k_alpha = upper_bound(Y, t_quantile(alpha, nu)) of the last alpha seen
   double ka_alpha = -1.0;
   uint32_t ka_k = 0;

@@ -175,7 +175,7 @@ def test_sigma_table_boundary(abi, oracle, samples):
         abi.destroy(h2)
 
 
-@pytest.mark.parametrize("n", [1000, 300_001])
+@pytest.mark.parametrize("n", [1000, 300_001, 1_000_000, 2_500_003])
 def test_host_call_pinned_zero_copy_equals_pageable(tie, mc, n):
     """tie_score_rank_host on pinned buffers (the score kernel reads the inputs and the sort
     writes the order through UVA-mapped host memory) == the same call on pageable NumPy
@@ -197,6 +197,20 @@ def test_host_call_pinned_zero_copy_equals_pageable(tie, mc, n):
                             0.5, s_h.ctypes.data, o_h.ctypes.data, 0)
     assert np.array_equal(s_p.numpy().view(np.uint64), s_h.view(np.uint64))
     assert np.array_equal(o_p.numpy().view(np.uint64), o_h)
+    # pinned inputs with a pageable order (staged output only), and the reverse
+    o_h2 = np.empty(n, np.uint64)
+    tie.score_rank_host_ptr(mc.handle, mu_p.data_ptr(), sg_p.data_ptr(), mt_p.data_ptr(), n,
+                            0.9, 0.5, 0, o_h2.ctypes.data, 0)
+    assert np.array_equal(o_h2, o_h)
+    o_p2 = torch.zeros(n, dtype=torch.int64).pin_memory()
+    tie.score_rank_host_ptr(mc.handle, mu.ctypes.data, sg.ctypes.data, mt.ctypes.data, n, 0.9,
+                            0.5, 0, o_p2.data_ptr(), 0)
+    assert np.array_equal(o_p2.numpy().view(np.uint64), o_h)
+    bad = sg.copy()
+    bad[n // 3] = -1.0  # the staged (pageable) inputs report the same item index
+    with pytest.raises(ValueError, match=f"item {n // 3}"):
+        tie.score_rank_host_ptr(mc.handle, mu.ctypes.data, bad.ctypes.data, mt.ctypes.data, n,
+                                0.9, 0.5, 0, o_h2.ctypes.data, 0)
     sg_p[n // 2] = -1.0  # LogTParams: sigma must be finite and > 0
     with pytest.raises(ValueError, match=f"item {n // 2}"):
         tie.score_rank_host_ptr(mc.handle, mu_p.data_ptr(), sg_p.data_ptr(), mt_p.data_ptr(),
