@@ -644,6 +644,8 @@ int tie_score_rank_host(tie_ctx* ctx, const double* mu, const double* sigma,
   if (int rc = check_ctx(ctx)) return rc;
   if (int rc = validate_alpha(alpha)) return rc;
   if (n == 0) return TIE_OK;
+  if (!mu || !sigma || !max_tokens || !order)
+    return set_error(TIE_EINVALID, "tie_score_rank_host: null pointer");
   DeviceGuard g(ctx->device);
   char* b = io_buffer(ctx, 2 * al(8 * n) + al(4 * n) + al(8 * n) + al(8 * n));
   if (!b) return set_error(TIE_ECUDA, "tie_score_rank_host: device allocation failed");

@@ -211,6 +211,9 @@ def test_host_call_pinned_zero_copy_equals_pageable(tie, mc, n):
     with pytest.raises(ValueError, match=f"item {n // 3}"):
         tie.score_rank_host_ptr(mc.handle, mu.ctypes.data, bad.ctypes.data, mt.ctypes.data, n,
                                 0.9, 0.5, 0, o_h2.ctypes.data, 0)
+    with pytest.raises(ValueError, match="null pointer"):  # not a crash in the staging copies
+        tie.score_rank_host_ptr(mc.handle, mu.ctypes.data, 0, mt.ctypes.data, n, 0.9, 0.5, 0,
+                                o_h2.ctypes.data, 0)
     sg_p[n // 2] = -1.0  # LogTParams: sigma must be finite and > 0
     with pytest.raises(ValueError, match=f"item {n // 2}"):
         tie.score_rank_host_ptr(mc.handle, mu_p.data_ptr(), sg_p.data_ptr(), mt_p.data_ptr(),
