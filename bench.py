@@ -590,6 +590,20 @@ def run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream, 
         fit_host()
         fts.append(time.perf_counter() - t0)
     fe2e = float(np.median(fts))
+    # the same call on PAGEABLE NumPy buffers (a reference caller's std::vector): staged by
+    # the library's host copy pool
+    xq = np.ascontiguousarray(x)
+    oq = [np.empty(P), np.empty(P), np.empty(P), np.empty(P, np.int32), np.empty(P, np.uint8),
+          np.empty(P, np.uint8)]
+    pts = []
+    for i in range(2 + 3):
+        t0 = time.perf_counter()
+        tie.fit_host_ptr(ctx, xq.ctypes.data, P, K, 3.5, *[o.ctypes.data for o in oq])
+        if i >= 2:
+            pts.append(time.perf_counter() - t0)
+    fe2e_pageable = float(np.median(pts))
+    fit_pageable_ok = bool(np.array_equal(oq[0], hb[0].numpy()) and
+                           np.array_equal(oq[1], hb[1].numpy()))
     # config 4 on one GPU: the 64M-request queue (the multi-GPU config's full size), resident
     try:
         n4 = 64 * 2 ** 20
@@ -721,7 +735,11 @@ def run_extras(tie, torch, ctx, dev, mu, sg, mt, S, order, flush, beta, stream, 
     out["fit"] = {"metric": "log-t fits/sec (config 3: 1M prompts x 16 lengths)",
                   "value": P / (fms * 1e-3), "unit": "fits/s", "ms": fms,
                   "e2e": {"value": P / fe2e, "unit": "fits/s", "h2d_bytes": 8 * P * K,
-                          "d2h_bytes": P * (8 * 3 + 4 + 2)},
+                          "d2h_bytes": P * (8 * 3 + 4 + 2),
+                          "pageable": {"value": P / fe2e_pageable, "unit": "fits/s",
+                                       "ms": fe2e_pageable * 1e3,
+                                       "api": "tie_fit_host on pageable NumPy buffers",
+                                       "equals_pinned_call": fit_pageable_ok}},
                   "iterations_mean": float(iters.mean()), "iterations_max": int(iters.max())}
     return out
 

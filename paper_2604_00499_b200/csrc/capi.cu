@@ -884,6 +884,39 @@ int tie_fit_host(tie_ctx* ctx, const double* x, uint64_t P, uint64_t K, double n
       return tie_sync(ctx, s);
     }
   }
+  // pageable samples (a caller's std::vector / NumPy array), >= 8 MB: the host copy pool
+  // fills the context's mapped pinned staging chunk by chunk, each chunk fitted zero-copy
+  // while the next is copied; the results land in the staging and the pool copies them out
+  // (the driver's pageable copies run single-threaded at ~10 GB/s)
+  static const bool no_stage = getenv("TIE_NO_HOST_STAGE") != nullptr;  // A/B switch
+  if (!no_stage && 8 * P * K >= (8u << 20)) {
+    const size_t ox = 0, omu = ox + al(8 * P * K), osg = omu + al(8 * P), oll = osg + al(8 * P),
+                 oit = oll + al(8 * P), ocv = oit + al(4 * P), odg = ocv + al(P),
+                 total = odg + al(P);
+    char* hs = host_stage(ctx, total);
+    char* dv = hs ? (char*)mapped_device_ptr(hs) : nullptr;
+    if (dv) {
+      CopyPool& pool = CopyPool::get();
+      constexpr int kChunks = 4;
+      const uint64_t step = (P + kChunks - 1) / kChunks;
+      for (uint64_t lo = 0; lo < P; lo += step) {
+        const uint64_t m = std::min<uint64_t>(step, P - lo);
+        pool.copy((double*)(hs + ox) + lo * K, x + lo * K, 8 * m * K);
+        const cudaError_t e = tie::dev::launch_fit(
+            ctx, (const double*)(dv + ox) + lo * K, m, K, nu, (double*)(dv + omu) + lo,
+            (double*)(dv + osg) + lo, (double*)(dv + oll) + lo, (int32_t*)(dv + oit) + lo,
+            (uint8_t*)(dv + ocv) + lo, (uint8_t*)(dv + odg) + lo, s, lo);
+        if (e != cudaSuccess) return cuda_error(e, "tie_fit_host");
+      }
+      if (int rc = tie_sync(ctx, s)) return rc;
+      pool.copy({{mu, hs + omu, 8 * P}, {sigma, hs + osg, 8 * P}});
+      if (log_likelihood) pool.copy(log_likelihood, hs + oll, 8 * P);
+      if (iterations) pool.copy(iterations, hs + oit, 4 * P);
+      if (converged) std::memcpy(converged, hs + ocv, P);
+      if (degenerate) std::memcpy(degenerate, hs + odg, P);
+      return TIE_OK;
+    }
+  }
   // pipeline over prompt chunks (fits are independent per prompt): all H2D copies queued on
   // the copy stream, chunk c's fit waits for its copy, its results go back on the copy
   // stream behind the H2Ds -- copies in both directions overlap the fits

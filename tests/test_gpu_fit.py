@@ -258,3 +258,30 @@ def test_fit_host_pinned_zero_copy_equals_device(tie, mc):
     tie.sync(mc.handle, sh)
     for h, d in zip(hb, db):
         assert torch.equal(h, d.cpu())
+
+
+@pytest.mark.parametrize("P", [70_001, 300_000])
+def test_fit_host_pageable_staged_equals_device(tie, mc, P):
+    """tie_fit_host on pageable NumPy buffers >= 8 MB (the host copy pool stages the samples
+    in chunks, fitted zero-copy, results copied out) == the device-buffer fit, bitwise; with
+    and without the optional outputs"""
+    import torch
+
+    K = 16
+    x, _, _ = tie.gen_fit_data(P, K, 4)
+    x = np.ascontiguousarray(x)
+    outs = [np.full(P, -7.0), np.full(P, -7.0), np.full(P, -7.0), np.zeros(P, np.int32),
+            np.zeros(P, np.uint8), np.zeros(P, np.uint8)]
+    tie.fit_host_ptr(mc.handle, x.ctypes.data, P, K, 3.5, *[o.ctypes.data for o in outs])
+    xd = torch.from_numpy(x).cuda()
+    db = [torch.empty(P, dtype=t, device="cuda") for t in
+          (torch.float64, torch.float64, torch.float64, torch.int32, torch.uint8, torch.uint8)]
+    sh = torch.cuda.current_stream().cuda_stream
+    tie.fit_device(mc.handle, xd.data_ptr(), P, K, 3.5, *[t.data_ptr() for t in db], sh)
+    tie.sync(mc.handle, sh)
+    for h, d in zip(outs, db):
+        assert np.array_equal(h, d.cpu().numpy())
+    mu2, sg2 = np.zeros(P), np.zeros(P)
+    tie.fit_host_ptr(mc.handle, x.ctypes.data, P, K, 3.5, mu2.ctypes.data, sg2.ctypes.data,
+                     0, 0, 0, 0)
+    assert np.array_equal(mu2, outs[0]) and np.array_equal(sg2, outs[1])

@@ -44,6 +44,10 @@ def main(bench, ref, tests):
           f"| config 3 fits (1M x 16), device | {fmt(d['fit']['value'])} fits/s "
           f"({d['fit']['ms']:.1f} ms) |",
           f"| config 3 fits, e2e (host buffers) | {fmt(d['fit']['e2e']['value'])} fits/s |",
+          *([f"| config 3 fits, e2e on pageable NumPy buffers | "
+             f"{fmt(d['fit']['e2e']['pageable']['value'])} fits/s "
+             f"({d['fit']['e2e']['pageable']['ms']:.1f} ms) |"]
+            if 'pageable' in d['fit']['e2e'] else []),
           f"| north-star fits, 10M x 16, one GPU | {fmt(d['fit_10M']['value'])} fits/s "
           f"({d['fit_10M']['ms']:.0f} ms) |",
           f"| config 5 trace simulation (run_sim, canonical.json, rebuild_threshold 0) | "
