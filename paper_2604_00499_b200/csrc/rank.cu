@@ -1268,6 +1268,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) part_fused_kernel(
   // the chunk's keys (after the local bases / cursors when the chunk is grouped locally)
   uint64_t* ck = reinterpret_cast<uint64_t*>(h + (q.local_scatter ? 3 : 1) * kPartMaxP);
   for (uint32_t p = threadIdx.x; p < P; p += kFusedThreads) h[p] = 0;
+  // launched as a programmatic dependent of the score kernel: the keys and their range are
+  // read only after the score grid has completed (a no-op without the dependency)
+  cudaGridDependencySynchronize();
   __syncthreads();
   const KeyRange r = key_range(q.mm, q.total_bits);
   const uint64_t lo = (uint64_t)blockIdx.x * q.chunk;
@@ -1777,8 +1780,30 @@ cudaError_t part_sort(tie_ctx* ctx, char* base, const Layout& L, const uint64_t*
     if (qf.ctas > 0 && 4 * kPartMaxP + 8 * qf.chunk <= smem) {
       ProfScope p(ctx, "rank.fused", s);
       void* args[] = {(void*)&qf, (void*)&n, (void*)&ids, (void*)&order};
-      cudaError_t e = cudaLaunchCooperativeKernel((const void*)part_fused_kernel, qf.ctas,
-                                                  kFusedThreads, args, smem, s);
+      // cooperative AND a programmatic dependent of the score kernel: the grid's launch and
+      // CTA setup overlap the score grid's tail; it waits (cudaGridDependencySynchronize)
+      // before reading the keys
+      static const bool no_pdl = getenv("TIE_NO_RANK_PDL") != nullptr;  // A/B switch
+      cudaError_t e = cudaErrorNotSupported;
+      if (!no_pdl) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(qf.ctas);
+        cfg.blockDim = dim3(kFusedThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        e = cudaLaunchKernelEx(&cfg, part_fused_kernel, qf, n, ids, order);
+        if (e != cudaSuccess) cudaGetLastError();
+      }
+      if (e != cudaSuccess)
+        e = cudaLaunchCooperativeKernel((const void*)part_fused_kernel, qf.ctas, kFusedThreads,
+                                        args, smem, s);
       if (e != cudaSuccess) return e;
       {  // programmatic dependent launch: its launch processing overlaps the sort grid
         // (measured 94.8 -> 93.2 us per 1M score+rank step)
