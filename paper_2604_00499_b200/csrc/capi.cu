@@ -9,6 +9,7 @@
 #include <condition_variable>
 #include <functional>
 #include <mutex>
+#include <pthread.h>
 #include <thread>
 #include <vector>
 #include <cstdio>
@@ -497,7 +498,8 @@ class CopyPool {
       total += (g.bytes + kTask - 1) / kTask;
     }
     job.ntask = total;
-    if (workers_.empty() || total <= 2) {
+    // (a forked child has no workers, and its mutexes may be mid-use: copy serially)
+    if (workers_.empty() || forked_.load() || total <= 2) {
       for (int g = 0; g < job.nseg; ++g) std::memcpy(job.seg[g].dst, job.seg[g].src, job.seg[g].bytes);
       return;
     }
@@ -530,6 +532,7 @@ class CopyPool {
     std::atomic<int> refs{0};
   };
   CopyPool() {
+    pthread_atfork(nullptr, nullptr, [] { forked_.store(true); });
     const unsigned hw = std::thread::hardware_concurrency();
     const unsigned nw = std::min(7u, hw > 1 ? hw - 1 : 0u);
     for (unsigned t = 0; t < nw; ++t)
@@ -582,6 +585,7 @@ class CopyPool {
   std::atomic<uint64_t> gen_{0};
   std::atomic<bool> stop_{false};
   Job* job_ = nullptr;
+  static inline std::atomic<bool> forked_{false};
 };
 }  // namespace
 
