@@ -813,13 +813,13 @@ constexpr int kCandCap = 2048;       // candidates held in shared memory
 // CTA argmin rounds over the threads' heads pop them in order; then the blocks are refreshed.
 // Used when the queue has fewer live blocks than pops (all their entries compete, which
 // would overflow the general path's candidate list).
+template <int kF>  // entries per thread: >= the chosen blocks (4 or 8)
 __device__ __forceinline__ void pop_from_blocks_regs(const QDev& q, const uint32_t* chosen,
                                                   uint32_t nchosen, uint64_t n_slots,
                                                   uint32_t pops, uint64_t* out_id,
                                                   uint32_t* out_slot, uint32_t* out_n,
                                                   uint64_t* out_key, uint64_t* dk,
                                                   uint64_t* di, uint32_t* ds) {
-  constexpr int kF = 8;
   uint64_t fk[kF], fi[kF];
   uint32_t fs[kF];
 #pragma unroll
@@ -978,8 +978,12 @@ __device__ __forceinline__ void pop_topb(const QDev& q, uint32_t nblocks, uint64
   }
   if (kSmallPath && nchosen < pops && nchosen <= 8 && blockDim.x == 1024) {
     // every live block is chosen (a small queue): select among all their entries directly
-    pop_from_blocks_regs(q, chosen, nchosen, n_slots, pops, out_id, out_slot, out_n, out_key,
-                         dk, di, ds);
+    if (nchosen <= 4)  // a 4-entry sort network instead of the 8-entry one
+      pop_from_blocks_regs<4>(q, chosen, nchosen, n_slots, pops, out_id, out_slot, out_n,
+                              out_key, dk, di, ds);
+    else
+      pop_from_blocks_regs<8>(q, chosen, nchosen, n_slots, pops, out_id, out_slot, out_n,
+                              out_key, dk, di, ds);
     return;
   }
   if (nchosen < pops) {  // every live block is chosen: all their live entries are candidates
